@@ -1,0 +1,139 @@
+"""Pins for oracle.increment (A-01, A-02, A-07, A-16, A-20-A-22) -- CPU only."""
+import dataclasses
+
+import numpy as np
+import pytest
+
+from oracle import material as M
+from oracle.increment import Cell, State, Tolerances, solve_increment
+from oracle.projection import apply_projection, mandel_to_tensor
+from oracle.spectral import Grid, rfftn
+from synth import INCLUSION_EL, MATRIX_J2, Material, config0
+
+TOL = Tolerances(tol_stag=1e-10, tol_newton=1e-11, tol_cg=1e-12, tol_helm=1e-12)
+
+
+def point_driver(mat, mask, load_comp, Es):
+    """Textbook 1-voxel mixed-control Newton + damage fixed point (a homogeneous cell)."""
+    mask = np.array(mask, bool)
+    epsp = np.zeros((6, 1)); ep = np.zeros(1); Dn = 0.0
+    eps = np.zeros(6)
+    out = []
+    for E in Es:
+        eps = eps.copy(); eps[load_comp] = E
+        D = Dn
+        for _ in range(200):
+            for _ in range(50):
+                s, C, pp, pe, _, _ = M.j2_lemaitre(eps.reshape(6, 1), epsp, ep, np.array([D]), mat)
+                r = s[mask, 0]
+                if np.linalg.norm(r) < 1e-13 * max(1.0, np.linalg.norm(s)):
+                    break
+                eps[mask] -= np.linalg.solve(C[np.ix_(mask, mask)][:, :, 0], r)
+            Dnew = max(Dn, float(M.lemaitre_damage(pe[0], mat.eps_c, mat.eps_r, mat.d_max)))
+            if abs(Dnew - D) < 1e-14:
+                break
+            D = Dnew
+        epsp, ep, Dn = pp, pe, max(Dn, float(M.lemaitre_damage(pe[0], mat.eps_c, mat.eps_r, mat.d_max)))
+        out.append(s[:, 0].copy())
+    return np.array(out)
+
+
+def test_homogeneous_cell_is_uniform_and_equals_material_point():
+    mat = dataclasses.replace(MATRIX_J2, eps_c=0.002, eps_r=0.012)
+    g = Grid((4, 4, 4))
+    mask = (1, 1, 0, 1, 1, 1)
+    cell = Cell(g, np.zeros(g.shape, np.uint8), [mat], np.array([[0.1]]), [0], mask)
+    st = State.zero(cell)
+    Es = [1e-3 * i for i in range(1, 9)]
+    ref = point_driver(mat, mask, 2, Es)
+    for i, E in enumerate(Es):
+        Et = np.zeros(6); Et[2] = E
+        st, rep = solve_increment(cell, st, Et, np.zeros(6), TOL)
+        assert rep.converged
+        e = st.eps.reshape(6, -1)
+        assert np.max(e.max(axis=1) - e.min(axis=1)) <= 1e-13 * max(1e-3, np.abs(e).max())
+        assert np.allclose(rep.macro_stress, ref[i], rtol=1e-9, atol=1e-7)
+    assert st.hist.max() > 0.1      # damage was active
+
+
+def test_elastic_uniaxial_stress_3d_and_plane_strain_2d():
+    mat = Material(model=0, E=70e3, nu=0.3)
+    for n, mask, expect in [((4, 4, 4), (0, 1, 1, 1, 1, 1), mat.E),
+                            ((8, 8, 1), (0, 1, 0, 0, 0, 1), mat.E / (1 - mat.nu ** 2))]:
+        g = Grid(n)
+        cell = Cell(g, np.zeros(g.shape, np.uint8), [mat], np.array([[0.1]]), [0], mask)
+        Et = np.zeros(6); Et[0] = 1e-3
+        st, rep = solve_increment(cell, State.zero(cell), Et, np.zeros(6), TOL)
+        assert abs(rep.macro_stress[0] - expect * 1e-3) < 1e-10 * expect * 1e-3
+
+
+def test_laminate_closed_form():
+    m0 = Material(model=0, E=70e3, nu=0.3)
+    m1 = Material(model=0, E=400e3, nu=0.2)
+    g = Grid((8, 2, 2))
+    ph = np.zeros(g.shape, np.uint8); ph[:, :, 5:] = 1          # layers normal to x, f1 = 3/8
+    cell = Cell(g, ph, [m0, m1], np.array([[0.1, 0.1]]), [0], (0,) * 6)
+    Et = np.zeros(6); Et[0] = 1e-3
+    st, rep = solve_increment(cell, State.zero(cell), Et, np.zeros(6), TOL)
+    f = np.array([5 / 8, 3 / 8])
+    lam, Pm = [], []
+    for m in (m0, m1):
+        K, mu = M.moduli(m.E, m.nu)
+        lam.append(K - 2 * mu / 3); Pm.append(K + 4 * mu / 3)
+    s11 = 1e-3 / np.sum(f / np.array(Pm))
+    e11 = s11 / np.array(Pm)
+    s22 = np.sum(f * np.array(lam) * e11)
+    assert abs(rep.macro_stress[0] - s11) < 1e-10 * s11
+    assert abs(rep.macro_stress[1] - s22) < 1e-10 * s11
+
+
+def small_disc(n=16):
+    cfg = config0(n, ell_over_L=2.0 / 16)
+    g = Grid(cfg.n, cfg.L)
+    return Cell(g, cfg.phases, cfg.materials, cfg.ell, cfg.source_phase, cfg.stress_mask)
+
+
+def test_equilibrium_compatibility_fixed_point():
+    cell = small_disc()
+    g = cell.grid
+    st = State.zero(cell)
+    for E in (2e-3, 4e-3, 6e-3):
+        Et = np.zeros(6); Et[0] = E
+        st, rep = solve_increment(cell, st, Et, np.zeros(6), TOL)
+        assert rep.converged
+    assert st.ep.max() > 1e-3                      # plastic
+    # equilibrium: sigma^ conj(k) = 0 at every xi != 0
+    T = mandel_to_tensor(rfftn(rep.sigma))
+    k = g.symbol()
+    t = np.einsum("ij...,j...->i...", T, np.conj(k))
+    t[:, 0, 0, 0] = 0
+    scale = np.max(np.abs(T)) * np.max(np.abs(k))
+    assert np.max(np.abs(t)) < 1e-9 * scale
+    # stress-controlled macroscopic components vanish (mask (0,1,0,0,0,1), Sigma = 0)
+    assert abs(rep.macro_stress[1]) < 1e-8 * abs(rep.macro_stress[0])
+    assert abs(rep.macro_stress[5]) < 1e-8 * abs(rep.macro_stress[0])
+    # compatibility: G*_{mask=0}(eps) = eps - <eps>
+    e = st.eps
+    fl = apply_projection(g, e, (0,) * 6)
+    assert np.max(np.abs(fl - (e - e.reshape(6, -1).mean(1).reshape(6, 1, 1, 1)))) < 1e-12
+    # fixed point: re-solving the converged increment changes nothing
+    st2, rep2 = solve_increment(cell, st, Et, np.zeros(6), TOL)
+    assert rep2.converged
+    assert np.max(np.abs(st2.eps - st.eps)) < 1e-9 * np.max(np.abs(st.eps))
+    assert np.allclose(rep2.macro_stress, rep.macro_stress, rtol=1e-7, atol=1e-6)
+
+
+def test_elastic_path_independence_and_two_staggered_iterations():
+    mat1 = Material(model=0, E=70e3, nu=0.3)
+    cfg = config0(8)
+    g = Grid(cfg.n, cfg.L)
+    cell = Cell(g, cfg.phases, [mat1, INCLUSION_EL], cfg.ell, cfg.source_phase, cfg.stress_mask)
+    Et = np.zeros(6); Et[0] = 4e-3
+    a, ra = solve_increment(cell, State.zero(cell), Et, np.zeros(6), TOL)
+    assert ra.stag_it == 2
+    st = State.zero(cell)
+    for E in (1e-3, 2e-3, 3e-3, 4e-3):
+        Et = np.zeros(6); Et[0] = E
+        st, rb = solve_increment(cell, st, Et, np.zeros(6), TOL)
+    assert np.max(np.abs(a.eps - st.eps)) < 1e-12
+    assert np.allclose(ra.macro_stress, rb.macro_stress, rtol=1e-10, atol=1e-9)
