@@ -1,0 +1,170 @@
+/* fgd.h -- C ABI of libfgd: the data-parallel hot path of the staggered FFT solver for
+ * implicit-gradient ductile damage of Magri, Lucarini, Lemoine, Adam, Segurado,
+ * "An FFT framework for simulating non-local ductile failure in heterogeneous materials"
+ * (arXiv 2103.04770).  Citations "P:<n>" are lines of the paper's source; "A-xx"
+ * are the readings listed in DESIGN.md.
+ *
+ * CONVENTIONS
+ *  - All reals are IEEE float64.  Moduli/stresses in the caller's unit (the tests use MPa).
+ *  - A "field" is contiguous [comp][z][y][x] (x fastest), N = N1*N2*N3 voxels per component.
+ *    Tensor fields have 6 Mandel components (11, 22, 33, sqrt2*23, sqrt2*13, sqrt2*12);
+ *    scalar fields have 1.  2D plane strain is N3 = 1 (A-19).
+ *  - Tangents are 21 packed components (upper triangle of the symmetric 6x6 Mandel matrix,
+ *    row-major: (0,0),(0,1)..(0,5),(1,1)..(5,5)), layout [21][z][y][x].
+ *  - POINTERS: every field pointer may be a DEVICE pointer (used in place, work enqueued on
+ *    the context stream; the call returns after the result is complete) or a HOST pointer
+ *    (pageable or pinned; staged through device memory by the library).  The library never
+ *    frees or retains caller pointers beyond the call.  Outputs must not alias inputs unless
+ *    stated.
+ *  - Grids: N1, N2 powers of two in [4, 512]; N3 = 1 or a power of two in [2, 512].
+ *  - Thread-compatible, not thread-safe: one host thread per context.
+ *  - ERRORS: no exception or abort crosses the ABI; every failure returns a negative
+ *    fgd_status and the message is available from fgd_last_error(ctx).
+ */
+#ifndef FGD_H
+#define FGD_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  FGD_OK = 0,
+  FGD_EINVAL = -1,   /* bad argument: N_i unsupported, L_i <= 0, nu out of range, unknown field */
+  FGD_ESHAPE = -2,   /* size/extent mismatch */
+  FGD_ECUDA = -3,    /* CUDA runtime error (message has the CUDA error string) */
+  FGD_ENCCL = -4,    /* collective error (multi-GPU) */
+  FGD_ENOMEM = -5,   /* device allocation failed */
+  FGD_ENOCONV = -6,  /* Newton/CG/PCG/staggered did not converge; increment state rolled back */
+  FGD_ESTATE = -7    /* call-order violation, e.g. apply before set_phases */
+} fgd_status;
+
+typedef struct fgd_ctx fgd_ctx;
+
+/* Grid.  scheme: 0 = continuous frequencies k = i xi (A-06),
+ * 1 = Willot rotated finite-difference scheme (A-04; default).
+ * The Helmholtz operator and solver are implemented for scheme 1 only (FGD_EINVAL otherwise). */
+typedef struct {
+  int dims;       /* 2 or 3 */
+  int n[3];       /* N1, N2, N3 (N3 = 1 for dims = 2) */
+  double L[3];    /* cell edge lengths, > 0 */
+  int scheme;
+} fgd_grid;
+
+/* Process placement.  This build supports nranks = 1 (one GPU); nranks > 1 returns FGD_EINVAL.
+ * stream: a cudaStream_t (may be NULL = the library creates its own). */
+typedef struct {
+  int rank, nranks, device;
+  const unsigned char* nccl_id; /* 128 bytes or NULL */
+  void* stream;
+} fgd_dist;
+
+fgd_status fgd_create(const fgd_grid* grid, const fgd_dist* dist, fgd_ctx** out);
+void fgd_destroy(fgd_ctx* ctx);
+const char* fgd_last_error(const fgd_ctx* ctx);
+fgd_status fgd_local_extent(const fgd_ctx* ctx, int* z0, int* nz);
+/* number of CUDA kernels this context has launched so far */
+unsigned long long fgd_launch_count(const fgd_ctx* ctx);
+
+/* Phase map (Omega = U Omega_q): one uint8 per voxel, values < nphases <= 16. */
+fgd_status fgd_set_phases(fgd_ctx* ctx, const uint8_t* phase, int nphases);
+
+/* Per-phase material (A-17, A-18).
+ * model 0 elastic (E, nu); 1 J2-Lemaitre with linear hardening sigma_0 = sigma_y + H eps_p and
+ * damage D(ebar) = clamp((ebar - eps_c)/(eps_r - eps_c), 0, d_max); 2 elastic-brittle particle
+ * with d = clamp((kappa - kappa0)/(kappa_f - kappa0), 0, d_max).  E > 0, -1 < nu < 0.5. */
+typedef struct {
+  int model;
+  double E, nu, sigma_y, H, eps_c, eps_r, d_max, kappa0, kappa_f;
+} fgd_material;
+fgd_status fgd_set_material(fgd_ctx* ctx, int phase, const fgd_material* m);
+
+/* Non-local fields: nfields <= 4; ell [nfields][nphases] in length units
+ * (piecewise-constant ell_j(x), Remark P:394-405); source_phase[j] = the phase whose local
+ * variable field j regularises (alpha_j = 0 elsewhere). */
+fgd_status fgd_set_nonlocal(fgd_ctx* ctx, int nfields, const double* ell, const int* source_phase);
+
+/* Mixed macroscopic control: stress_mask[6], 1 = stress-controlled. */
+fgd_status fgd_set_control(fgd_ctx* ctx, const int* stress_mask);
+
+/* Set the per-voxel tangent used by the projected-tangent apply and the mechanical CG
+ * (config 1 supplies a random SPD tangent; fgd_constitutive overwrites it). */
+fgd_status fgd_set_tangent(fgd_ctx* ctx, const double* C);
+
+/* y = G*(C : x): the FFT-Galerkin projected tangent apply.  G* is the orthogonal
+ * projection onto compatible fields with the zero-frequency Mandel mask of fgd_set_control
+ * (A-07, A-08).  x, y: 6-component fields. */
+fgd_status fgd_apply_projected_tangent(fgd_ctx* ctx, const double* x, double* y);
+
+/* y = G*(tau - Sigma) with Sigma = S (6 doubles, may be NULL = 0) removed from the mean
+ * (the Newton residual is -fgd_apply_projection(sigma, Sigma_bar)). */
+fgd_status fgd_apply_projection(fgd_ctx* ctx, const double* tau, const double* S, double* y);
+
+/* y = a - div(ell_j^2(x) grad a) for non-local field j (A-09), real space in/out. */
+fgd_status fgd_apply_helmholtz(fgd_ctx* ctx, int field, const double* a, double* y);
+
+/* z = F^-1[ F(r) / (1 + <ell_j^2> |k|^2) ] (A-11). */
+fgd_status fgd_apply_helmholtz_precond(fgd_ctx* ctx, int field, const double* r, double* z);
+
+/* Algorithm 2: abar = L_j^{-1} src by preconditioned CG from abar = 0, stop when
+ * ||L abar - src|| < tol ||src|| or after maxit iterations (tol <= 0: exactly maxit).
+ * src == NULL uses the source alpha_j of the last fgd_constitutive call; abar == NULL keeps
+ * the result internal (it becomes the frozen non-local field for the next fgd_constitutive).
+ * *iters (may be NULL) receives the iteration count, *relres the final relative residual. */
+fgd_status fgd_solve_helmholtz(fgd_ctx* ctx, int field, const double* src, double* abar, double tol,
+                               int maxit, int* iters, double* relres);
+
+/* Mechanical linear solve of one Newton step: unpreconditioned CG for
+ * G*(C : de) = b with de_0 = 0; b must lie in range(G*) (e.g. a Newton residual).  Same
+ * stopping rule and NULL conventions as fgd_solve_helmholtz (b == NULL: the residual of the
+ * last fgd_mech_residual; de == NULL: keep the correction internal). */
+fgd_status fgd_solve_tangent_cg(fgd_ctx* ctx, const double* b, double* de, double tol, int maxit,
+                                int* iters, double* relres);
+
+/* Per-voxel constitutive update (A-14..A-18) at strain eps (6 comps;
+ * NULL = the internal iterate) with the committed state and damage frozen from the current
+ * non-local fields (A-16).  Produces sigma, the packed consistent tangent and the
+ * Helmholtz sources alpha_j internally; sigma_out (may be NULL) receives sigma; macro[6]
+ * (may be NULL) receives <sigma>. */
+fgd_status fgd_constitutive(fgd_ctx* ctx, const double* eps, double* sigma_out, double* macro);
+
+/* Newton residual b = -G*(sigma - Sigma_bar) of the last fgd_constitutive,
+ * kept internal; b_out (may be NULL) receives it, *rms (may be NULL) its RMS over voxels. */
+fgd_status fgd_mech_residual(fgd_ctx* ctx, const double* S_target, double* b_out, double* rms);
+
+/* One increment of Algorithm 1: mixed-control Newton + CG mechanics and J
+ * Helmholtz PCG solves iterated until ERR < tol_stag (A-01, A-02).  Commits on FGD_OK;
+ * on FGD_ENOCONV the committed state is unchanged (rollback) and the caller cuts back. */
+typedef struct {
+  double E_target[6], S_target[6];
+  double tol_stag, tol_newton, tol_cg, tol_helm;
+  int max_stag, max_newton, max_cg, max_helm;
+} fgd_increment;
+typedef struct {
+  double macro_stress[6], macro_strain[6], err;
+  int stag_it, newton_it, cg_it, helm_it;
+} fgd_report;
+fgd_status fgd_solve_increment(fgd_ctx* ctx, const fgd_increment* inc, fgd_report* rep);
+
+/* Field access.  which: */
+enum {
+  FGD_FIELD_STRESS = 0,     /* 6 comps, last mechanical solve (get only) */
+  FGD_FIELD_STRAIN = 1,     /* 6 comps, committed strain eps_n */
+  FGD_FIELD_EPS_P = 2,      /* 6 comps, committed plastic strain */
+  FGD_FIELD_EQPS = 3,       /* 1 comp, committed equivalent plastic strain */
+  FGD_FIELD_HIST = 4,       /* 1 comp, committed damage history (D_n / kappa_n) */
+  FGD_FIELD_TANGENT = 5,    /* 21 comps, packed tangent in use (get only) */
+  FGD_FIELD_NONLOCAL = 16,  /* + j: 1 comp, non-local field abar_j */
+  FGD_FIELD_SOURCE = 32,    /* + j: 1 comp, local source alpha_j of the last constitutive call (get only) */
+  FGD_FIELD_ITERATE = 48    /* 6 comps, current strain iterate */
+};
+fgd_status fgd_get_field(fgd_ctx* ctx, int which, double* out);
+fgd_status fgd_set_field(fgd_ctx* ctx, int which, const double* in);
+fgd_status fgd_macro_stress(fgd_ctx* ctx, double out[6]);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FGD_H */

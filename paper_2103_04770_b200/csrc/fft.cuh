@@ -1,0 +1,162 @@
+// Shared-memory FP64 line FFTs for sm_100a (Stockham auto-sort, radix 2/4/8 butterflies in
+// registers, one warp or a sub-warp group per line).
+//
+// Convention: forward F(u)(k) = sum_n u(n) e^{-2 pi i k n / N} (unnormalised),
+// inverse with +i and no scaling here (the 1/N of F^-1 is folded into the spectral multiply).
+//
+// A line of N complex doubles lives in shared memory with one 16 B pad slot every 8 elements
+// (PAD) to break the stride-8 bank pattern of the first Stockham passes.  Each line is owned by
+// TPL = N / E threads that sit in one warp (E = elements per thread per pass), so passes are
+// separated by __syncwarp() only.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace fgd {
+
+__host__ __device__ constexpr int ilog2(int n) { return n <= 1 ? 0 : 1 + ilog2(n >> 1); }
+__host__ __device__ constexpr int fft_E(int N) { return N < 8 ? N : (N >= 512 ? 16 : 8); }
+__host__ __device__ constexpr int fft_TPL(int N) { return N / fft_E(N); }
+__host__ __device__ constexpr int fft_npass(int N) {
+  return N <= 1 ? 0 : (N <= 8 ? 1 : (N <= 64 ? 2 : 3));
+}
+// radix of pass p: 2:{2} 4:{4} 8:{8} 16:{4,4} 32:{8,4} 64:{8,8} 128:{8,4,4} 256:{8,8,4} 512:{8,8,8}
+__host__ __device__ constexpr int fft_radix(int N, int p) {
+  return N <= 8 ? N
+       : N == 16 ? 4
+       : N == 32 ? (p == 0 ? 8 : 4)
+       : N == 64 ? 8
+       : N == 128 ? (p == 0 ? 8 : 4)
+       : N == 256 ? (p < 2 ? 8 : 4)
+       : 8;
+}
+__host__ __device__ constexpr int pad_len(int N) { return N + (N >> 3); }
+__device__ __forceinline__ int PAD(int i) { return i + (i >> 3); }
+
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+__device__ __forceinline__ double2 conjg(double2 a) { return make_double2(a.x, -a.y); }
+__device__ __forceinline__ double2 cscale(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
+// multiply by -i (forward) or +i (inverse)
+template <bool INV> __device__ __forceinline__ double2 mul_mi(double2 a) {
+  return INV ? make_double2(-a.y, a.x) : make_double2(a.y, -a.x);
+}
+
+template <int P, bool INV> __device__ __forceinline__ void dft(double2* v);
+
+template <> __device__ __forceinline__ void dft<1, false>(double2*) {}
+template <> __device__ __forceinline__ void dft<1, true>(double2*) {}
+
+template <int P, bool INV> __device__ __forceinline__ void dft2(double2* v) {
+  double2 a = v[0], b = v[1];
+  v[0] = cadd(a, b);
+  v[1] = csub(a, b);
+}
+template <> __device__ __forceinline__ void dft<2, false>(double2* v) { dft2<2, false>(v); }
+template <> __device__ __forceinline__ void dft<2, true>(double2* v) { dft2<2, true>(v); }
+
+template <bool INV> __device__ __forceinline__ void dft4(double2& v0, double2& v1, double2& v2, double2& v3) {
+  double2 t0 = cadd(v0, v2), t1 = csub(v0, v2), t2 = cadd(v1, v3), t3 = mul_mi<INV>(csub(v1, v3));
+  v0 = cadd(t0, t2);
+  v2 = csub(t0, t2);
+  v1 = cadd(t1, t3);
+  v3 = csub(t1, t3);
+}
+template <> __device__ __forceinline__ void dft<4, false>(double2* v) { dft4<false>(v[0], v[1], v[2], v[3]); }
+template <> __device__ __forceinline__ void dft<4, true>(double2* v) { dft4<true>(v[0], v[1], v[2], v[3]); }
+
+template <bool INV> __device__ __forceinline__ void dft8(double2* v) {
+  constexpr double c = 0.70710678118654752440;
+  double2 e0 = v[0], e1 = v[2], e2 = v[4], e3 = v[6];
+  double2 o0 = v[1], o1 = v[3], o2 = v[5], o3 = v[7];
+  dft4<INV>(e0, e1, e2, e3);
+  dft4<INV>(o0, o1, o2, o3);
+  // w = e^{-i pi/4} (forward) / e^{+i pi/4} (inverse)
+  double2 w1o1 = INV ? make_double2(c * (o1.x - o1.y), c * (o1.x + o1.y))
+                     : make_double2(c * (o1.x + o1.y), c * (o1.y - o1.x));
+  double2 w2o2 = mul_mi<INV>(o2);
+  double2 w3o3 = INV ? make_double2(-c * (o3.x + o3.y), c * (o3.x - o3.y))
+                     : make_double2(c * (o3.y - o3.x), -c * (o3.x + o3.y));
+  v[0] = cadd(e0, o0);
+  v[4] = csub(e0, o0);
+  v[1] = cadd(e1, w1o1);
+  v[5] = csub(e1, w1o1);
+  v[2] = cadd(e2, w2o2);
+  v[6] = csub(e2, w2o2);
+  v[3] = cadd(e3, w3o3);
+  v[7] = csub(e3, w3o3);
+}
+template <> __device__ __forceinline__ void dft<8, false>(double2* v) { dft8<false>(v); }
+template <> __device__ __forceinline__ void dft<8, true>(double2* v) { dft8<true>(v); }
+
+// One Stockham pass of radix P over a line of N (padded, in shared memory).  Thread t in
+// [0, TPL) owns E/P butterflies j = t + b*TPL.  tw = table e^{-2 pi i m / N}, m in [0, N).
+template <int N, int P, int NS, bool INV>
+__device__ __forceinline__ void stockham_pass(double2* line, int t, bool active, const double2* __restrict__ tw) {
+  constexpr int E = fft_E(N);
+  constexpr int TPL = fft_TPL(N);
+  constexpr int NB = E / P;          // butterflies per thread
+  constexpr int NP = N / P;          // butterflies per line
+  double2 v[E];
+  if (active) {
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      const int j = t + b * TPL;
+#pragma unroll
+      for (int r = 0; r < P; ++r) v[b * P + r] = line[PAD(j + r * NP)];
+    }
+  }
+  __syncwarp();
+  if (active) {
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      const int j = t + b * TPL;
+      const int k = j % NS;
+      if (NS > 1) {
+        constexpr int STEP = N / (NS * P);
+#pragma unroll
+        for (int r = 1; r < P; ++r) {
+          double2 w = __ldg(&tw[r * k * STEP]);
+          if (INV) w.y = -w.y;
+          v[b * P + r] = cmul(v[b * P + r], w);
+        }
+      }
+      dft<P, INV>(&v[b * P]);
+      const int base = (j / NS) * NS * P + k;
+#pragma unroll
+      for (int r = 0; r < P; ++r) line[PAD(base + r * NS)] = v[b * P + r];
+    }
+  }
+  __syncwarp();
+}
+
+template <int N, int PASS, int NS, bool INV>
+__device__ __forceinline__ void fft_passes(double2* line, int t, bool active, const double2* __restrict__ tw) {
+  if constexpr (PASS < fft_npass(N)) {
+    constexpr int P = fft_radix(N, PASS);
+    stockham_pass<N, P, NS, INV>(line, t, active, tw);
+    fft_passes<N, PASS + 1, NS * P, INV>(line, t, active, tw);
+  }
+}
+
+// FFT all `nl` lines (stride ldl elements) of a CTA's shared buffer.  Every thread of the CTA
+// must call this (warp-synchronous inside); lines are distributed TPL threads per line.
+template <int N, bool INV>
+__device__ __forceinline__ void fft_lines(double2* buf, int nl, int ldl, const double2* __restrict__ tw) {
+  if constexpr (N > 1) {
+    constexpr int TPL = fft_TPL(N);
+    const int lines_per_round = blockDim.x / TPL;
+    const int slot = threadIdx.x / TPL;
+    const int t = threadIdx.x % TPL;
+    for (int base = 0; base < nl; base += lines_per_round) {
+      const int l = base + slot;
+      const bool active = l < nl;
+      fft_passes<N, 0, 1, INV>(buf + (size_t)(active ? l : 0) * ldl, t, active, tw);
+    }
+  }
+}
+
+}  // namespace fgd

@@ -1,0 +1,844 @@
+// libfgd C ABI (include/fgd.h): context, data setting, operator applies, Krylov solvers,
+// Newton and the Algorithm 1 staggered increment.  Host orchestration only: every step of the
+// hot path runs in the kernels of passes.cu / helmholtz.cu / constitutive.cu; the Krylov
+// scalars live on the device and the host reads one or two doubles per iteration to decide
+// convergence.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+
+#include "fgd_internal.cuh"
+
+namespace fgd {
+
+fgd_status set_err(fgd_ctx* c, fgd_status s, const std::string& m) {
+  if (c) c->err = m;
+  return s;
+}
+
+static bool is_pow2(int v) { return v > 0 && (v & (v - 1)) == 0; }
+
+template <typename T>
+static fgd_status dalloc(fgd_ctx* c, T** p, size_t count) {
+  if (*p) return FGD_OK;
+  cudaError_t e = cudaMalloc((void**)p, count * sizeof(T) + 16);
+  if (e != cudaSuccess) {
+    *p = nullptr;
+    cudaGetLastError();
+    return set_err(c, FGD_ENOMEM, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+  }
+  return FGD_OK;
+}
+
+fgd_status ensure_spectral(fgd_ctx* c) {
+  fgd_status s = dalloc(c, &c->specA, 6 * c->nspec);
+  if (s != FGD_OK) return s;
+  return dalloc(c, &c->specB, 6 * c->nspec);
+}
+
+fgd_status ensure_partials(fgd_ctx* c, size_t nblocks) {
+  const size_t need = nblocks * 16;
+  if (need <= c->partials_cap) return FGD_OK;
+  if (c->partials) {
+    cudaStreamSynchronize(c->stream);
+    cudaFree(c->partials);
+    c->partials = nullptr;
+  }
+  fgd_status s = dalloc(c, &c->partials, need);
+  if (s != FGD_OK) return s;
+  c->partials_cap = need;
+  return FGD_OK;
+}
+
+static bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes at;
+  cudaError_t e = cudaPointerGetAttributes(&at, p);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+// Host/device argument staging.  in(): returns a device pointer holding `count` doubles of p.
+struct Stage {
+  fgd_ctx* c;
+  std::vector<void*> bufs;
+  explicit Stage(fgd_ctx* cc) : c(cc) {}
+  ~Stage() {
+    for (void* b : bufs) cudaFreeAsync(b, c->stream);
+  }
+  template <typename T>
+  fgd_status in(const T* p, size_t count, const T** out) {
+    if (!p || is_device_ptr(p)) {
+      *out = p;
+      return FGD_OK;
+    }
+    void* d = nullptr;
+    cudaError_t e = cudaMallocAsync(&d, count * sizeof(T) + 16, c->stream);
+    if (e != cudaSuccess) return set_err(c, FGD_ENOMEM, std::string("staging: ") + cudaGetErrorString(e));
+    bufs.push_back(d);
+    e = cudaMemcpyAsync(d, p, count * sizeof(T), cudaMemcpyHostToDevice, c->stream);
+    if (e != cudaSuccess) return set_err(c, FGD_ECUDA, std::string("H2D: ") + cudaGetErrorString(e));
+    *out = (const T*)d;
+    return FGD_OK;
+  }
+  // out(): device destination for a result that must end in p (copied back by finish()).
+  struct Pending {
+    void* host;
+    const void* dev;
+    size_t bytes;
+  };
+  std::vector<Pending> pend;
+  template <typename T>
+  fgd_status out(T* p, size_t count, T** dst) {
+    if (!p || is_device_ptr(p)) {
+      *dst = p;
+      return FGD_OK;
+    }
+    void* d = nullptr;
+    cudaError_t e = cudaMallocAsync(&d, count * sizeof(T) + 16, c->stream);
+    if (e != cudaSuccess) return set_err(c, FGD_ENOMEM, std::string("staging: ") + cudaGetErrorString(e));
+    bufs.push_back(d);
+    pend.push_back({(void*)p, d, count * sizeof(T)});
+    *dst = (T*)d;
+    return FGD_OK;
+  }
+  fgd_status finish() {
+    for (auto& q : pend) {
+      cudaError_t e = cudaMemcpyAsync(q.host, q.dev, q.bytes, cudaMemcpyDeviceToHost, c->stream);
+      if (e != cudaSuccess) return set_err(c, FGD_ECUDA, std::string("D2H: ") + cudaGetErrorString(e));
+    }
+    cudaError_t e = cudaStreamSynchronize(c->stream);
+    if (e != cudaSuccess) return set_err(c, FGD_ECUDA, std::string("sync: ") + cudaGetErrorString(e));
+    return FGD_OK;
+  }
+};
+
+static fgd_status sync_read(fgd_ctx* c, const void* dev, size_t bytes, void* host) {
+  FGD_CUDA(c, cudaMemcpyAsync(c->pinned, dev, bytes, cudaMemcpyDeviceToHost, c->stream));
+  FGD_CUDA(c, cudaStreamSynchronize(c->stream));
+  std::memcpy(host, c->pinned, bytes);
+  return FGD_OK;
+}
+
+#define TRY(x)                         \
+  do {                                 \
+    fgd_status s_ = (x);               \
+    if (s_ != FGD_OK) return s_;       \
+  } while (0)
+
+// twiddle tables e^{-2 pi i m/N} for N = 1..512 (long double, exact at quarter turns)
+static fgd_status build_tables(fgd_ctx* c) {
+  std::vector<double2> h;
+  size_t off[11];
+  for (int l = 0; l <= 9; ++l) {
+    const int N = 1 << l;
+    off[l] = h.size();
+    for (int m = 0; m < N; ++m) {
+      double re, im;
+      if ((4 * m) % N == 0) {
+        const int qd = (4 * m / N) % 4;
+        const double cs[4] = {1, 0, -1, 0}, sn[4] = {0, 1, 0, -1};
+        re = cs[qd];
+        im = -sn[qd];
+      } else {
+        const long double ang = 2.0L * 3.141592653589793238462643383279502884L * (long double)m / (long double)N;
+        re = (double)cosl(ang);
+        im = (double)(-sinl(ang));
+      }
+      h.push_back(make_double2(re, im));
+    }
+  }
+  TRY(dalloc(c, &c->tw_all, h.size()));
+  FGD_CUDA(c, cudaMemcpy(c->tw_all, h.data(), h.size() * sizeof(double2), cudaMemcpyHostToDevice));
+  for (int l = 0; l <= 9; ++l) c->tabs.tw[l] = c->tw_all + off[l];
+  c->tabs.tw[10] = nullptr;
+  return FGD_OK;
+}
+
+static double inv_nvox(const fgd_ctx* c) { return 1.0 / (double)c->nvox; }
+
+// ---- composite operators (all enqueued on c->stream) -----------------------------------------
+// y = G*(C : x)
+static fgd_status op_projected_tangent(fgd_ctx* c, const double* x, double* y) {
+  TRY(ensure_spectral(c));
+  TRY(launch_xfwd(c, 6, XF_TANGENT, x, nullptr, nullptr, c->C, RED_NONE, 0));
+  TRY(launch_yfwd(c, 6));
+  TRY(launch_z(c, 6, Z_PROJECT, inv_nvox(c), nullptr, 0.0));
+  TRY(launch_yinv(c, 6));
+  return launch_xinv(c, 6, XI_STORE, y, nullptr, nullptr, nullptr, RED_NONE, 0);
+}
+
+// y = scale * G*(tau - S); optional reduction of y.y into op/slot
+static fgd_status op_projection(fgd_ctx* c, const double* tau, const double* S, double scale, double* y, int red_op,
+                                int red_slot) {
+  TRY(ensure_spectral(c));
+  double shift[6] = {0, 0, 0, 0, 0, 0};
+  if (S)
+    for (int i = 0; i < 6; ++i) shift[i] = S[i] * (double)c->nvox;
+  TRY(launch_xfwd(c, 6, XF_PLAIN, tau, nullptr, nullptr, nullptr, RED_NONE, 0));
+  TRY(launch_yfwd(c, 6));
+  TRY(launch_z(c, 6, Z_PROJECT, scale * inv_nvox(c), shift, 0.0));
+  TRY(launch_yinv(c, 6));
+  if (red_op == RED_NONE) return launch_xinv(c, 6, XI_STORE, y, nullptr, nullptr, nullptr, RED_NONE, 0);
+  return launch_xinv(c, 6, XI_STORE_RR, y, nullptr, nullptr, nullptr, red_op, red_slot);
+}
+
+// z = F^-1 M F r ; if r_for_dot != null: reduce r.z with red_op
+static fgd_status op_precond(fgd_ctx* c, int field, const double* r, double* z, int red_op) {
+  TRY(ensure_spectral(c));
+  TRY(launch_xfwd(c, 1, XF_PLAIN, r, nullptr, nullptr, nullptr, RED_NONE, 0));
+  TRY(launch_yfwd(c, 1));
+  TRY(launch_z(c, 1, Z_PRECOND, inv_nvox(c), nullptr, mean_ell2(c, field)));
+  TRY(launch_yinv(c, 1));
+  if (red_op == RED_NONE) return launch_xinv(c, 1, XI_STORE, z, nullptr, nullptr, nullptr, RED_NONE, 0);
+  return launch_xinv(c, 1, XI_HELM_Z, z, nullptr, nullptr, r, red_op, 0);
+}
+
+static fgd_status ensure_helm(fgd_ctx* c) {
+  for (int i = 0; i < 6; ++i) TRY(dalloc(c, &c->hb[i], c->nvox));
+  return FGD_OK;
+}
+static fgd_status ensure_cg(fgd_ctx* c) {
+  TRY(dalloc(c, &c->cg_x, 6 * c->nvox));
+  TRY(dalloc(c, &c->cg_r, 6 * c->nvox));
+  return dalloc(c, &c->cg_p, 6 * c->nvox);
+}
+static fgd_status ensure_state(fgd_ctx* c) {
+  const size_t n = c->nvox;
+  const size_t J = std::max(1, c->nfields);
+  if (c->st_eps) return FGD_OK;
+  TRY(dalloc(c, &c->st_eps, 6 * n));
+  TRY(dalloc(c, &c->st_epsp, 6 * n));
+  TRY(dalloc(c, &c->st_ep, n));
+  TRY(dalloc(c, &c->st_hist, n));
+  TRY(dalloc(c, &c->st_abar, J * n));
+  TRY(dalloc(c, &c->w_eps, 6 * n));
+  TRY(dalloc(c, &c->w_eps_prev, 6 * n));
+  TRY(dalloc(c, &c->w_sig, 6 * n));
+  TRY(dalloc(c, &c->w_alpha, J * n));
+  TRY(dalloc(c, &c->w_abar, J * n));
+  TRY(dalloc(c, &c->w_D, J * n));
+  TRY(dalloc(c, &c->cm_epsp, 6 * n));
+  TRY(dalloc(c, &c->cm_ep, n));
+  TRY(dalloc(c, &c->cm_hist, n));
+  TRY(dalloc(c, &c->w_b, 6 * n));
+  TRY(dalloc(c, &c->w_de, 6 * n));
+  TRY(dalloc(c, &c->C, 21 * n));
+  FGD_CUDA(c, cudaMemsetAsync(c->st_eps, 0, 6 * n * 8, c->stream));
+  FGD_CUDA(c, cudaMemsetAsync(c->st_epsp, 0, 6 * n * 8, c->stream));
+  FGD_CUDA(c, cudaMemsetAsync(c->st_ep, 0, n * 8, c->stream));
+  FGD_CUDA(c, cudaMemsetAsync(c->st_hist, 0, n * 8, c->stream));
+  FGD_CUDA(c, cudaMemsetAsync(c->st_abar, 0, J * n * 8, c->stream));
+  FGD_CUDA(c, cudaMemsetAsync(c->w_abar, 0, J * n * 8, c->stream));
+  FGD_CUDA(c, cudaMemcpyAsync(c->w_eps, c->st_eps, 6 * n * 8, cudaMemcpyDeviceToDevice, c->stream));
+  return FGD_OK;
+}
+
+// Algorithm 2 in real space (equivalent to the Fourier-space PCG: F is unitary up to N).
+static fgd_status pcg_helmholtz(fgd_ctx* c, int field, const double* b, double* x_out, double tol, int maxit,
+                                int* iters, double* relres) {
+  TRY(ensure_helm(c));
+  TRY(ensure_spectral(c));
+  const size_t n = c->nvox;
+  double* x = c->hb[0];
+  double* r = c->hb[1];
+  double* z = c->hb[2];
+  double* P[2] = {c->hb[3], c->hb[4]};
+  double* q = c->hb[5];
+  FGD_CUDA(c, cudaMemsetAsync(x, 0, n * 8, c->stream));
+  FGD_CUDA(c, cudaMemsetAsync(P[0], 0, n * 8, c->stream));
+  FGD_CUDA(c, cudaMemcpyAsync(r, b, n * 8, cudaMemcpyDeviceToDevice, c->stream));
+  TRY(launch_dot(c, n, r, r, RED_BB, 0));
+  double bb = 0.0;
+  TRY(sync_read(c, &c->sc->bb, 8, &bb));
+  int it = 0;
+  double rel = 0.0;
+  if (bb > 0.0) {
+    TRY(op_precond(c, field, r, z, RED_HELM_INIT));
+    int cur = 0;
+    rel = 1.0;
+    while (it < maxit) {
+      TRY(launch_stencil(c, field, 1, nullptr, z, P[cur], P[cur ^ 1], q, RED_HELM_PQ));
+      cur ^= 1;
+      TRY(launch_xfwd_io(c, 1, XF_HELM_UPDATE, P[cur], q, x, r, nullptr, RED_HELM_RN, 0));
+      ++it;
+      if (tol > 0.0) {
+        double rn2;
+        TRY(sync_read(c, &c->sc->rn2, 8, &rn2));
+        rel = std::sqrt(rn2 / bb);
+        if (rel < tol) break;
+      }
+      TRY(launch_yfwd(c, 1));
+      TRY(launch_z(c, 1, Z_PRECOND, inv_nvox(c), nullptr, mean_ell2(c, field)));
+      TRY(launch_yinv(c, 1));
+      TRY(launch_xinv(c, 1, XI_HELM_Z, z, nullptr, nullptr, r, RED_HELM_RZ, 0));
+    }
+    if (tol <= 0.0) {
+      double rn2;
+      TRY(sync_read(c, &c->sc->rn2, 8, &rn2));
+      rel = std::sqrt(rn2 / bb);
+    }
+  }
+  if (x_out) FGD_CUDA(c, cudaMemcpyAsync(x_out, x, n * 8, cudaMemcpyDeviceToDevice, c->stream));
+  if (iters) *iters = it;
+  if (relres) *relres = rel;
+  if (tol > 0.0 && bb > 0.0 && rel >= tol) return set_err(c, FGD_ENOCONV, "Helmholtz PCG did not converge");
+  return FGD_OK;
+}
+
+// Mechanical CG on G*(C : de) = b, de_0 = 0.  p.q = p.Cp for p in range(G*).
+static fgd_status cg_mech(fgd_ctx* c, const double* b, double* x_out, double tol, int maxit, int* iters,
+                          double* relres) {
+  TRY(ensure_cg(c));
+  TRY(ensure_spectral(c));
+  const size_t n6 = 6 * c->nvox;
+  FGD_CUDA(c, cudaMemsetAsync(c->cg_x, 0, n6 * 8, c->stream));
+  FGD_CUDA(c, cudaMemsetAsync(c->cg_p, 0, n6 * 8, c->stream));
+  FGD_CUDA(c, cudaMemcpyAsync(c->cg_r, b, n6 * 8, cudaMemcpyDeviceToDevice, c->stream));
+  TRY(launch_dot(c, n6, c->cg_r, c->cg_r, RED_MECH_INIT, 0));
+  double bb = 0.0;
+  TRY(sync_read(c, &c->sc->bb, 8, &bb));
+  int it = 0;
+  double rel = 0.0;
+  if (bb > 0.0) {
+    rel = 1.0;
+    while (it < maxit) {
+      TRY(launch_xfwd(c, 6, XF_TANGENT_CG, c->cg_r, nullptr, c->cg_p, c->C, RED_MECH_PQ, 0));
+      TRY(launch_yfwd(c, 6));
+      TRY(launch_z(c, 6, Z_PROJECT, inv_nvox(c), nullptr, 0.0));
+      TRY(launch_yinv(c, 6));
+      TRY(launch_xinv(c, 6, XI_MECH_CG, nullptr, c->cg_x, c->cg_r, c->cg_p, RED_MECH_RR, 0));
+      ++it;
+      if (tol > 0.0) {
+        double rr;
+        TRY(sync_read(c, &c->sc->rr, 8, &rr));
+        rel = std::sqrt(rr / bb);
+        if (rel < tol) break;
+      }
+    }
+    if (tol <= 0.0) {
+      double rr;
+      TRY(sync_read(c, &c->sc->rr, 8, &rr));
+      rel = std::sqrt(rr / bb);
+    }
+  }
+  if (x_out) FGD_CUDA(c, cudaMemcpyAsync(x_out, c->cg_x, n6 * 8, cudaMemcpyDeviceToDevice, c->stream));
+  if (iters) *iters = it;
+  if (relres) *relres = rel;
+  if (tol > 0.0 && bb > 0.0 && rel >= tol) return set_err(c, FGD_ENOCONV, "mechanical CG did not converge");
+  return FGD_OK;
+}
+
+static fgd_status check_ready(fgd_ctx* c, bool need_phase, bool need_nonlocal, bool need_mat) {
+  if (!c) return FGD_EINVAL;
+  if (need_phase && !c->phase) return set_err(c, FGD_ESTATE, "fgd_set_phases has not been called");
+  if (need_nonlocal && !c->nonlocal_set) return set_err(c, FGD_ESTATE, "fgd_set_nonlocal has not been called");
+  if (need_mat) {
+    for (int q = 0; q < c->nphases; ++q)
+      if (!c->mat_set[q]) return set_err(c, FGD_ESTATE, "material of phase " + std::to_string(q) + " not set");
+  }
+  return FGD_OK;
+}
+
+}  // namespace fgd
+
+using namespace fgd;
+
+extern "C" {
+
+fgd_status fgd_create(const fgd_grid* g, const fgd_dist* d, fgd_ctx** out) {
+  if (!g || !out) return FGD_EINVAL;
+  *out = nullptr;
+  fgd_ctx* c = new fgd_ctx();
+  auto fail = [&](fgd_status s, const std::string& m) {
+    fprintf(stderr, "fgd_create: %s\n", m.c_str());
+    fgd_destroy(c);
+    return s;
+  };
+  if (g->dims != 2 && g->dims != 3) return fail(FGD_EINVAL, "dims must be 2 or 3");
+  for (int i = 0; i < 3; ++i) {
+    c->n[i] = g->n[i];
+    c->L[i] = g->L[i];
+  }
+  if (g->dims == 2) c->n[2] = 1;
+  for (int i = 0; i < 2; ++i)
+    if (!is_pow2(c->n[i]) || c->n[i] < 4 || c->n[i] > kMaxN) return fail(FGD_EINVAL, "N1, N2 must be powers of two in [4, 512]");
+  if (!is_pow2(c->n[2]) || c->n[2] > kMaxN) return fail(FGD_EINVAL, "N3 must be 1 or a power of two <= 512");
+  if (c->n[2] == 1 && g->dims == 3) return fail(FGD_EINVAL, "dims = 3 needs N3 >= 2");
+  for (int i = 0; i < 3; ++i) {
+    if (!(c->L[i] > 0.0)) {
+      if (i == 2 && c->n[2] == 1) c->L[2] = c->L[0] / c->n[0];
+      else return fail(FGD_EINVAL, "L_i must be > 0");
+    }
+    c->h[i] = c->L[i] / c->n[i];
+  }
+  if (g->scheme != 0 && g->scheme != 1) return fail(FGD_EINVAL, "scheme must be 0 or 1");
+  c->scheme = g->scheme;
+  c->dims = g->dims;
+  c->nvox = (size_t)c->n[0] * c->n[1] * c->n[2];
+  c->Hx = c->n[0] / 2 + 1;
+  c->nspec = (size_t)c->Hx * c->n[1] * c->n[2];
+  if (d) {
+    if (d->nranks != 1 || d->rank != 0) return fail(FGD_EINVAL, "this build supports nranks = 1");
+    c->device = d->device;
+    c->stream = (cudaStream_t)d->stream;
+  }
+  if (cudaSetDevice(c->device) != cudaSuccess) return fail(FGD_ECUDA, "cudaSetDevice failed");
+  if (!c->stream) {
+    if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess)
+      return fail(FGD_ECUDA, "cudaStreamCreate failed");
+    c->own_stream = true;
+  }
+  {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, c->device) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  }
+  if (build_tables(c) != FGD_OK) return fail(FGD_ECUDA, c->err);
+  if (dalloc(c, &c->sc, 1) != FGD_OK) return fail(FGD_ENOMEM, c->err);
+  if (cudaMemset(c->sc, 0, sizeof(DevScalars)) != cudaSuccess) return fail(FGD_ECUDA, "memset");
+  if (cudaMallocHost((void**)&c->pinned, 4096) != cudaSuccess) return fail(FGD_ENOMEM, "cudaMallocHost");
+  if (ensure_partials(c, 148 * 64) != FGD_OK) return fail(FGD_ENOMEM, c->err);
+  *out = c;
+  return FGD_OK;
+}
+
+void fgd_destroy(fgd_ctx* c) {
+  if (!c) return;
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  void* bufs[] = {c->tw_all, c->phase, c->C, c->specA, c->specB, c->cg_x, c->cg_r, c->cg_p, c->sc, c->partials,
+                  c->st_eps, c->st_epsp, c->st_ep, c->st_hist, c->st_abar, c->w_eps, c->w_eps_prev, c->w_sig,
+                  c->w_alpha, c->w_abar, c->w_D, c->cm_epsp, c->cm_ep, c->cm_hist, c->w_b, c->w_de};
+  for (void* b : bufs)
+    if (b) cudaFree(b);
+  for (int i = 0; i < 6; ++i)
+    if (c->hb[i]) cudaFree(c->hb[i]);
+  if (c->pinned) cudaFreeHost(c->pinned);
+  if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+const char* fgd_last_error(const fgd_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+fgd_status fgd_local_extent(const fgd_ctx* c, int* z0, int* nz) {
+  if (!c) return FGD_EINVAL;
+  if (z0) *z0 = 0;
+  if (nz) *nz = c->n[2];
+  return FGD_OK;
+}
+
+unsigned long long fgd_launch_count(const fgd_ctx* c) { return c ? c->launches : 0ull; }
+
+fgd_status fgd_set_phases(fgd_ctx* c, const uint8_t* phase, int nphases) {
+  if (!c || !phase) return set_err(c, FGD_EINVAL, "null argument");
+  if (nphases < 1 || nphases > kMaxPhases) return set_err(c, FGD_EINVAL, "nphases must be in [1, 16]");
+  TRY(dalloc(c, &c->phase, c->nvox));
+  if (is_device_ptr(phase))
+    FGD_CUDA(c, cudaMemcpyAsync(c->phase, phase, c->nvox, cudaMemcpyDeviceToDevice, c->stream));
+  else
+    FGD_CUDA(c, cudaMemcpyAsync(c->phase, phase, c->nvox, cudaMemcpyHostToDevice, c->stream));
+  unsigned long long* cnt = nullptr;
+  int* bad = nullptr;
+  FGD_CUDA(c, cudaMallocAsync((void**)&cnt, 8 * kMaxPhases + 16, c->stream));
+  FGD_CUDA(c, cudaMemsetAsync(cnt, 0, 8 * kMaxPhases + 16, c->stream));
+  bad = (int*)(cnt + kMaxPhases);
+  TRY(launch_phase_count(c, c->phase, cnt, nphases, bad));
+  unsigned long long h[kMaxPhases + 2];
+  FGD_CUDA(c, cudaMemcpyAsync(h, cnt, 8 * kMaxPhases + 16, cudaMemcpyDeviceToHost, c->stream));
+  FGD_CUDA(c, cudaStreamSynchronize(c->stream));
+  cudaFreeAsync(cnt, c->stream);
+  if (*(int*)(h + kMaxPhases)) return set_err(c, FGD_EINVAL, "phase id >= nphases");
+  c->nphases = nphases;
+  c->phase_count.assign(h, h + nphases);
+  return FGD_OK;
+}
+
+fgd_status fgd_set_material(fgd_ctx* c, int phase, const fgd_material* m) {
+  if (!c || !m) return set_err(c, FGD_EINVAL, "null argument");
+  if (phase < 0 || phase >= kMaxPhases) return set_err(c, FGD_EINVAL, "phase out of range");
+  if (m->model < 0 || m->model > 2) return set_err(c, FGD_EINVAL, "unknown material model");
+  if (!(m->E > 0.0) || !(m->nu > -1.0 && m->nu < 0.5)) return set_err(c, FGD_EINVAL, "E > 0 and -1 < nu < 0.5 required");
+  if (m->model == 1 && !(m->eps_r > m->eps_c)) return set_err(c, FGD_EINVAL, "eps_r must exceed eps_c");
+  if (m->model == 2 && !(m->kappa_f > m->kappa0)) return set_err(c, FGD_EINVAL, "kappa_f must exceed kappa0");
+  c->mat[phase] = Material{m->model, m->E, m->nu, m->sigma_y, m->H, m->eps_c, m->eps_r, m->d_max, m->kappa0, m->kappa_f};
+  c->mat_set[phase] = true;
+  return FGD_OK;
+}
+
+fgd_status fgd_set_nonlocal(fgd_ctx* c, int nfields, const double* ell, const int* source_phase) {
+  if (!c) return FGD_EINVAL;
+  if (!c->phase) return set_err(c, FGD_ESTATE, "fgd_set_phases must precede fgd_set_nonlocal");
+  if (nfields < 0 || nfields > kMaxFields) return set_err(c, FGD_EINVAL, "nfields must be in [0, 4]");
+  if (nfields > 0 && (!ell || !source_phase)) return set_err(c, FGD_EINVAL, "null argument");
+  if (c->st_eps && nfields != c->nfields) return set_err(c, FGD_ESTATE, "nfields cannot change after the state exists");
+  for (int j = 0; j < nfields; ++j) {
+    if (source_phase[j] < 0 || source_phase[j] >= c->nphases) return set_err(c, FGD_EINVAL, "source_phase out of range");
+    for (int q = 0; q < c->nphases; ++q) {
+      if (!(ell[j * c->nphases + q] >= 0.0)) return set_err(c, FGD_EINVAL, "ell must be >= 0");
+      c->ell[j][q] = ell[j * c->nphases + q];
+    }
+    c->source_phase[j] = source_phase[j];
+  }
+  c->nfields = nfields;
+  c->nonlocal_set = true;
+  return FGD_OK;
+}
+
+fgd_status fgd_set_control(fgd_ctx* c, const int* mask) {
+  if (!c || !mask) return set_err(c, FGD_EINVAL, "null argument");
+  for (int i = 0; i < 6; ++i) c->stress_mask[i] = mask[i] ? 1 : 0;
+  c->control_set = true;
+  return FGD_OK;
+}
+
+fgd_status fgd_set_tangent(fgd_ctx* c, const double* C) {
+  if (!c || !C) return set_err(c, FGD_EINVAL, "null argument");
+  TRY(dalloc(c, &c->C, 21 * c->nvox));
+  if (is_device_ptr(C))
+    FGD_CUDA(c, cudaMemcpyAsync(c->C, C, 21 * c->nvox * 8, cudaMemcpyDeviceToDevice, c->stream));
+  else
+    FGD_CUDA(c, cudaMemcpyAsync(c->C, C, 21 * c->nvox * 8, cudaMemcpyHostToDevice, c->stream));
+  FGD_CUDA(c, cudaStreamSynchronize(c->stream));
+  c->tangent_set = true;
+  return FGD_OK;
+}
+
+fgd_status fgd_apply_projected_tangent(fgd_ctx* c, const double* x, double* y) {
+  if (!c || !x || !y) return set_err(c, FGD_EINVAL, "null argument");
+  if (!c->tangent_set) return set_err(c, FGD_ESTATE, "no tangent (fgd_set_tangent or fgd_constitutive)");
+  Stage st(c);
+  const double* dx;
+  double* dy;
+  TRY(st.in(x, 6 * c->nvox, &dx));
+  TRY(st.out(y, 6 * c->nvox, &dy));
+  TRY(op_projected_tangent(c, dx, dy));
+  return st.finish();
+}
+
+fgd_status fgd_apply_projection(fgd_ctx* c, const double* tau, const double* S, double* y) {
+  if (!c || !tau || !y) return set_err(c, FGD_EINVAL, "null argument");
+  Stage st(c);
+  const double* dt;
+  double* dy;
+  TRY(st.in(tau, 6 * c->nvox, &dt));
+  TRY(st.out(y, 6 * c->nvox, &dy));
+  TRY(op_projection(c, dt, S, 1.0, dy, RED_NONE, 0));
+  return st.finish();
+}
+
+static fgd_status check_field(fgd_ctx* c, int field) {
+  TRY(check_ready(c, true, true, false));
+  if (field < 0 || field >= c->nfields) return set_err(c, FGD_EINVAL, "field out of range");
+  if (c->scheme != 1) return set_err(c, FGD_EINVAL, "the Helmholtz operator is implemented for the Willot scheme only");
+  return FGD_OK;
+}
+
+fgd_status fgd_apply_helmholtz(fgd_ctx* c, int field, const double* a, double* y) {
+  if (!c || !a || !y) return set_err(c, FGD_EINVAL, "null argument");
+  TRY(check_field(c, field));
+  Stage st(c);
+  const double* da;
+  double* dy;
+  TRY(st.in(a, c->nvox, &da));
+  TRY(st.out(y, c->nvox, &dy));
+  TRY(launch_stencil(c, field, 0, da, nullptr, nullptr, nullptr, dy, RED_NONE));
+  return st.finish();
+}
+
+fgd_status fgd_apply_helmholtz_precond(fgd_ctx* c, int field, const double* r, double* z) {
+  if (!c || !r || !z) return set_err(c, FGD_EINVAL, "null argument");
+  TRY(check_ready(c, true, true, false));
+  if (field < 0 || field >= c->nfields) return set_err(c, FGD_EINVAL, "field out of range");
+  Stage st(c);
+  const double* dr;
+  double* dz;
+  TRY(st.in(r, c->nvox, &dr));
+  TRY(st.out(z, c->nvox, &dz));
+  TRY(op_precond(c, field, dr, dz, RED_NONE));
+  return st.finish();
+}
+
+fgd_status fgd_solve_helmholtz(fgd_ctx* c, int field, const double* src, double* abar, double tol, int maxit,
+                               int* iters, double* relres) {
+  if (!c) return FGD_EINVAL;
+  TRY(check_field(c, field));
+  if (maxit < 0) return set_err(c, FGD_EINVAL, "maxit < 0");
+  Stage st(c);
+  const double* ds = nullptr;
+  if (src) {
+    TRY(st.in(src, c->nvox, &ds));
+  } else {
+    if (!c->have_sigma) return set_err(c, FGD_ESTATE, "src == NULL needs a previous fgd_constitutive");
+    ds = c->w_alpha + (size_t)field * c->nvox;
+  }
+  double* dout = nullptr;
+  if (abar) {
+    TRY(st.out(abar, c->nvox, &dout));
+  } else {
+    TRY(ensure_state(c));
+    dout = c->w_abar + (size_t)field * c->nvox;
+  }
+  fgd_status s = pcg_helmholtz(c, field, ds, dout, tol, maxit, iters, relres);
+  fgd_status f = st.finish();
+  return s != FGD_OK ? s : f;
+}
+
+fgd_status fgd_solve_tangent_cg(fgd_ctx* c, const double* b, double* de, double tol, int maxit, int* iters,
+                                double* relres) {
+  if (!c) return FGD_EINVAL;
+  if (!c->tangent_set) return set_err(c, FGD_ESTATE, "no tangent");
+  if (maxit < 0) return set_err(c, FGD_EINVAL, "maxit < 0");
+  Stage st(c);
+  const double* db = nullptr;
+  if (b) {
+    TRY(st.in(b, 6 * c->nvox, &db));
+  } else {
+    if (!c->have_residual) return set_err(c, FGD_ESTATE, "b == NULL needs a previous fgd_mech_residual");
+    db = c->w_b;
+  }
+  double* dx = nullptr;
+  if (de) {
+    TRY(st.out(de, 6 * c->nvox, &dx));
+  } else {
+    TRY(ensure_state(c));
+    dx = c->w_de;
+  }
+  fgd_status s = cg_mech(c, db, dx, tol, maxit, iters, relres);
+  fgd_status f = st.finish();
+  return s != FGD_OK ? s : f;
+}
+
+fgd_status fgd_constitutive(fgd_ctx* c, const double* eps, double* sigma_out, double* macro) {
+  if (!c) return FGD_EINVAL;
+  TRY(check_ready(c, true, true, true));
+  TRY(ensure_state(c));
+  Stage st(c);
+  const double* de = c->w_eps;
+  if (eps) {
+    TRY(st.in(eps, 6 * c->nvox, &de));
+    if (de != c->w_eps)
+      FGD_CUDA(c, cudaMemcpyAsync(c->w_eps, de, 6 * c->nvox * 8, cudaMemcpyDeviceToDevice, c->stream));
+  }
+  TRY(launch_constitutive(c, c->w_eps));
+  c->tangent_set = true;
+  c->have_sigma = true;
+  if (sigma_out) {
+    double* ds;
+    TRY(st.out(sigma_out, 6 * c->nvox, &ds));
+    FGD_CUDA(c, cudaMemcpyAsync(ds, c->w_sig, 6 * c->nvox * 8, cudaMemcpyDeviceToDevice, c->stream));
+  }
+  double m[6];
+  TRY(sync_read(c, c->sc->red, 48, m));
+  for (int i = 0; i < 6; ++i) c->last_macro[i] = m[i] / (double)c->nvox;
+  if (macro)
+    for (int i = 0; i < 6; ++i) macro[i] = c->last_macro[i];
+  return st.finish();
+}
+
+fgd_status fgd_mech_residual(fgd_ctx* c, const double* S_target, double* b_out, double* rms) {
+  if (!c) return FGD_EINVAL;
+  if (!c->have_sigma) return set_err(c, FGD_ESTATE, "fgd_mech_residual needs a previous fgd_constitutive");
+  double S[6] = {0, 0, 0, 0, 0, 0};
+  if (S_target)
+    for (int i = 0; i < 6; ++i) S[i] = S_target[i] * c->stress_mask[i];
+  TRY(op_projection(c, c->w_sig, S, -1.0, c->w_b, RED_STORE, 8));
+  c->have_residual = true;
+  double ss;
+  TRY(sync_read(c, &c->sc->red[8], 8, &ss));
+  if (rms) *rms = std::sqrt(ss / (double)c->nvox);
+  if (b_out) {
+    Stage st(c);
+    double* db;
+    TRY(st.out(b_out, 6 * c->nvox, &db));
+    FGD_CUDA(c, cudaMemcpyAsync(db, c->w_b, 6 * c->nvox * 8, cudaMemcpyDeviceToDevice, c->stream));
+    return st.finish();
+  }
+  return FGD_OK;
+}
+
+static double sigma_ref(const fgd_ctx* c) {
+  double s = 0.0, e = 0.0;
+  for (int q = 0; q < c->nphases; ++q) {
+    s = std::max(s, c->mat[q].model == 1 ? c->mat[q].sigma_y : 0.0);
+    e = std::max(e, c->mat[q].E);
+  }
+  return s > 0.0 ? s : e * 1e-3;
+}
+
+fgd_status fgd_solve_increment(fgd_ctx* c, const fgd_increment* inc, fgd_report* rep) {
+  if (!c || !inc) return set_err(c, FGD_EINVAL, "null argument");
+  TRY(check_ready(c, true, true, true));
+  TRY(ensure_state(c));
+  const size_t n = c->nvox;
+  const int J = c->nfields;
+  // 1. eps^(0) = eps_n + dE on strain-controlled comps; abar^(0) = abar_n  (A-22)
+  double mean_n[6];
+  {
+    // <eps_n> : use the err kernel's sums with eps_prev = eps
+    FGD_CUDA(c, cudaMemsetAsync(&c->sc->maxbits, 0, 8, c->stream));
+    TRY(launch_err(c, c->st_eps, c->st_eps, c->st_abar, c->st_abar, &c->sc->maxbits));
+    double red[6];
+    TRY(sync_read(c, &c->sc->red[16], 48, red));
+    for (int i = 0; i < 6; ++i) mean_n[i] = red[i] / (double)n;
+  }
+  double dE[6];
+  for (int i = 0; i < 6; ++i) dE[i] = c->stress_mask[i] ? 0.0 : inc->E_target[i] - mean_n[i];
+  std::memcpy(c->pinned + 64, dE, 48);
+  FGD_CUDA(c, cudaMemcpyAsync(&c->sc->red[40], c->pinned + 64, 48, cudaMemcpyHostToDevice, c->stream));
+  TRY(launch_init_iterate(c, c->st_eps, c->w_eps, &c->sc->red[40]));
+  if (J > 0) FGD_CUDA(c, cudaMemcpyAsync(c->w_abar, c->st_abar, (size_t)J * n * 8, cudaMemcpyDeviceToDevice, c->stream));
+  double S[6];
+  for (int i = 0; i < 6; ++i) S[i] = inc->S_target[i] * c->stress_mask[i];
+  const double sref = sigma_ref(c);
+  int newton_total = 0, cg_total = 0, helm_total = 0, k = 0;
+  double err = INFINITY;
+  bool converged = false;
+  double macro[6] = {0, 0, 0, 0, 0, 0};
+  for (k = 0; k < inc->max_stag; ++k) {
+    FGD_CUDA(c, cudaMemcpyAsync(c->w_eps_prev, c->w_eps, 6 * n * 8, cudaMemcpyDeviceToDevice, c->stream));
+    bool newton_ok = false;
+    for (int r = 0; r <= inc->max_newton; ++r) {
+      TRY(fgd_constitutive(c, nullptr, nullptr, macro));
+      double rms;
+      TRY(fgd_mech_residual(c, S, nullptr, &rms));
+      const double nm = std::sqrt(macro[0] * macro[0] + macro[1] * macro[1] + macro[2] * macro[2] + macro[3] * macro[3] +
+                                  macro[4] * macro[4] + macro[5] * macro[5]);
+      if (rms < inc->tol_newton * std::max(nm, 1e-6 * sref)) {
+        newton_ok = true;
+        break;
+      }
+      if (r == inc->max_newton) break;
+      int it = 0;
+      fgd_status s = cg_mech(c, c->w_b, c->w_de, inc->tol_cg, inc->max_cg, &it, nullptr);
+      cg_total += it;
+      if (s != FGD_OK && s != FGD_ENOCONV) return s;
+      ++newton_total;
+      TRY(launch_axpy(c, 6 * n, c->w_eps, c->w_de, 1.0));
+    }
+    if (!newton_ok) break;
+    // Helmholtz solves with the converged sources (A-28)
+    for (int j = 0; j < J; ++j) {
+      int it = 0;
+      fgd_status s = pcg_helmholtz(c, j, c->w_alpha + (size_t)j * n, nullptr, inc->tol_helm, inc->max_helm, &it,
+                                   nullptr);
+      helm_total += it;
+      if (s != FGD_OK) return s == FGD_ENOCONV ? set_err(c, FGD_ENOCONV, "Helmholtz PCG failed in increment") : s;
+      // the new non-local field is in hb[0]; w_D holds abar^(k+1) until ERR is known
+      FGD_CUDA(c, cudaMemcpyAsync(c->w_D + (size_t)j * n, c->hb[0], n * 8, cudaMemcpyDeviceToDevice, c->stream));
+    }
+    // ERR (A-02)
+    FGD_CUDA(c, cudaMemsetAsync(&c->sc->maxbits, 0, 8, c->stream));
+    TRY(launch_err(c, c->w_eps, c->w_eps_prev, c->w_D, c->w_abar, &c->sc->maxbits));
+    double red[14];
+    unsigned long long mb;
+    TRY(sync_read(c, &c->sc->red[16], 8 * 14, red));
+    TRY(sync_read(c, &c->sc->maxbits, 8, &mb));
+    double mx;
+    std::memcpy(&mx, &mb, 8);
+    double den = 0.0;
+    for (int i = 0; i < 6; ++i) den += (red[i] / n) * (red[i] / n);
+    den = std::sqrt(den);
+    err = den > 1e-12 ? mx / den : mx;
+    for (int j = 0; j < J; ++j) {
+      const double dn = std::sqrt(red[7 + 2 * j]), nm = std::sqrt(red[6 + 2 * j]);
+      err = std::max(err, dn > 1e-12 ? nm / dn : nm);
+    }
+    if (J > 0) FGD_CUDA(c, cudaMemcpyAsync(c->w_abar, c->w_D, (size_t)J * n * 8, cudaMemcpyDeviceToDevice, c->stream));
+    if (err < inc->tol_stag) {
+      converged = true;
+      break;
+    }
+  }
+  if (rep) {
+    for (int i = 0; i < 6; ++i) rep->macro_stress[i] = macro[i];
+    rep->err = err;
+    rep->stag_it = k + (converged ? 1 : 0);
+    rep->newton_it = newton_total;
+    rep->cg_it = cg_total;
+    rep->helm_it = helm_total;
+  }
+  if (!converged) {
+    // rollback: committed state untouched; reset the iterate
+    FGD_CUDA(c, cudaMemcpyAsync(c->w_eps, c->st_eps, 6 * n * 8, cudaMemcpyDeviceToDevice, c->stream));
+    if (J > 0) FGD_CUDA(c, cudaMemcpyAsync(c->w_abar, c->st_abar, (size_t)J * n * 8, cudaMemcpyDeviceToDevice, c->stream));
+    FGD_CUDA(c, cudaStreamSynchronize(c->stream));
+    return set_err(c, FGD_ENOCONV, "increment did not converge");
+  }
+  // 3. commit (A-16): eps^p, eps_p recomputed at the converged strain; history max-updated
+  TRY(launch_commit(c, c->w_eps, c->cm_epsp, c->cm_ep, c->cm_hist));
+  std::swap(c->st_epsp, c->cm_epsp);
+  std::swap(c->st_ep, c->cm_ep);
+  std::swap(c->st_hist, c->cm_hist);
+  FGD_CUDA(c, cudaMemcpyAsync(c->st_eps, c->w_eps, 6 * n * 8, cudaMemcpyDeviceToDevice, c->stream));
+  if (J > 0) FGD_CUDA(c, cudaMemcpyAsync(c->st_abar, c->w_abar, (size_t)J * n * 8, cudaMemcpyDeviceToDevice, c->stream));
+  if (rep) {
+    FGD_CUDA(c, cudaMemsetAsync(&c->sc->maxbits, 0, 8, c->stream));
+    TRY(launch_err(c, c->st_eps, c->st_eps, c->st_abar, c->st_abar, &c->sc->maxbits));
+    double red[6];
+    TRY(sync_read(c, &c->sc->red[16], 48, red));
+    for (int i = 0; i < 6; ++i) rep->macro_strain[i] = red[i] / (double)n;
+  }
+  FGD_CUDA(c, cudaStreamSynchronize(c->stream));
+  return FGD_OK;
+}
+
+fgd_status fgd_get_field(fgd_ctx* c, int which, double* out) {
+  if (!c || !out) return set_err(c, FGD_EINVAL, "null argument");
+  TRY(ensure_state(c));
+  const size_t n = c->nvox;
+  const double* src = nullptr;
+  size_t cnt = n;
+  if (which == FGD_FIELD_STRESS) src = c->w_sig, cnt = 6 * n;
+  else if (which == FGD_FIELD_STRAIN) src = c->st_eps, cnt = 6 * n;
+  else if (which == FGD_FIELD_EPS_P) src = c->st_epsp, cnt = 6 * n;
+  else if (which == FGD_FIELD_EQPS) src = c->st_ep;
+  else if (which == FGD_FIELD_HIST) src = c->st_hist;
+  else if (which == FGD_FIELD_TANGENT) src = c->C, cnt = 21 * n;
+  else if (which == FGD_FIELD_ITERATE) src = c->w_eps, cnt = 6 * n;
+  else if (which >= FGD_FIELD_NONLOCAL && which < FGD_FIELD_NONLOCAL + c->nfields)
+    src = c->w_abar + (size_t)(which - FGD_FIELD_NONLOCAL) * n;
+  else if (which >= FGD_FIELD_SOURCE && which < FGD_FIELD_SOURCE + c->nfields)
+    src = c->w_alpha + (size_t)(which - FGD_FIELD_SOURCE) * n;
+  else return set_err(c, FGD_EINVAL, "unknown field");
+  Stage st(c);
+  double* d;
+  TRY(st.out(out, cnt, &d));
+  FGD_CUDA(c, cudaMemcpyAsync(d, src, cnt * 8, cudaMemcpyDeviceToDevice, c->stream));
+  return st.finish();
+}
+
+fgd_status fgd_set_field(fgd_ctx* c, int which, const double* in) {
+  if (!c || !in) return set_err(c, FGD_EINVAL, "null argument");
+  if (!c->nonlocal_set) return set_err(c, FGD_ESTATE, "fgd_set_nonlocal must precede fgd_set_field");
+  TRY(ensure_state(c));
+  const size_t n = c->nvox;
+  double* dst[2] = {nullptr, nullptr};
+  size_t cnt = n;
+  if (which == FGD_FIELD_STRAIN) dst[0] = c->st_eps, dst[1] = c->w_eps, cnt = 6 * n;
+  else if (which == FGD_FIELD_EPS_P) dst[0] = c->st_epsp, cnt = 6 * n;
+  else if (which == FGD_FIELD_EQPS) dst[0] = c->st_ep;
+  else if (which == FGD_FIELD_HIST) dst[0] = c->st_hist;
+  else if (which == FGD_FIELD_ITERATE) dst[0] = c->w_eps, cnt = 6 * n;
+  else if (which >= FGD_FIELD_NONLOCAL && which < FGD_FIELD_NONLOCAL + c->nfields)
+    dst[0] = c->st_abar + (size_t)(which - FGD_FIELD_NONLOCAL) * n, dst[1] = c->w_abar + (size_t)(which - FGD_FIELD_NONLOCAL) * n;
+  else return set_err(c, FGD_EINVAL, "unknown or read-only field");
+  Stage st(c);
+  const double* d;
+  TRY(st.in(in, cnt, &d));
+  for (double* t : dst)
+    if (t) FGD_CUDA(c, cudaMemcpyAsync(t, d, cnt * 8, cudaMemcpyDeviceToDevice, c->stream));
+  return st.finish();
+}
+
+fgd_status fgd_macro_stress(fgd_ctx* c, double out[6]) {
+  if (!c || !out) return set_err(c, FGD_EINVAL, "null argument");
+  for (int i = 0; i < 6; ++i) out[i] = c->last_macro[i];
+  return FGD_OK;
+}
+
+}  // extern "C"

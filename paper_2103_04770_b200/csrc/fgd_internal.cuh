@@ -1,0 +1,180 @@
+// Internal declarations of libfgd (not part of the public ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "../../include/fgd.h"
+#include "fft.cuh"
+
+namespace fgd {
+
+constexpr int kMaxPhases = 16;
+constexpr int kMaxFields = 4;
+constexpr int kMaxN = 512;
+constexpr int kRedSlots = 48;            // doubles per reduction record
+
+// Device-resident Krylov / reduction scalars.  Written by the "last CTA" of a reducing kernel.
+struct DevScalars {
+  double rr;        // mech: r.r        | helm: r.z
+  double pq;        // mech: p.C p      | helm: p.L p
+  double alpha;
+  double beta;
+  double bb;        // |b|^2 (stopping reference)
+  double rn2;       // helm: r.r after the update
+  double red[kRedSlots];   // generic reduction results
+  unsigned int counter[8];
+  unsigned long long maxbits;
+};
+
+enum RedOp : int {
+  RED_NONE = 0,
+  RED_STORE = 1,          // red[0..nv) = sums
+  RED_MECH_INIT = 2,      // rr = bb = s0, beta = 0
+  RED_MECH_PQ = 3,        // pq = s0, alpha = rr / pq
+  RED_MECH_RR = 4,        // beta = s0 / rr, rr = s0
+  RED_HELM_INIT = 5,      // rr(=r.z) = s0, beta = 0
+  RED_HELM_PQ = 6,        // pq = s0, alpha = rr / pq
+  RED_HELM_RN = 7,        // rn2 = s0
+  RED_HELM_RZ = 8,        // beta = s0 / rr, rr = s0
+  RED_BB = 9,             // bb = s0
+};
+
+struct Material {
+  int model;
+  double E, nu, sigma_y, H, eps_c, eps_r, d_max, kappa0, kappa_f;
+};
+
+struct ConstTables {
+  const double2* tw[11];   // tw[log2 N] : e^{-2 pi i m / N}, m in [0, N)
+};
+
+}  // namespace fgd
+
+struct fgd_ctx {
+  int dims = 3;
+  int n[3] = {1, 1, 1};        // Nx, Ny, Nz
+  double L[3] = {1, 1, 1};
+  double h[3] = {1, 1, 1};
+  int scheme = 1;
+  size_t nvox = 0;
+  int Hx = 1;
+  size_t nspec = 0;            // Hx * Ny * Nz complex per component
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  std::string err;
+  unsigned long long launches = 0;
+
+  // tables
+  double2* tw_all = nullptr;
+  fgd::ConstTables tabs{};
+
+  // geometry / materials
+  uint8_t* phase = nullptr;
+  int nphases = 0;
+  std::vector<long long> phase_count;
+  fgd::Material mat[fgd::kMaxPhases]{};
+  bool mat_set[fgd::kMaxPhases]{};
+  int nfields = 0;
+  double ell[fgd::kMaxFields][fgd::kMaxPhases]{};
+  int source_phase[fgd::kMaxFields]{};
+  bool nonlocal_set = false;
+  int stress_mask[6] = {0, 0, 0, 0, 0, 0};
+  bool control_set = false;
+
+  // device buffers (lazily allocated)
+  double* C = nullptr;         // 21 * nvox packed tangent
+  bool tangent_set = false;
+  double2* specA = nullptr;    // 6 * nspec
+  double2* specB = nullptr;    // 6 * nspec
+  double* cg_x = nullptr;      // 6 * nvox
+  double* cg_r = nullptr;
+  double* cg_p = nullptr;
+  double* hb[6] = {};          // helmholtz work vectors: x r z p0 p1 q
+  fgd::DevScalars* sc = nullptr;
+  double* partials = nullptr;  // per-CTA partial sums
+  size_t partials_cap = 0;
+  double* pinned = nullptr;    // host pinned scalars
+
+  // solver state (increment)
+  double* st_eps = nullptr;    // 6 * nvox committed strain
+  double* st_epsp = nullptr;   // 6 * nvox
+  double* st_ep = nullptr;     // nvox
+  double* st_hist = nullptr;   // nvox
+  double* st_abar = nullptr;   // J * nvox
+  double* w_eps = nullptr;     // 6 * nvox current iterate
+  double* w_eps_prev = nullptr;
+  double* w_sig = nullptr;     // 6 * nvox
+  double* w_alpha = nullptr;   // J * nvox
+  double* w_abar = nullptr;    // J * nvox
+  double* w_D = nullptr;       // nvox frozen damage
+  double* cm_epsp = nullptr;   // commit scratch (swapped with st_*)
+  double* cm_ep = nullptr;
+  double* cm_hist = nullptr;
+  double* w_b = nullptr;       // 6 * nvox Newton residual
+  double* w_de = nullptr;      // 6 * nvox Newton correction
+  bool have_sigma = false;
+  bool have_residual = false;
+  double last_macro[6] = {0, 0, 0, 0, 0, 0};
+};
+
+namespace fgd {
+
+// error helpers
+fgd_status set_err(fgd_ctx* c, fgd_status s, const std::string& m);
+#define FGD_CUDA(ctx, call)                                                                   \
+  do {                                                                                        \
+    cudaError_t e_ = (call);                                                                  \
+    if (e_ != cudaSuccess)                                                                    \
+      return ::fgd::set_err(ctx, FGD_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+// launchers (passes.cu)
+fgd_status launch_xfwd(fgd_ctx* c, int ncomp, int mode, const double* in0, const double* in1, double* out0,
+                       const double* Cp, int red_op, int red_slot);
+fgd_status launch_xfwd_io(fgd_ctx* c, int ncomp, int mode, const double* in0, const double* in1, double* out0,
+                          double* io1, const double* Cp, int red_op, int red_slot);
+fgd_status launch_yfwd(fgd_ctx* c, int ncomp);
+fgd_status launch_z(fgd_ctx* c, int ncomp, int mode, double scale, const double* dc_shift, double mean_ell2);
+fgd_status launch_yinv(fgd_ctx* c, int ncomp);
+fgd_status launch_xinv(fgd_ctx* c, int ncomp, int mode, double* out0, double* io1, double* io2,
+                       const double* in1, int red_op, int red_slot);
+fgd_status ensure_spectral(fgd_ctx* c);
+fgd_status ensure_partials(fgd_ctx* c, size_t nblocks);
+
+// helmholtz.cu
+fgd_status launch_stencil(fgd_ctx* c, int field, int mode, const double* a, const double* zin,
+                          const double* pold, double* pout, double* q, int red_op);
+double mean_ell2(const fgd_ctx* c, int field);
+
+// constitutive.cu
+fgd_status launch_constitutive(fgd_ctx* c, const double* eps);
+fgd_status launch_commit(fgd_ctx* c, const double* eps, double* epsp_out, double* ep_out, double* hist_out);
+fgd_status launch_err(fgd_ctx* c, const double* eps, const double* eps_prev, const double* abar_new,
+                      const double* abar_old, unsigned long long* maxbits);
+fgd_status launch_dot(fgd_ctx* c, size_t n, const double* a, const double* b, int op, int slot);
+fgd_status launch_axpy(fgd_ctx* c, size_t n, double* y, const double* x, double s);
+fgd_status launch_init_iterate(fgd_ctx* c, const double* eps_n, double* eps, const double* dE6_dev);
+fgd_status launch_phase_count(fgd_ctx* c, const uint8_t* ph, unsigned long long* cnt, int nph, int* bad);
+
+// x-pass modes
+enum XFwdMode : int {
+  XF_PLAIN = 0,        // tau_c = in0[c]
+  XF_TANGENT = 1,      // tau = C : in0
+  XF_TANGENT_CG = 2,   // p = r(in0) + beta p(out0); tau = C p; write p; reduce p.tau
+  XF_HELM_UPDATE = 3,  // x(out0) += alpha p(in0); r(io) -= alpha q(in1); tau = r ; reduce r.r
+  XF_PLAIN_RED = 4,    // tau_c = in0[c]; reduce sum_c tau_c (means)
+};
+enum ZMode : int { Z_PROJECT = 0, Z_PRECOND = 1 };
+enum XInvMode : int {
+  XI_STORE = 0,        // out0 = q
+  XI_MECH_CG = 1,      // x(io1) += alpha p(in3); r(io2) -= alpha q ; reduce r.r
+  XI_HELM_Z = 2,       // z(out0) = q ; reduce r(in3).q
+  XI_STORE_RR = 3,     // out0 = q ; reduce q.q
+};
+
+}  // namespace fgd
