@@ -1,0 +1,350 @@
+#!/usr/bin/env python
+"""Benchmark of the FFT-Galerkin / Helmholtz Krylov hot path (BASELINE.json metric:
+"FP64 FFT-Galerkin Krylov voxel*iter/s at 256^3/512^3; % of HBM roofline").
+
+One STEP = one staggered Krylov sweep over the whole hot path on
+the BASELINE config-1 recipe at the metric size (default 256^3; --n 512 for 512^3):
+  a1      constitutive update at the strain field (J2-Lemaitre matrix / elastic inclusion,
+          damage frozen from the non-local field) -> sigma, consistent tangent, source alpha
+  a3-a5   Newton residual b = -G*(sigma - Sigma_bar)  (5-pass FFT with the projection)
+  a2-a6   KCG mechanical CG iterations  (5 fused passes per iteration)
+  a7-a9   KH Helmholtz PCG iterations   (27-point stencil + 5-pass preconditioner)
+  a10     the device reductions inside the above
+value = N_vox * KCG / (step time)  [voxel*iter/s of the mechanical Krylov solver], all ranks.
+Inputs are generated on the device (seeded) and stay resident; every field (134 MB/comp at
+256^3) and the tangent (2.8 GB) exceed the 126 MB L2, so no explicit flush is needed.
+
+--impl reference: the CPU oracle (oracle/, NumPy/SciPy FP64) on a bounded 64^3 sample of the
+same recipe, same metric and unit.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "FP64 FFT-Galerkin Krylov voxel·iter/s at 256³/512³; % of HBM roofline"
+UNIT = "voxel*iter/s"
+CPU_SAMPLE_N = 64
+
+
+def args_():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--n", type=int, default=256)
+    p.add_argument("--kcg", type=int, default=10)
+    p.add_argument("--khelm", type=int, default=10)
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu", action="store_true")
+    return p.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def workload_name(n):
+    return (f"config-1 recipe at {n}^3: Bernoulli(0.2) phases (J2-Lemaitre matrix / elastic inclusion), "
+            f"strain ~N(0,1e-3), one non-local field l=(2,4) voxels, mask (1,1,0,1,1,1)")
+
+
+# ---------------------------------------------------------------------------------------------
+# reference arm / cpu baseline: the oracle
+# ---------------------------------------------------------------------------------------------
+def oracle_sweep(n, kcg, khelm):
+    import numpy as np
+
+    import synth
+    from oracle.helmholtz import ell2_field, solve_helmholtz
+    from oracle.increment import Cell, State, evaluate, frozen_damage
+    from oracle.mech import cg
+    from oracle.projection import apply_projection
+    from oracle.spectral import Grid
+
+    g = Grid((n, n, n), (float(n),) * 3)
+    ph = synth.config1_phases(n, 0)
+    cell = Cell(g, ph, [synth.MATRIX_J2, synth.INCLUSION_EL], synth.CONFIG1_ELL, [0], synth.CONFIG1_MASK)
+    st = State.zero(cell)
+    eps = synth.gaussian_field(6, g.shape, 1e-3, 2)
+    e2 = ell2_field(ph, synth.CONFIG1_ELL[0])
+
+    def step():
+        D = frozen_damage(cell, st, st.abar)
+        sig, C, alpha, _, _ = evaluate(cell, eps, st, D)
+        b = -apply_projection(g, sig, cell.stress_mask)
+        cg(g, C, b, cell.stress_mask, tol=0.0, maxit=kcg)
+        solve_helmholtz(g, alpha[0], e2, tol=0.0, maxit=khelm)
+
+    return step
+
+
+def cpu_baseline(kcg, khelm, reps=3):
+    step = oracle_sweep(CPU_SAMPLE_N, kcg, khelm)
+    step()
+    ts = []
+    for _ in range(reps):
+        t = time.perf_counter()
+        step()
+        ts.append(time.perf_counter() - t)
+    t = statistics.median(ts)
+    return {"value": CPU_SAMPLE_N ** 3 * kcg / t, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle",
+            "sample": f"one sweep of the same recipe at {CPU_SAMPLE_N}^3 ({kcg} CG + {khelm} PCG iterations), "
+                      f"median of {reps}, scipy.fft workers={os.cpu_count()}; {t:.2f} s per sweep"}
+
+
+def run_reference(a):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    step = oracle_sweep(CPU_SAMPLE_N, a.kcg, a.khelm)
+    for _ in range(a.warmup):
+        step()
+    t = time.perf_counter()
+    for _ in range(a.steps):
+        step()
+    dt = (time.perf_counter() - t) / a.steps
+    v = CPU_SAMPLE_N ** 3 * a.kcg / dt
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": a.gpus, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": workload_name(a.n), "sample_n": CPU_SAMPLE_N, "kcg": a.kcg, "khelm": a.khelm},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle",
+                             "sample": f"each step = one sweep at {CPU_SAMPLE_N}^3 of the same recipe"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------------------------
+# clocks sampler
+# ---------------------------------------------------------------------------------------------
+class Clocks:
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+
+    def __init__(self, dev):
+        self.dev = dev
+        self.p = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                       "-i", str(self.dev), "-lms", "200"], stdout=subprocess.PIPE,
+                                      stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.p = None
+
+    def _read(self):
+        for ln in self.p.stdout:
+            self.lines.append(ln.strip())
+
+    def stop(self):
+        if not self.p:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=2)
+        except Exception:
+            self.p.kill()
+        sm, mx, reasons = [], [], set()
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 6:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for name, v in zip(self.NAMES, f[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------------------------
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(path))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, STREAM-style copy)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def class_bytes(n, kcg, khelm):
+    """Algorithmic (compulsory) bytes per STEP for each kernel class of the fused 5-pass design
+    (K2 360 B/voxel, K3/K4/K3 96 B each, K5 288 B; 1-comp analogues; stencil 33 B;
+    constitutive 345 B).  S = spectral bytes of one component (16 B x Hx*Ny*Nz)."""
+    V = n ** 3
+    S = 16 * (n // 2 + 1) * n * n
+    b = {}
+    b["xfwd6"] = (48 * V + 6 * S) + kcg * (48 * 3 * V + 168 * V + 6 * S)        # residual + CG (p, C, spec)
+    b["yfwd6"] = b["yinv6"] = b["z6"] = (1 + kcg) * 2 * 6 * S
+    b["xinv6"] = (6 * S + 48 * V) + kcg * (6 * S + 144 * V + 96 * V)            # residual store + CG update
+    b["xfwd1"] = (8 * V + S) + khelm * (32 * V + 16 * V + S)                      # precond init + PCG x/r update
+    b["yfwd1"] = b["yinv1"] = b["z1"] = (1 + khelm) * 2 * S
+    b["xinv1"] = (1 + khelm) * (S + 16 * V)
+    b["stencil"] = khelm * 33 * V
+    b["constitutive"] = (48 + 48 + 8 + 8 + 8 + 1 + 48 + 168 + 8) * V
+    return b
+
+
+def run_ours(a):
+    import numpy as np
+    import torch
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import synth
+    from paper_2103_04770_b200 import Context, Material
+
+    n = a.n
+    V = n ** 3
+    dev = torch.device("cuda", local)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1234 + rank)
+    ph = torch.from_numpy(synth.config1_phases(n, 0)).to(dev)
+    eps = torch.randn((6, n, n, n), generator=gen, dtype=torch.float64, device=dev) * 1e-3
+    ctx = Context((n, n, n), (float(n),) * 3, device=local)
+    ctx.set_phases(ph, 2)
+    m0, m1 = synth.MATRIX_J2, synth.INCLUSION_EL
+    for q, m in enumerate((m0, m1)):
+        ctx.set_material(q, Material(m.model, m.E, m.nu, m.sigma_y, m.H, m.eps_c, m.eps_r, m.d_max, m.kappa0,
+                                     m.kappa_f))
+    ctx.set_nonlocal(synth.CONFIG1_ELL, [0])
+    ctx.set_control(synth.CONFIG1_MASK)
+    zero6 = np.zeros(6)
+
+    def step(e=eps):
+        m = ctx.constitutive(e)
+        rms = ctx.mech_residual(zero6)
+        _, rel = ctx.solve_tangent_cg(None, None, tol=0.0, maxit=a.kcg)
+        ctx.solve_helmholtz(0, None, None, tol=0.0, maxit=a.khelm)
+        return m, rms, rel
+
+    for _ in range(a.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    clocks = Clocks(local)
+    clocks.start()
+    time.sleep(0.3)
+    stream = torch.cuda.current_stream(dev)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ctx.set_timing(True)
+    l0 = ctx.launch_count
+    torch.cuda.synchronize()
+    ev0.record(stream)
+    for _ in range(a.steps):
+        step()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    launches = ctx.launch_count - l0
+    kt = ctx.kernel_times()
+    ctx.set_timing(False)
+    clk = clocks.stop()
+    ms = ev0.elapsed_time(ev1) / a.steps
+    if world > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    value = world * V * a.kcg / (ms * 1e-3)
+
+    # roofline of the dominant kernel class (its launches inside the timed region)
+    peak, peak_src = peaks()
+    cb = class_bytes(n, a.kcg, a.khelm)
+    per_class = {}
+    step_ms_sum = sum(v[0] for v in kt.values())
+    for k, (tms, cnt) in kt.items():
+        if cnt == 0:
+            continue
+        entry = {"ms_per_step": tms / a.steps, "launches_per_step": cnt / a.steps,
+                 "share": tms / step_ms_sum if step_ms_sum else None}
+        if k in cb:
+            entry["GBs"] = cb[k] * a.steps / (tms * 1e-3) / 1e9
+            entry["frac"] = entry["GBs"] / peak
+        per_class[k] = entry
+    dom = max((k for k in per_class if k in cb), key=lambda k: per_class[k]["ms_per_step"])
+    d = per_class[dom]
+    roof = {"bound": "hbm", "kernel": dom, "achieved": d["GBs"], "peak": peak, "unit": "GB/s", "frac": d["frac"],
+            "traffic": None, "peak_source": peak_src,
+            "algorithmic_bytes_per_launch": cb[dom] / d["launches_per_step"]}
+    # whole-step efficiency against the fused-design byte model
+    step_bytes = sum(cb.values())
+    step_eff = {"bytes_per_step": step_bytes, "GBs": step_bytes / (ms * 1e-3) / 1e9,
+                "frac": step_bytes / (ms * 1e-3) / 1e9 / peak}
+
+    e2e = None
+    if not a.no_e2e:
+        host = torch.empty((6, n, n, n), dtype=torch.float64, pin_memory=True)
+        host.copy_(eps.cpu())
+        step(host)
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        for _ in range(a.steps):
+            m, rms, rel = step(host)       # H2D of the strain inside fgd_constitutive; D2H of <sigma>, rms, relres
+        torch.cuda.synchronize()
+        te = (time.perf_counter() - t) / a.steps
+        if world > 1:
+            tt = torch.tensor([te], device=dev, dtype=torch.float64)
+            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+            te = float(tt.item())
+        e2e = {"value": world * V * a.kcg / te, "unit": UNIT, "h2d_bytes_per_step": 48 * V,
+               "d2h_bytes_per_step": 48 + 8 + 8 + 8, "ms_per_step": te * 1e3}
+
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu:
+        cpu = cpu_baseline(a.kcg, a.khelm)
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
+                "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": workload_name(n), "n": n, "kcg": a.kcg, "khelm": a.khelm,
+                           "parallelism": "single GPU" if world == 1 else f"{world} independent replicas (slab decomposition not built yet)",
+                           "l2": "no flush: every input field (>=134 MB) and the tangent (2.8 GB) exceed the 126 MB L2"},
+                "roofline": roof, "step_roofline": step_eff, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": launches, "clocks": clk, "kernels": per_class,
+                "rates": {"mech_cg_iter_per_s": 1e3 / ms * a.kcg}}
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    a = args_()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)
+
+
+if __name__ == "__main__":
+    main()

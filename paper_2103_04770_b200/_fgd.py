@@ -78,7 +78,11 @@ _SIGS = {
     "fgd_get_field": ([_P, _I, _P], _I),
     "fgd_set_field": ([_P, _I, _P], _I),
     "fgd_macro_stress": ([_P, _P], _I),
+    "fgd_set_timing": ([_P, _I], _I),
+    "fgd_kernel_times": ([_P, _P, _P, _I], _I),
 }
+KCLASS = ("xfwd6", "yfwd6", "z6", "yinv6", "xinv6", "xfwd1", "yfwd1", "z1", "yinv1", "xinv1", "stencil",
+          "constitutive", "other")
 EXPORTED = tuple(_SIGS)
 for _name, (_args, _res) in _SIGS.items():
     _f = getattr(lib, _name)

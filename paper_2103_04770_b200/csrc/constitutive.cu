@@ -286,6 +286,7 @@ fgd_status launch_constitutive(fgd_ctx* c, const double* eps) {
   KArgs a{c->nvox, eps, c->st_epsp, c->st_ep, c->st_hist, c->w_abar, c->phase, c->w_sig, c->C, c->w_alpha, c->sc,
           c->partials};
   c->launches++;
+  KTimer kt(c, KC_CONST);
   k_constitutive<<<nb, 256, 0, c->stream>>>(a, make_table(c));
   FGD_CHECK_LAUNCH(c, "k_constitutive");
   return FGD_OK;
@@ -296,6 +297,7 @@ fgd_status launch_commit(fgd_ctx* c, const double* eps, double* epsp_out, double
   KArgs a{c->nvox, eps, c->st_epsp, c->st_ep, c->st_hist, c->w_abar, c->phase, nullptr, nullptr, nullptr, c->sc,
           nullptr};
   c->launches++;
+  KTimer kt(c, KC_OTHER);
   k_commit<<<nb, 256, 0, c->stream>>>(a, make_table(c), epsp_out, ep_out, hist_out);
   FGD_CHECK_LAUNCH(c, "k_commit");
   return FGD_OK;
@@ -307,6 +309,7 @@ fgd_status launch_err(fgd_ctx* c, const double* eps, const double* eps_prev, con
   fgd_status s = ensure_partials(c, (size_t)nb * 14);
   if (s != FGD_OK) return s;
   c->launches++;
+  KTimer kt(c, KC_OTHER);
   k_err<<<nb, 256, 0, c->stream>>>(c->nvox, eps, eps_prev, c->nfields, abar_new, abar_old, maxbits, c->sc,
                                    c->partials);
   FGD_CHECK_LAUNCH(c, "k_err");
@@ -318,6 +321,7 @@ fgd_status launch_dot(fgd_ctx* c, size_t n, const double* a, const double* b, in
   fgd_status s = ensure_partials(c, nb);
   if (s != FGD_OK) return s;
   c->launches++;
+  KTimer kt(c, KC_OTHER);
   k_dot<<<nb, 256, 0, c->stream>>>(n, a, b, c->sc, c->partials, op, slot);
   FGD_CHECK_LAUNCH(c, "k_dot");
   return FGD_OK;
@@ -325,6 +329,7 @@ fgd_status launch_dot(fgd_ctx* c, size_t n, const double* a, const double* b, in
 
 fgd_status launch_axpy(fgd_ctx* c, size_t n, double* y, const double* x, double s) {
   c->launches++;
+  KTimer kt(c, KC_OTHER);
   k_axpy<<<ew_blocks(c, n), 256, 0, c->stream>>>(n, y, x, s);
   FGD_CHECK_LAUNCH(c, "k_axpy");
   return FGD_OK;
@@ -332,6 +337,7 @@ fgd_status launch_axpy(fgd_ctx* c, size_t n, double* y, const double* x, double 
 
 fgd_status launch_init_iterate(fgd_ctx* c, const double* eps_n, double* eps, const double* dE6_dev) {
   c->launches++;
+  KTimer kt(c, KC_OTHER);
   k_init_iterate<<<ew_blocks(c, 6 * c->nvox), 256, 0, c->stream>>>(c->nvox, eps_n, eps, dE6_dev);
   FGD_CHECK_LAUNCH(c, "k_init_iterate");
   return FGD_OK;
@@ -339,6 +345,7 @@ fgd_status launch_init_iterate(fgd_ctx* c, const double* eps_n, double* eps, con
 
 fgd_status launch_phase_count(fgd_ctx* c, const uint8_t* ph, unsigned long long* cnt, int nph, int* bad) {
   c->launches++;
+  KTimer kt(c, KC_OTHER);
   k_phase_count<<<ew_blocks(c, c->nvox), 256, 0, c->stream>>>(c->nvox, ph, cnt, nph, bad);
   FGD_CHECK_LAUNCH(c, "k_phase_count");
   return FGD_OK;

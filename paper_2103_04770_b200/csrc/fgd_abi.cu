@@ -16,6 +16,29 @@ fgd_status set_err(fgd_ctx* c, fgd_status s, const std::string& m) {
   return s;
 }
 
+static int next_event(fgd_ctx* c) {
+  if (c->ev_used == c->ev_pool.size()) {
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return -1;
+    c->ev_pool.push_back(e);
+  }
+  return (int)c->ev_used++;
+}
+
+KTimer::KTimer(fgd_ctx* cc, int k) : c(cc), cls(k) {
+  if (!c->timing) return;
+  e0 = next_event(c);
+  if (e0 >= 0) cudaEventRecord(c->ev_pool[e0], c->stream);
+}
+
+KTimer::~KTimer() {
+  if (e0 < 0) return;
+  const int e1 = next_event(c);
+  if (e1 < 0) return;
+  cudaEventRecord(c->ev_pool[e1], c->stream);
+  c->ev_rec.push_back({cls, {e0, e1}});
+}
+
 static bool is_pow2(int v) { return v > 0 && (v & (v - 1)) == 0; }
 
 template <typename T>
@@ -419,6 +442,7 @@ void fgd_destroy(fgd_ctx* c) {
   for (int i = 0; i < 6; ++i)
     if (c->hb[i]) cudaFree(c->hb[i]);
   if (c->pinned) cudaFreeHost(c->pinned);
+  for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -833,6 +857,43 @@ fgd_status fgd_set_field(fgd_ctx* c, int which, const double* in) {
   for (double* t : dst)
     if (t) FGD_CUDA(c, cudaMemcpyAsync(t, d, cnt * 8, cudaMemcpyDeviceToDevice, c->stream));
   return st.finish();
+}
+
+static fgd_status flush_timing(fgd_ctx* c) {
+  if (c->ev_rec.empty()) return FGD_OK;
+  FGD_CUDA(c, cudaStreamSynchronize(c->stream));
+  for (auto& r : c->ev_rec) {
+    float ms = 0.f;
+    FGD_CUDA(c, cudaEventElapsedTime(&ms, c->ev_pool[r.second.first], c->ev_pool[r.second.second]));
+    c->kt_ms[r.first] += ms;
+    c->kt_cnt[r.first] += 1;
+  }
+  c->ev_rec.clear();
+  c->ev_used = 0;
+  return FGD_OK;
+}
+
+fgd_status fgd_set_timing(fgd_ctx* c, int enable) {
+  if (!c) return FGD_EINVAL;
+  if (enable) {
+    TRY(flush_timing(c));
+    for (int i = 0; i < FGD_NUM_KCLASS; ++i) {
+      c->kt_ms[i] = 0.0;
+      c->kt_cnt[i] = 0;
+    }
+  }
+  c->timing = enable != 0;
+  return FGD_OK;
+}
+
+fgd_status fgd_kernel_times(fgd_ctx* c, double* ms, unsigned long long* count, int n) {
+  if (!c) return FGD_EINVAL;
+  TRY(flush_timing(c));
+  for (int i = 0; i < n && i < FGD_NUM_KCLASS; ++i) {
+    if (ms) ms[i] = c->kt_ms[i];
+    if (count) count[i] = c->kt_cnt[i];
+  }
+  return FGD_OK;
 }
 
 fgd_status fgd_macro_stress(fgd_ctx* c, double out[6]) {

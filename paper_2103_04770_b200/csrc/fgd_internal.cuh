@@ -120,6 +120,14 @@ struct fgd_ctx {
   bool have_sigma = false;
   bool have_residual = false;
   double last_macro[6] = {0, 0, 0, 0, 0, 0};
+
+  // per-kernel-class event timing
+  bool timing = false;
+  std::vector<cudaEvent_t> ev_pool;
+  std::vector<std::pair<int, std::pair<int, int>>> ev_rec;   // class, (start, end) event indices
+  size_t ev_used = 0;
+  double kt_ms[FGD_NUM_KCLASS] = {};
+  unsigned long long kt_cnt[FGD_NUM_KCLASS] = {};
 };
 
 namespace fgd {
@@ -132,6 +140,16 @@ fgd_status set_err(fgd_ctx* c, fgd_status s, const std::string& m);
     if (e_ != cudaSuccess)                                                                    \
       return ::fgd::set_err(ctx, FGD_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
   } while (0)
+
+// scoped event timer around one kernel launch (no-op unless ctx->timing)
+enum KClass : int { KC_XFWD6 = 0, KC_YFWD6, KC_Z6, KC_YINV6, KC_XINV6, KC_XFWD1, KC_YFWD1, KC_Z1, KC_YINV1, KC_XINV1,
+                    KC_STENCIL, KC_CONST, KC_OTHER };
+struct KTimer {
+  fgd_ctx* c;
+  int cls, e0 = -1;
+  KTimer(fgd_ctx* cc, int k);
+  ~KTimer();
+};
 
 // launchers (passes.cu)
 fgd_status launch_xfwd(fgd_ctx* c, int ncomp, int mode, const double* in0, const double* in1, double* out0,

@@ -124,6 +124,7 @@ fgd_status launch_stencil(fgd_ctx* c, int field, int mode, const double* a, cons
     attr_set = true;
   }
   c->launches++;
+  KTimer kt(c, KC_STENCIL);
   if (mode == ST_APPLY)
     k_stencil<ST_APPLY><<<grid, 256, smem, c->stream>>>(s, a, nullptr, nullptr, q, c->phase, c->sc, c->partials, red_op);
   else

@@ -419,6 +419,7 @@ fgd_status launch_xfwd_io(fgd_ctx* c, int ncomp, int mode, const double* in0, co
     a.partials = c->partials;
   }
   const double2* tw = c->tabs.tw[ilog2(Nx)];
+  KTimer kt(c, ncomp == 6 ? KC_XFWD6 : KC_XFWD1);
 #define XF(NN)                                                                                   \
   if (ncomp == 6 && mode == XF_PLAIN) FGD_LAUNCH(c, (k_xfwd<NN, 6, XF_PLAIN>), grid, thr, smem, a, tw);            \
   else if (ncomp == 6 && mode == XF_TANGENT) FGD_LAUNCH(c, (k_xfwd<NN, 6, XF_TANGENT>), grid, thr, smem, a, tw);   \
@@ -446,6 +447,7 @@ fgd_status launch_xinv(fgd_ctx* c, int ncomp, int mode, double* out0, double* io
     a.partials = c->partials;
   }
   const double2* tw = c->tabs.tw[ilog2(Nx)];
+  KTimer kt(c, ncomp == 6 ? KC_XINV6 : KC_XINV1);
 #define XI(NN)                                                                                   \
   if (ncomp == 6 && mode == XI_STORE) FGD_LAUNCH(c, (k_xinv<NN, 6, XI_STORE>), grid, thr, smem, a, tw);            \
   else if (ncomp == 6 && mode == XI_STORE_RR) FGD_LAUNCH(c, (k_xinv<NN, 6, XI_STORE_RR>), grid, thr, smem, a, tw); \
@@ -474,6 +476,7 @@ static fgd_status launch_y(fgd_ctx* c, int ncomp, bool inv) {
   const size_t smem = (size_t)TZ * pad_len(Ny) * sizeof(double2);
   dim3 grid(Nz / TZ, c->Hx, ncomp);
   const double2* tw = c->tabs.tw[ilog2(Ny)];
+  KTimer kt(c, inv ? (ncomp == 6 ? KC_YINV6 : KC_YINV1) : (ncomp == 6 ? KC_YFWD6 : KC_YFWD1));
 #define YP(NN)                                                                                               \
   if (inv) FGD_LAUNCH(c, (k_ypass<NN, true>), grid, thr, smem, c->specA, c->specB, Nz, c->Hx, TZ, tw);     \
   else FGD_LAUNCH(c, (k_ypass<NN, false>), grid, thr, smem, c->specA, c->specB, Nz, c->Hx, TZ, tw);
@@ -514,6 +517,7 @@ fgd_status launch_z(fgd_ctx* c, int ncomp, int mode, double scale, const double*
   const double2* twx = c->tabs.tw[ilog2(c->n[0])];
   const double2* twy = c->tabs.tw[ilog2(Ny)];
   const double2* twz = c->tabs.tw[ilog2(Nz)];
+  KTimer kt(c, ncomp == 6 ? KC_Z6 : KC_Z1);
 #define ZP(NN)                                                                                             \
   if (ncomp == 6 && mode == Z_PROJECT) FGD_LAUNCH(c, (k_zpass<NN, 6, Z_PROJECT>), grid, thr, smem, c->specB, a, twx, twy, twz); \
   else if (ncomp == 1 && mode == Z_PRECOND) FGD_LAUNCH(c, (k_zpass<NN, 1, Z_PRECOND>), grid, thr, smem, c->specB, a, twx, twy, twz); \
