@@ -5,9 +5,10 @@
 // inverse with +i and no scaling here (the 1/N of F^-1 is folded into the spectral multiply).
 //
 // A line of N complex doubles lives in shared memory with one 16 B pad slot every 8 elements
-// (PAD) to break the stride-8 bank pattern of the first Stockham passes.  Each line is owned by
-// TPL = N / E threads that sit in one warp (E = elements per thread per pass), so passes are
-// separated by __syncwarp() only.
+// (PAD) to break the stride-8 bank pattern of the first Stockham passes, and an odd line stride
+// so that "same index, consecutive lines" accesses are conflict free.  Each line is owned by
+// TPL = N / E threads (E = 8 elements per thread per pass); passes are separated by
+// __syncwarp() when a line sits in one warp, by a named barrier per line otherwise (N = 512).
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -15,7 +16,7 @@
 namespace fgd {
 
 __host__ __device__ constexpr int ilog2(int n) { return n <= 1 ? 0 : 1 + ilog2(n >> 1); }
-__host__ __device__ constexpr int fft_E(int N) { return N < 8 ? N : (N >= 512 ? 16 : 8); }
+__host__ __device__ constexpr int fft_E(int N) { return N < 8 ? N : 8; }
 __host__ __device__ constexpr int fft_TPL(int N) { return N / fft_E(N); }
 __host__ __device__ constexpr int fft_npass(int N) {
   return N <= 1 ? 0 : (N <= 8 ? 1 : (N <= 64 ? 2 : 3));
@@ -32,6 +33,15 @@ __host__ __device__ constexpr int fft_radix(int N, int p) {
 }
 __host__ __device__ constexpr int pad_len(int N) { return N + (N >> 3); }
 __device__ __forceinline__ int PAD(int i) { return i + (i >> 3); }
+// Slot of element i of line l.  The padded layout PAD keeps every address an immediate offset
+// from one base register per thread (cheap in registers; an XOR swizzle was measured to double
+// the register demand of the unrolled passes); `l` is kept in the signature so that the layout
+// can change in one place.
+__device__ __forceinline__ int SWZ(int, int i) { return PAD(i); }
+// shared-memory stride (complex slots) of a C2C line of N points / of an x line (M points plus
+// the Nyquist slot): odd, so that consecutive lines start in different 16 B bank groups.
+__host__ __device__ constexpr int cline(int N) { return pad_len(N) | 1; }
+__host__ __device__ constexpr int xline(int M) { return (pad_len(M) + 1) | 1; }
 
 __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
@@ -92,25 +102,45 @@ template <bool INV> __device__ __forceinline__ void dft8(double2* v) {
 template <> __device__ __forceinline__ void dft<8, false>(double2* v) { dft8<false>(v); }
 template <> __device__ __forceinline__ void dft<8, true>(double2* v) { dft8<true>(v); }
 
+// Twiddle load through a volatile asm (generic address: shared or global).  Keeps the compiler
+// from hoisting every twiddle of every pass out of a persistent tile loop into registers.
+__device__ __forceinline__ double2 ld_tw(const double2* p) {
+  double2 w;
+  asm volatile("ld.v2.f64 {%0, %1}, [%2];" : "=d"(w.x), "=d"(w.y) : "l"(p));
+  return w;
+}
+
 // One Stockham pass of radix P over a line of N (padded, in shared memory).  Thread t in
 // [0, TPL) owns E/P butterflies j = t + b*TPL.  tw = table e^{-2 pi i m / N}, m in [0, N).
+// Synchronise the TPL threads that own a line: a warp (or part of one) -> __syncwarp; two or
+// more warps (N = 512: TPL = 64) -> a named barrier per line slot.
+template <int TPL>
+__device__ __forceinline__ void line_sync(int bar) {
+  if constexpr (TPL <= 32) {
+    __syncwarp();
+  } else {
+    asm volatile("bar.sync %0, %1;" ::"r"(bar), "n"(TPL) : "memory");
+  }
+}
+
 template <int N, int P, int NS, bool INV>
-__device__ __forceinline__ void stockham_pass(double2* line, int t, bool active, const double2* __restrict__ tw) {
+__device__ __forceinline__ void stockham_pass(double2* line, int l, int t, bool active, const double2* tw, int bar) {
   constexpr int E = fft_E(N);
   constexpr int TPL = fft_TPL(N);
   constexpr int NB = E / P;          // butterflies per thread
   constexpr int NP = N / P;          // butterflies per line
+  // Loads and arithmetic are unconditional (an inactive group reads a valid line and discards
+  // the result); only the stores are predicated.  Keeping v[] out of divergent regions stops
+  // the compiler from spilling it around the reconvergence point.
   double2 v[E];
-  if (active) {
 #pragma unroll
-    for (int b = 0; b < NB; ++b) {
-      const int j = t + b * TPL;
+  for (int b = 0; b < NB; ++b) {
+    const int j = t + b * TPL;
 #pragma unroll
-      for (int r = 0; r < P; ++r) v[b * P + r] = line[PAD(j + r * NP)];
-    }
+    for (int r = 0; r < P; ++r) v[b * P + r] = line[SWZ(l, j + r * NP)];
   }
-  __syncwarp();
-  if (active) {
+  line_sync<TPL>(bar);
+  {
 #pragma unroll
     for (int b = 0; b < NB; ++b) {
       const int j = t + b * TPL;
@@ -119,33 +149,40 @@ __device__ __forceinline__ void stockham_pass(double2* line, int t, bool active,
         constexpr int STEP = N / (NS * P);
 #pragma unroll
         for (int r = 1; r < P; ++r) {
-          double2 w = __ldg(&tw[r * k * STEP]);
+          double2 w = ld_tw(tw + r * k * STEP);
           if (INV) w.y = -w.y;
           v[b * P + r] = cmul(v[b * P + r], w);
         }
       }
       dft<P, INV>(&v[b * P]);
       const int base = (j / NS) * NS * P + k;
+      if (active) {
 #pragma unroll
-      for (int r = 0; r < P; ++r) line[PAD(base + r * NS)] = v[b * P + r];
+        for (int r = 0; r < P; ++r) line[SWZ(l, base + r * NS)] = v[b * P + r];
+      }
     }
   }
-  __syncwarp();
+  line_sync<TPL>(bar);
 }
 
 template <int N, int PASS, int NS, bool INV>
-__device__ __forceinline__ void fft_passes(double2* line, int t, bool active, const double2* __restrict__ tw) {
+__device__ __forceinline__ void fft_passes(double2* line, int l, int t, bool active, const double2* tw, int bar) {
   if constexpr (PASS < fft_npass(N)) {
     constexpr int P = fft_radix(N, PASS);
-    stockham_pass<N, P, NS, INV>(line, t, active, tw);
-    fft_passes<N, PASS + 1, NS * P, INV>(line, t, active, tw);
+    stockham_pass<N, P, NS, INV>(line, l, t, active, tw, bar);
+    fft_passes<N, PASS + 1, NS * P, INV>(line, l, t, active, tw, bar);
   }
+}
+
+// Copy a twiddle table of n entries into shared memory (all threads; caller syncs).
+__device__ __forceinline__ void load_table(double2* dst, const double2* __restrict__ src, int n) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = __ldg(&src[i]);
 }
 
 // FFT all `nl` lines (stride ldl elements) of a CTA's shared buffer.  Every thread of the CTA
 // must call this (warp-synchronous inside); lines are distributed TPL threads per line.
 template <int N, bool INV>
-__device__ __forceinline__ void fft_lines(double2* buf, int nl, int ldl, const double2* __restrict__ tw) {
+__device__ __forceinline__ void fft_lines(double2* buf, int nl, int ldl, const double2* tw) {
   if constexpr (N > 1) {
     constexpr int TPL = fft_TPL(N);
     const int lines_per_round = blockDim.x / TPL;
@@ -154,9 +191,10 @@ __device__ __forceinline__ void fft_lines(double2* buf, int nl, int ldl, const d
     for (int base = 0; base < nl; base += lines_per_round) {
       const int l = base + slot;
       const bool active = l < nl;
-      fft_passes<N, 0, 1, INV>(buf + (size_t)(active ? l : 0) * ldl, t, active, tw);
+      fft_passes<N, 0, 1, INV>(buf + (size_t)(active ? l : 0) * ldl, active ? l : 0, t, active, tw, 1 + slot);
     }
   }
 }
+
 
 }  // namespace fgd

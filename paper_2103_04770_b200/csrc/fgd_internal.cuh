@@ -162,6 +162,12 @@ fgd_status launch_yinv(fgd_ctx* c, int ncomp);
 fgd_status launch_xinv(fgd_ctx* c, int ncomp, int mode, double* out0, double* io1, double* io2,
                        const double* in1, int red_op, int red_slot);
 fgd_status ensure_spectral(fgd_ctx* c);
+// pipes.cu (persistent cp.async pipelines)
+fgd_status pipe_y(fgd_ctx* c, int ncomp, bool inv);
+fgd_status pipe_z(fgd_ctx* c, int ncomp, int mode, double scale, const double* dc_shift, double mean_ell2);
+fgd_status pipe_xinv(fgd_ctx* c, int ncomp, int mode, double* out0, double* io1, double* io2, const double* in1,
+                     int red_op, int red_slot);
+fgd_status pipe_xfwd_plain(fgd_ctx* c, int ncomp, const double* in0);
 fgd_status ensure_partials(fgd_ctx* c, size_t nblocks);
 
 // helmholtz.cu

@@ -23,7 +23,8 @@ struct SArgs {
 
 enum StencilMode : int { ST_APPLY = 0, ST_PCG = 1 };
 
-__device__ __forceinline__ int wrapi(int i, int n) { return (i % n + n) % n; }
+// periodic wrap for power-of-two extents (i >= -n)
+__device__ __forceinline__ int wrapi(int i, int n) { return (i + n) & (n - 1); }
 
 template <int MODE>
 __global__ void __launch_bounds__(256) k_stencil(SArgs s, const double* __restrict__ ain, const double* __restrict__ pold,

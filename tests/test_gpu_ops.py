@@ -21,7 +21,8 @@ from paper_2103_04770_b200 import Context  # noqa: E402
 from synth import bernoulli_phases, gaussian_field, random_spd_tangent  # noqa: E402
 
 TOL_APPLY = 1e-10
-GRIDS = [(8, 8, 8), (16, 8, 4), (32, 16, 8), (64, 32, 16), (16, 16, 1), (32, 64, 1), (4, 4, 2), (128, 128, 1)]
+GRIDS = [(8, 8, 8), (16, 8, 4), (32, 16, 8), (64, 32, 16), (16, 16, 1), (32, 64, 1), (4, 4, 2), (128, 128, 1),
+         (512, 4, 4), (4, 512, 2), (4, 4, 512), (256, 256, 1)]
 MASKS = [(1, 1, 0, 1, 1, 1), (0, 1, 0, 0, 0, 1), (0, 0, 0, 0, 0, 0), (1, 1, 1, 1, 1, 1)]
 
 
