@@ -102,11 +102,12 @@ template <bool INV> __device__ __forceinline__ void dft8(double2* v) {
 template <> __device__ __forceinline__ void dft<8, false>(double2* v) { dft8<false>(v); }
 template <> __device__ __forceinline__ void dft<8, true>(double2* v) { dft8<true>(v); }
 
-// Twiddle load through a volatile asm (generic address: shared or global).  Keeps the compiler
+// Twiddle load from the shared-memory table through a volatile asm.  Keeps the compiler
 // from hoisting every twiddle of every pass out of a persistent tile loop into registers.
 __device__ __forceinline__ double2 ld_tw(const double2* p) {
   double2 w;
-  asm volatile("ld.v2.f64 {%0, %1}, [%2];" : "=d"(w.x), "=d"(w.y) : "l"(p));
+  const unsigned s = (unsigned)__cvta_generic_to_shared(p);
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(w.x), "=d"(w.y) : "r"(s));
   return w;
 }
 

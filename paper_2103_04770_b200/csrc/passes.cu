@@ -120,9 +120,11 @@ __global__ void __launch_bounds__(kMaxThr, 2) k_xfwd(XArgs a, const double2* __r
 #pragma unroll
     for (int c = 0; c < NC; ++c) smd[(size_t)((c * TY + yy) * LP + SWZ(c * TY + yy, x >> 1)) * 2 + (x & 1)] = tau[c];
   }
-  __syncthreads();
   const int nl = NC * TY;
-  fft_lines<M, false>(sm, nl, LP, twM);
+  double2* tws = sm + (size_t)nl * LP;
+  load_table(tws, twM, M);
+  __syncthreads();
+  fft_lines<M, false>(sm, nl, LP, tws);
   __syncthreads();
   for (int idx = threadIdx.x; idx < nl * (M / 2 + 1); idx += blockDim.x) {
     const int k = idx % (M / 2 + 1), l = idx / (M / 2 + 1);
@@ -206,7 +208,7 @@ fgd_status launch_xfwd_io(fgd_ctx* c, int ncomp, int mode, const double* in0, co
   const int TY = choose_TY(Nx, ncomp, Ny);
   const int nl = ncomp * TY;
   const int thr = std::min(kMaxThr, std::max(64, round32(nl * fft_TPL(Nx / 2))));
-  const size_t smem = (size_t)nl * xline(Nx / 2) * sizeof(double2);
+  const size_t smem = ((size_t)nl * xline(Nx / 2) + Nx / 2) * sizeof(double2);
   dim3 grid(Ny / TY, Nz);
   XArgs a{Ny, Nz, TY, c->Hx, c->nvox, in0, in1, out0, io1, nullptr, Cp, c->specA, c->sc, c->partials, red_op, red_slot};
   if (red_op != RED_NONE) {

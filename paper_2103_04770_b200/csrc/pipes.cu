@@ -65,7 +65,7 @@ __device__ __forceinline__ void c2r_pre_p(double2* line, int l, int k, const dou
 struct YArgs {
   double2* A;
   double2* B;
-  int Nz, Hx, TZ, ncomp;
+  int Nz, Hx, TZ, ncomp, lgTZ;
   const double2* tw;
 };
 
@@ -82,7 +82,7 @@ __device__ __forceinline__ void y_issue(const YArgs& a, int t, double2* buf) {
     }
   } else {
     for (int idx = threadIdx.x; idx < TZ * N; idx += blockDim.x) {
-      const int zz = idx % TZ, ky = idx / TZ;
+      const int zz = idx & (TZ - 1), ky = idx >> a.lgTZ;
       cp_async16(&buf[zz * LP + SWZ(zz, ky)], &a.B[((size_t)(c * a.Hx + kx) * N + ky) * a.Nz + z0 + zz]);
     }
   }
@@ -113,7 +113,7 @@ __global__ void __launch_bounds__(256, 2) k_ypipe(YArgs a) {
     const int z0 = zt * TZ;
     if (!INV) {
       for (int idx = threadIdx.x; idx < TZ * N; idx += blockDim.x) {
-        const int zz = idx % TZ, ky = idx / TZ;
+        const int zz = idx & (TZ - 1), ky = idx >> a.lgTZ;
         a.B[((size_t)(c * a.Hx + kx) * N + ky) * a.Nz + z0 + zz] = buf[zz * LP + SWZ(zz, ky)];
       }
     } else {
@@ -132,7 +132,7 @@ __global__ void __launch_bounds__(256, 2) k_ypipe(YArgs a) {
 // ---------------------------------------------------------------------------------------------
 struct ZPArgs {
   double2* B;
-  int Nx, Ny, Hx, TL, scheme;
+  int Nx, Ny, Hx, TL, scheme, lgTL;
   double h[3], L[3];
   double scale;
   double shift[6];
@@ -224,13 +224,13 @@ __device__ __forceinline__ void z_issue(const ZPArgs& a, int t, double2* buf) {
   const int kx = t / nyt, ky0 = (t % nyt) * TL;
   for (int idx = threadIdx.x; idx < NC * TL * N; idx += blockDim.x) {
     const int kz = idx % N, rest = idx / N;
-    const int ll = rest % TL, c = rest / TL;
+    const int ll = rest & (TL - 1), c = rest >> a.lgTL;
     cp_async16(&buf[(c * TL + ll) * LP + SWZ(c * TL + ll, kz)], &a.B[((size_t)(c * a.Hx + kx) * a.Ny + ky0 + ll) * N + kz]);
   }
 }
 
 template <int N, int NC, int MODE>
-__global__ void __launch_bounds__(192, 2) k_zpipe(ZPArgs a) {
+__global__ void __launch_bounds__(192, 3) k_zpipe(ZPArgs a) {
   extern __shared__ double2 sm[];
   constexpr int LP = cline(N);
   const int TL = a.TL;
@@ -274,7 +274,7 @@ __global__ void __launch_bounds__(192, 2) k_zpipe(ZPArgs a) {
     __syncthreads();
     for (int idx = threadIdx.x; idx < NC * TL * N; idx += blockDim.x) {
       const int kz = idx % N, rest = idx / N;
-      const int ll = rest % TL, c = rest / TL;
+      const int ll = rest & (TL - 1), c = rest >> a.lgTL;
       a.B[((size_t)(c * a.Hx + kx) * a.Ny + ky0 + ll) * N + kz] = buf[(c * TL + ll) * LP + SWZ(c * TL + ll, kz)];
     }
     __syncthreads();
@@ -286,7 +286,7 @@ __global__ void __launch_bounds__(192, 2) k_zpipe(ZPArgs a) {
 // X passes, one component per tile
 // ---------------------------------------------------------------------------------------------
 struct XPArgs {
-  int Ny, Nz, TY, ncomp;
+  int Ny, Nz, TY, ncomp, lgTY;
   size_t nvox;
   double2* spec;
   const double* in0;   // XF: real input ; XI: p (MECH_CG) or r (HELM_Z)
@@ -308,13 +308,13 @@ __device__ __forceinline__ void xi_issue(const XPArgs& a, int t, double2* buf) {
   const int yt = t % nyt, r = t / nyt, z = r % a.Nz, c = r / a.Nz;
   const int y0 = yt * TY;
   for (int idx = threadIdx.x; idx < Hx * TY; idx += blockDim.x) {
-    const int yy = idx % TY, kx = idx / TY;
+    const int yy = idx & (TY - 1), kx = idx >> a.lgTY;
     cp_async16(&buf[yy * LP + SWZ(yy, kx)], &a.spec[((size_t)(c * a.Nz + z) * Hx + kx) * a.Ny + y0 + yy]);
   }
 }
 
 template <int N, int MODE>
-__global__ void __launch_bounds__(256, 2) k_xipipe(XPArgs a) {
+__global__ void __launch_bounds__(256, 3) k_xipipe(XPArgs a) {
   extern __shared__ double2 sm[];
   constexpr int M = N / 2;
   constexpr int LP = xline(M);
@@ -420,7 +420,7 @@ __global__ void __launch_bounds__(256, 2) k_xfpipe(XPArgs a) {
     const int yt = t % nyt, r = t / nyt, z = r % a.Nz, c = r / a.Nz;
     const int y0 = yt * TY;
     for (int idx = threadIdx.x; idx < Hx * TY; idx += blockDim.x) {
-      const int yy = idx % TY, kx = idx / TY;
+      const int yy = idx & (TY - 1), kx = idx >> a.lgTY;
       a.spec[((size_t)(c * a.Nz + z) * Hx + kx) * a.Ny + y0 + yy] = buf[yy * LP + SWZ(yy, kx)];
     }
     __syncthreads();
@@ -493,7 +493,7 @@ fgd_status pipe_y(fgd_ctx* c, int ncomp, bool inv) {
   const int thr = std::min(256, r32(TZ * TPL));
   const size_t smem = (2 * (size_t)TZ * cline(Ny) + Ny) * sizeof(double2);
   const int ntiles = ncomp * c->Hx * (Nz / TZ);
-  YArgs a{c->specA, c->specB, Nz, c->Hx, TZ, ncomp, c->tabs.tw[ilog2(Ny)]};
+  YArgs a{c->specA, c->specB, Nz, c->Hx, TZ, ncomp, ilog2(TZ), c->tabs.tw[ilog2(Ny)]};
   KTimer kt(c, inv ? (ncomp == 6 ? KC_YINV6 : KC_YINV1) : (ncomp == 6 ? KC_YFWD6 : KC_YFWD1));
 #define YPP(NN)                                                                  \
   if (inv) FGD_PLAUNCH(c, (k_ypipe<NN, true>), thr, smem, ntiles, a);            \
@@ -518,6 +518,7 @@ fgd_status pipe_z(fgd_ctx* c, int ncomp, int mode, double scale, const double* d
   a.Ny = Ny;
   a.Hx = c->Hx;
   a.TL = TL;
+  a.lgTL = ilog2(TL);
   a.scheme = c->scheme;
   for (int i = 0; i < 3; ++i) {
     a.h[i] = c->h[i];
@@ -556,7 +557,7 @@ fgd_status pipe_z(fgd_ctx* c, int ncomp, int mode, double scale, const double* d
 
 static int choose_TYp(int N, int Ny) {
   const int TPL = fft_TPL(N / 2);
-  int TY = p2floor(std::max(1, 256 / TPL));
+  int TY = p2floor(std::max(1, 128 / TPL));
   TY = std::min(TY, 32);
   return std::min(TY, Ny);
 }
@@ -568,7 +569,7 @@ fgd_status pipe_xinv(fgd_ctx* c, int ncomp, int mode, double* out0, double* io1,
   const int thr = std::min(256, r32(TY * fft_TPL(Nx / 2)));
   const size_t smem = (2 * (size_t)TY * xline(Nx / 2) + Nx / 2 + Nx) * sizeof(double2);
   const int ntiles = ncomp * Nz * (Ny / TY);
-  XPArgs a{Ny, Nz, TY, ncomp, c->nvox, c->specA, in1, out0, io1, io2, c->sc, nullptr, red_op, red_slot,
+  XPArgs a{Ny, Nz, TY, ncomp, ilog2(TY), c->nvox, c->specA, in1, out0, io1, io2, c->sc, nullptr, red_op, red_slot,
            c->tabs.tw[ilog2(Nx / 2)], c->tabs.tw[ilog2(Nx)]};
   if (mode != XI_STORE) {
     fgd_status s = ensure_partials(c, (size_t)num_sms() * 8);
@@ -593,7 +594,7 @@ fgd_status pipe_xfwd_plain(fgd_ctx* c, int ncomp, const double* in0) {
   const int thr = std::min(256, r32(TY * fft_TPL(Nx / 2)));
   const size_t smem = (2 * (size_t)TY * xline(Nx / 2) + Nx / 2 + Nx) * sizeof(double2);
   const int ntiles = ncomp * Nz * (Ny / TY);
-  XPArgs a{Ny, Nz, TY, ncomp, c->nvox, c->specA, in0, nullptr, nullptr, nullptr, c->sc, nullptr, RED_NONE, 0,
+  XPArgs a{Ny, Nz, TY, ncomp, ilog2(TY), c->nvox, c->specA, in0, nullptr, nullptr, nullptr, c->sc, nullptr, RED_NONE, 0,
            c->tabs.tw[ilog2(Nx / 2)], c->tabs.tw[ilog2(Nx)]};
   KTimer kt(c, ncomp == 6 ? KC_XFWD6 : KC_XFWD1);
 #define XFP(NN) FGD_PLAUNCH(c, (k_xfpipe<NN>), thr, smem, ntiles, a);
