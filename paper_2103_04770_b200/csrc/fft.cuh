@@ -138,7 +138,8 @@ __device__ __forceinline__ void stockham_pass(double2* line, int l, int t, bool 
   for (int b = 0; b < NB; ++b) {
     const int j = t + b * TPL;
 #pragma unroll
-    for (int r = 0; r < P; ++r) v[b * P + r] = line[SWZ(l, j + r * NP)];
+    for (int r = 0; r < P; ++r)
+      v[b * P + r] = (NP % 8 == 0) ? line[SWZ(l, j) + r * (NP / 8 * 9)] : line[SWZ(l, j + r * NP)];
   }
   line_sync<TPL>(bar);
   {
@@ -159,7 +160,13 @@ __device__ __forceinline__ void stockham_pass(double2* line, int l, int t, bool 
       const int base = (j / NS) * NS * P + k;
       if (active) {
 #pragma unroll
-        for (int r = 0; r < P; ++r) line[SWZ(l, base + r * NS)] = v[b * P + r];
+        for (int r = 0; r < P; ++r) {
+          // PAD(base + r NS) as one base register + immediate: NS % 8 == 0 -> 9 NS/8 per step;
+          // NS == 1 -> [base, base + P) never crosses a multiple of 8 (P | 8)
+          const int o = (NS % 8 == 0) ? SWZ(l, base) + r * (NS / 8 * 9)
+                      : (NS == 1) ? SWZ(l, base) + r : SWZ(l, base + r * NS);
+          line[o] = v[b * P + r];
+        }
       }
     }
   }
