@@ -31,6 +31,17 @@ __host__ __device__ constexpr int fft_radix(int N, int p) {
        : N == 256 ? (p < 2 ? 8 : 4)
        : 8;
 }
+__host__ __device__ constexpr int fft_ns(int N, int p) { return p == 0 ? 1 : fft_ns(N, p - 1) * fft_radix(N, p - 1); }
+// Per-pass twiddle tables: pass p with stride NS > 1 stores w^{r k}, r = 1..P-1, k = 0..NS-1, at
+// offset tw_off(N, p) + (r - 1) NS + k, so that the threads of a warp (consecutive k) read
+// consecutive 16 B words (no bank conflicts) -- w = e^{-2 pi i / (NS P)}.
+__host__ __device__ constexpr int tw_off(int N, int p) {
+  return p == 0 ? 0 : tw_off(N, p - 1) + (fft_ns(N, p - 1) > 1 ? (fft_radix(N, p - 1) - 1) * fft_ns(N, p - 1) : 0);
+}
+__host__ __device__ constexpr int tw_total(int N) { return N <= 1 ? 0 : tw_off(N, fft_npass(N)); }
+__host__ __device__ constexpr int pass_of_ns(int N, int NS, int p = 0) {
+  return fft_ns(N, p) == NS ? p : pass_of_ns(N, NS, p + 1);
+}
 __host__ __device__ constexpr int pad_len(int N) { return N + (N >> 3); }
 __device__ __forceinline__ int PAD(int i) { return i + (i >> 3); }
 // Slot of element i of line l.  The padded layout PAD keeps every address an immediate offset
@@ -148,10 +159,10 @@ __device__ __forceinline__ void stockham_pass(double2* line, int l, int t, bool 
       const int j = t + b * TPL;
       const int k = j % NS;
       if (NS > 1) {
-        constexpr int STEP = N / (NS * P);
+        constexpr int OFF = tw_off(N, ilog2(NS) == 0 ? 0 : pass_of_ns(N, NS));
 #pragma unroll
         for (int r = 1; r < P; ++r) {
-          double2 w = ld_tw(tw + r * k * STEP);
+          double2 w = ld_tw(tw + OFF + (r - 1) * NS + k);
           if (INV) w.y = -w.y;
           v[b * P + r] = cmul(v[b * P + r], w);
         }
@@ -182,9 +193,30 @@ __device__ __forceinline__ void fft_passes(double2* line, int l, int t, bool act
   }
 }
 
-// Copy a twiddle table of n entries into shared memory (all threads; caller syncs).
+// Copy a table of n entries into shared memory (all threads; caller syncs).
 __device__ __forceinline__ void load_table(double2* dst, const double2* __restrict__ src, int n) {
-  for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = __ldg(&src[i]);
+  const int nt = blockDim.x * blockDim.y * blockDim.z;
+  const int tid = threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z);
+  for (int i = tid; i < n; i += nt) dst[i] = __ldg(&src[i]);
+}
+
+// Build the per-pass twiddle tables of an N-point FFT (tw_total(N) entries) in shared memory from
+// the global table e^{-2 pi i m / N} (all threads; caller syncs).
+template <int N, int PASS = 0>
+__device__ __forceinline__ void build_pass_tables(double2* dst, const double2* __restrict__ twN) {
+  if constexpr (PASS < fft_npass(N)) {
+    constexpr int NS = fft_ns(N, PASS), P = fft_radix(N, PASS);
+    if constexpr (NS > 1) {
+      constexpr int STEP = N / (NS * P), OFF = tw_off(N, PASS);
+      const int nt = blockDim.x * blockDim.y * blockDim.z;
+      const int tid = threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z);
+      for (int i = tid; i < (P - 1) * NS; i += nt) {
+        const int r = 1 + i / NS, k = i % NS;
+        dst[OFF + i] = __ldg(&twN[r * k * STEP]);
+      }
+    }
+    build_pass_tables<N, PASS + 1>(dst, twN);
+  }
 }
 
 // FFT all `nl` lines (stride ldl elements) of a CTA's shared buffer.  Every thread of the CTA

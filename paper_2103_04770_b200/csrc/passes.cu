@@ -122,7 +122,7 @@ __global__ void __launch_bounds__(kMaxThr, 2) k_xfwd(XArgs a, const double2* __r
   }
   const int nl = NC * TY;
   double2* tws = sm + (size_t)nl * LP;
-  load_table(tws, twM, M);
+  build_pass_tables<M>(tws, twM);
   __syncthreads();
   fft_lines<M, false>(sm, nl, LP, tws);
   __syncthreads();

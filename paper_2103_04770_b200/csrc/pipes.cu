@@ -94,7 +94,7 @@ __global__ void __launch_bounds__(256, 2) k_ypipe(YArgs a) {
   constexpr int LP = cline(N);
   const int TZ = a.TZ;
   double2* tws = sm + 2 * TZ * LP;
-  load_table(tws, a.tw, N);
+  build_pass_tables<N>(tws, a.tw);
   const int ntiles = a.ncomp * a.Hx * (a.Nz / TZ);
   int t = blockIdx.x;
   if (t < ntiles) y_issue<N, INV>(a, t, sm);
@@ -234,8 +234,10 @@ __global__ void __launch_bounds__(192, 3) k_zpipe(ZPArgs a) {
   extern __shared__ double2 sm[];
   constexpr int LP = cline(N);
   const int TL = a.TL;
-  double2* tws = sm + 2 * NC * TL * LP;
+  double2* tws = sm + 2 * NC * TL * LP;    // e^{-2 pi i m/N} (symbol)
+  double2* tpz = tws + N;                    // per-pass FFT twiddles
   load_table(tws, a.twz, N);
+  build_pass_tables<N>(tpz, a.twz);
   const int nyt = a.Ny / TL;
   const int ntiles = a.Hx * nyt;
   int t = blockIdx.x;
@@ -249,7 +251,7 @@ __global__ void __launch_bounds__(192, 3) k_zpipe(ZPArgs a) {
     __syncthreads();
     double2* buf = sm + (i & 1) * NC * TL * LP;
     const int kx = t / nyt, ky0 = (t % nyt) * TL;
-    fft_lines<N, false>(buf, NC * TL, LP, tws);
+    fft_lines<N, false>(buf, NC * TL, LP, tpz);
     __syncthreads();
     for (int idx = threadIdx.x; idx < TL * N; idx += blockDim.x) {
       const int kz = idx % N, ll = idx / N;
@@ -270,7 +272,7 @@ __global__ void __launch_bounds__(192, 3) k_zpipe(ZPArgs a) {
       }
     }
     __syncthreads();
-    fft_lines<N, true>(buf, NC * TL, LP, tws);
+    fft_lines<N, true>(buf, NC * TL, LP, tpz);
     __syncthreads();
     for (int idx = threadIdx.x; idx < NC * TL * N; idx += blockDim.x) {
       const int kz = idx % N, rest = idx / N;
@@ -321,7 +323,7 @@ __global__ void __launch_bounds__(256, 3) k_xipipe(XPArgs a) {
   const int TY = a.TY, nyt = a.Ny / TY;
   double2* twM = sm + 2 * TY * LP;
   double2* twN = twM + M;
-  load_table(twM, a.twM, M);
+  build_pass_tables<M>(twM, a.twM);
   load_table(twN, a.twN, N);
   const int ntiles = a.ncomp * a.Nz * nyt;
   const size_t n = a.nvox;
@@ -397,7 +399,7 @@ __global__ void __launch_bounds__(256, 2) k_xfpipe(XPArgs a) {
   const int TY = a.TY, nyt = a.Ny / TY;
   double2* twM = sm + 2 * TY * LP;
   double2* twN = twM + M;
-  load_table(twM, a.twM, M);
+  build_pass_tables<M>(twM, a.twM);
   load_table(twN, a.twN, N);
   const int ntiles = a.ncomp * a.Nz * nyt;
   int t = blockIdx.x;
@@ -510,7 +512,7 @@ fgd_status pipe_z(fgd_ctx* c, int ncomp, int mode, double scale, const double* d
   if (Nz == 1) TL = 32;
   TL = std::min(TL, Ny);
   const int thr = std::min(192, std::max(r32(ncomp * TL * TPL), r32(std::min(TL * Nz, 192))));
-  const size_t smem = (2 * (size_t)ncomp * TL * cline(Nz) + Nz) * sizeof(double2);
+  const size_t smem = (2 * (size_t)ncomp * TL * cline(Nz) + 2 * Nz) * sizeof(double2);
   const int ntiles = c->Hx * (Ny / TL);
   ZPArgs a{};
   a.B = c->specB;

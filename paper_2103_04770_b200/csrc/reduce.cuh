@@ -5,10 +5,14 @@
 
 namespace fgd {
 
+__device__ __forceinline__ int lin_tid() { return threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z); }
+__device__ __forceinline__ int block_threads() { return blockDim.x * blockDim.y * blockDim.z; }
+
 template <int NV>
 __device__ __forceinline__ void block_sum(double (&v)[NV], double* sred) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int nw = (blockDim.x + 31) >> 5;
+  const int tid = lin_tid();
+  const int lane = tid & 31, warp = tid >> 5;
+  const int nw = (block_threads() + 31) >> 5;
 #pragma unroll
   for (int i = 0; i < NV; ++i) {
 #pragma unroll
@@ -20,7 +24,7 @@ __device__ __forceinline__ void block_sum(double (&v)[NV], double* sred) {
     for (int i = 0; i < NV; ++i) sred[warp * NV + i] = v[i];
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
+  if (tid == 0) {
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
       double s = 0.0;
@@ -73,8 +77,9 @@ __device__ __forceinline__ void reduce_finalize(double (&v)[NV], double* partial
   __shared__ int am_last;
   const unsigned nblk = gridDim.x * gridDim.y * gridDim.z;
   const unsigned bid = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+  const int tid = lin_tid();
   block_sum<NV>(v, sred);
-  if (threadIdx.x == 0) {
+  if (tid == 0) {
 #pragma unroll
     for (int i = 0; i < NV; ++i) partials[(size_t)bid * NV + i] = v[i];
     __threadfence();
@@ -87,12 +92,12 @@ __device__ __forceinline__ void reduce_finalize(double (&v)[NV], double* partial
     double t[NV];
 #pragma unroll
     for (int i = 0; i < NV; ++i) t[i] = 0.0;
-    for (unsigned b = threadIdx.x; b < nblk; b += blockDim.x) {
+    for (unsigned b = tid; b < nblk; b += block_threads()) {
 #pragma unroll
       for (int i = 0; i < NV; ++i) t[i] += __ldcg(&partials[(size_t)b * NV + i]);
     }
     block_sum<NV>(t, sred);
-    if (threadIdx.x == 0) {
+    if (tid == 0) {
       finalize(sc, op, slot, t, NV);
       sc->counter[0] = 0;
       __threadfence();
