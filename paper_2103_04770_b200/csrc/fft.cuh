@@ -16,32 +16,37 @@
 namespace fgd {
 
 __host__ __device__ constexpr int ilog2(int n) { return n <= 1 ? 0 : 1 + ilog2(n >> 1); }
-__host__ __device__ constexpr int fft_E(int N) { return N < 8 ? N : 8; }
-__host__ __device__ constexpr int fft_TPL(int N) { return N / fft_E(N); }
-__host__ __device__ constexpr int fft_npass(int N) {
-  return N <= 1 ? 0 : (N <= 8 ? 1 : (N <= 64 ? 2 : 3));
+// Two plan families: W = false (8 points per thread; radix-8/4 passes, more threads per line) and
+// W = true ("wide": 16 points per thread for N = 128/256 with radix-16 passes -- two shared-memory
+// exchanges instead of three, for the shared-memory-bound C2C passes).
+__host__ __device__ constexpr int fft_E(int N, bool W = false) { return N < 8 ? N : ((W && (N == 128 || N == 256)) ? 16 : 8); }
+__host__ __device__ constexpr int fft_TPL(int N, bool W = false) { return N / fft_E(N, W); }
+__host__ __device__ constexpr int fft_npass(int N, bool W = false) {
+  return N <= 1 ? 0 : (N <= 8 ? 1 : (N <= 64 ? 2 : ((W && N <= 256) ? 2 : 3)));
 }
-// radix of pass p: 2:{2} 4:{4} 8:{8} 16:{4,4} 32:{8,4} 64:{8,8} 128:{8,4,4} 256:{8,8,4} 512:{8,8,8}
-__host__ __device__ constexpr int fft_radix(int N, int p) {
+// W = false: 2:{2} 4:{4} 8:{8} 16:{4,4} 32:{8,4} 64:{8,8} 128:{8,4,4} 256:{8,8,4} 512:{8,8,8}
+// W = true : as above except 128:{8,16} 256:{16,16}
+__host__ __device__ constexpr int fft_radix(int N, int p, bool W = false) {
   return N <= 8 ? N
        : N == 16 ? 4
        : N == 32 ? (p == 0 ? 8 : 4)
        : N == 64 ? 8
-       : N == 128 ? (p == 0 ? 8 : 4)
-       : N == 256 ? (p < 2 ? 8 : 4)
+       : N == 128 ? (W ? (p == 0 ? 8 : 16) : (p == 0 ? 8 : 4))
+       : N == 256 ? (W ? 16 : (p < 2 ? 8 : 4))
        : 8;
 }
-__host__ __device__ constexpr int fft_ns(int N, int p) { return p == 0 ? 1 : fft_ns(N, p - 1) * fft_radix(N, p - 1); }
+__host__ __device__ constexpr int fft_ns(int N, int p, bool W = false) {
+  return p == 0 ? 1 : fft_ns(N, p - 1, W) * fft_radix(N, p - 1, W);
+}
 // Per-pass twiddle tables: pass p with stride NS > 1 stores w^{r k}, r = 1..P-1, k = 0..NS-1, at
 // offset tw_off(N, p) + (r - 1) NS + k, so that the threads of a warp (consecutive k) read
 // consecutive 16 B words (no bank conflicts) -- w = e^{-2 pi i / (NS P)}.
-__host__ __device__ constexpr int tw_off(int N, int p) {
-  return p == 0 ? 0 : tw_off(N, p - 1) + (fft_ns(N, p - 1) > 1 ? (fft_radix(N, p - 1) - 1) * fft_ns(N, p - 1) : 0);
+__host__ __device__ constexpr int tw_off(int N, int p, bool W = false) {
+  return p == 0 ? 0
+                : tw_off(N, p - 1, W) +
+                      (fft_ns(N, p - 1, W) > 1 ? (fft_radix(N, p - 1, W) - 1) * fft_ns(N, p - 1, W) : 0);
 }
-__host__ __device__ constexpr int tw_total(int N) { return N <= 1 ? 0 : tw_off(N, fft_npass(N)); }
-__host__ __device__ constexpr int pass_of_ns(int N, int NS, int p = 0) {
-  return fft_ns(N, p) == NS ? p : pass_of_ns(N, NS, p + 1);
-}
+__host__ __device__ constexpr int tw_total(int N, bool W = false) { return N <= 1 ? 0 : tw_off(N, fft_npass(N, W), W); }
 __host__ __device__ constexpr int pad_len(int N) { return N + (N >> 3); }
 __device__ __forceinline__ int PAD(int i) { return i + (i >> 3); }
 // Slot of element i of line l.  The padded layout PAD keeps every address an immediate offset
@@ -113,6 +118,47 @@ template <bool INV> __device__ __forceinline__ void dft8(double2* v) {
 template <> __device__ __forceinline__ void dft<8, false>(double2* v) { dft8<false>(v); }
 template <> __device__ __forceinline__ void dft<8, true>(double2* v) { dft8<true>(v); }
 
+// radix-16 as 4 x 4: n = 4 n1 + n2, k = k1 + 4 k2; DFT4 over n1, twiddle W16^{n2 k1}, DFT4 over n2
+template <bool INV> __device__ __forceinline__ double2 w16(double2 a, int e) {
+  constexpr double c1 = 0.92387953251128675613, s1 = 0.38268343236508977173, h = 0.70710678118654752440;
+  // a * W16^e, W16 = e^{-i pi/8} (forward) / e^{+i pi/8} (inverse); e in {1,2,3,4,6,9}
+  double2 w;
+  switch (e) {
+    case 1: w = make_double2(c1, -s1); break;
+    case 2: w = make_double2(h, -h); break;
+    case 3: w = make_double2(s1, -c1); break;
+    case 4: w = make_double2(0.0, -1.0); break;
+    case 6: w = make_double2(-h, -h); break;
+    default: w = make_double2(-c1, s1); break;   // 9
+  }
+  if (INV) w.y = -w.y;
+  return cmul(a, w);
+}
+template <bool INV> __device__ __forceinline__ void dft16(double2* v) {
+#pragma unroll
+  for (int n2 = 0; n2 < 4; ++n2) dft4<INV>(v[n2], v[4 + n2], v[8 + n2], v[12 + n2]);   // v[4 k1 + n2] = y[n2][k1]
+  v[5] = w16<INV>(v[5], 1);
+  v[6] = w16<INV>(v[6], 2);
+  v[7] = w16<INV>(v[7], 3);
+  v[9] = w16<INV>(v[9], 2);
+  v[10] = mul_mi<INV>(v[10]);
+  v[11] = w16<INV>(v[11], 6);
+  v[13] = w16<INV>(v[13], 3);
+  v[14] = w16<INV>(v[14], 6);
+  v[15] = w16<INV>(v[15], 9);
+#pragma unroll
+  for (int k1 = 0; k1 < 4; ++k1) dft4<INV>(v[4 * k1], v[4 * k1 + 1], v[4 * k1 + 2], v[4 * k1 + 3]);  // X[k1+4k2] at v[4k1+k2]
+  double2 t[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) t[i] = v[i];
+#pragma unroll
+  for (int k1 = 0; k1 < 4; ++k1)
+#pragma unroll
+    for (int k2 = 0; k2 < 4; ++k2) v[k1 + 4 * k2] = t[4 * k1 + k2];
+}
+template <> __device__ __forceinline__ void dft<16, false>(double2* v) { dft16<false>(v); }
+template <> __device__ __forceinline__ void dft<16, true>(double2* v) { dft16<true>(v); }
+
 // Twiddle load from the shared-memory table through a volatile asm.  Keeps the compiler
 // from hoisting every twiddle of every pass out of a persistent tile loop into registers.
 __device__ __forceinline__ double2 ld_tw(const double2* p) {
@@ -135,10 +181,10 @@ __device__ __forceinline__ void line_sync(int bar) {
   }
 }
 
-template <int N, int P, int NS, bool INV>
+template <int N, int P, int NS, bool INV, bool W, int PASS>
 __device__ __forceinline__ void stockham_pass(double2* line, int l, int t, bool active, const double2* tw, int bar) {
-  constexpr int E = fft_E(N);
-  constexpr int TPL = fft_TPL(N);
+  constexpr int E = fft_E(N, W);
+  constexpr int TPL = fft_TPL(N, W);
   constexpr int NB = E / P;          // butterflies per thread
   constexpr int NP = N / P;          // butterflies per line
   // Loads and arithmetic are unconditional (an inactive group reads a valid line and discards
@@ -159,7 +205,7 @@ __device__ __forceinline__ void stockham_pass(double2* line, int l, int t, bool 
       const int j = t + b * TPL;
       const int k = j % NS;
       if (NS > 1) {
-        constexpr int OFF = tw_off(N, ilog2(NS) == 0 ? 0 : pass_of_ns(N, NS));
+        constexpr int OFF = tw_off(N, PASS, W);
 #pragma unroll
         for (int r = 1; r < P; ++r) {
           double2 w = ld_tw(tw + OFF + (r - 1) * NS + k);
@@ -173,9 +219,10 @@ __device__ __forceinline__ void stockham_pass(double2* line, int l, int t, bool 
 #pragma unroll
         for (int r = 0; r < P; ++r) {
           // PAD(base + r NS) as one base register + immediate: NS % 8 == 0 -> 9 NS/8 per step;
-          // NS == 1 -> [base, base + P) never crosses a multiple of 8 (P | 8)
+          // NS == 1 -> base is a multiple of P, so PAD(base + r) = PAD(base) + r + r/8 for P >= 8
+          // and PAD(base) + r for P < 8 ([base, base + P) does not cross a multiple of 8)
           const int o = (NS % 8 == 0) ? SWZ(l, base) + r * (NS / 8 * 9)
-                      : (NS == 1) ? SWZ(l, base) + r : SWZ(l, base + r * NS);
+                      : (NS == 1) ? SWZ(l, base) + r + (r >> 3) : SWZ(l, base + r * NS);
           line[o] = v[b * P + r];
         }
       }
@@ -184,12 +231,12 @@ __device__ __forceinline__ void stockham_pass(double2* line, int l, int t, bool 
   line_sync<TPL>(bar);
 }
 
-template <int N, int PASS, int NS, bool INV>
+template <int N, int PASS, int NS, bool INV, bool W>
 __device__ __forceinline__ void fft_passes(double2* line, int l, int t, bool active, const double2* tw, int bar) {
-  if constexpr (PASS < fft_npass(N)) {
-    constexpr int P = fft_radix(N, PASS);
-    stockham_pass<N, P, NS, INV>(line, l, t, active, tw, bar);
-    fft_passes<N, PASS + 1, NS * P, INV>(line, l, t, active, tw, bar);
+  if constexpr (PASS < fft_npass(N, W)) {
+    constexpr int P = fft_radix(N, PASS, W);
+    stockham_pass<N, P, NS, INV, W, PASS>(line, l, t, active, tw, bar);
+    fft_passes<N, PASS + 1, NS * P, INV, W>(line, l, t, active, tw, bar);
   }
 }
 
@@ -202,12 +249,12 @@ __device__ __forceinline__ void load_table(double2* dst, const double2* __restri
 
 // Build the per-pass twiddle tables of an N-point FFT (tw_total(N) entries) in shared memory from
 // the global table e^{-2 pi i m / N} (all threads; caller syncs).
-template <int N, int PASS = 0>
+template <int N, bool W = false, int PASS = 0>
 __device__ __forceinline__ void build_pass_tables(double2* dst, const double2* __restrict__ twN) {
-  if constexpr (PASS < fft_npass(N)) {
-    constexpr int NS = fft_ns(N, PASS), P = fft_radix(N, PASS);
+  if constexpr (PASS < fft_npass(N, W)) {
+    constexpr int NS = fft_ns(N, PASS, W), P = fft_radix(N, PASS, W);
     if constexpr (NS > 1) {
-      constexpr int STEP = N / (NS * P), OFF = tw_off(N, PASS);
+      constexpr int STEP = N / (NS * P), OFF = tw_off(N, PASS, W);
       const int nt = blockDim.x * blockDim.y * blockDim.z;
       const int tid = threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z);
       for (int i = tid; i < (P - 1) * NS; i += nt) {
@@ -215,23 +262,23 @@ __device__ __forceinline__ void build_pass_tables(double2* dst, const double2* _
         dst[OFF + i] = __ldg(&twN[r * k * STEP]);
       }
     }
-    build_pass_tables<N, PASS + 1>(dst, twN);
+    build_pass_tables<N, W, PASS + 1>(dst, twN);
   }
 }
 
 // FFT all `nl` lines (stride ldl elements) of a CTA's shared buffer.  Every thread of the CTA
 // must call this (warp-synchronous inside); lines are distributed TPL threads per line.
-template <int N, bool INV>
+template <int N, bool INV, bool W = false>
 __device__ __forceinline__ void fft_lines(double2* buf, int nl, int ldl, const double2* tw) {
   if constexpr (N > 1) {
-    constexpr int TPL = fft_TPL(N);
+    constexpr int TPL = fft_TPL(N, W);
     const int lines_per_round = blockDim.x / TPL;
     const int slot = threadIdx.x / TPL;
     const int t = threadIdx.x % TPL;
     for (int base = 0; base < nl; base += lines_per_round) {
       const int l = base + slot;
       const bool active = l < nl;
-      fft_passes<N, 0, 1, INV>(buf + (size_t)(active ? l : 0) * ldl, active ? l : 0, t, active, tw, 1 + slot);
+      fft_passes<N, 0, 1, INV, W>(buf + (size_t)(active ? l : 0) * ldl, active ? l : 0, t, active, tw, 1 + slot);
     }
   }
 }

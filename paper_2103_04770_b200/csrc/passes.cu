@@ -74,7 +74,7 @@ __device__ __forceinline__ void r2c_post(double2* line, int l, int k, const doub
 }
 
 template <int N, int NC, int MODE>
-__global__ void __launch_bounds__(kMaxThr, 2) k_xfwd(XArgs a, const double2* __restrict__ twM,
+__global__ void __launch_bounds__(kMaxThr, 1) k_xfwd(XArgs a, const double2* __restrict__ twM,
                                                       const double2* __restrict__ twN) {
   extern __shared__ double2 sm[];
   constexpr int M = N / 2;

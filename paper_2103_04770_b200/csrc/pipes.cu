@@ -94,7 +94,7 @@ __global__ void __launch_bounds__(256, 2) k_ypipe(YArgs a) {
   constexpr int LP = cline(N);
   const int TZ = a.TZ;
   double2* tws = sm + 2 * TZ * LP;
-  build_pass_tables<N>(tws, a.tw);
+  build_pass_tables<N, true>(tws, a.tw);
   const int ntiles = a.ncomp * a.Hx * (a.Nz / TZ);
   int t = blockIdx.x;
   if (t < ntiles) y_issue<N, INV>(a, t, sm);
@@ -106,7 +106,7 @@ __global__ void __launch_bounds__(256, 2) k_ypipe(YArgs a) {
     cp_async_wait<1>();
     __syncthreads();
     double2* buf = sm + (i & 1) * TZ * LP;
-    fft_lines<N, INV>(buf, TZ, LP, tws);
+    fft_lines<N, INV, true>(buf, TZ, LP, tws);
     __syncthreads();
     const int nzt = a.Nz / TZ;
     const int zt = t % nzt, r = t / nzt, kx = r % a.Hx, c = r / a.Hx;
@@ -316,7 +316,7 @@ __device__ __forceinline__ void xi_issue(const XPArgs& a, int t, double2* buf) {
 }
 
 template <int N, int MODE>
-__global__ void __launch_bounds__(256, 3) k_xipipe(XPArgs a) {
+__global__ void __launch_bounds__(128, 4) k_xipipe(XPArgs a) {
   extern __shared__ double2 sm[];
   constexpr int M = N / 2;
   constexpr int LP = xline(M);
@@ -392,7 +392,7 @@ __device__ __forceinline__ void xf_issue(const XPArgs& a, int t, double2* buf) {
 }
 
 template <int N>
-__global__ void __launch_bounds__(256, 2) k_xfpipe(XPArgs a) {
+__global__ void __launch_bounds__(128, 4) k_xfpipe(XPArgs a) {
   extern __shared__ double2 sm[];
   constexpr int M = N / 2, Hx = M + 1;
   constexpr int LP = xline(M);
@@ -489,8 +489,8 @@ static fgd_status launch_persistent(fgd_ctx* c, K kernel, int threads, size_t sm
 
 fgd_status pipe_y(fgd_ctx* c, int ncomp, bool inv) {
   const int Ny = c->n[1], Nz = c->n[2];
-  const int TPL = fft_TPL(Ny);
-  int TZ = p2floor(std::max(1, 256 / TPL));
+  const int TPL = fft_TPL(Ny, true);
+  int TZ = p2floor(std::max(1, 128 / TPL));
   TZ = std::min(TZ, Nz);
   const int thr = std::min(256, r32(TZ * TPL));
   const size_t smem = (2 * (size_t)TZ * cline(Ny) + Ny) * sizeof(double2);
@@ -560,7 +560,7 @@ fgd_status pipe_z(fgd_ctx* c, int ncomp, int mode, double scale, const double* d
 static int choose_TYp(int N, int Ny) {
   const int TPL = fft_TPL(N / 2);
   int TY = p2floor(std::max(1, 128 / TPL));
-  TY = std::min(TY, 32);
+  TY = std::min(TY, 16);
   return std::min(TY, Ny);
 }
 
@@ -568,7 +568,7 @@ fgd_status pipe_xinv(fgd_ctx* c, int ncomp, int mode, double* out0, double* io1,
                      int red_op, int red_slot) {
   const int Nx = c->n[0], Ny = c->n[1], Nz = c->n[2];
   const int TY = choose_TYp(Nx, Ny);
-  const int thr = std::min(256, r32(TY * fft_TPL(Nx / 2)));
+  const int thr = std::min(128, r32(TY * fft_TPL(Nx / 2)));
   const size_t smem = (2 * (size_t)TY * xline(Nx / 2) + Nx / 2 + Nx) * sizeof(double2);
   const int ntiles = ncomp * Nz * (Ny / TY);
   XPArgs a{Ny, Nz, TY, ncomp, ilog2(TY), c->nvox, c->specA, in1, out0, io1, io2, c->sc, nullptr, red_op, red_slot,
@@ -593,7 +593,7 @@ fgd_status pipe_xinv(fgd_ctx* c, int ncomp, int mode, double* out0, double* io1,
 fgd_status pipe_xfwd_plain(fgd_ctx* c, int ncomp, const double* in0) {
   const int Nx = c->n[0], Ny = c->n[1], Nz = c->n[2];
   const int TY = choose_TYp(Nx, Ny);
-  const int thr = std::min(256, r32(TY * fft_TPL(Nx / 2)));
+  const int thr = std::min(128, r32(TY * fft_TPL(Nx / 2)));
   const size_t smem = (2 * (size_t)TY * xline(Nx / 2) + Nx / 2 + Nx) * sizeof(double2);
   const int ntiles = ncomp * Nz * (Ny / TY);
   XPArgs a{Ny, Nz, TY, ncomp, ilog2(TY), c->nvox, c->specA, in0, nullptr, nullptr, nullptr, c->sc, nullptr, RED_NONE, 0,
