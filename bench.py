@@ -193,6 +193,22 @@ def peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+TRAFFIC_KERNEL = {"xfwd6": "k_xfwd<{n}, 6, 2>", "xinv6": "k_xipipe<{n}, 1>", "z6": "k_zpipe<{n}, 6, 0>",
+                  "yfwd6": "k_ypipe<{n}, 0>", "yinv6": "k_ypipe<{n}, 1>", "stencil": "k_stencil<1>"}
+
+
+def measured_traffic(cls, n):
+    """DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum) of the class's main
+    kernel from the newest committed `ncu --set full` summary (profiles/r*_traffic.json), or None."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_traffic.json")))
+    if not files or cls not in TRAFFIC_KERNEL:
+        return None, None
+    d = json.load(open(files[-1]))
+    k = TRAFFIC_KERNEL[cls].format(n=n)
+    return d.get(k), os.path.basename(files[-1]) + ":" + k
+
+
 def class_bytes(n, kcg, khelm):
     """Algorithmic (compulsory) bytes per STEP for each kernel class of the fused 5-pass design
     (SURVEY 8(d): K2 360 B/voxel, K3/K4/K3 96 B each, K5 288 B; 1-comp analogues; stencil 33 B;
@@ -292,8 +308,9 @@ def run_ours(a):
         per_class[k] = entry
     dom = max((k for k in per_class if k in cb), key=lambda k: per_class[k]["ms_per_step"])
     d = per_class[dom]
+    traffic, traffic_src = measured_traffic(dom, n)
     roof = {"bound": "hbm", "kernel": dom, "achieved": d["GBs"], "peak": peak, "unit": "GB/s", "frac": d["frac"],
-            "traffic": None, "peak_source": peak_src,
+            "traffic": traffic, "traffic_source": traffic_src, "peak_source": peak_src,
             "algorithmic_bytes_per_launch": cb[dom] / d["launches_per_step"]}
     # whole-step efficiency against the fused-design byte model
     step_bytes = sum(cb.values())
