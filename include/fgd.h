@@ -54,7 +54,9 @@ typedef struct {
 } fgd_grid;
 
 /* Process placement.  This build supports nranks = 1 (one GPU); nranks > 1 returns FGD_EINVAL.
- * stream: a cudaStream_t (may be NULL = the library creates its own). */
+ * stream: the cudaStream_t all work is enqueued on; NULL = the legacy default stream (orders
+ * against the caller's work on any blocking stream).  With a non-default stream the caller
+ * must order its producers of input data against it. */
 typedef struct {
   int rank, nranks, device;
   const unsigned char* nccl_id; /* 128 bytes or NULL */

@@ -410,11 +410,8 @@ fgd_status fgd_create(const fgd_grid* g, const fgd_dist* d, fgd_ctx** out) {
     c->stream = (cudaStream_t)d->stream;
   }
   if (cudaSetDevice(c->device) != cudaSuccess) return fail(FGD_ECUDA, "cudaSetDevice failed");
-  if (!c->stream) {
-    if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess)
-      return fail(FGD_ECUDA, "cudaStreamCreate failed");
-    c->own_stream = true;
-  }
+  // stream == NULL is the legacy default stream (it orders against every other blocking stream,
+  // e.g. PyTorch's default stream, so inputs produced there are complete before our kernels run)
   {
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, c->device) == cudaSuccess) {

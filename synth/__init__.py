@@ -131,8 +131,13 @@ def random_spd_tangent_torch(nvox: int, seed: int, device="cuda", lo: float = 1.
     for s in range(0, nvox, chunk):
         m = min(chunk, nvox - s)
         G = torch.randn((m, 6, 6), generator=g, dtype=torch.float64, device=device)
-        Q, R = torch.linalg.qr(G)
-        Q = Q * torch.sign(torch.diagonal(R, dim1=1, dim2=2))[:, None, :]
+        # modified Gram-Schmidt on the columns = QR with a positive diagonal of R (Haar Q)
+        Q = torch.empty_like(G)
+        for i in range(6):
+            v = G[:, :, i].clone()
+            for j in range(i):
+                v -= (Q[:, :, j] * v).sum(dim=1, keepdim=True) * Q[:, :, j]
+            Q[:, :, i] = v / v.norm(dim=1, keepdim=True)
         lam = lo + (hi - lo) * torch.rand((m, 6), generator=g, dtype=torch.float64, device=device)
         C = torch.einsum("nik,nk,njk->nij", Q, lam, Q)
         out[:, s:s + m] = C[:, iu, ju].T

@@ -22,7 +22,7 @@ from synth import bernoulli_phases, gaussian_field, random_spd_tangent  # noqa: 
 
 TOL_APPLY = 1e-10
 GRIDS = [(8, 8, 8), (16, 8, 4), (32, 16, 8), (64, 32, 16), (16, 16, 1), (32, 64, 1), (4, 4, 2), (128, 128, 1),
-         (512, 4, 4), (4, 512, 2), (4, 4, 512), (256, 256, 1)]
+         (512, 4, 4), (4, 512, 2), (4, 4, 512), (256, 256, 1), (4, 4, 256), (8, 4, 128), (4, 8, 64), (16, 256, 4)]
 MASKS = [(1, 1, 0, 1, 1, 1), (0, 1, 0, 0, 0, 1), (0, 0, 0, 0, 0, 0), (1, 1, 1, 1, 1, 1)]
 
 
@@ -136,3 +136,62 @@ def test_errors_and_edge_cases():
     # constant field with all strain-controlled components: projection is exactly zero
     y = ctx.apply_projection(dev(np.ones((6,) + g.shape))).cpu().numpy()
     assert np.max(np.abs(y)) < 1e-15
+
+
+@pytest.mark.parametrize("n", [128, 256])
+def test_full_size_operators_256(n):
+    """The bench workload size (config-1 recipe at 256^3) in the launch configuration bench.py
+    times.  Projected tangent: at sampled frequencies xi the oracle evaluates, one by one,
+    F(y)(xi) = G^*(xi) F(C:x)(xi) (explicit separable DFT sums of the inputs and of the GPU
+    output); Helmholtz apply and preconditioner: every voxel against the oracle."""
+    import synth
+    from oracle.projection import project_spectrum
+    from oracle.spectral import cis
+    g = Grid((n, n, n), (float(n),) * 3)
+    ctx = Context((n, n, n), (float(n),) * 3)
+    mask = synth.CONFIG1_MASK
+    ctx.set_control(mask)
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(7)
+    Cd = synth.random_spd_tangent_torch(g.nvox, 1, device="cuda")
+    ctx.set_tangent(Cd)
+    x = torch.randn((6,) + g.shape, generator=gen, dtype=torch.float64, device="cuda") * 1e-3
+    y = ctx.apply_projected_tangent(x)
+    # tau = C : x on the device (test infrastructure), then DFT samples on the host
+    from oracle.mech import PACKED21
+    tau = torch.zeros_like(x)
+    for t, (i, j) in enumerate(PACKED21):
+        cij = Cd[t].reshape(g.shape)
+        tau[i] += cij * x[j]
+        if i != j:
+            tau[j] += cij * x[i]
+    ks = g.symbol(half=True)
+    rng = np.random.default_rng(3)
+    samples = [(0, 0, 0), (n // 2, 0, 0), (0, n // 2, n // 2), (1, 2, 3)] + \
+              [tuple(int(v) for v in rng.integers(0, (n // 2 + 1, n, n))) for _ in range(6)]
+    idx = torch.arange(n, device="cuda", dtype=torch.float64)
+    for (kx, ky, kz) in samples:
+        ex = torch.exp(-2j * np.pi * kx * idx / n)
+        ey = torch.exp(-2j * np.pi * ky * idx / n)
+        ez = torch.exp(-2j * np.pi * kz * idx / n)
+        ft = torch.einsum("czyx,x,y,z->c", tau.to(torch.complex128), ex, ey, ez).cpu().numpy()
+        fy = torch.einsum("czyx,x,y,z->c", y.to(torch.complex128), ex, ey, ez).cpu().numpy()
+        k = ks[:, kz, ky, kx]
+        # batch of two frequencies: a dummy DC slot (index 0) and the sample, unless it is DC
+        if (kx, ky, kz) == (0, 0, 0):
+            ref = np.asarray(mask) * ft
+        else:
+            ref = project_spectrum(np.stack([np.zeros(6), ft], 1), np.stack([np.zeros(3), k], 1), mask,
+                                   dc_index=(0,))[:, 1]
+        scale = max(np.linalg.norm(ft), 1e-300)
+        assert np.linalg.norm(fy - ref) <= 1e-10 * scale, (kx, ky, kz)
+    del tau, Cd
+    ph = synth.config1_phases(n, 0)
+    ctx.set_phases(dev(ph), 2)
+    ctx.set_nonlocal(synth.CONFIG1_ELL, [0])
+    e2 = ell2_field(ph, synth.CONFIG1_ELL[0])
+    a = x[0].cpu().numpy()
+    ya = ctx.apply_helmholtz(0, x[0].contiguous()).cpu().numpy()
+    assert rel(ya, apply_helmholtz(g, a, e2)) <= TOL_APPLY
+    za = ctx.apply_helmholtz_precond(0, x[0].contiguous()).cpu().numpy()
+    assert rel(za, apply_precond(g, a, e2)) <= TOL_APPLY
