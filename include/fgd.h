@@ -53,7 +53,11 @@ typedef struct {
   int scheme;
 } fgd_grid;
 
-/* Process placement.  This build supports nranks = 1 (one GPU); nranks > 1 returns FGD_EINVAL.
+/* Process placement: one process per GPU.  nranks > 1 slab-decomposes the cell along z
+ * (N3 and N2 divisible by nranks, powers of two): every field argument is then this rank's
+ * z-slab [comp][z0 .. z0+nz)[y][x] (fgd_local_extent), FFT transposes are NCCL block
+ * all-to-alls, reductions NCCL allreduces.  nccl_id: 128 bytes from
+ * fgd_nccl_id() on rank 0, broadcast to all ranks (ignored for nranks = 1).
  * stream: the cudaStream_t all work is enqueued on; NULL = the legacy default stream (orders
  * against the caller's work on any blocking stream).  With a non-default stream the caller
  * must order its producers of input data against it. */
@@ -64,6 +68,8 @@ typedef struct {
 } fgd_dist;
 
 fgd_status fgd_create(const fgd_grid* grid, const fgd_dist* dist, fgd_ctx** out);
+/* 128-byte NCCL unique id for fgd_dist.nccl_id (call on rank 0 only). */
+fgd_status fgd_nccl_id(unsigned char* out);
 void fgd_destroy(fgd_ctx* ctx);
 const char* fgd_last_error(const fgd_ctx* ctx);
 fgd_status fgd_local_extent(const fgd_ctx* ctx, int* z0, int* nz);

@@ -15,7 +15,7 @@ import numpy as np
 from . import _fgd
 from ._fgd import FgdError, ptr
 
-__all__ = ["Context", "FgdError", "Material"]
+__all__ = ["Context", "FgdError", "Material", "nccl_id"]
 
 
 class Material:
@@ -32,10 +32,22 @@ def _like(x, shape=None):
     return torch.empty(shape if shape is not None else x.shape, dtype=torch.float64, device=x.device)
 
 
-class Context:
-    """One libfgd context (one GPU, one stream).  n = (N1, N2, N3); N3 = 1 for 2D."""
+def nccl_id() -> bytes:
+    """128-byte NCCL unique id (rank 0); broadcast it to the other ranks and pass to Context."""
+    buf = (C.c_ubyte * 128)()
+    st = _fgd.fgd_nccl_id(C.cast(buf, C.c_void_p))
+    if st != 0:
+        raise FgdError(st, "fgd_nccl_id failed")
+    return bytes(buf)
 
-    def __init__(self, n, L=None, scheme: int = 1, device: int = 0, stream=None):
+
+class Context:
+    """One libfgd context (one GPU, one stream).  n = (N1, N2, N3); N3 = 1 for 2D.
+    Multi-GPU: rank/nranks/nccl_id (from nccl_id() on rank 0); fields are then the rank's
+    z-slab (see `local_extent`)."""
+
+    def __init__(self, n, L=None, scheme: int = 1, device: int = 0, stream=None, rank: int = 0, nranks: int = 1,
+                 nccl_id: bytes | None = None):
         n = tuple(int(v) for v in n)
         if len(n) == 2:
             n = (n[0], n[1], 1)
@@ -50,15 +62,20 @@ class Context:
                     stream = torch.cuda.current_stream(device).cuda_stream
             except ImportError:  # pragma: no cover
                 stream = None
-        d = _fgd.fgd_dist(0, 1, int(device), None, stream)
+        self._id = (C.c_ubyte * 128).from_buffer_copy(nccl_id) if nccl_id is not None else None
+        d = _fgd.fgd_dist(int(rank), int(nranks), int(device),
+                          C.cast(self._id, C.c_void_p) if self._id is not None else None, stream)
         h = C.c_void_p()
         st = _fgd.fgd_create(C.byref(g), C.byref(d), C.byref(h))
         if st != 0:
             raise FgdError(st, "fgd_create failed (see stderr)")
         self.h = h
         self.n = n
-        self.nvox = n[0] * n[1] * n[2]
-        self.shape = (n[2], n[1], n[0])
+        z0, nz = C.c_int(0), C.c_int(0)
+        _fgd.fgd_local_extent(h, C.byref(z0), C.byref(nz))
+        self.z0, self.nz = z0.value, nz.value
+        self.nvox = n[0] * n[1] * self.nz
+        self.shape = (self.nz, n[1], n[0])
 
     # ---- plumbing ---------------------------------------------------------------------------
     def _chk(self, st):

@@ -56,6 +56,10 @@ static fgd_status dalloc(fgd_ctx* c, T** p, size_t count) {
 fgd_status ensure_spectral(fgd_ctx* c) {
   fgd_status s = dalloc(c, &c->specA, 6 * c->nspec);
   if (s != FGD_OK) return s;
+  if (c->P > 1) {
+    s = dalloc(c, &c->specC, 6 * c->nspec);
+    if (s != FGD_OK) return s;
+  }
   return dalloc(c, &c->specB, 6 * c->nspec);
 }
 
@@ -181,7 +185,11 @@ static fgd_status build_tables(fgd_ctx* c) {
   return FGD_OK;
 }
 
-static double inv_nvox(const fgd_ctx* c) { return 1.0 / (double)c->nvox; }
+static double inv_nvox(const fgd_ctx* c) { return 1.0 / (double)c->nvox_g; }
+
+// a reducing launch: (op, slot) as the kernel must see them, then the distributed finalisation
+#define RED(op) red_op_for(c, op), red_slot_for(c, op, 0)
+#define RED_S(op, slot) red_op_for(c, op), red_slot_for(c, op, slot)
 
 // ---- composite operators (all enqueued on c->stream) -----------------------------------------
 // y = G*(C : x)
@@ -189,7 +197,9 @@ static fgd_status op_projected_tangent(fgd_ctx* c, const double* x, double* y) {
   TRY(ensure_spectral(c));
   TRY(launch_xfwd(c, 6, XF_TANGENT, x, nullptr, nullptr, c->C, RED_NONE, 0));
   TRY(launch_yfwd(c, 6));
+  TRY(exchange(c, 6, true));
   TRY(launch_z(c, 6, Z_PROJECT, inv_nvox(c), nullptr, 0.0));
+  TRY(exchange(c, 6, false));
   TRY(launch_yinv(c, 6));
   return launch_xinv(c, 6, XI_STORE, y, nullptr, nullptr, nullptr, RED_NONE, 0);
 }
@@ -200,13 +210,17 @@ static fgd_status op_projection(fgd_ctx* c, const double* tau, const double* S, 
   TRY(ensure_spectral(c));
   double shift[6] = {0, 0, 0, 0, 0, 0};
   if (S)
-    for (int i = 0; i < 6; ++i) shift[i] = S[i] * (double)c->nvox;
+    for (int i = 0; i < 6; ++i) shift[i] = S[i] * (double)c->nvox_g;
   TRY(launch_xfwd(c, 6, XF_PLAIN, tau, nullptr, nullptr, nullptr, RED_NONE, 0));
   TRY(launch_yfwd(c, 6));
+  TRY(exchange(c, 6, true));
   TRY(launch_z(c, 6, Z_PROJECT, scale * inv_nvox(c), shift, 0.0));
+  TRY(exchange(c, 6, false));
   TRY(launch_yinv(c, 6));
   if (red_op == RED_NONE) return launch_xinv(c, 6, XI_STORE, y, nullptr, nullptr, nullptr, RED_NONE, 0);
-  return launch_xinv(c, 6, XI_STORE_RR, y, nullptr, nullptr, nullptr, red_op, red_slot);
+  TRY(launch_xinv(c, 6, XI_STORE_RR, y, nullptr, nullptr, nullptr, red_op_for(c, red_op), red_slot_for(c, red_op, red_slot)));
+  if (red_op == RED_STORE) return allreduce_sum(c, &c->sc->red[red_slot], 1);
+  return post_reduce(c, red_op);
 }
 
 // z = F^-1 M F r ; if r_for_dot != null: reduce r.z with red_op
@@ -214,10 +228,13 @@ static fgd_status op_precond(fgd_ctx* c, int field, const double* r, double* z, 
   TRY(ensure_spectral(c));
   TRY(launch_xfwd(c, 1, XF_PLAIN, r, nullptr, nullptr, nullptr, RED_NONE, 0));
   TRY(launch_yfwd(c, 1));
+  TRY(exchange(c, 1, true));
   TRY(launch_z(c, 1, Z_PRECOND, inv_nvox(c), nullptr, mean_ell2(c, field)));
+  TRY(exchange(c, 1, false));
   TRY(launch_yinv(c, 1));
   if (red_op == RED_NONE) return launch_xinv(c, 1, XI_STORE, z, nullptr, nullptr, nullptr, RED_NONE, 0);
-  return launch_xinv(c, 1, XI_HELM_Z, z, nullptr, nullptr, r, red_op, 0);
+  TRY(launch_xinv(c, 1, XI_HELM_Z, z, nullptr, nullptr, r, RED(red_op)));
+  return post_reduce(c, red_op);
 }
 
 static fgd_status ensure_helm(fgd_ctx* c) {
@@ -274,7 +291,8 @@ static fgd_status pcg_helmholtz(fgd_ctx* c, int field, const double* b, double* 
   FGD_CUDA(c, cudaMemsetAsync(x, 0, n * 8, c->stream));
   FGD_CUDA(c, cudaMemsetAsync(P[0], 0, n * 8, c->stream));
   FGD_CUDA(c, cudaMemcpyAsync(r, b, n * 8, cudaMemcpyDeviceToDevice, c->stream));
-  TRY(launch_dot(c, n, r, r, RED_BB, 0));
+  TRY(launch_dot(c, n, r, r, RED(RED_BB)));
+  TRY(post_reduce(c, RED_BB));
   double bb = 0.0;
   TRY(sync_read(c, &c->sc->bb, 8, &bb));
   int it = 0;
@@ -285,8 +303,10 @@ static fgd_status pcg_helmholtz(fgd_ctx* c, int field, const double* b, double* 
     rel = 1.0;
     while (it < maxit) {
       TRY(launch_stencil(c, field, 1, nullptr, z, P[cur], P[cur ^ 1], q, RED_HELM_PQ));
+      TRY(post_reduce(c, RED_HELM_PQ));
       cur ^= 1;
-      TRY(launch_xfwd_io(c, 1, XF_HELM_UPDATE, P[cur], q, x, r, nullptr, RED_HELM_RN, 0));
+      TRY(launch_xfwd_io(c, 1, XF_HELM_UPDATE, P[cur], q, x, r, nullptr, RED(RED_HELM_RN)));
+      TRY(post_reduce(c, RED_HELM_RN));
       ++it;
       if (tol > 0.0) {
         double rn2;
@@ -295,9 +315,12 @@ static fgd_status pcg_helmholtz(fgd_ctx* c, int field, const double* b, double* 
         if (rel < tol) break;
       }
       TRY(launch_yfwd(c, 1));
+      TRY(exchange(c, 1, true));
       TRY(launch_z(c, 1, Z_PRECOND, inv_nvox(c), nullptr, mean_ell2(c, field)));
+      TRY(exchange(c, 1, false));
       TRY(launch_yinv(c, 1));
-      TRY(launch_xinv(c, 1, XI_HELM_Z, z, nullptr, nullptr, r, RED_HELM_RZ, 0));
+      TRY(launch_xinv(c, 1, XI_HELM_Z, z, nullptr, nullptr, r, RED(RED_HELM_RZ)));
+      TRY(post_reduce(c, RED_HELM_RZ));
     }
     if (tol <= 0.0) {
       double rn2;
@@ -321,7 +344,8 @@ static fgd_status cg_mech(fgd_ctx* c, const double* b, double* x_out, double tol
   FGD_CUDA(c, cudaMemsetAsync(c->cg_x, 0, n6 * 8, c->stream));
   FGD_CUDA(c, cudaMemsetAsync(c->cg_p, 0, n6 * 8, c->stream));
   FGD_CUDA(c, cudaMemcpyAsync(c->cg_r, b, n6 * 8, cudaMemcpyDeviceToDevice, c->stream));
-  TRY(launch_dot(c, n6, c->cg_r, c->cg_r, RED_MECH_INIT, 0));
+  TRY(launch_dot(c, n6, c->cg_r, c->cg_r, RED(RED_MECH_INIT)));
+  TRY(post_reduce(c, RED_MECH_INIT));
   double bb = 0.0;
   TRY(sync_read(c, &c->sc->bb, 8, &bb));
   int it = 0;
@@ -329,11 +353,15 @@ static fgd_status cg_mech(fgd_ctx* c, const double* b, double* x_out, double tol
   if (bb > 0.0) {
     rel = 1.0;
     while (it < maxit) {
-      TRY(launch_xfwd(c, 6, XF_TANGENT_CG, c->cg_r, nullptr, c->cg_p, c->C, RED_MECH_PQ, 0));
+      TRY(launch_xfwd(c, 6, XF_TANGENT_CG, c->cg_r, nullptr, c->cg_p, c->C, RED(RED_MECH_PQ)));
       TRY(launch_yfwd(c, 6));
+      TRY(exchange(c, 6, true));
       TRY(launch_z(c, 6, Z_PROJECT, inv_nvox(c), nullptr, 0.0));
+      TRY(exchange(c, 6, false));
+      TRY(post_reduce(c, RED_MECH_PQ));
       TRY(launch_yinv(c, 6));
-      TRY(launch_xinv(c, 6, XI_MECH_CG, nullptr, c->cg_x, c->cg_r, c->cg_p, RED_MECH_RR, 0));
+      TRY(launch_xinv(c, 6, XI_MECH_CG, nullptr, c->cg_x, c->cg_r, c->cg_p, RED(RED_MECH_RR)));
+      TRY(post_reduce(c, RED_MECH_RR));
       ++it;
       if (tol > 0.0) {
         double rr;
@@ -401,15 +429,16 @@ fgd_status fgd_create(const fgd_grid* g, const fgd_dist* d, fgd_ctx** out) {
   if (g->scheme != 0 && g->scheme != 1) return fail(FGD_EINVAL, "scheme must be 0 or 1");
   c->scheme = g->scheme;
   c->dims = g->dims;
-  c->nvox = (size_t)c->n[0] * c->n[1] * c->n[2];
   c->Hx = c->n[0] / 2 + 1;
-  c->nspec = (size_t)c->Hx * c->n[1] * c->n[2];
   if (d) {
-    if (d->nranks != 1 || d->rank != 0) return fail(FGD_EINVAL, "this build supports nranks = 1");
     c->device = d->device;
     c->stream = (cudaStream_t)d->stream;
   }
   if (cudaSetDevice(c->device) != cudaSuccess) return fail(FGD_ECUDA, "cudaSetDevice failed");
+  if (dist_init(c, d) != FGD_OK) return fail(FGD_EINVAL, c->err);
+  c->nvox_g = (size_t)c->n[0] * c->n[1] * c->n[2];
+  c->nvox = (size_t)c->n[0] * c->n[1] * c->nz_l;
+  c->nspec = (size_t)c->Hx * c->n[1] * c->nz_l;
   // stream == NULL is the legacy default stream (it orders against every other blocking stream,
   // e.g. PyTorch's default stream, so inputs produced there are complete before our kernels run)
   {
@@ -441,6 +470,10 @@ void fgd_destroy(fgd_ctx* c) {
   if (c->pinned) cudaFreeHost(c->pinned);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+  dist_destroy(c);
+  if (c->specC) cudaFree(c->specC);
+  if (c->halo) cudaFree(c->halo);
+  if (c->phase_halo) cudaFree(c->phase_halo);
   delete c;
 }
 
@@ -448,8 +481,8 @@ const char* fgd_last_error(const fgd_ctx* c) { return c ? c->err.c_str() : "null
 
 fgd_status fgd_local_extent(const fgd_ctx* c, int* z0, int* nz) {
   if (!c) return FGD_EINVAL;
-  if (z0) *z0 = 0;
-  if (nz) *nz = c->n[2];
+  if (z0) *z0 = c->z0;
+  if (nz) *nz = c->nz_l;
   return FGD_OK;
 }
 
@@ -476,6 +509,19 @@ fgd_status fgd_set_phases(fgd_ctx* c, const uint8_t* phase, int nphases) {
   if (*(int*)(h + kMaxPhases)) return set_err(c, FGD_EINVAL, "phase id >= nphases");
   c->nphases = nphases;
   c->phase_count.assign(h, h + nphases);
+  if (c->nranks > 1) {
+    // global phase counts (for <l^2>) and the one-plane phase halo of the Helmholtz stencil
+    for (int q = 0; q < nphases; ++q) c->pinned[256 + q] = (double)h[q];
+    FGD_CUDA(c, cudaMemcpyAsync(&c->sc->red[0], c->pinned + 256, 8 * nphases, cudaMemcpyHostToDevice, c->stream));
+    TRY(allreduce_sum(c, &c->sc->red[0], nphases));
+    double tot[kMaxPhases];
+    TRY(sync_read(c, &c->sc->red[0], 8 * nphases, tot));
+    for (int q = 0; q < nphases; ++q) c->phase_count[q] = (long long)(tot[q] + 0.5);
+    const size_t plane = (size_t)c->n[0] * c->n[1];
+    TRY(dalloc(c, &c->phase_halo, 2 * plane));
+    TRY(halo_exchange(c, c->phase, plane, c->phase_halo, c->phase_halo + plane));
+    FGD_CUDA(c, cudaStreamSynchronize(c->stream));
+  }
   return FGD_OK;
 }
 
@@ -646,6 +692,7 @@ fgd_status fgd_constitutive(fgd_ctx* c, const double* eps, double* sigma_out, do
       FGD_CUDA(c, cudaMemcpyAsync(c->w_eps, de, 6 * c->nvox * 8, cudaMemcpyDeviceToDevice, c->stream));
   }
   TRY(launch_constitutive(c, c->w_eps));
+  TRY(allreduce_sum(c, &c->sc->red[0], 6));
   c->tangent_set = true;
   c->have_sigma = true;
   if (sigma_out) {
@@ -655,7 +702,7 @@ fgd_status fgd_constitutive(fgd_ctx* c, const double* eps, double* sigma_out, do
   }
   double m[6];
   TRY(sync_read(c, c->sc->red, 48, m));
-  for (int i = 0; i < 6; ++i) c->last_macro[i] = m[i] / (double)c->nvox;
+  for (int i = 0; i < 6; ++i) c->last_macro[i] = m[i] / (double)c->nvox_g;
   if (macro)
     for (int i = 0; i < 6; ++i) macro[i] = c->last_macro[i];
   return st.finish();
@@ -671,7 +718,7 @@ fgd_status fgd_mech_residual(fgd_ctx* c, const double* S_target, double* b_out, 
   c->have_residual = true;
   double ss;
   TRY(sync_read(c, &c->sc->red[8], 8, &ss));
-  if (rms) *rms = std::sqrt(ss / (double)c->nvox);
+  if (rms) *rms = std::sqrt(ss / (double)c->nvox_g);
   if (b_out) {
     Stage st(c);
     double* db;
@@ -680,6 +727,15 @@ fgd_status fgd_mech_residual(fgd_ctx* c, const double* S_target, double* b_out, 
     return st.finish();
   }
   return FGD_OK;
+}
+
+// staggered-error ingredients over all ranks (sums of red[16..29], max of the strain change)
+static fgd_status err_reduce(fgd_ctx* c, const double* eps, const double* eps_prev, const double* anew,
+                             const double* aold) {
+  FGD_CUDA(c, cudaMemsetAsync(&c->sc->maxbits, 0, 8, c->stream));
+  TRY(launch_err(c, eps, eps_prev, anew, aold, &c->sc->maxbits));
+  TRY(allreduce_sum(c, &c->sc->red[16], 14));
+  return allreduce_max_u64(c, &c->sc->maxbits);
 }
 
 static double sigma_ref(const fgd_ctx* c) {
@@ -696,16 +752,17 @@ fgd_status fgd_solve_increment(fgd_ctx* c, const fgd_increment* inc, fgd_report*
   TRY(check_ready(c, true, true, true));
   TRY(ensure_state(c));
   const size_t n = c->nvox;
+  const double ng = (double)c->nvox_g;
   const int J = c->nfields;
   // 1. eps^(0) = eps_n + dE on strain-controlled comps; abar^(0) = abar_n  (A-22)
   double mean_n[6];
   {
     // <eps_n> : use the err kernel's sums with eps_prev = eps
     FGD_CUDA(c, cudaMemsetAsync(&c->sc->maxbits, 0, 8, c->stream));
-    TRY(launch_err(c, c->st_eps, c->st_eps, c->st_abar, c->st_abar, &c->sc->maxbits));
+    TRY(err_reduce(c, c->st_eps, c->st_eps, c->st_abar, c->st_abar));
     double red[6];
     TRY(sync_read(c, &c->sc->red[16], 48, red));
-    for (int i = 0; i < 6; ++i) mean_n[i] = red[i] / (double)n;
+    for (int i = 0; i < 6; ++i) mean_n[i] = red[i] / ng;
   }
   double dE[6];
   for (int i = 0; i < 6; ++i) dE[i] = c->stress_mask[i] ? 0.0 : inc->E_target[i] - mean_n[i];
@@ -754,7 +811,7 @@ fgd_status fgd_solve_increment(fgd_ctx* c, const fgd_increment* inc, fgd_report*
     }
     // ERR (A-02)
     FGD_CUDA(c, cudaMemsetAsync(&c->sc->maxbits, 0, 8, c->stream));
-    TRY(launch_err(c, c->w_eps, c->w_eps_prev, c->w_D, c->w_abar, &c->sc->maxbits));
+    TRY(err_reduce(c, c->w_eps, c->w_eps_prev, c->w_D, c->w_abar));
     double red[14];
     unsigned long long mb;
     TRY(sync_read(c, &c->sc->red[16], 8 * 14, red));
@@ -762,7 +819,7 @@ fgd_status fgd_solve_increment(fgd_ctx* c, const fgd_increment* inc, fgd_report*
     double mx;
     std::memcpy(&mx, &mb, 8);
     double den = 0.0;
-    for (int i = 0; i < 6; ++i) den += (red[i] / n) * (red[i] / n);
+    for (int i = 0; i < 6; ++i) den += (red[i] / ng) * (red[i] / ng);
     den = std::sqrt(den);
     err = den > 1e-12 ? mx / den : mx;
     for (int j = 0; j < J; ++j) {
@@ -799,10 +856,10 @@ fgd_status fgd_solve_increment(fgd_ctx* c, const fgd_increment* inc, fgd_report*
   if (J > 0) FGD_CUDA(c, cudaMemcpyAsync(c->st_abar, c->w_abar, (size_t)J * n * 8, cudaMemcpyDeviceToDevice, c->stream));
   if (rep) {
     FGD_CUDA(c, cudaMemsetAsync(&c->sc->maxbits, 0, 8, c->stream));
-    TRY(launch_err(c, c->st_eps, c->st_eps, c->st_abar, c->st_abar, &c->sc->maxbits));
+    TRY(err_reduce(c, c->st_eps, c->st_eps, c->st_abar, c->st_abar));
     double red[6];
     TRY(sync_read(c, &c->sc->red[16], 48, red));
-    for (int i = 0; i < 6; ++i) rep->macro_strain[i] = red[i] / (double)n;
+    for (int i = 0; i < 6; ++i) rep->macro_strain[i] = red[i] / ng;
   }
   FGD_CUDA(c, cudaStreamSynchronize(c->stream));
   return FGD_OK;

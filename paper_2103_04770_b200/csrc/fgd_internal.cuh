@@ -16,6 +16,7 @@ constexpr int kMaxPhases = 16;
 constexpr int kMaxFields = 4;
 constexpr int kMaxN = 512;
 constexpr int kRedSlots = 48;            // doubles per reduction record
+constexpr int kDistSlot = 47;            // local partial of a finalising reduction (nranks > 1)
 
 // Device-resident Krylov / reduction scalars.  Written by the "last CTA" of a reducing kernel.
 struct DevScalars {
@@ -60,7 +61,16 @@ struct fgd_ctx {
   double L[3] = {1, 1, 1};
   double h[3] = {1, 1, 1};
   int scheme = 1;
-  size_t nvox = 0;
+  size_t nvox = 0;             // LOCAL voxels (this rank's z-slab)
+  size_t nvox_g = 0;           // global voxels
+  int nz_l = 1;                // local z planes
+  int z0 = 0;                  // first global z plane of this rank
+  int rank = 0, nranks = 1;    // processes (one GPU each)
+  int P = 1;                   // slab count of the transposed-spectrum layout (nranks, or emulated)
+  void* comm = nullptr;        // ncclComm_t
+  double2* specC = nullptr;    // z-pass buffer when P > 1
+  double* halo = nullptr;      // stencil halo planes (nranks > 1): [field 0 lo, hi][field 1 lo, hi]
+  uint8_t* phase_halo = nullptr;
   int Hx = 1;
   size_t nspec = 0;            // Hx * Ny * Nz complex per component
   int device = 0;
@@ -169,6 +179,17 @@ fgd_status pipe_xinv(fgd_ctx* c, int ncomp, int mode, double* out0, double* io1,
                      int red_op, int red_slot);
 fgd_status pipe_xfwd_plain(fgd_ctx* c, int ncomp, const double* in0);
 fgd_status ensure_partials(fgd_ctx* c, size_t nblocks);
+
+// dist.cu
+fgd_status dist_init(fgd_ctx* c, const fgd_dist* d);
+void dist_destroy(fgd_ctx* c);
+fgd_status exchange(fgd_ctx* c, int ncomp, bool fwd);
+fgd_status allreduce_sum(fgd_ctx* c, double* dev, int count);
+fgd_status allreduce_max_u64(fgd_ctx* c, unsigned long long* dev);
+int red_op_for(const fgd_ctx* c, int op);
+int red_slot_for(const fgd_ctx* c, int op, int slot);
+fgd_status post_reduce(fgd_ctx* c, int op);
+fgd_status halo_exchange(fgd_ctx* c, const void* field, size_t plane_bytes, void* lo, void* hi);
 
 // helmholtz.cu
 fgd_status launch_stencil(fgd_ctx* c, int field, int mode, const double* a, const double* zin,

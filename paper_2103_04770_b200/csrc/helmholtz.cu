@@ -15,10 +15,16 @@
 namespace fgd {
 
 struct SArgs {
-  int Nx, Ny, Nz, TX, TY, TZ;
+  int Nx, Ny, Nz, TX, TY, TZ;   // Nz: local planes
   size_t nvox;
   double ih[3];          // 1 / (4 h_j)
   double lut[kMaxPhases];  // l^2 per phase
+  int dist;              // 1: z-slab of a multi-GPU run -> planes -1 and Nz come from the halos
+  const double* a_lo;
+  const double* a_hi;
+  const double* p_lo;
+  const double* p_hi;
+  const uint8_t* ph_lo;
 };
 
 enum StencilMode : int { ST_APPLY = 0, ST_PCG = 1 };
@@ -49,7 +55,7 @@ template <int MODE>
 __global__ void __launch_bounds__(256, 2) k_stencil(SArgs s, const double* __restrict__ ain, const double* __restrict__ pold,
                                                      double* __restrict__ pout, double* __restrict__ q,
                                                      const uint8_t* __restrict__ phase, DevScalars* sc, double* partials,
-                                                     int red_op) {
+                                                     int red_op, int red_slot) {
   __shared__ double planes[2][SBY + 2][SBX + 2];
   __shared__ double lut[kMaxPhases];
   const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * SBX + tx;
@@ -70,14 +76,26 @@ __global__ void __launch_bounds__(256, 2) k_stencil(SArgs s, const double* __res
   const size_t r1 = (size_t)wrapi(y0 - 1 + py1, Ny) * Nx + wrapi(x0 - 1 + px1, Nx);
   double v0 = 0.0, v1 = 0.0;
   auto gload = [&](int zl) {
-    const size_t base = (size_t)wrapi(zl, Nz) * Ny * Nx;
+    const double* pa;
+    const double* pp;
+    if (s.dist && zl < 0) {
+      pa = s.a_lo;
+      pp = s.p_lo;
+    } else if (s.dist && zl >= Nz) {
+      pa = s.a_hi;
+      pp = s.p_hi;
+    } else {
+      const size_t base = (size_t)wrapi(zl, Nz) * Ny * Nx;
+      pa = ain + base;
+      pp = pold + base;
+    }
     if (i0 < PN) {
-      v0 = __ldcs(ain + base + r0);
-      if (MODE == ST_PCG) v0 = fma(beta, pold[base + r0], v0);
+      v0 = __ldcs(pa + r0);
+      if (MODE == ST_PCG) v0 = fma(beta, pp[r0], v0);
     }
     if (i1 < PN) {
-      v1 = __ldcs(ain + base + r1);
-      if (MODE == ST_PCG) v1 = fma(beta, pold[base + r1], v1);
+      v1 = __ldcs(pa + r1);
+      if (MODE == ST_PCG) v1 = fma(beta, pp[r1], v1);
     }
   };
   auto sstore = [&](int b) {
@@ -94,10 +112,10 @@ __global__ void __launch_bounds__(256, 2) k_stencil(SArgs s, const double* __res
       for (int dx = 0; dx < 3; ++dx) A[dy][dx] = planes[b][ty + dy][tx + dx];
   };
   auto fluxes = [&](int zl, double (&F)[4][3]) {
-    const size_t base = (size_t)wrapi(zl, Nz) * Ny * Nx;
-    const size_t row0 = base + (size_t)ym * Nx, row1 = base + (size_t)gy * Nx;
-    const double l00 = lut[__ldg(phase + row0 + xm)], l10 = lut[__ldg(phase + row0 + gx)];
-    const double l01 = lut[__ldg(phase + row1 + xm)], l11 = lut[__ldg(phase + row1 + gx)];
+    const uint8_t* pb = (s.dist && zl < 0) ? s.ph_lo : phase + (size_t)wrapi(zl, Nz) * Ny * Nx;
+    const size_t row0 = (size_t)ym * Nx, row1 = (size_t)gy * Nx;
+    const double l00 = lut[__ldg(pb + row0 + xm)], l10 = lut[__ldg(pb + row0 + gx)];
+    const double l01 = lut[__ldg(pb + row1 + xm)], l11 = lut[__ldg(pb + row1 + gx)];
     corner_flux(A0, A1, 0, 0, l00, ih, F[0]);   // corner (x-1, y-1)
     corner_flux(A0, A1, 1, 0, l10, ih, F[1]);   // corner (x,   y-1)
     corner_flux(A0, A1, 0, 1, l01, ih, F[2]);   // corner (x-1, y)
@@ -148,14 +166,14 @@ __global__ void __launch_bounds__(256, 2) k_stencil(SArgs s, const double* __res
   }
   if (MODE == ST_PCG) {
     double rr[1] = {red};
-    reduce_finalize<1>(rr, partials, sc, red_op, 0);
+    reduce_finalize<1>(rr, partials, sc, red_op, red_slot);
   }
 }
 
 double mean_ell2(const fgd_ctx* c, int field) {
   double s = 0.0;
   for (int q = 0; q < c->nphases; ++q) s += (double)c->phase_count[q] * c->ell[field][q] * c->ell[field][q];
-  return s / (double)c->nvox;
+  return s / (double)c->nvox_g;
 }
 
 fgd_status launch_stencil(fgd_ctx* c, int field, int mode, const double* a, const double* zin, const double* pold,
@@ -163,7 +181,7 @@ fgd_status launch_stencil(fgd_ctx* c, int field, int mode, const double* a, cons
   SArgs s{};
   s.Nx = c->n[0];
   s.Ny = c->n[1];
-  s.Nz = c->n[2];
+  s.Nz = c->nz_l;
   s.TX = std::min(SBX, s.Nx);
   s.TY = std::min(SBY, s.Ny);
   s.TZ = std::min(16, s.Nz);
@@ -172,16 +190,35 @@ fgd_status launch_stencil(fgd_ctx* c, int field, int mode, const double* a, cons
   for (int p = 0; p < kMaxPhases; ++p) s.lut[p] = (p < c->nphases) ? c->ell[field][p] * c->ell[field][p] : 0.0;
   dim3 grid(s.Nx / s.TX, s.Ny / s.TY, s.Nz / s.TZ);
   dim3 block(SBX, SBY);
+  if (c->nranks > 1) {
+    const size_t plane = (size_t)s.Nx * s.Ny;
+    if (!c->halo && cudaMalloc((void**)&c->halo, 4 * plane * sizeof(double)) != cudaSuccess)
+      return set_err(c, FGD_ENOMEM, "halo planes");
+    s.dist = 1;
+    s.a_lo = c->halo;
+    s.a_hi = c->halo + plane;
+    s.p_lo = c->halo + 2 * plane;
+    s.p_hi = c->halo + 3 * plane;
+    s.ph_lo = c->phase_halo;
+    const double* src = (mode == ST_APPLY) ? a : zin;
+    fgd_status st = halo_exchange(c, src, plane * sizeof(double), c->halo, c->halo + plane);
+    if (st != FGD_OK) return st;
+    if (mode == ST_PCG) {
+      st = halo_exchange(c, pold, plane * sizeof(double), c->halo + 2 * plane, c->halo + 3 * plane);
+      if (st != FGD_OK) return st;
+    }
+  }
   if (mode == ST_PCG) {
     fgd_status st = ensure_partials(c, (size_t)grid.x * grid.y * grid.z);
     if (st != FGD_OK) return st;
   }
   c->launches++;
   KTimer kt(c, KC_STENCIL);
+  const int rop = red_op_for(c, red_op), rslot = red_slot_for(c, red_op, 0);
   if (mode == ST_APPLY)
-    k_stencil<ST_APPLY><<<grid, block, 0, c->stream>>>(s, a, nullptr, nullptr, q, c->phase, c->sc, c->partials, red_op);
+    k_stencil<ST_APPLY><<<grid, block, 0, c->stream>>>(s, a, nullptr, nullptr, q, c->phase, c->sc, c->partials, rop, rslot);
   else
-    k_stencil<ST_PCG><<<grid, block, 0, c->stream>>>(s, zin, pold, pout, q, c->phase, c->sc, c->partials, red_op);
+    k_stencil<ST_PCG><<<grid, block, 0, c->stream>>>(s, zin, pold, pout, q, c->phase, c->sc, c->partials, rop, rslot);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_err(c, FGD_ECUDA, std::string("k_stencil: ") + cudaGetErrorString(e));
   return FGD_OK;

@@ -204,7 +204,7 @@ fgd_status launch_xfwd(fgd_ctx* c, int ncomp, int mode, const double* in0, const
 fgd_status launch_xfwd_io(fgd_ctx* c, int ncomp, int mode, const double* in0, const double* in1, double* out0,
                           double* io1, const double* Cp, int red_op, int red_slot) {
   if (mode == XF_PLAIN && ((uintptr_t)in0 & 15) == 0) return pipe_xfwd_plain(c, ncomp, in0);
-  const int Nx = c->n[0], Ny = c->n[1], Nz = c->n[2];
+  const int Nx = c->n[0], Ny = c->n[1], Nz = c->nz_l;
   const int TY = choose_TY(Nx, ncomp, Ny);
   const int nl = ncomp * TY;
   const int thr = std::min(kMaxThr, std::max(64, round32(nl * fft_TPL(Nx / 2))));

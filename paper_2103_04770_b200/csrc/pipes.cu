@@ -62,11 +62,32 @@ __device__ __forceinline__ void c2r_pre_p(double2* line, int l, int k, const dou
 // ---------------------------------------------------------------------------------------------
 // Y pass
 // ---------------------------------------------------------------------------------------------
+// Slab layout of the transposed spectra: P z-slabs of nzs planes in real space,
+// P y-slabs of nys rows in the z pass.  The y pass writes S[r][s][c][kx][kyl][zl] (r = z-slab,
+// s = destination y-slab), the all-to-all moves block S[r][s] to R[s][r], the z pass works on
+// R[s][src][c][kx][kyl][zl].  P = 1 is the plain B[c][kx][ky][z] layout.
+struct SlabL {
+  int P, nys, nzs, lg_nys, lg_nzs;
+};
+__device__ __forceinline__ size_t slab_index(const SlabL& L, int C, int Hx, int c, int kx, int blk0_idx, int blk1_idx,
+                                             int row, int col) {
+  return (((((size_t)(blk0_idx * L.P + blk1_idx) * C + c) * Hx + kx) * L.nys + row) << L.lg_nzs) + col;
+}
+// S: y pass output / y-inv input, indexed by (c, kx, ky, z local)
+__device__ __forceinline__ size_t s_index(const SlabL& L, int C, int Hx, int c, int kx, int ky, int z) {
+  return slab_index(L, C, Hx, c, kx, z >> L.lg_nzs, ky >> L.lg_nys, ky & (L.nys - 1), z & (L.nzs - 1));
+}
+// R: z pass buffer, indexed by (c, kx, ky local, z global)
+__device__ __forceinline__ size_t r_index(const SlabL& L, int C, int Hx, int c, int kx, int ky, int z) {
+  return slab_index(L, C, Hx, c, kx, ky >> L.lg_nys, z >> L.lg_nzs, ky & (L.nys - 1), z & (L.nzs - 1));
+}
+
 struct YArgs {
   double2* A;
   double2* B;
   int Nz, Hx, TZ, ncomp, lgTZ;
   const double2* tw;
+  SlabL L;
 };
 
 template <int N, bool INV>
@@ -83,7 +104,7 @@ __device__ __forceinline__ void y_issue(const YArgs& a, int t, double2* buf) {
   } else {
     for (int idx = threadIdx.x; idx < TZ * N; idx += blockDim.x) {
       const int zz = idx & (TZ - 1), ky = idx >> a.lgTZ;
-      cp_async16(&buf[zz * LP + SWZ(zz, ky)], &a.B[((size_t)(c * a.Hx + kx) * N + ky) * a.Nz + z0 + zz]);
+      cp_async16(&buf[zz * LP + SWZ(zz, ky)], &a.B[s_index(a.L, a.ncomp, a.Hx, c, kx, ky, z0 + zz)]);
     }
   }
 }
@@ -114,7 +135,7 @@ __global__ void __launch_bounds__(256, 2) k_ypipe(YArgs a) {
     if (!INV) {
       for (int idx = threadIdx.x; idx < TZ * N; idx += blockDim.x) {
         const int zz = idx & (TZ - 1), ky = idx >> a.lgTZ;
-        a.B[((size_t)(c * a.Hx + kx) * N + ky) * a.Nz + z0 + zz] = buf[zz * LP + SWZ(zz, ky)];
+        a.B[s_index(a.L, a.ncomp, a.Hx, c, kx, ky, z0 + zz)] = buf[zz * LP + SWZ(zz, ky)];
       }
     } else {
       for (int idx = threadIdx.x; idx < TZ * N; idx += blockDim.x) {
@@ -132,6 +153,9 @@ __global__ void __launch_bounds__(256, 2) k_ypipe(YArgs a) {
 // ---------------------------------------------------------------------------------------------
 struct ZPArgs {
   double2* B;
+  SlabL SL;
+  int ky_off;          // global index of the first local ky (distributed y-slab)
+  int Nyl;             // local ky rows
   int Nx, Ny, Hx, TL, scheme, lgTL;
   double h[3], L[3];
   double scale;
@@ -220,12 +244,12 @@ template <int N, int NC>
 __device__ __forceinline__ void z_issue(const ZPArgs& a, int t, double2* buf) {
   constexpr int LP = cline(N);
   const int TL = a.TL;
-  const int nyt = a.Ny / TL;
+  const int nyt = a.Nyl / TL;
   const int kx = t / nyt, ky0 = (t % nyt) * TL;
   for (int idx = threadIdx.x; idx < NC * TL * N; idx += blockDim.x) {
     const int kz = idx % N, rest = idx / N;
     const int ll = rest & (TL - 1), c = rest >> a.lgTL;
-    cp_async16(&buf[(c * TL + ll) * LP + SWZ(c * TL + ll, kz)], &a.B[((size_t)(c * a.Hx + kx) * a.Ny + ky0 + ll) * N + kz]);
+    cp_async16(&buf[(c * TL + ll) * LP + SWZ(c * TL + ll, kz)], &a.B[r_index(a.SL, NC, a.Hx, c, kx, ky0 + ll, kz)]);
   }
 }
 
@@ -238,7 +262,7 @@ __global__ void __launch_bounds__(192, 3) k_zpipe(ZPArgs a) {
   double2* tpz = tws + N;                    // per-pass FFT twiddles
   load_table(tws, a.twz, N);
   build_pass_tables<N>(tpz, a.twz);
-  const int nyt = a.Ny / TL;
+  const int nyt = a.Nyl / TL;
   const int ntiles = a.Hx * nyt;
   int t = blockIdx.x;
   if (t < ntiles) z_issue<N, NC>(a, t, sm);
@@ -255,7 +279,7 @@ __global__ void __launch_bounds__(192, 3) k_zpipe(ZPArgs a) {
     __syncthreads();
     for (int idx = threadIdx.x; idx < TL * N; idx += blockDim.x) {
       const int kz = idx % N, ll = idx / N;
-      const int ky = ky0 + ll;
+      const int ky = ky0 + ll + a.ky_off;
       double2 k[3];
       zsymbol(a, N, kx, ky, kz, k, tws);
       const bool dc = (kx == 0 && ky == 0 && kz == 0);
@@ -277,7 +301,7 @@ __global__ void __launch_bounds__(192, 3) k_zpipe(ZPArgs a) {
     for (int idx = threadIdx.x; idx < NC * TL * N; idx += blockDim.x) {
       const int kz = idx % N, rest = idx / N;
       const int ll = rest & (TL - 1), c = rest >> a.lgTL;
-      a.B[((size_t)(c * a.Hx + kx) * a.Ny + ky0 + ll) * N + kz] = buf[(c * TL + ll) * LP + SWZ(c * TL + ll, kz)];
+      a.B[r_index(a.SL, NC, a.Hx, c, kx, ky0 + ll, kz)] = buf[(c * TL + ll) * LP + SWZ(c * TL + ll, kz)];
     }
     __syncthreads();
   }
@@ -487,15 +511,25 @@ static fgd_status launch_persistent(fgd_ctx* c, K kernel, int threads, size_t sm
     default: return set_err(c, FGD_EINVAL, "unsupported FFT length"); \
   }
 
+static SlabL slab_layout(const fgd_ctx* c) {
+  SlabL L{};
+  L.P = c->P;
+  L.nys = c->n[1] / c->P;
+  L.nzs = c->n[2] / c->P;
+  L.lg_nys = ilog2(L.nys);
+  L.lg_nzs = ilog2(L.nzs);
+  return L;
+}
+
 fgd_status pipe_y(fgd_ctx* c, int ncomp, bool inv) {
-  const int Ny = c->n[1], Nz = c->n[2];
+  const int Ny = c->n[1], Nz = c->nz_l;
   const int TPL = fft_TPL(Ny, true);
   int TZ = p2floor(std::max(1, 128 / TPL));
-  TZ = std::min(TZ, Nz);
+  TZ = std::min(TZ, std::min(Nz, c->n[2] / c->P));
   const int thr = std::min(256, r32(TZ * TPL));
   const size_t smem = (2 * (size_t)TZ * cline(Ny) + Ny) * sizeof(double2);
   const int ntiles = ncomp * c->Hx * (Nz / TZ);
-  YArgs a{c->specA, c->specB, Nz, c->Hx, TZ, ncomp, ilog2(TZ), c->tabs.tw[ilog2(Ny)]};
+  YArgs a{c->specA, c->specB, Nz, c->Hx, TZ, ncomp, ilog2(TZ), c->tabs.tw[ilog2(Ny)], slab_layout(c)};
   KTimer kt(c, inv ? (ncomp == 6 ? KC_YINV6 : KC_YINV1) : (ncomp == 6 ? KC_YFWD6 : KC_YFWD1));
 #define YPP(NN)                                                                  \
   if (inv) FGD_PLAUNCH(c, (k_ypipe<NN, true>), thr, smem, ntiles, a);            \
@@ -507,15 +541,19 @@ fgd_status pipe_y(fgd_ctx* c, int ncomp, bool inv) {
 
 fgd_status pipe_z(fgd_ctx* c, int ncomp, int mode, double scale, const double* dc_shift, double mean_ell2) {
   const int Ny = c->n[1], Nz = c->n[2];
+  const int Nyl = c->nranks > 1 ? Ny / c->P : Ny;
   const int TPL = fft_TPL(Nz);
   int TL = p2floor(std::max(1, 192 / (ncomp * TPL)));
   if (Nz == 1) TL = 32;
-  TL = std::min(TL, Ny);
+  TL = std::min(TL, Nyl);
   const int thr = std::min(192, std::max(r32(ncomp * TL * TPL), r32(std::min(TL * Nz, 192))));
   const size_t smem = (2 * (size_t)ncomp * TL * cline(Nz) + 2 * Nz) * sizeof(double2);
-  const int ntiles = c->Hx * (Ny / TL);
+  const int ntiles = c->Hx * (Nyl / TL);
   ZPArgs a{};
-  a.B = c->specB;
+  a.B = c->P > 1 ? c->specC : c->specB;
+  a.SL = slab_layout(c);
+  a.ky_off = c->nranks > 1 ? c->rank * (Ny / c->P) : 0;
+  a.Nyl = Nyl;
   a.Nx = c->n[0];
   a.Ny = Ny;
   a.Hx = c->Hx;
@@ -566,7 +604,7 @@ static int choose_TYp(int N, int Ny) {
 
 fgd_status pipe_xinv(fgd_ctx* c, int ncomp, int mode, double* out0, double* io1, double* io2, const double* in1,
                      int red_op, int red_slot) {
-  const int Nx = c->n[0], Ny = c->n[1], Nz = c->n[2];
+  const int Nx = c->n[0], Ny = c->n[1], Nz = c->nz_l;
   const int TY = choose_TYp(Nx, Ny);
   const int thr = std::min(128, r32(TY * fft_TPL(Nx / 2)));
   const size_t smem = (2 * (size_t)TY * xline(Nx / 2) + Nx / 2 + Nx) * sizeof(double2);
@@ -591,7 +629,7 @@ fgd_status pipe_xinv(fgd_ctx* c, int ncomp, int mode, double* out0, double* io1,
 }
 
 fgd_status pipe_xfwd_plain(fgd_ctx* c, int ncomp, const double* in0) {
-  const int Nx = c->n[0], Ny = c->n[1], Nz = c->n[2];
+  const int Nx = c->n[0], Ny = c->n[1], Nz = c->nz_l;
   const int TY = choose_TYp(Nx, Ny);
   const int thr = std::min(128, r32(TY * fft_TPL(Nx / 2)));
   const size_t smem = (2 * (size_t)TY * xline(Nx / 2) + Nx / 2 + Nx) * sizeof(double2);

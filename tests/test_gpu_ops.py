@@ -195,3 +195,38 @@ def test_full_size_operators_256(n):
     assert rel(ya, apply_helmholtz(g, a, e2)) <= TOL_APPLY
     za = ctx.apply_helmholtz_precond(0, x[0].contiguous()).cpu().numpy()
     assert rel(za, apply_precond(g, a, e2)) <= TOL_APPLY
+
+
+@pytest.mark.parametrize("P", [2, 4])
+def test_emulated_slab_layout(P, monkeypatch):
+    """Multi-GPU transposition layout (S[r][s] -> R[s][r] block all-to-all, y-slab z pass)
+    emulated on one GPU with FGD_EMULATE_SLABS=P: projection, projected tangent, precond,
+    CG and PCG must equal the oracle exactly as in the single-slab layout."""
+    monkeypatch.setenv("FGD_EMULATE_SLABS", str(P))
+    n = (16, 8, 16)
+    ctx, g = make_ctx(n)
+    mask = (1, 1, 0, 1, 1, 1)
+    ctx.set_control(mask)
+    tau = gaussian_field(6, g.shape, 1.0, 12)
+    assert rel(ctx.apply_projection(dev(tau)).cpu().numpy(), apply_projection(g, tau, mask)) <= TOL_APPLY
+    Cp = random_spd_tangent(g.nvox, 4)
+    ctx.set_tangent(dev(Cp))
+    C = unpack21(Cp).reshape((6, 6) + g.shape)
+    x = gaussian_field(6, g.shape, 1e-3, 13)
+    assert rel(ctx.apply_projected_tangent(dev(x)).cpu().numpy(),
+               apply_projected_tangent(g, C, x, mask)) <= TOL_APPLY
+    b = apply_projection(g, gaussian_field(6, g.shape, 1.0, 14), mask)
+    out = torch.empty((6,) + g.shape, dtype=torch.float64, device="cuda")
+    ctx.solve_tangent_cg(dev(b), out, tol=0.0, maxit=6)
+    ref, _, _ = cg(g, C, b, mask, tol=0.0, maxit=6)
+    assert rel(out.cpu().numpy(), ref) <= 1e-10
+    ph = bernoulli_phases(g.shape, 0.3, 2)
+    ctx.set_phases(dev(ph), 2)
+    ctx.set_nonlocal(np.array([[0.1, 0.002]]), [0])
+    e2 = ell2_field(ph, [0.1, 0.002])
+    a = gaussian_field(1, g.shape, 1.0, 15)[0]
+    assert rel(ctx.apply_helmholtz_precond(0, dev(a)).cpu().numpy(), apply_precond(g, a, e2)) <= TOL_APPLY
+    o1 = torch.empty(g.shape, dtype=torch.float64, device="cuda")
+    ctx.solve_helmholtz(0, dev(np.abs(a)), o1, tol=0.0, maxit=5)
+    ref5, _, _ = solve_helmholtz(g, np.abs(a), e2, tol=0.0, maxit=5)
+    assert rel(o1.cpu().numpy(), ref5) <= 1e-10
