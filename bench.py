@@ -43,7 +43,7 @@ def args_():
     p.add_argument("--steps", type=int, default=10)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--n", type=int, default=256)
+    p.add_argument("--size", dest="n", type=int, default=256, help="cell edge (voxels)")
     p.add_argument("--kcg", type=int, default=10)
     p.add_argument("--khelm", type=int, default=10)
     p.add_argument("--no-e2e", action="store_true")
@@ -120,7 +120,7 @@ def run_reference(a):
     dt = (time.perf_counter() - t) / a.steps
     v = CPU_SAMPLE_N ** 3 * a.kcg / dt
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": a.gpus, "steps": a.steps,
-            "warmup": a.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
+            "warmup": a.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": workload_name(a.n), "sample_n": CPU_SAMPLE_N, "kcg": a.kcg, "khelm": a.khelm},
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle",
@@ -209,12 +209,12 @@ def measured_traffic(cls, n):
     return d.get(k), os.path.basename(files[-1]) + ":" + k
 
 
-def class_bytes(n, kcg, khelm):
-    """Algorithmic (compulsory) bytes per STEP for each kernel class of the fused 5-pass design
-    (SURVEY 8(d): K2 360 B/voxel, K3/K4/K3 96 B each, K5 288 B; 1-comp analogues; stencil 33 B;
-    constitutive 345 B).  S = spectral bytes of one component (16 B x Hx*Ny*Nz)."""
-    V = n ** 3
-    S = 16 * (n // 2 + 1) * n * n
+def class_bytes(n, kcg, khelm, world=1):
+    """Algorithmic (compulsory) bytes per STEP and per rank for each kernel class of the fused
+    5-pass design (SURVEY 8(d): K2 360 B/voxel, K3/K4/K3 96 B each, K5 288 B; 1-comp analogues;
+    stencil 33 B; constitutive 345 B).  S = spectral bytes of one component (16 B x Hx*Ny*Nz)."""
+    V = n ** 3 // world
+    S = 16 * (n // 2 + 1) * n * n // world
     b = {}
     b["xfwd6"] = (48 * V + 6 * S) + kcg * (48 * 3 * V + 168 * V + 6 * S)        # residual + CG (p, C, spec)
     b["yfwd6"] = b["yinv6"] = b["z6"] = (1 + kcg) * 2 * 6 * S
@@ -233,20 +233,27 @@ def run_ours(a):
 
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
+    import synth
+    from paper_2103_04770_b200 import Context, Material, nccl_id
+
+    nid = None
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    import synth
-    from paper_2103_04770_b200 import Context, Material
-
+        t = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            t.copy_(torch.frombuffer(bytearray(nccl_id()), dtype=torch.uint8))
+        dist.broadcast(t, 0)
+        nid = bytes(t.cpu().numpy().tobytes())
     n = a.n
     V = n ** 3
     dev = torch.device("cuda", local)
+    ctx = Context((n, n, n), (float(n),) * 3, device=local, rank=rank, nranks=world, nccl_id=nid)
+    nz, z0 = ctx.nz, ctx.z0
     gen = torch.Generator(device=dev)
     gen.manual_seed(1234 + rank)
-    ph = torch.from_numpy(synth.config1_phases(n, 0)).to(dev)
-    eps = torch.randn((6, n, n, n), generator=gen, dtype=torch.float64, device=dev) * 1e-3
-    ctx = Context((n, n, n), (float(n),) * 3, device=local)
+    ph = torch.from_numpy(synth.config1_phases(n, 0)[z0:z0 + nz].copy()).to(dev)
+    eps = torch.randn((6, nz, n, n), generator=gen, dtype=torch.float64, device=dev) * 1e-3
     ctx.set_phases(ph, 2)
     m0, m1 = synth.MATRIX_J2, synth.INCLUSION_EL
     for q, m in enumerate((m0, m1)):
@@ -290,11 +297,11 @@ def run_ours(a):
         t = torch.tensor([ms], device=dev, dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t.item())
-    value = world * V * a.kcg / (ms * 1e-3)
+    value = V * a.kcg / (ms * 1e-3)          # strong scaling: the global n^3 cell, all ranks
 
     # roofline of the dominant kernel class (its launches inside the timed region)
     peak, peak_src = peaks()
-    cb = class_bytes(n, a.kcg, a.khelm)
+    cb = class_bytes(n, a.kcg, a.khelm, world)
     per_class = {}
     step_ms_sum = sum(v[0] for v in kt.values())
     for k, (tms, cnt) in kt.items():
@@ -319,7 +326,7 @@ def run_ours(a):
 
     e2e = None
     if not a.no_e2e:
-        host = torch.empty((6, n, n, n), dtype=torch.float64, pin_memory=True)
+        host = torch.empty((6, nz, n, n), dtype=torch.float64, pin_memory=True)
         host.copy_(eps.cpu())
         step(host)
         torch.cuda.synchronize()
@@ -332,8 +339,8 @@ def run_ours(a):
             tt = torch.tensor([te], device=dev, dtype=torch.float64)
             torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
             te = float(tt.item())
-        e2e = {"value": world * V * a.kcg / te, "unit": UNIT, "h2d_bytes_per_step": 48 * V,
-               "d2h_bytes_per_step": 48 + 8 + 8 + 8, "ms_per_step": te * 1e3}
+        e2e = {"value": V * a.kcg / te, "unit": UNIT, "h2d_bytes_per_step": 48 * V,
+               "d2h_bytes_per_step": world * (48 + 8 + 8 + 8), "ms_per_step": te * 1e3}
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu:
@@ -341,10 +348,12 @@ def run_ours(a):
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
-                "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+                "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True,
+                "scaling": "strong",
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": {"workload": workload_name(n), "n": n, "kcg": a.kcg, "khelm": a.khelm,
-                           "parallelism": "single GPU" if world == 1 else f"{world} independent replicas (slab decomposition not built yet)",
+                           "parallelism": "single GPU" if world == 1 else
+                           f"z-slab decomposition over {world} GPUs (NCCL all-to-all transposes, allreduce)",
                            "l2": "no flush: every input field (>=134 MB) and the tangent (2.8 GB) exceed the 126 MB L2"},
                 "roofline": roof, "step_roofline": step_eff, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": launches, "clocks": clk, "kernels": per_class,
