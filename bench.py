@@ -216,14 +216,15 @@ def class_bytes(n, kcg, khelm, world=1):
     V = n ** 3 // world
     S = 16 * (n // 2 + 1) * n * n // world
     b = {}
-    b["xfwd6"] = (48 * V + 6 * S) + kcg * (48 * 3 * V + 168 * V + 6 * S)        # residual + CG (p, C, spec)
+    TB = 72                                                                       # compact J2 tangent (9 doubles)
+    b["xfwd6"] = (48 * V + 6 * S) + kcg * (48 * 3 * V + TB * V + 6 * S)         # residual + CG (r, p, C, p, spec)
     b["yfwd6"] = b["yinv6"] = b["z6"] = (1 + kcg) * 2 * 6 * S
     b["xinv6"] = (6 * S + 48 * V) + kcg * (6 * S + 144 * V + 96 * V)            # residual store + CG update
     b["xfwd1"] = (8 * V + S) + khelm * (32 * V + 16 * V + S)                      # precond init + PCG x/r update
     b["yfwd1"] = b["yinv1"] = b["z1"] = (1 + khelm) * 2 * S
     b["xinv1"] = (1 + khelm) * (S + 16 * V)
     b["stencil"] = khelm * 33 * V
-    b["constitutive"] = (48 + 48 + 8 + 8 + 8 + 1 + 48 + 168 + 8) * V
+    b["constitutive"] = (48 + 48 + 8 + 8 + 8 + 1 + 48 + TB + 8) * V
     return b
 
 

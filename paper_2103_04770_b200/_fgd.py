@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libfgd.so")
+LIB_PATH = os.environ.get("FGD_LIB", os.path.join(_HERE, "libfgd.so"))
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"libfgd.so not built ({LIB_PATH}); run `python -m paper_2103_04770_b200.build` "
                       "(there is no CPU fallback)")

@@ -28,20 +28,25 @@ __device__ __forceinline__ double clamp01cap(double v, double cap) {
   return v < cap ? v : cap;
 }
 
+// The consistent tangent of every model here has the structure
+//   C = ca 1(x)1 + cb I - cc n(x)n        (1 = (1,1,1,0,0,0) in Mandel form)
+// so it is stored compactly as 9 doubles per voxel [n0..n5, ca, cb, cc] (72 B instead of the
+// 168 B of the packed 6x6; the CG reads it every iteration).
 struct PointOut {
   double sig[6];
-  double C[21];
+  double n[6];
+  double ca, cb, cc;
   double epsp[6];
   double ep;
   double alpha;
 };
 
-__device__ __forceinline__ void elastic_C(double K, double mu, double f, double* C) {
-  // K 1x1 + 2 mu I_dev, times f
-  const double a = f * (K + 4.0 * mu / 3.0), b = f * (K - 2.0 * mu / 3.0), d = f * 2.0 * mu;
-  int t = 0;
-  for (int i = 0; i < 6; ++i)
-    for (int j = i; j < 6; ++j, ++t) C[t] = (i < 3 && j < 3) ? (i == j ? a : b) : (i == j ? d : 0.0);
+__device__ __forceinline__ void elastic_C(double K, double mu, double f, PointOut& o) {
+  // f (K 1x1 + 2 mu I_dev) = f (K - 2mu/3) 1x1 + f 2mu I
+  o.ca = f * (K - 2.0 * mu / 3.0);
+  o.cb = f * 2.0 * mu;
+  o.cc = 0.0;
+  for (int i = 0; i < 6; ++i) o.n[i] = 0.0;
 }
 
 __device__ void point_update(const Material& m, int has_field, const double* e, const double* epsp_n, double ep_n,
@@ -54,7 +59,7 @@ __device__ void point_update(const Material& m, int has_field, const double* e, 
   o.ep = ep_n;
   for (int i = 0; i < 6; ++i) o.epsp[i] = epsp_n[i];
   if (m.model == 0) {
-    elastic_C(K, mu, 1.0, o.C);
+    elastic_C(K, mu, 1.0, o);
     for (int i = 0; i < 6; ++i) o.sig[i] = 2.0 * mu * de[i] + (i < 3 ? K * tr : 0.0);
   } else if (m.model == 1) {
     double D = 0.0;
@@ -84,17 +89,12 @@ __device__ void point_update(const Material& m, int has_field, const double* e, 
       const double theta = 1.0 - 2.0 * mu * dlam / q;
       const double thetab = 1.0 / (1.0 + m.H / (3.0 * mu)) - (1.0 - theta);
       // C = w [K 1x1 + 2 mu theta (I - 1x1/3) - 2 mu thetab n x n]
-      const double a = K - 2.0 * mu * theta / 3.0;
-      int t = 0;
-      for (int i = 0; i < 6; ++i)
-        for (int j = i; j < 6; ++j, ++t) {
-          double v = -2.0 * mu * thetab * n[i] * n[j];
-          if (i < 3 && j < 3) v += a;
-          if (i == j) v += 2.0 * mu * theta;
-          o.C[t] = w * v;
-        }
+      o.ca = w * (K - 2.0 * mu * theta / 3.0);
+      o.cb = w * 2.0 * mu * theta;
+      o.cc = w * 2.0 * mu * thetab;
+      for (int i = 0; i < 6; ++i) o.n[i] = n[i];
     } else {
-      elastic_C(K, mu, w, o.C);
+      elastic_C(K, mu, w, o);
     }
     for (int i = 0; i < 6; ++i) o.sig[i] = w * (2.0 * mu * (de[i] - o.epsp[i]) + (i < 3 ? K * tr : 0.0));
     o.alpha = o.ep;
@@ -111,7 +111,7 @@ __device__ void point_update(const Material& m, int has_field, const double* e, 
     o.alpha = sqrt((ee > 0.0 ? ee : 0.0) / m.E);
     const double w = 1.0 - d;
     for (int i = 0; i < 6; ++i) o.sig[i] = w * ce[i];
-    elastic_C(K, mu, w, o.C);
+    elastic_C(K, mu, w, o);
   }
 }
 
@@ -149,7 +149,10 @@ __global__ void __launch_bounds__(256) k_constitutive(KArgs a, MatTable mt) {
       a.sig[i * n + g] = o.sig[i];
       red[i] += o.sig[i];
     }
-    for (int t = 0; t < 21; ++t) a.C[(size_t)t * n + g] = o.C[t];
+    for (int i = 0; i < 6; ++i) a.C[(size_t)i * n + g] = o.n[i];
+    a.C[6 * n + g] = o.ca;
+    a.C[7 * n + g] = o.cb;
+    a.C[8 * n + g] = o.cc;
     for (int f = 0; f < mt.nfields; ++f) a.alpha[(size_t)f * n + g] = (f == j) ? o.alpha : 0.0;
   }
   reduce_finalize<6>(red, a.partials, a.sc, RED_STORE, 0);
@@ -218,6 +221,19 @@ __global__ void __launch_bounds__(256) k_err(size_t n, const double* eps, const 
   reduce_finalize<14>(red, partials, sc, RED_STORE, 16);
 }
 
+// compact [n0..n5, ca, cb, cc] -> packed upper triangle (21) of ca 1x1 + cb I - cc n x n
+__global__ void k_expand_tangent(size_t n, const double* __restrict__ Cc, double* __restrict__ Cp) {
+  for (size_t g = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g < n; g += (size_t)gridDim.x * blockDim.x) {
+    double v[6];
+    for (int i = 0; i < 6; ++i) v[i] = Cc[i * n + g];
+    const double ca = Cc[6 * n + g], cb = Cc[7 * n + g], cc = Cc[8 * n + g];
+    int t = 0;
+    for (int i = 0; i < 6; ++i)
+      for (int j = i; j < 6; ++j, ++t)
+        Cp[(size_t)t * n + g] = (i < 3 && j < 3 ? ca : 0.0) + (i == j ? cb : 0.0) - cc * v[i] * v[j];
+  }
+}
+
 __global__ void k_dot(size_t n, const double* a, const double* b, DevScalars* sc, double* partials, int op, int slot) {
   double red[1] = {0.0};
   for (size_t g = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g < n; g += (size_t)gridDim.x * blockDim.x)
@@ -283,7 +299,7 @@ fgd_status launch_constitutive(fgd_ctx* c, const double* eps) {
   const int nb = ew_blocks(c, c->nvox);
   fgd_status s = ensure_partials(c, nb);
   if (s != FGD_OK) return s;
-  KArgs a{c->nvox, eps, c->st_epsp, c->st_ep, c->st_hist, c->w_abar, c->phase, c->w_sig, c->C, c->w_alpha, c->sc,
+  KArgs a{c->nvox, eps, c->st_epsp, c->st_ep, c->st_hist, c->w_abar, c->phase, c->w_sig, c->Cc, c->w_alpha, c->sc,
           c->partials};
   c->launches++;
   KTimer kt(c, KC_CONST);
@@ -340,6 +356,14 @@ fgd_status launch_init_iterate(fgd_ctx* c, const double* eps_n, double* eps, con
   KTimer kt(c, KC_OTHER);
   k_init_iterate<<<ew_blocks(c, 6 * c->nvox), 256, 0, c->stream>>>(c->nvox, eps_n, eps, dE6_dev);
   FGD_CHECK_LAUNCH(c, "k_init_iterate");
+  return FGD_OK;
+}
+
+fgd_status launch_expand_tangent(fgd_ctx* c, const double* Cc, double* Cp) {
+  c->launches++;
+  KTimer kt(c, KC_OTHER);
+  k_expand_tangent<<<ew_blocks(c, c->nvox), 256, 0, c->stream>>>(c->nvox, Cc, Cp);
+  FGD_CHECK_LAUNCH(c, "k_expand_tangent");
   return FGD_OK;
 }
 

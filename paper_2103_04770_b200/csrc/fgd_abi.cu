@@ -195,7 +195,7 @@ static double inv_nvox(const fgd_ctx* c) { return 1.0 / (double)c->nvox_g; }
 // y = G*(C : x)
 static fgd_status op_projected_tangent(fgd_ctx* c, const double* x, double* y) {
   TRY(ensure_spectral(c));
-  TRY(launch_xfwd(c, 6, XF_TANGENT, x, nullptr, nullptr, c->C, RED_NONE, 0));
+  TRY(launch_xfwd(c, 6, XF_TANGENT, x, nullptr, nullptr, c->compact ? c->Cc : c->C, RED_NONE, 0));
   TRY(launch_yfwd(c, 6));
   TRY(exchange(c, 6, true));
   TRY(launch_z(c, 6, Z_PROJECT, inv_nvox(c), nullptr, 0.0));
@@ -266,7 +266,7 @@ static fgd_status ensure_state(fgd_ctx* c) {
   TRY(dalloc(c, &c->cm_hist, n));
   TRY(dalloc(c, &c->w_b, 6 * n));
   TRY(dalloc(c, &c->w_de, 6 * n));
-  TRY(dalloc(c, &c->C, 21 * n));
+  TRY(dalloc(c, &c->Cc, 9 * n));
   FGD_CUDA(c, cudaMemsetAsync(c->st_eps, 0, 6 * n * 8, c->stream));
   FGD_CUDA(c, cudaMemsetAsync(c->st_epsp, 0, 6 * n * 8, c->stream));
   FGD_CUDA(c, cudaMemsetAsync(c->st_ep, 0, n * 8, c->stream));
@@ -353,7 +353,7 @@ static fgd_status cg_mech(fgd_ctx* c, const double* b, double* x_out, double tol
   if (bb > 0.0) {
     rel = 1.0;
     while (it < maxit) {
-      TRY(launch_xfwd(c, 6, XF_TANGENT_CG, c->cg_r, nullptr, c->cg_p, c->C, RED(RED_MECH_PQ)));
+      TRY(launch_xfwd(c, 6, XF_TANGENT_CG, c->cg_r, nullptr, c->cg_p, c->compact ? c->Cc : c->C, RED(RED_MECH_PQ)));
       TRY(launch_yfwd(c, 6));
       TRY(exchange(c, 6, true));
       TRY(launch_z(c, 6, Z_PROJECT, inv_nvox(c), nullptr, 0.0));
@@ -460,7 +460,7 @@ fgd_status fgd_create(const fgd_grid* g, const fgd_dist* d, fgd_ctx** out) {
 void fgd_destroy(fgd_ctx* c) {
   if (!c) return;
   if (c->stream) cudaStreamSynchronize(c->stream);
-  void* bufs[] = {c->tw_all, c->phase, c->C, c->specA, c->specB, c->cg_x, c->cg_r, c->cg_p, c->sc, c->partials,
+  void* bufs[] = {c->tw_all, c->phase, c->C, c->Cc, c->specA, c->specB, c->cg_x, c->cg_r, c->cg_p, c->sc, c->partials,
                   c->st_eps, c->st_epsp, c->st_ep, c->st_hist, c->st_abar, c->w_eps, c->w_eps_prev, c->w_sig,
                   c->w_alpha, c->w_abar, c->w_D, c->cm_epsp, c->cm_ep, c->cm_hist, c->w_b, c->w_de};
   for (void* b : bufs)
@@ -572,6 +572,7 @@ fgd_status fgd_set_tangent(fgd_ctx* c, const double* C) {
     FGD_CUDA(c, cudaMemcpyAsync(c->C, C, 21 * c->nvox * 8, cudaMemcpyHostToDevice, c->stream));
   FGD_CUDA(c, cudaStreamSynchronize(c->stream));
   c->tangent_set = true;
+  c->compact = 0;
   return FGD_OK;
 }
 
@@ -694,6 +695,7 @@ fgd_status fgd_constitutive(fgd_ctx* c, const double* eps, double* sigma_out, do
   TRY(launch_constitutive(c, c->w_eps));
   TRY(allreduce_sum(c, &c->sc->red[0], 6));
   c->tangent_set = true;
+  c->compact = 1;
   c->have_sigma = true;
   if (sigma_out) {
     double* ds;
@@ -876,7 +878,13 @@ fgd_status fgd_get_field(fgd_ctx* c, int which, double* out) {
   else if (which == FGD_FIELD_EPS_P) src = c->st_epsp, cnt = 6 * n;
   else if (which == FGD_FIELD_EQPS) src = c->st_ep;
   else if (which == FGD_FIELD_HIST) src = c->st_hist;
-  else if (which == FGD_FIELD_TANGENT) src = c->C, cnt = 21 * n;
+  else if (which == FGD_FIELD_TANGENT) {
+    if (c->compact) {
+      TRY(dalloc(c, &c->C, 21 * n));
+      TRY(launch_expand_tangent(c, c->Cc, c->C));
+    }
+    src = c->C, cnt = 21 * n;
+  }
   else if (which == FGD_FIELD_ITERATE) src = c->w_eps, cnt = 6 * n;
   else if (which >= FGD_FIELD_NONLOCAL && which < FGD_FIELD_NONLOCAL + c->nfields)
     src = c->w_abar + (size_t)(which - FGD_FIELD_NONLOCAL) * n;

@@ -97,7 +97,9 @@ struct fgd_ctx {
   bool control_set = false;
 
   // device buffers (lazily allocated)
-  double* C = nullptr;         // 21 * nvox packed tangent
+  double* C = nullptr;         // 21 * nvox packed tangent (fgd_set_tangent)
+  double* Cc = nullptr;        // 9 * nvox compact tangent [n, ca, cb, cc] (fgd_constitutive)
+  int compact = 0;             // 1: the CG uses Cc, 0: C
   bool tangent_set = false;
   double2* specA = nullptr;    // 6 * nspec
   double2* specB = nullptr;    // 6 * nspec
@@ -205,6 +207,7 @@ fgd_status launch_dot(fgd_ctx* c, size_t n, const double* a, const double* b, in
 fgd_status launch_axpy(fgd_ctx* c, size_t n, double* y, const double* x, double s);
 fgd_status launch_init_iterate(fgd_ctx* c, const double* eps_n, double* eps, const double* dE6_dev);
 fgd_status launch_phase_count(fgd_ctx* c, const uint8_t* ph, unsigned long long* cnt, int nph, int* bad);
+fgd_status launch_expand_tangent(fgd_ctx* c, const double* Cc, double* Cp);
 
 // x-pass modes
 enum XFwdMode : int {

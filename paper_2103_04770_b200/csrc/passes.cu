@@ -32,6 +32,7 @@ struct XArgs {
   DevScalars* sc;
   double* partials;
   int red_op, red_slot;
+  int compact;
 };
 
 // packed upper-triangle offsets of row i
@@ -73,8 +74,24 @@ __device__ __forceinline__ void r2c_post(double2* line, int l, int k, const doub
   if (k != M - k) line[SWZ(l, M - k)] = conjg(csub(E, WO));
 }
 
+// compact tangent (constitutive.cu): tau = ca tr(p) 1 + cb p - cc (n.p) n
+__device__ __forceinline__ void tangent_apply_c(const double* __restrict__ Cc, size_t g, size_t n, const double* p,
+                                                double* tau) {
+  double v[6];
+#pragma unroll
+  for (int i = 0; i < 6; ++i) v[i] = __ldcs(Cc + (size_t)i * n + g);
+  const double ca = __ldcs(Cc + 6 * n + g), cb = __ldcs(Cc + 7 * n + g), cc = __ldcs(Cc + 8 * n + g);
+  const double tr = ca * (p[0] + p[1] + p[2]);
+  double np = 0.0;
+#pragma unroll
+  for (int i = 0; i < 6; ++i) np = fma(v[i], p[i], np);
+  np *= cc;
+#pragma unroll
+  for (int i = 0; i < 6; ++i) tau[i] = fma(cb, p[i], fma(-np, v[i], i < 3 ? tr : 0.0));
+}
+
 template <int N, int NC, int MODE>
-__global__ void __launch_bounds__(kMaxThr, 1) k_xfwd(XArgs a, const double2* __restrict__ twM,
+__global__ void __launch_bounds__(kMaxThr, 2) k_xfwd(XArgs a, const double2* __restrict__ twM,
                                                       const double2* __restrict__ twN) {
   extern __shared__ double2 sm[];
   constexpr int M = N / 2;
@@ -99,14 +116,16 @@ __global__ void __launch_bounds__(kMaxThr, 1) k_xfwd(XArgs a, const double2* __r
       double p[6];
 #pragma unroll
       for (int c = 0; c < 6; ++c) p[c] = a.in0[c * n + g];
-      tangent_apply(a.Cp, g, n, p, tau);
+      if (a.compact) tangent_apply_c(a.Cp, g, n, p, tau);
+      else tangent_apply(a.Cp, g, n, p, tau);
     } else if (MODE == XF_TANGENT_CG) {
       double p[6];
 #pragma unroll
       for (int c = 0; c < 6; ++c) p[c] = fma(beta, a.out0[c * n + g], a.in0[c * n + g]);
 #pragma unroll
       for (int c = 0; c < 6; ++c) a.out0[c * n + g] = p[c];
-      tangent_apply(a.Cp, g, n, p, tau);
+      if (a.compact) tangent_apply_c(a.Cp, g, n, p, tau);
+      else tangent_apply(a.Cp, g, n, p, tau);
 #pragma unroll
       for (int c = 0; c < 6; ++c) red[0] = fma(p[c], tau[c], red[0]);
     } else if (MODE == XF_HELM_UPDATE) {
@@ -210,7 +229,8 @@ fgd_status launch_xfwd_io(fgd_ctx* c, int ncomp, int mode, const double* in0, co
   const int thr = std::min(kMaxThr, std::max(64, round32(nl * fft_TPL(Nx / 2))));
   const size_t smem = ((size_t)nl * xline(Nx / 2) + Nx / 2) * sizeof(double2);
   dim3 grid(Ny / TY, Nz);
-  XArgs a{Ny, Nz, TY, c->Hx, c->nvox, in0, in1, out0, io1, nullptr, Cp, c->specA, c->sc, c->partials, red_op, red_slot};
+  XArgs a{Ny, Nz, TY, c->Hx, c->nvox, in0, in1, out0, io1, nullptr, Cp, c->specA, c->sc, c->partials, red_op, red_slot,
+          (Cp != nullptr && Cp == c->Cc) ? 1 : 0};
   if (red_op != RED_NONE) {
     fgd_status s = ensure_partials(c, (size_t)grid.x * grid.y);
     if (s != FGD_OK) return s;
