@@ -211,15 +211,17 @@ def measured_traffic(cls, n):
 
 def class_bytes(n, kcg, khelm, world=1):
     """Algorithmic (compulsory) bytes per STEP and per rank for each kernel class of the fused
-    5-pass design (SURVEY 8(d): K2 360 B/voxel, K3/K4/K3 96 B each, K5 288 B; 1-comp analogues;
-    stencil 33 B; constitutive 345 B).  S = spectral bytes of one component (16 B x Hx*Ny*Nz)."""
+    5-pass design.  Mechanical CG with the solution update deferred into the next forward pass:
+    K2 = read r, p, x (144) + compact tangent (72) + write p, x (96) + spectrum (~48) B/voxel,
+    K3/K4/K3 ~96 B each, K5 = spectrum (~48) + read/write r (96); 1-comp analogues; stencil 33 B;
+    constitutive ~300 B.  S = spectral bytes of one component (16 B x Hx*Ny*Nz)."""
     V = n ** 3 // world
     S = 16 * (n // 2 + 1) * n * n // world
     b = {}
     TB = 72                                                                       # compact J2 tangent (9 doubles)
-    b["xfwd6"] = (48 * V + 6 * S) + kcg * (48 * 3 * V + TB * V + 6 * S)         # residual + CG (r, p, C, p, spec)
+    b["xfwd6"] = (48 * V + 6 * S) + kcg * (48 * 5 * V + TB * V + 6 * S)         # residual + CG (r, p, x, C -> p, x, spec)
     b["yfwd6"] = b["yinv6"] = b["z6"] = (1 + kcg) * 2 * 6 * S
-    b["xinv6"] = (6 * S + 48 * V) + kcg * (6 * S + 144 * V + 96 * V)            # residual store + CG update
+    b["xinv6"] = (6 * S + 48 * V) + kcg * (6 * S + 96 * V)                      # residual store + CG r update
     b["xfwd1"] = (8 * V + S) + khelm * (32 * V + 16 * V + S)                      # precond init + PCG x/r update
     b["yfwd1"] = b["yinv1"] = b["z1"] = (1 + khelm) * 2 * S
     b["xinv1"] = (1 + khelm) * (S + 16 * V)

@@ -246,6 +246,13 @@ __global__ void k_axpy(size_t n, double* y, const double* x, double s) {
     y[g] = fma(s, x[g], y[g]);
 }
 
+// y += alpha x with alpha the device-resident Krylov step (final deferred CG solution update)
+__global__ void k_axpy_alpha(size_t n, double* y, const double* x, const DevScalars* sc) {
+  const double s = sc->alpha;
+  for (size_t g = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g < n; g += (size_t)gridDim.x * blockDim.x)
+    y[g] = fma(s, x[g], y[g]);
+}
+
 // eps = eps_n + dE (uniform on strain-controlled components)
 __global__ void k_init_iterate(size_t n, const double* eps_n, double* eps, const double* dE6) {
   for (size_t g = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g < 6 * n; g += (size_t)gridDim.x * blockDim.x)
@@ -348,6 +355,14 @@ fgd_status launch_axpy(fgd_ctx* c, size_t n, double* y, const double* x, double 
   KTimer kt(c, KC_OTHER);
   k_axpy<<<ew_blocks(c, n), 256, 0, c->stream>>>(n, y, x, s);
   FGD_CHECK_LAUNCH(c, "k_axpy");
+  return FGD_OK;
+}
+
+fgd_status launch_axpy_alpha(fgd_ctx* c, size_t n, double* y, const double* x) {
+  c->launches++;
+  KTimer kt(c, KC_OTHER);
+  k_axpy_alpha<<<ew_blocks(c, n), 256, 0, c->stream>>>(n, y, x, c->sc);
+  FGD_CHECK_LAUNCH(c, "k_axpy_alpha");
   return FGD_OK;
 }
 

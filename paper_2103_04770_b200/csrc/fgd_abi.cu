@@ -54,7 +54,7 @@ static fgd_status dalloc(fgd_ctx* c, T** p, size_t count) {
 }
 
 fgd_status ensure_spectral(fgd_ctx* c) {
-  fgd_status s = dalloc(c, &c->specA, 6 * c->nspec);
+  fgd_status s = dalloc(c, &c->specA, 6 * c->nspecA);
   if (s != FGD_OK) return s;
   if (c->P > 1) {
     s = dalloc(c, &c->specC, 6 * c->nspec);
@@ -353,14 +353,15 @@ static fgd_status cg_mech(fgd_ctx* c, const double* b, double* x_out, double tol
   if (bb > 0.0) {
     rel = 1.0;
     while (it < maxit) {
-      TRY(launch_xfwd(c, 6, XF_TANGENT_CG, c->cg_r, nullptr, c->cg_p, c->compact ? c->Cc : c->C, RED(RED_MECH_PQ)));
+      TRY(launch_xfwd_io(c, 6, XF_TANGENT_CG, c->cg_r, nullptr, c->cg_p, c->cg_x, c->compact ? c->Cc : c->C,
+                         RED(RED_MECH_PQ)));
       TRY(launch_yfwd(c, 6));
       TRY(exchange(c, 6, true));
       TRY(launch_z(c, 6, Z_PROJECT, inv_nvox(c), nullptr, 0.0));
       TRY(exchange(c, 6, false));
       TRY(post_reduce(c, RED_MECH_PQ));
       TRY(launch_yinv(c, 6));
-      TRY(launch_xinv(c, 6, XI_MECH_CG, nullptr, c->cg_x, c->cg_r, c->cg_p, RED(RED_MECH_RR)));
+      TRY(launch_xinv(c, 6, XI_MECH_CG, nullptr, nullptr, c->cg_r, nullptr, RED(RED_MECH_RR)));
       TRY(post_reduce(c, RED_MECH_RR));
       ++it;
       if (tol > 0.0) {
@@ -375,6 +376,7 @@ static fgd_status cg_mech(fgd_ctx* c, const double* b, double* x_out, double tol
       TRY(sync_read(c, &c->sc->rr, 8, &rr));
       rel = std::sqrt(rr / bb);
     }
+    if (it > 0) TRY(launch_axpy_alpha(c, n6, c->cg_x, c->cg_p));   // x += alpha_last p_last
   }
   if (x_out) FGD_CUDA(c, cudaMemcpyAsync(x_out, c->cg_x, n6 * 8, cudaMemcpyDeviceToDevice, c->stream));
   if (iters) *iters = it;
@@ -439,6 +441,8 @@ fgd_status fgd_create(const fgd_grid* g, const fgd_dist* d, fgd_ctx** out) {
   c->nvox_g = (size_t)c->n[0] * c->n[1] * c->n[2];
   c->nvox = (size_t)c->n[0] * c->n[1] * c->nz_l;
   c->nspec = (size_t)c->Hx * c->n[1] * c->nz_l;
+  c->HxA = (c->Hx + 3) & ~3;
+  c->nspecA = (size_t)c->HxA * c->n[1] * c->nz_l;
   // stream == NULL is the legacy default stream (it orders against every other blocking stream,
   // e.g. PyTorch's default stream, so inputs produced there are complete before our kernels run)
   {

@@ -55,6 +55,15 @@ struct ConstTables {
 
 }  // namespace fgd
 
+// Layout A of the x-pass half spectra: A[c][z][kx / kKB][y][kx % kKB] (HxA = Hx rounded up to 4
+// kx slots, the padding never read).  A y-pass tile of kKB kx reads kKB * Ny * 16 B contiguous per
+// plane; an x-pass tile of kXR rows writes runs of kXR * kKB * 16 B.
+constexpr int kKB = 2;   // kx block of layout A
+constexpr int kXR = 2;   // rows per tile of the bulk-copy tangent x pass (k_xtan)
+__host__ __device__ __forceinline__ size_t aidx(int HxA, int Ny, int Nz, int c, int z, int y, int kx) {
+  return (((size_t)(c * Nz + z) * (HxA / kKB) + kx / kKB) * Ny + y) * kKB + (kx & (kKB - 1));
+}
+
 struct fgd_ctx {
   int dims = 3;
   int n[3] = {1, 1, 1};        // Nx, Ny, Nz
@@ -72,7 +81,9 @@ struct fgd_ctx {
   double* halo = nullptr;      // stencil halo planes (nranks > 1): [field 0 lo, hi][field 1 lo, hi]
   uint8_t* phase_halo = nullptr;
   int Hx = 1;
+  int HxA = 1;                 // kx stride of the x-pass spectrum layout A[c][z][y][kx] (Hx rounded up to 4)
   size_t nspec = 0;            // Hx * Ny * Nz complex per component
+  size_t nspecA = 0;           // HxA * Ny * Nz
   int device = 0;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
@@ -101,7 +112,7 @@ struct fgd_ctx {
   double* Cc = nullptr;        // 9 * nvox compact tangent [n, ca, cb, cc] (fgd_constitutive)
   int compact = 0;             // 1: the CG uses Cc, 0: C
   bool tangent_set = false;
-  double2* specA = nullptr;    // 6 * nspec
+  double2* specA = nullptr;    // 6 * nspecA, layout A (see aidx)
   double2* specB = nullptr;    // 6 * nspec
   double* cg_x = nullptr;      // 6 * nvox
   double* cg_r = nullptr;
@@ -205,6 +216,7 @@ fgd_status launch_err(fgd_ctx* c, const double* eps, const double* eps_prev, con
                       const double* abar_old, unsigned long long* maxbits);
 fgd_status launch_dot(fgd_ctx* c, size_t n, const double* a, const double* b, int op, int slot);
 fgd_status launch_axpy(fgd_ctx* c, size_t n, double* y, const double* x, double s);
+fgd_status launch_axpy_alpha(fgd_ctx* c, size_t n, double* y, const double* x);   // y += sc->alpha x
 fgd_status launch_init_iterate(fgd_ctx* c, const double* eps_n, double* eps, const double* dE6_dev);
 fgd_status launch_phase_count(fgd_ctx* c, const uint8_t* ph, unsigned long long* cnt, int nph, int* bad);
 fgd_status launch_expand_tangent(fgd_ctx* c, const double* Cc, double* Cp);
@@ -213,14 +225,15 @@ fgd_status launch_expand_tangent(fgd_ctx* c, const double* Cc, double* Cp);
 enum XFwdMode : int {
   XF_PLAIN = 0,        // tau_c = in0[c]
   XF_TANGENT = 1,      // tau = C : in0
-  XF_TANGENT_CG = 2,   // p = r(in0) + beta p(out0); tau = C p; write p; reduce p.tau
+  XF_TANGENT_CG = 2,   // x(io1) += alpha p(out0) [previous step]; p = r(in0) + beta p; tau = C p; write p, x;
+                       // reduce p.tau
   XF_HELM_UPDATE = 3,  // x(out0) += alpha p(in0); r(io) -= alpha q(in1); tau = r ; reduce r.r
   XF_PLAIN_RED = 4,    // tau_c = in0[c]; reduce sum_c tau_c (means)
 };
 enum ZMode : int { Z_PROJECT = 0, Z_PRECOND = 1 };
 enum XInvMode : int {
   XI_STORE = 0,        // out0 = q
-  XI_MECH_CG = 1,      // x(io1) += alpha p(in3); r(io2) -= alpha q ; reduce r.r
+  XI_MECH_CG = 1,      // r(io2) -= alpha q ; reduce r.r   (x is updated one step late, in XF_TANGENT_CG)
   XI_HELM_Z = 2,       // z(out0) = q ; reduce r(in3).q
   XI_STORE_RR = 3,     // out0 = q ; reduce q.q
 };

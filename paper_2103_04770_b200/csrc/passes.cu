@@ -13,14 +13,17 @@
 // the 1/N of F^-1 is folded into it.  x-fwd producers: plain load, tangent contraction
 // tau = C:p, the CG direction update p = r + beta p with p.Cp, or the PCG
 // x/r update.  x-inv epilogues: store, or the CG update x += alpha p, r -= alpha q with r.r.
+#include <cstdlib>
+
 #include "reduce.cuh"
+#include "tma.cuh"
 
 namespace fgd {
 
 constexpr int kMaxThr = 384;
 
 struct XArgs {
-  int Ny, Nz, TY, Hx;
+  int Ny, Nz, TY, HxA;   // HxA: kx stride of layout A
   size_t nvox;
   const double* in0;
   const double* in1;
@@ -58,7 +61,7 @@ __device__ __forceinline__ void tangent_apply(const double* __restrict__ Cp, siz
 // inverse FFT of Z'' is then x[2n] + i x[2n+1] (the 1/N is folded into the spectral multiply).
 // A line holds M complex points (SWZ layout, xline(M) slots) plus the Nyquist slot at SWZ(l, M).
 template <int N>
-__device__ __forceinline__ void r2c_post(double2* line, int l, int k, const double2* __restrict__ twN) {
+__device__ __forceinline__ void r2c_post(double2* line, int l, int k, const double2* twN) {
   constexpr int M = N / 2;
   if (k == 0) {
     const double2 z = line[SWZ(l, 0)];
@@ -69,7 +72,7 @@ __device__ __forceinline__ void r2c_post(double2* line, int l, int k, const doub
   const double2 zk = line[SWZ(l, k)], zm = line[SWZ(l, M - k)];
   const double2 E = make_double2(0.5 * (zk.x + zm.x), 0.5 * (zk.y - zm.y));
   const double2 O = make_double2(0.5 * (zk.y + zm.y), -0.5 * (zk.x - zm.x));
-  const double2 WO = cmul(__ldg(&twN[k]), O);
+  const double2 WO = cmul(twN[k], O);   // twN: global or shared table
   line[SWZ(l, k)] = cadd(E, WO);
   if (k != M - k) line[SWZ(l, M - k)] = conjg(csub(E, WO));
 }
@@ -103,7 +106,10 @@ __global__ void __launch_bounds__(kMaxThr, 2) k_xfwd(XArgs a, const double2* __r
   double* smd = reinterpret_cast<double*>(sm);
   double red[1] = {0.0};
   double beta = 0.0, alpha = 0.0;
-  if (MODE == XF_TANGENT_CG) beta = a.sc->beta;
+  if (MODE == XF_TANGENT_CG) {
+    beta = a.sc->beta;
+    alpha = a.sc->alpha;
+  }
   if (MODE == XF_HELM_UPDATE) alpha = a.sc->alpha;
   for (int idx = threadIdx.x; idx < TY * N; idx += blockDim.x) {
     const int yy = idx / N, x = idx % N;
@@ -119,9 +125,15 @@ __global__ void __launch_bounds__(kMaxThr, 2) k_xfwd(XArgs a, const double2* __r
       if (a.compact) tangent_apply_c(a.Cp, g, n, p, tau);
       else tangent_apply(a.Cp, g, n, p, tau);
     } else if (MODE == XF_TANGENT_CG) {
+      // CG with the solution update one step late: x += alpha_{k-1} p_{k-1} here (p_{k-1} is read
+      // anyway), so that the inverse pass only touches r.  cg_mech adds the last alpha p at the end.
       double p[6];
 #pragma unroll
-      for (int c = 0; c < 6; ++c) p[c] = fma(beta, a.out0[c * n + g], a.in0[c * n + g]);
+      for (int c = 0; c < 6; ++c) {
+        const double po = a.out0[c * n + g];
+        a.io1[c * n + g] = fma(alpha, po, a.io1[c * n + g]);
+        p[c] = fma(beta, po, a.in0[c * n + g]);
+      }
 #pragma unroll
       for (int c = 0; c < 6; ++c) a.out0[c * n + g] = p[c];
       if (a.compact) tangent_apply_c(a.Cp, g, n, p, tau);
@@ -151,14 +163,187 @@ __global__ void __launch_bounds__(kMaxThr, 2) k_xfwd(XArgs a, const double2* __r
   }
   __syncthreads();
   const int Hx = M + 1;
+  constexpr int NB = (Hx + kKB - 1) / kKB;
 #pragma unroll 4
-  for (int idx = threadIdx.x; idx < NC * Hx * TY; idx += blockDim.x) {
-    const int yy = idx % TY;
-    const int rest = idx / TY;
-    const int kx = rest % Hx, c = rest / Hx;
-    a.spec[((size_t)(c * a.Nz + z) * Hx + kx) * a.Ny + y0 + yy] = sm[(c * TY + yy) * LP + SWZ(c * TY + yy, kx)];
+  for (int idx = threadIdx.x; idx < NC * NB * TY * kKB; idx += blockDim.x) {
+    // order (kx % kKB, yy, kx / kKB, c): runs of TY * kKB contiguous elements of layout A
+    const int kl = idx % kKB, yy = (idx / kKB) % TY, rest = idx / (kKB * TY);
+    const int kx = (rest % NB) * kKB + kl, c = rest / NB;
+    if (kx < Hx) a.spec[aidx(a.HxA, a.Ny, a.Nz, c, z, y0 + yy, kx)] = sm[(c * TY + yy) * LP + SWZ(c * TY + yy, kx)];
   }
   if (MODE == XF_TANGENT_CG || MODE == XF_HELM_UPDATE) reduce_finalize<1>(red, a.partials, a.sc, a.red_op, a.red_slot);
+}
+
+// ---------------------------------------------------------------------------------------------
+// Tangent x-forward pass as a persistent bulk-copy (TMA) pipeline
+// ---------------------------------------------------------------------------------------------
+// A tile is a pair of rows (z, y = 2 yb + {0, 1}) -- the kXR rows of one block of layout A.  The
+// producer operands of a row chunk (CW voxels: r, p, x and the tangent for the CG step; p and the
+// tangent for the plain apply) arrive in a ring of S shared-memory stages by 1-D bulk copies, one
+// per operand row, completing on the stage's mbarrier; S - 1 chunks are in flight while one is
+// consumed.  The consumer updates x and p (CG), contracts tau = C p voxel by voxel into the FFT
+// buffer (12 lines: 6 components x 2 rows), and after the last chunk of the pair runs the R2C
+// line transforms and stores the half spectra as one contiguous block per component.
+struct XTArgs {
+  int Ny, Nz, HxA, CW, S;
+  size_t nvox;
+  const double* r;     // CG: residual (in)
+  double* p;           // CG: direction (in/out); TANGENT: operand (in)
+  double* x;           // CG: solution (in/out, one step late)
+  const double* C;     // tangent, 9 (compact) or 21 (packed) rows of nvox
+  double2* spec;
+  DevScalars* sc;
+  double* partials;
+  int red_op, red_slot;
+  const double2* twM;
+  const double2* twN;
+};
+
+template <int MODE, bool CMP>
+__host__ __device__ constexpr int xt_rows() { return (MODE == XF_TANGENT_CG ? 18 : 6) + (CMP ? 9 : 21); }
+template <int N>
+__host__ __device__ constexpr size_t xt_fixed_bytes() {
+  return 64 + (6 * kXR * (size_t)xline(N / 2) + N / 2 + N) * sizeof(double2);
+}
+
+// tau = C p with the tangent rows in shared memory (stride cs between rows)
+template <bool CMP>
+__device__ __forceinline__ void tangent_smem(const double* C, int v, int cs, const double* p, double* tau) {
+  if (CMP) {
+    double nv[6];
+#pragma unroll
+    for (int i = 0; i < 6; ++i) nv[i] = C[i * cs + v];
+    const double ca = C[6 * cs + v], cb = C[7 * cs + v], cc = C[8 * cs + v];
+    const double tr = ca * (p[0] + p[1] + p[2]);
+    double np = 0.0;
+#pragma unroll
+    for (int i = 0; i < 6; ++i) np = fma(nv[i], p[i], np);
+    np *= cc;
+#pragma unroll
+    for (int i = 0; i < 6; ++i) tau[i] = fma(cb, p[i], fma(-np, nv[i], i < 3 ? tr : 0.0));
+  } else {
+    double c[21];
+#pragma unroll
+    for (int t = 0; t < 21; ++t) c[t] = C[t * cs + v];
+    tau[0] = c[0] * p[0] + c[1] * p[1] + c[2] * p[2] + c[3] * p[3] + c[4] * p[4] + c[5] * p[5];
+    tau[1] = c[1] * p[0] + c[6] * p[1] + c[7] * p[2] + c[8] * p[3] + c[9] * p[4] + c[10] * p[5];
+    tau[2] = c[2] * p[0] + c[7] * p[1] + c[11] * p[2] + c[12] * p[3] + c[13] * p[4] + c[14] * p[5];
+    tau[3] = c[3] * p[0] + c[8] * p[1] + c[12] * p[2] + c[15] * p[3] + c[16] * p[4] + c[17] * p[5];
+    tau[4] = c[4] * p[0] + c[9] * p[1] + c[13] * p[2] + c[16] * p[3] + c[18] * p[4] + c[19] * p[5];
+    tau[5] = c[5] * p[0] + c[10] * p[1] + c[14] * p[2] + c[17] * p[3] + c[19] * p[4] + c[20] * p[5];
+  }
+}
+
+template <int N, int MODE, bool CMP>
+__global__ void __launch_bounds__(128) k_xtan(XTArgs a) {
+  constexpr int M = N / 2, Hx = M + 1;
+  constexpr int LP = xline(M);
+  constexpr int NOP = xt_rows<MODE, CMP>();
+  constexpr int C0 = MODE == XF_TANGENT_CG ? 18 : 6;   // first tangent row
+  extern __shared__ __align__(16) unsigned char smraw[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smraw);                  // [S], S <= 8
+  double2* fb = reinterpret_cast<double2*>(smraw + 64);                // FFT buffer: 12 lines of LP
+  double2* twM = fb + 6 * kXR * LP;
+  double2* twN = twM + M;
+  double* stg = reinterpret_cast<double*>(twN + N);                    // [S][NOP][CW]
+  const int CW = a.CW, S = a.S;
+  const int nch = N / CW;
+  const int ntiles = a.Nz * (a.Ny / kXR);
+  const size_t n = a.nvox;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+  }
+  build_pass_tables<M>(twM, a.twM);
+  load_table(twN, a.twN, N);
+  __syncthreads();
+  const int myrows = (int)blockIdx.x < ntiles ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+  // chunk q: tile t = blockIdx.x + (q / (kXR nch)) gridDim.x, row rr = (q / nch) % kXR, part h = q % nch
+  const int nq = myrows * nch * kXR;
+  auto issue = [&](int q) {      // warp 0
+    const int t = blockIdx.x + (q / (kXR * nch)) * gridDim.x, rr = (q / nch) % kXR, h = q % nch;
+    const size_t g0 = ((size_t)t * kXR + rr) * N + (size_t)h * CW;   // row z Ny + kXR yb + rr
+    double* dst = stg + (size_t)(q % S) * NOP * CW;
+    uint64_t* bar = &bars[q % S];
+    const unsigned bytes = CW * 8;
+    if (threadIdx.x == 0) {
+      fence_proxy_async();
+      mbar_arrive_expect_tx(bar, bytes * NOP);
+    }
+    __syncwarp();
+    for (int i = threadIdx.x; i < NOP; i += 32) {
+      const double* src;
+      if (MODE == XF_TANGENT_CG)
+        src = i < 6 ? a.r + i * n : i < 12 ? a.p + (i - 6) * n : i < 18 ? a.x + (i - 12) * n : a.C + (i - 18) * n;
+      else
+        src = i < 6 ? a.p + i * n : a.C + (i - 6) * n;
+      bulk_g2s(dst + (size_t)i * CW, src + g0, bytes, bar);
+    }
+  };
+  if (threadIdx.x < 32)
+    for (int q = 0; q < S - 1 && q < nq; ++q) issue(q);
+  double beta = 0.0, alpha = 0.0;
+  if (MODE == XF_TANGENT_CG) {
+    beta = a.sc->beta;
+    alpha = a.sc->alpha;
+  }
+  double red = 0.0;
+  double* fbd = reinterpret_cast<double*>(fb);
+  for (int q = 0; q < nq; ++q) {
+    // refill the stage consumed at q - 1 (released by the barriers at the end of that iteration)
+    if (threadIdx.x < 32 && q + S - 1 < nq) issue(q + S - 1);
+    mbar_wait(&bars[q % S], (q / S) & 1);
+    const int t = blockIdx.x + (q / (kXR * nch)) * gridDim.x, rr = (q / nch) % kXR, h = q % nch;
+    const double* st = stg + (size_t)(q % S) * NOP * CW;
+    for (int v = threadIdx.x; v < CW; v += blockDim.x) {
+      const int xg = h * CW + v;
+      const size_t g = ((size_t)t * kXR + rr) * N + xg;
+      double p[6], tau[6];
+      if (MODE == XF_TANGENT_CG) {
+        // CG with the solution update one step late (x += alpha_{k-1} p_{k-1}); see cg_mech
+#pragma unroll
+        for (int c = 0; c < 6; ++c) {
+          const double po = st[(6 + c) * CW + v];
+          a.x[c * n + g] = fma(alpha, po, st[(12 + c) * CW + v]);
+          p[c] = fma(beta, po, st[c * CW + v]);
+          a.p[c * n + g] = p[c];
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < 6; ++c) p[c] = st[c * CW + v];
+      }
+      tangent_smem<CMP>(st + C0 * CW, v, CW, p, tau);
+#pragma unroll
+      for (int c = 0; c < 6; ++c) {
+        if (MODE == XF_TANGENT_CG) red = fma(p[c], tau[c], red);
+        const int l = c * kXR + rr;
+        fbd[(size_t)(l * LP + SWZ(l, xg >> 1)) * 2 + (xg & 1)] = tau[c];
+      }
+    }
+    __syncthreads();
+    if (rr == kXR - 1 && h == nch - 1) {
+      fft_lines<M, false>(fb, 6 * kXR, LP, twM);
+      __syncthreads();
+      for (int idx = threadIdx.x; idx < 6 * kXR * (M / 2 + 1); idx += blockDim.x) {
+        const int k = idx % (M / 2 + 1), l = idx / (M / 2 + 1);
+        r2c_post<N>(fb + (size_t)l * LP, l, k, twN);
+      }
+      __syncthreads();
+      const int z = t / (a.Ny / kXR), yb = t % (a.Ny / kXR);
+      constexpr int NB = (Hx + kKB - 1) / kKB;   // kx blocks holding data
+      for (int idx = threadIdx.x; idx < 6 * NB * kXR * kKB; idx += blockDim.x) {
+        // order (kx % kKB, row, kx / kKB, c): runs of kXR * kKB contiguous elements
+        const int kl = idx % kKB, r2 = (idx / kKB) % kXR, kb = (idx / (kKB * kXR)) % NB, c = idx / (kKB * kXR * NB);
+        const int kx = kb * kKB + kl, l = c * kXR + r2;
+        if (kx < Hx) a.spec[aidx(a.HxA, a.Ny, a.Nz, c, z, yb * kXR + r2, kx)] = fb[l * LP + SWZ(l, kx)];
+      }
+      __syncthreads();
+    }
+  }
+  if (MODE == XF_TANGENT_CG) {
+    double rr[1] = {red};
+    reduce_finalize<1>(rr, a.partials, a.sc, a.red_op, a.red_slot);
+  }
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -215,6 +400,72 @@ static fgd_status launch(fgd_ctx* c, K kernel, dim3 grid, int threads, size_t sm
     default: return set_err(c, FGD_EINVAL, "unsupported FFT length"); \
   }
 
+static int sm_count() {
+  static int s = 0;
+  if (!s) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&s, cudaDevAttrMultiProcessorCount, dev);
+    if (s <= 0) s = 148;
+  }
+  return s;
+}
+
+// returns FGD_OK and *done = false when the bulk-copy path does not apply (alignment, N > 512)
+static fgd_status launch_xtan(fgd_ctx* c, int mode, const double* r, double* p, double* x, const double* Cp,
+                              int red_op, int red_slot, bool* done) {
+  *done = false;
+  const int Nx = c->n[0];
+  const bool cmp = Cp == c->Cc;
+  auto al = [](const void* q) { return ((uintptr_t)q & 15) == 0; };
+  if (!al(p) || !al(Cp) || (mode == XF_TANGENT_CG && (!al(r) || !al(x)))) return FGD_OK;
+  static const int cw_env = [] {
+    const char* e = std::getenv("FGD_XT_CW");
+    return e ? std::atoi(e) : 128;
+  }();
+  const int CW = std::min(Nx, std::max(16, cw_env));
+  const int nop = (mode == XF_TANGENT_CG ? 18 : 6) + (cmp ? 9 : 21);
+  const size_t stage = (size_t)nop * CW * 8;
+  size_t fixed = 0;
+#define XTF(NN) fixed = xt_fixed_bytes<NN>();
+  FGD_DISPATCH_N(Nx, XTF)
+#undef XTF
+  // as many stages (2..4) as leave room for two CTAs per SM
+  const size_t budget = 112 * 1024;
+  int S = (int)std::min<size_t>(4, budget > fixed ? (budget - fixed) / stage : 0);
+  if (S < 2) S = 2;
+  const size_t smem = fixed + S * stage;
+  if (smem > 227 * 1024) return FGD_OK;
+  XTArgs a{c->n[1], c->nz_l, c->HxA, CW, S, c->nvox, r, p, x, Cp, c->specA, c->sc, c->partials, red_op, red_slot,
+           c->tabs.tw[ilog2(Nx / 2)], c->tabs.tw[ilog2(Nx)]};
+  const int ntiles = (c->n[1] / kXR) * c->nz_l;
+  KTimer kt(c, KC_XFWD6);
+  int grid = 1;
+#define XTL(NN)                                                                                       \
+  {                                                                                                   \
+    auto kern = mode == XF_TANGENT_CG ? (cmp ? k_xtan<NN, XF_TANGENT_CG, true> : k_xtan<NN, XF_TANGENT_CG, false>) \
+                                      : (cmp ? k_xtan<NN, XF_TANGENT, true> : k_xtan<NN, XF_TANGENT, false>);     \
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);          \
+    if (e != cudaSuccess) return set_err(c, FGD_ECUDA, std::string("k_xtan smem attr: ") + cudaGetErrorString(e)); \
+    int occ = 0;                                                                                      \
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 128, smem) != cudaSuccess || occ < 1) occ = 1; \
+    grid = std::max(1, std::min(ntiles, sm_count() * occ));                                           \
+    if (red_op != RED_NONE) {                                                                         \
+      fgd_status s_ = ensure_partials(c, (size_t)grid);                                               \
+      if (s_ != FGD_OK) return s_;                                                                    \
+      a.partials = c->partials;                                                                       \
+    }                                                                                                 \
+    c->launches++;                                                                                    \
+    kern<<<grid, 128, smem, c->stream>>>(a);                                                          \
+    e = cudaGetLastError();                                                                           \
+    if (e != cudaSuccess) return set_err(c, FGD_ECUDA, std::string("k_xtan: ") + cudaGetErrorString(e));         \
+  }
+  FGD_DISPATCH_N(Nx, XTL)
+#undef XTL
+  *done = true;
+  return FGD_OK;
+}
+
 fgd_status launch_xfwd(fgd_ctx* c, int ncomp, int mode, const double* in0, const double* in1, double* out0,
                        const double* Cp, int red_op, int red_slot) {
   return launch_xfwd_io(c, ncomp, mode, in0, in1, out0, nullptr, Cp, red_op, red_slot);
@@ -223,13 +474,20 @@ fgd_status launch_xfwd(fgd_ctx* c, int ncomp, int mode, const double* in0, const
 fgd_status launch_xfwd_io(fgd_ctx* c, int ncomp, int mode, const double* in0, const double* in1, double* out0,
                           double* io1, const double* Cp, int red_op, int red_slot) {
   if (mode == XF_PLAIN && ((uintptr_t)in0 & 15) == 0) return pipe_xfwd_plain(c, ncomp, in0);
+  if (ncomp == 6 && (mode == XF_TANGENT || mode == XF_TANGENT_CG) && !std::getenv("FGD_NO_XTAN")) {
+    bool done = false;
+    fgd_status s = mode == XF_TANGENT_CG ? launch_xtan(c, mode, in0, out0, io1, Cp, red_op, red_slot, &done)
+                                         : launch_xtan(c, mode, nullptr, const_cast<double*>(in0), nullptr, Cp,
+                                                       red_op, red_slot, &done);
+    if (s != FGD_OK || done) return s;
+  }
   const int Nx = c->n[0], Ny = c->n[1], Nz = c->nz_l;
   const int TY = choose_TY(Nx, ncomp, Ny);
   const int nl = ncomp * TY;
   const int thr = std::min(kMaxThr, std::max(64, round32(nl * fft_TPL(Nx / 2))));
   const size_t smem = ((size_t)nl * xline(Nx / 2) + Nx / 2) * sizeof(double2);
   dim3 grid(Ny / TY, Nz);
-  XArgs a{Ny, Nz, TY, c->Hx, c->nvox, in0, in1, out0, io1, nullptr, Cp, c->specA, c->sc, c->partials, red_op, red_slot,
+  XArgs a{Ny, Nz, TY, c->HxA, c->nvox, in0, in1, out0, io1, nullptr, Cp, c->specA, c->sc, c->partials, red_op, red_slot,
           (Cp != nullptr && Cp == c->Cc) ? 1 : 0};
   if (red_op != RED_NONE) {
     fgd_status s = ensure_partials(c, (size_t)grid.x * grid.y);

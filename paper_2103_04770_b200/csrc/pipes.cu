@@ -7,10 +7,12 @@
 // the number of CTAs the device keeps resident (SMs x occupancy).
 //
 // Passes (same layouts as passes.cu):
-//   YP    C2C along y, A[c][z][kx][y] <-> B[c][kx][ky][z]        tile (c, kx, TZ z's)
+//   YP    C2C along y, A[c][z][y][kx] <-> B[c][kx][ky][z]        tile (c, TK kx's, TZ z's)
 //   ZP    C2C along z in place on B with the spectral multiply  tile (kx, TL ky's), NC comps
 //   XI    C2R along x, one component per tile, with epilogue    tile (c, z, TY rows)
 //   XF    R2C along x of a plain real field, one comp per tile  tile (c, z, TY rows)
+#include <cstdlib>
+
 #include "reduce.cuh"
 
 namespace fgd {
@@ -82,29 +84,44 @@ __device__ __forceinline__ size_t r_index(const SlabL& L, int C, int Hx, int c, 
   return slab_index(L, C, Hx, c, kx, ky >> L.lg_nys, z >> L.lg_nzs, ky & (L.nys - 1), z & (L.nzs - 1));
 }
 
+// A y-pass tile holds TK = kKB consecutive kx (one contiguous kKB * Ny run per plane of layout A) times TZ consecutive
+// z (runs of TZ * 16 B in B, z fastest); line l = zz * TK + kk.  kx >= Hx (padding of the last kx
+// block, HxA = Hx rounded up to 4) is neither loaded nor stored.
 struct YArgs {
   double2* A;
   double2* B;
-  int Nz, Hx, TZ, ncomp, lgTZ;
+  int Nz, Hx, HxA, TZ, TK, ncomp, lgTZ, lgTK;
   const double2* tw;
   SlabL L;
 };
 
+struct YTile {
+  int c, kx0, z0;
+};
+__device__ __forceinline__ YTile y_tile(const YArgs& a, int t) {
+  const int nzt = a.Nz / a.TZ, nkb = a.HxA / a.TK;
+  const int zt = t % nzt, r = t / nzt;
+  return YTile{r / nkb, (r % nkb) * a.TK, zt * a.TZ};
+}
+
 template <int N, bool INV>
 __device__ __forceinline__ void y_issue(const YArgs& a, int t, double2* buf) {
   constexpr int LP = cline(N);
-  const int nzt = a.Nz / a.TZ;
-  const int zt = t % nzt, r = t / nzt, kx = r % a.Hx, c = r / a.Hx;
-  const int z0 = zt * a.TZ, TZ = a.TZ;
+  const YTile T = y_tile(a, t);
+  const int TZ = a.TZ, TK = a.TK;
   if (!INV) {
-    for (int idx = threadIdx.x; idx < TZ * N; idx += blockDim.x) {
-      const int zz = idx / N, y = idx % N;
-      cp_async16(&buf[zz * LP + SWZ(zz, y)], &a.A[((size_t)(c * a.Nz + z0 + zz) * a.Hx + kx) * N + y]);
+    for (int idx = threadIdx.x; idx < TZ * TK * N; idx += blockDim.x) {
+      // order (kk, y, zz): contiguous runs of TK * N elements in layout A when TK = kKB
+      const int kk = idx & (TK - 1), y = (idx >> a.lgTK) & (N - 1), zz = idx >> (a.lgTK + ilog2(N));
+      const int kx = T.kx0 + kk, l = zz * TK + kk;
+      if (kx < a.Hx) cp_async16(&buf[l * LP + SWZ(l, y)], &a.A[aidx(a.HxA, N, a.Nz, T.c, T.z0 + zz, y, kx)]);
     }
   } else {
-    for (int idx = threadIdx.x; idx < TZ * N; idx += blockDim.x) {
-      const int zz = idx & (TZ - 1), ky = idx >> a.lgTZ;
-      cp_async16(&buf[zz * LP + SWZ(zz, ky)], &a.B[s_index(a.L, a.ncomp, a.Hx, c, kx, ky, z0 + zz)]);
+    for (int idx = threadIdx.x; idx < TZ * TK * N; idx += blockDim.x) {
+      const int zz = idx & (TZ - 1), ky = (idx >> a.lgTZ) & (N - 1), kk = idx >> (a.lgTZ + ilog2(N));
+      const int kx = T.kx0 + kk, l = zz * TK + kk;
+      if (kx < a.Hx)
+        cp_async16(&buf[l * LP + SWZ(l, ky)], &a.B[s_index(a.L, a.ncomp, a.Hx, T.c, kx, ky, T.z0 + zz)]);
     }
   }
 }
@@ -113,34 +130,35 @@ template <int N, bool INV>
 __global__ void __launch_bounds__(256, 2) k_ypipe(YArgs a) {
   extern __shared__ double2 sm[];
   constexpr int LP = cline(N);
-  const int TZ = a.TZ;
-  double2* tws = sm + 2 * TZ * LP;
+  const int NL = a.TZ * a.TK;
+  double2* tws = sm + 2 * NL * LP;
   build_pass_tables<N, true>(tws, a.tw);
-  const int ntiles = a.ncomp * a.Hx * (a.Nz / TZ);
+  const int ntiles = a.ncomp * (a.HxA / a.TK) * (a.Nz / a.TZ);
   int t = blockIdx.x;
   if (t < ntiles) y_issue<N, INV>(a, t, sm);
   cp_async_commit();
   for (int i = 0; t < ntiles; ++i, t += gridDim.x) {
     const int tn = t + gridDim.x;
-    if (tn < ntiles) y_issue<N, INV>(a, tn, sm + ((i + 1) & 1) * TZ * LP);
+    if (tn < ntiles) y_issue<N, INV>(a, tn, sm + ((i + 1) & 1) * NL * LP);
     cp_async_commit();
     cp_async_wait<1>();
     __syncthreads();
-    double2* buf = sm + (i & 1) * TZ * LP;
-    fft_lines<N, INV, true>(buf, TZ, LP, tws);
+    double2* buf = sm + (i & 1) * NL * LP;
+    fft_lines<N, INV, true>(buf, NL, LP, tws);
     __syncthreads();
-    const int nzt = a.Nz / TZ;
-    const int zt = t % nzt, r = t / nzt, kx = r % a.Hx, c = r / a.Hx;
-    const int z0 = zt * TZ;
+    const YTile T = y_tile(a, t);
+    const int TZ = a.TZ, TK = a.TK;
     if (!INV) {
-      for (int idx = threadIdx.x; idx < TZ * N; idx += blockDim.x) {
-        const int zz = idx & (TZ - 1), ky = idx >> a.lgTZ;
-        a.B[s_index(a.L, a.ncomp, a.Hx, c, kx, ky, z0 + zz)] = buf[zz * LP + SWZ(zz, ky)];
+      for (int idx = threadIdx.x; idx < TZ * TK * N; idx += blockDim.x) {
+        const int zz = idx & (TZ - 1), ky = (idx >> a.lgTZ) & (N - 1), kk = idx >> (a.lgTZ + ilog2(N));
+        const int kx = T.kx0 + kk, l = zz * TK + kk;
+        if (kx < a.Hx) a.B[s_index(a.L, a.ncomp, a.Hx, T.c, kx, ky, T.z0 + zz)] = buf[l * LP + SWZ(l, ky)];
       }
     } else {
-      for (int idx = threadIdx.x; idx < TZ * N; idx += blockDim.x) {
-        const int zz = idx / N, y = idx % N;
-        a.A[((size_t)(c * a.Nz + z0 + zz) * a.Hx + kx) * N + y] = buf[zz * LP + SWZ(zz, y)];
+      for (int idx = threadIdx.x; idx < TZ * TK * N; idx += blockDim.x) {
+        const int kk = idx & (TK - 1), y = (idx >> a.lgTK) & (N - 1), zz = idx >> (a.lgTK + ilog2(N));
+        const int kx = T.kx0 + kk, l = zz * TK + kk;
+        if (kx < a.Hx) a.A[aidx(a.HxA, N, a.Nz, T.c, T.z0 + zz, y, kx)] = buf[l * LP + SWZ(l, y)];
       }
     }
     __syncthreads();
@@ -158,6 +176,9 @@ struct ZPArgs {
   int Nyl;             // local ky rows
   int Nx, Ny, Hx, TL, scheme, lgTL;
   double h[3], L[3];
+  double qh[3];        // 0.25 / h_j      (host-side reciprocals: no FP64 division in the passes)
+  double qh2[3];       // 1 / (16 h_j^2)
+  double tpl[3];       // 2 pi / L_j
   double scale;
   double shift[6];
   int mask[6];
@@ -176,9 +197,9 @@ __device__ __forceinline__ void zsymbol(const ZPArgs& a, int Nz, int kx, int ky,
                   dz = make_double2(ez.x - 1.0, ez.y);
     const double2 cx = make_double2(ex.x + 1.0, ex.y), cy = make_double2(ey.x + 1.0, ey.y),
                   cz = make_double2(ez.x + 1.0, ez.y);
-    k[0] = cscale(cmul(dx, cmul(cy, cz)), 0.25 / a.h[0]);
-    k[1] = cscale(cmul(cx, cmul(dy, cz)), 0.25 / a.h[1]);
-    k[2] = cscale(cmul(cx, cmul(cy, dz)), 0.25 / a.h[2]);
+    k[0] = cscale(cmul(dx, cmul(cy, cz)), a.qh[0]);
+    k[1] = cscale(cmul(cx, cmul(dy, cz)), a.qh[1]);
+    k[2] = cscale(cmul(cx, cmul(cy, dz)), a.qh[2]);
   } else {
     const int Ns[3] = {a.Nx, a.Ny, Nz};
     const int ms[3] = {kx, ky, kz};
@@ -190,9 +211,28 @@ __device__ __forceinline__ void zsymbol(const ZPArgs& a, int Nz, int kx, int ky,
         k[j] = make_double2(0.0, 0.0);
       } else {
         if (m > Nj / 2) m -= Nj;
-        k[j] = make_double2(0.0, 2.0 * 3.14159265358979323846 * m / a.L[j]);
+        k[j] = make_double2(0.0, a.tpl[j] * m);
       }
     }
+  }
+}
+
+// Per-axis factors of |k|^2.  Willot: f[0] = (2 - 2 cos th) / (16 h^2), f[1] = 2 + 2 cos th, so
+// that |k|^2 = f0x f1y f1z + f1x f0y f1z + f1x f1y f0z.  Continuous: f[0] = (2 pi m / L)^2.
+__device__ __forceinline__ void zaxis(const ZPArgs& a, int j, int m, int Nj, const double2* tw_s, double* f) {
+  if (a.scheme == 1) {
+    const double cs = tw_s ? tw_s[m].x : __ldg(&(j == 0 ? a.twx : a.twy)[m]).x;
+    f[0] = (2.0 - 2.0 * cs) * a.qh2[j];
+    f[1] = 2.0 + 2.0 * cs;
+  } else {
+    if ((Nj % 2 == 0) && m == Nj / 2) {
+      f[0] = 0.0;
+    } else {
+      if (m > Nj / 2) m -= Nj;
+      const double x = a.tpl[j] * m;
+      f[0] = x * x;
+    }
+    f[1] = 0.0;
   }
 }
 
@@ -309,10 +349,132 @@ __global__ void __launch_bounds__(192, 3) k_zpipe(ZPArgs a) {
 }
 
 // ---------------------------------------------------------------------------------------------
+// Z pass for Nz = 256 as a register four-step FFT (256 = 16 x 16)
+// ---------------------------------------------------------------------------------------------
+// A z line is owned by 16 threads (half a warp); n = n1 + 16 n2, k = k2 + 16 k1.
+//   forward: thread t (= n1) loads x[t + 16 j] straight from global memory (256 contiguous bytes
+//   per half warp and j), DFT16 over j in registers, twiddle W256^{t k2}, 16 x 16 transpose
+//   through shared memory, DFT16 -> thread t holds X[t + 16 k1], k1 = 0..15;
+//   inverse: the mirror image, starting from the same "kz = t mod 16" layout and ending with a
+//   coalesced store of z[t + 16 n2].
+// Shared-memory traffic per element: 2 accesses per transform, +4 for the 6-component projection
+// (which mixes the lines of one (kx, ky) and so goes through shared memory), against ~8 per
+// transform for the three-pass Stockham of k_zpipe.  A line occupies 16 rows of 17 slots, so that
+// row and column accesses of the transpose are both free of bank conflicts; the padded position of
+// frequency kz is kz + kz / 16.
+constexpr int kZRowPad = 17;
+constexpr int kZLine = 16 * kZRowPad;
+
+template <int NC, int MODE>
+__global__ void __launch_bounds__(NC == 6 ? 96 : 128) __maxnreg__(NC == 6 ? 128 : 128) k_zreg256(ZPArgs a) {
+  extern __shared__ double2 sm[];
+  constexpr int N = 256;
+  const int TL = a.TL;
+  const int nl = NC * TL;                       // blockDim.x == 16 * nl
+  double2* tw = sm + (size_t)nl * kZLine;       // W256^{t k2} at (k2 - 1) * 16 + t
+  double2* tws = tw + 240;                      // e^{-2 pi i m / 256} (symbol)
+  for (int i = threadIdx.x; i < 240; i += blockDim.x) tw[i] = __ldg(&a.twz[(i & 15) * (1 + (i >> 4))]);
+  load_table(tws, a.twz, N);
+  __syncthreads();
+  const int line = threadIdx.x >> 4, t = threadIdx.x & 15;
+  const int c = line >> a.lgTL, ll = line & (TL - 1);
+  double2* ls = sm + (size_t)line * kZLine;
+  const int nyt = a.Nyl / TL;
+  const int ntiles = a.Hx * nyt;
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int kx = tile / nyt, ky0 = (tile % nyt) * TL;
+    const int kyl = ky0 + ll;
+    // z -> offset from the line start: z-slab block (z >> lg_nzs) of stride BS, then z within it
+    double2* Bl = a.B + r_index(a.SL, NC, a.Hx, c, kx, kyl, 0);
+    const int BS = NC * a.Hx * a.SL.nys * a.SL.nzs, zm = a.SL.nzs - 1, lgz = a.SL.lg_nzs;
+    double2 v[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int z = t + 16 * j;
+      v[j] = __ldcg(Bl + ((z >> lgz) * BS + (z & zm)));
+    }
+    // ---- forward ----
+    dft16<false>(v);
+#pragma unroll
+    for (int k2 = 1; k2 < 16; ++k2) v[k2] = cmul(v[k2], ld_tw(tw + (k2 - 1) * 16 + t));
+    __syncwarp();
+#pragma unroll
+    for (int k2 = 0; k2 < 16; ++k2) ls[k2 * kZRowPad + t] = v[k2];
+    __syncwarp();
+#pragma unroll
+    for (int n1 = 0; n1 < 16; ++n1) v[n1] = ls[t * kZRowPad + n1];
+    dft16<false>(v);                            // v[k1] = X[t + 16 k1]
+    // ---- spectral multiply ----
+    const int ky = kyl + a.ky_off;
+    if (MODE == Z_PRECOND) {
+      // Pointwise multiply, one rolled loop over this thread's own column of the line buffer (no
+      // cross-thread traffic; keeps the 16 divisions out of the unrolled register code).
+      // |k|^2 from per-axis factors (same value as |zsymbol|^2 up to rounding):
+      //   Willot: |k_1|^2 = (2 - 2 cos th1)(2 + 2 cos th2)(2 + 2 cos th3) / (16 h1^2), cyclic;
+      //   continuous: sum_j (2 pi m_j / L_j)^2 with the Nyquist index zeroed (A-06).
+      __syncwarp();
+#pragma unroll
+      for (int k1 = 0; k1 < 16; ++k1) ls[k1 * kZRowPad + t] = v[k1];
+      double fx[2], fy[2];
+      zaxis(a, 0, kx, a.Nx, nullptr, fx);
+      zaxis(a, 1, ky, a.Ny, nullptr, fy);
+#pragma unroll 1
+      for (int k1 = 0; k1 < 16; ++k1) {
+        double fz[2];
+        zaxis(a, 2, t + 16 * k1, N, tws, fz);
+        const double k2 = a.scheme == 1 ? (fx[0] * fy[1] * fz[1] + fx[1] * fy[0] * fz[1] + fx[1] * fy[1] * fz[0])
+                                        : fx[0] + fy[0] + fz[0];
+        ls[k1 * kZRowPad + t] = cscale(ls[k1 * kZRowPad + t], a.scale / (1.0 + a.mean_ell2 * k2));
+      }
+#pragma unroll
+      for (int k1 = 0; k1 < 16; ++k1) v[k1] = ls[k1 * kZRowPad + t];
+    } else {
+      __syncwarp();
+#pragma unroll
+      for (int k1 = 0; k1 < 16; ++k1) ls[k1 * kZRowPad + t] = v[k1];
+      __syncthreads();
+      for (int idx = threadIdx.x; idx < TL * N; idx += blockDim.x) {
+        const int kz = idx & (N - 1), l2 = idx >> 8;
+        const int kyg = ky0 + l2 + a.ky_off;
+        double2 k[3];
+        zsymbol(a, N, kx, kyg, kz, k, tws);
+        double2* pv[6];
+#pragma unroll
+        for (int cc = 0; cc < 6; ++cc) pv[cc] = &sm[(size_t)(cc * TL + l2) * kZLine + kz + (kz >> 4)];
+        project6(a, pv, k, kx == 0 && kyg == 0 && kz == 0);
+      }
+      __syncthreads();
+#pragma unroll
+      for (int k1 = 0; k1 < 16; ++k1) v[k1] = ls[k1 * kZRowPad + t];
+    }
+    // ---- inverse ----
+    dft16<true>(v);                             // v[n1] = U[k2 = t][n1]
+#pragma unroll
+    for (int n1 = 1; n1 < 16; ++n1) {
+      double2 w = ld_tw(tw + (n1 - 1) * 16 + t);
+      w.y = -w.y;
+      v[n1] = cmul(v[n1], w);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int n1 = 0; n1 < 16; ++n1) ls[n1 * kZRowPad + t] = v[n1];
+    __syncwarp();
+#pragma unroll
+    for (int k2 = 0; k2 < 16; ++k2) v[k2] = ls[t * kZRowPad + k2];
+    dft16<true>(v);                             // v[n2] = z[t + 16 n2]
+#pragma unroll
+    for (int n2 = 0; n2 < 16; ++n2) {
+      const int z = t + 16 * n2;
+      Bl[(z >> lgz) * BS + (z & zm)] = v[n2];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
 // X passes, one component per tile
 // ---------------------------------------------------------------------------------------------
 struct XPArgs {
-  int Ny, Nz, TY, ncomp, lgTY;
+  int Ny, Nz, TY, ncomp, lgTY, HxA;
   size_t nvox;
   double2* spec;
   const double* in0;   // XF: real input ; XI: p (MECH_CG) or r (HELM_Z)
@@ -326,16 +488,28 @@ struct XPArgs {
   const double2* twN;
 };
 
-template <int N>
-__device__ __forceinline__ void xi_issue(const XPArgs& a, int t, double2* buf) {
+// Modes whose epilogue reads one real operand row per output row (MECH_CG: r, HELM_Z: r of the
+// PCG): that operand is staged by cp.async together with the spectrum of the tile.
+template <int MODE>
+__host__ __device__ constexpr bool xi_prefetch() { return MODE == XI_MECH_CG || MODE == XI_HELM_Z; }
+
+template <int N, int MODE>
+__device__ __forceinline__ void xi_issue(const XPArgs& a, int t, double2* buf, double* ebuf) {
   constexpr int M = N / 2, Hx = M + 1;
   constexpr int LP = xline(M);
   const int TY = a.TY, nyt = a.Ny / TY;
   const int yt = t % nyt, r = t / nyt, z = r % a.Nz, c = r / a.Nz;
   const int y0 = yt * TY;
-  for (int idx = threadIdx.x; idx < Hx * TY; idx += blockDim.x) {
-    const int yy = idx & (TY - 1), kx = idx >> a.lgTY;
-    cp_async16(&buf[yy * LP + SWZ(yy, kx)], &a.spec[((size_t)(c * a.Nz + z) * Hx + kx) * a.Ny + y0 + yy]);
+  constexpr int NB = (Hx + kKB - 1) / kKB;
+  for (int idx = threadIdx.x; idx < NB * TY * kKB; idx += blockDim.x) {
+    // order (kx % kKB, yy, kx / kKB): runs of TY * kKB contiguous elements of layout A
+    const int kl = idx % kKB, yy = (idx / kKB) & (TY - 1), kx = (idx / kKB >> a.lgTY) * kKB + kl;
+    if (kx < Hx) cp_async16(&buf[yy * LP + SWZ(yy, kx)], &a.spec[aidx(a.HxA, a.Ny, a.Nz, c, z, y0 + yy, kx)]);
+  }
+  if constexpr (xi_prefetch<MODE>()) {
+    // rows y0 .. y0 + TY - 1 of plane z are contiguous: TY * N doubles
+    const double* src = (MODE == XI_MECH_CG ? a.io2 : a.in0) + (size_t)c * a.nvox + ((size_t)z * a.Ny + y0) * N;
+    for (int idx = threadIdx.x; idx < TY * N / 2; idx += blockDim.x) cp_async16(ebuf + 2 * idx, src + 2 * idx);
   }
 }
 
@@ -347,6 +521,7 @@ __global__ void __launch_bounds__(128, 4) k_xipipe(XPArgs a) {
   const int TY = a.TY, nyt = a.Ny / TY;
   double2* twM = sm + 2 * TY * LP;
   double2* twN = twM + M;
+  double* ebuf = reinterpret_cast<double*>(twN + N);   // [2][TY * N] epilogue operand (xi_prefetch)
   build_pass_tables<M>(twM, a.twM);
   load_table(twN, a.twN, N);
   const int ntiles = a.ncomp * a.Nz * nyt;
@@ -355,11 +530,11 @@ __global__ void __launch_bounds__(128, 4) k_xipipe(XPArgs a) {
   double alpha = 0.0;
   if (MODE == XI_MECH_CG) alpha = a.sc->alpha;
   int t = blockIdx.x;
-  if (t < ntiles) xi_issue<N>(a, t, sm);
+  if (t < ntiles) xi_issue<N, MODE>(a, t, sm, ebuf);
   cp_async_commit();
   for (int i = 0; t < ntiles; ++i, t += gridDim.x) {
     const int tn = t + gridDim.x;
-    if (tn < ntiles) xi_issue<N>(a, tn, sm + ((i + 1) & 1) * TY * LP);
+    if (tn < ntiles) xi_issue<N, MODE>(a, tn, sm + ((i + 1) & 1) * TY * LP, ebuf + ((i + 1) & 1) * TY * N);
     cp_async_commit();
     cp_async_wait<1>();
     __syncthreads();
@@ -374,6 +549,7 @@ __global__ void __launch_bounds__(128, 4) k_xipipe(XPArgs a) {
     const int yt = t % nyt, r = t / nyt, z = r % a.Nz, c = r / a.Nz;
     const int y0 = yt * TY;
     const double* bd = reinterpret_cast<const double*>(buf);
+    const double* eb = ebuf + (i & 1) * TY * N;
 #pragma unroll 4
     for (int idx = threadIdx.x; idx < TY * N; idx += blockDim.x) {
       const int yy = idx / N, x = idx % N;
@@ -385,14 +561,12 @@ __global__ void __launch_bounds__(128, 4) k_xipipe(XPArgs a) {
         a.out0[g] = q;
         red[0] = fma(q, q, red[0]);
       } else if (MODE == XI_MECH_CG) {
-        const double p = a.in0[g], xo = a.io1[g], ro = a.io2[g];
-        a.io1[g] = fma(alpha, p, xo);
-        const double rn = fma(-alpha, q, ro);
+        const double rn = fma(-alpha, q, eb[idx]);
         a.io2[g] = rn;
         red[0] = fma(rn, rn, red[0]);
       } else if (MODE == XI_HELM_Z) {
         a.out0[g] = q;
-        red[0] = fma(a.in0[g], q, red[0]);
+        red[0] = fma(eb[idx], q, red[0]);
       }
     }
     __syncthreads();
@@ -445,9 +619,10 @@ __global__ void __launch_bounds__(128, 4) k_xfpipe(XPArgs a) {
     __syncthreads();
     const int yt = t % nyt, r = t / nyt, z = r % a.Nz, c = r / a.Nz;
     const int y0 = yt * TY;
-    for (int idx = threadIdx.x; idx < Hx * TY; idx += blockDim.x) {
-      const int yy = idx & (TY - 1), kx = idx >> a.lgTY;
-      a.spec[((size_t)(c * a.Nz + z) * Hx + kx) * a.Ny + y0 + yy] = buf[yy * LP + SWZ(yy, kx)];
+    constexpr int NB = (Hx + kKB - 1) / kKB;
+    for (int idx = threadIdx.x; idx < NB * TY * kKB; idx += blockDim.x) {
+      const int kl = idx % kKB, yy = (idx / kKB) & (TY - 1), kx = (idx / kKB >> a.lgTY) * kKB + kl;
+      if (kx < Hx) a.spec[aidx(a.HxA, a.Ny, a.Nz, c, z, y0 + yy, kx)] = buf[yy * LP + SWZ(yy, kx)];
     }
     __syncthreads();
   }
@@ -524,12 +699,23 @@ static SlabL slab_layout(const fgd_ctx* c) {
 fgd_status pipe_y(fgd_ctx* c, int ncomp, bool inv) {
   const int Ny = c->n[1], Nz = c->nz_l;
   const int TPL = fft_TPL(Ny, true);
-  int TZ = p2floor(std::max(1, 128 / TPL));
-  TZ = std::min(TZ, std::min(Nz, c->n[2] / c->P));
-  const int thr = std::min(256, r32(TZ * TPL));
-  const size_t smem = (2 * (size_t)TZ * cline(Ny) + Ny) * sizeof(double2);
-  const int ntiles = ncomp * c->Hx * (Nz / TZ);
-  YArgs a{c->specA, c->specB, Nz, c->Hx, TZ, ncomp, ilog2(TZ), c->tabs.tw[ilog2(Ny)], slab_layout(c)};
+  static const int nl_env = [] {
+    const char* e = std::getenv("FGD_YL");
+    return e ? std::atoi(e) : 8;
+  }();
+  static const int tk_env = [] {
+    const char* e = std::getenv("FGD_YTK");
+    return e ? std::atoi(e) : kKB;
+  }();
+  const int NL = p2floor(std::max(1, std::min(nl_env, 256) * 16 / TPL));   // lines per tile = TZ * TK
+  int TK = p2floor(std::max(1, std::min(std::min(tk_env, NL), 4)));
+  int TZ = std::min(NL / TK, std::min(Nz, c->n[2] / c->P));
+  TK = std::min(NL / TZ, 4);
+  const int thr = std::min(256, r32(TZ * TK * TPL));
+  const size_t smem = (2 * (size_t)TZ * TK * cline(Ny) + Ny) * sizeof(double2);
+  const int ntiles = ncomp * (c->HxA / TK) * (Nz / TZ);
+  YArgs a{c->specA, c->specB, Nz, c->Hx, c->HxA, TZ, TK, ncomp, ilog2(TZ), ilog2(TK), c->tabs.tw[ilog2(Ny)],
+          slab_layout(c)};
   KTimer kt(c, inv ? (ncomp == 6 ? KC_YINV6 : KC_YINV1) : (ncomp == 6 ? KC_YFWD6 : KC_YFWD1));
 #define YPP(NN)                                                                  \
   if (inv) FGD_PLAUNCH(c, (k_ypipe<NN, true>), thr, smem, ntiles, a);            \
@@ -563,6 +749,9 @@ fgd_status pipe_z(fgd_ctx* c, int ncomp, int mode, double scale, const double* d
   for (int i = 0; i < 3; ++i) {
     a.h[i] = c->h[i];
     a.L[i] = c->L[i];
+    a.qh[i] = 0.25 / c->h[i];
+    a.qh2[i] = 0.0625 / (c->h[i] * c->h[i]);
+    a.tpl[i] = 2.0 * 3.14159265358979323846 / c->L[i];
   }
   a.scale = scale;
   for (int i = 0; i < 6; ++i) {
@@ -574,7 +763,18 @@ fgd_status pipe_z(fgd_ctx* c, int ncomp, int mode, double scale, const double* d
   a.twy = c->tabs.tw[ilog2(Ny)];
   a.twz = c->tabs.tw[ilog2(Nz)];
   KTimer kt(c, ncomp == 6 ? KC_Z6 : KC_Z1);
-#define ZPP(NN)                                                                                          \
+  if (Nz == 256 && ((ncomp == 6 && mode == Z_PROJECT) || (ncomp == 1 && mode == Z_PRECOND))) {
+    const int TLr = std::min(ncomp == 6 ? 1 : 8, Nyl);
+    a.TL = TLr;
+    a.lgTL = ilog2(TLr);
+    const int thr_r = 16 * ncomp * TLr;
+    const size_t smem_r = ((size_t)ncomp * TLr * kZLine + 240 + 256) * sizeof(double2);
+    const int nt_r = c->Hx * (Nyl / TLr);
+    if (ncomp == 6) FGD_PLAUNCH(c, (k_zreg256<6, Z_PROJECT>), thr_r, smem_r, nt_r, a);
+    else FGD_PLAUNCH(c, (k_zreg256<1, Z_PRECOND>), thr_r, smem_r, nt_r, a);
+    return FGD_OK;
+  }
+#define ZPP(NN)                                                                                         \
   if (ncomp == 6 && mode == Z_PROJECT) FGD_PLAUNCH(c, (k_zpipe<NN, 6, Z_PROJECT>), thr, smem, ntiles, a);      \
   else if (ncomp == 1 && mode == Z_PRECOND) FGD_PLAUNCH(c, (k_zpipe<NN, 1, Z_PRECOND>), thr, smem, ntiles, a); \
   else return set_err(c, FGD_EINVAL, "z mode");
@@ -607,9 +807,13 @@ fgd_status pipe_xinv(fgd_ctx* c, int ncomp, int mode, double* out0, double* io1,
   const int Nx = c->n[0], Ny = c->n[1], Nz = c->nz_l;
   const int TY = choose_TYp(Nx, Ny);
   const int thr = std::min(128, r32(TY * fft_TPL(Nx / 2)));
-  const size_t smem = (2 * (size_t)TY * xline(Nx / 2) + Nx / 2 + Nx) * sizeof(double2);
+  const bool pre = mode == XI_MECH_CG || mode == XI_HELM_Z;
+  const size_t smem = (2 * (size_t)TY * xline(Nx / 2) + Nx / 2 + Nx) * sizeof(double2) +
+                      (pre ? 2 * (size_t)TY * Nx * sizeof(double) : 0);
+  const double* eop = mode == XI_MECH_CG ? io2 : in1;
+  if (pre && ((uintptr_t)eop & 15) != 0) return set_err(c, FGD_EINVAL, "xinv: epilogue operand not 16 B aligned");
   const int ntiles = ncomp * Nz * (Ny / TY);
-  XPArgs a{Ny, Nz, TY, ncomp, ilog2(TY), c->nvox, c->specA, in1, out0, io1, io2, c->sc, nullptr, red_op, red_slot,
+  XPArgs a{Ny, Nz, TY, ncomp, ilog2(TY), c->HxA, c->nvox, c->specA, in1, out0, io1, io2, c->sc, nullptr, red_op, red_slot,
            c->tabs.tw[ilog2(Nx / 2)], c->tabs.tw[ilog2(Nx)]};
   if (mode != XI_STORE) {
     fgd_status s = ensure_partials(c, (size_t)num_sms() * 8);
@@ -634,7 +838,7 @@ fgd_status pipe_xfwd_plain(fgd_ctx* c, int ncomp, const double* in0) {
   const int thr = std::min(128, r32(TY * fft_TPL(Nx / 2)));
   const size_t smem = (2 * (size_t)TY * xline(Nx / 2) + Nx / 2 + Nx) * sizeof(double2);
   const int ntiles = ncomp * Nz * (Ny / TY);
-  XPArgs a{Ny, Nz, TY, ncomp, ilog2(TY), c->nvox, c->specA, in0, nullptr, nullptr, nullptr, c->sc, nullptr, RED_NONE, 0,
+  XPArgs a{Ny, Nz, TY, ncomp, ilog2(TY), c->HxA, c->nvox, c->specA, in0, nullptr, nullptr, nullptr, c->sc, nullptr, RED_NONE, 0,
            c->tabs.tw[ilog2(Nx / 2)], c->tabs.tw[ilog2(Nx)]};
   KTimer kt(c, ncomp == 6 ? KC_XFWD6 : KC_XFWD1);
 #define XFP(NN) FGD_PLAUNCH(c, (k_xfpipe<NN>), thr, smem, ntiles, a);

@@ -43,6 +43,7 @@ __device__ __forceinline__ void finalize(DevScalars* sc, int op, int slot, const
       sc->rr = t[0];
       sc->bb = t[0];
       sc->beta = 0.0;
+      sc->alpha = 0.0;
       break;
     case RED_MECH_PQ:
     case RED_HELM_PQ:
