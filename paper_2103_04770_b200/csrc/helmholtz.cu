@@ -51,12 +51,29 @@ __device__ __forceinline__ void corner_flux(const double (&A0)[3][3], const doub
   f[2] = l2 * ih[2] * ((a001 - a000) + (a101 - a100) + (a011 - a010) + (a111 - a110));
 }
 
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit_s() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int K>
+__device__ __forceinline__ void cp_async_wait_s() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(K) : "memory");
+}
+
+// Planes of `a` (and p_old for PCG) arrive in a ring of kRing shared-memory slots by cp.async, up
+// to kRing - 2 planes ahead of the level being computed, so that every SM keeps several planes of
+// loads in flight through the z march.
+constexpr int kRing = 6;
+constexpr int kPlane = (SBY + 2) * (SBX + 2);
+
 template <int MODE>
 __global__ void __launch_bounds__(256, 2) k_stencil(SArgs s, const double* __restrict__ ain, const double* __restrict__ pold,
                                                      double* __restrict__ pout, double* __restrict__ q,
                                                      const uint8_t* __restrict__ phase, DevScalars* sc, double* partials,
                                                      int red_op, int red_slot) {
-  __shared__ double planes[2][SBY + 2][SBX + 2];
+  constexpr int NA = MODE == ST_PCG ? 2 : 1;
+  __shared__ double ring[kRing][NA][kPlane];
   __shared__ double lut[kMaxPhases];
   const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * SBX + tx;
   const int TX = s.TX, TY = s.TY, TZ = s.TZ;
@@ -68,48 +85,55 @@ __global__ void __launch_bounds__(256, 2) k_stencil(SArgs s, const double* __res
   const int gx = x0 + tx, gy = y0 + ty;
   const int xm = wrapi(gx - 1, Nx), ym = wrapi(gy - 1, Ny);
   const double ih[3] = {s.ih[0], s.ih[1], s.ih[2]};
-  // plane elements owned by this thread for staging (at most 2 of (TY+2) x (TX+2) <= 340)
+  // plane elements staged by this thread (at most 2 of (TY+2) x (TX+2) <= 340), stored at the
+  // fixed (SBY+2) x (SBX+2) pitch
   const int PW = TX + 2, PN = (TY + 2) * PW;
   const int i0 = tid, i1 = tid + SBX * SBY;
   const int py0 = i0 / PW, px0 = i0 - py0 * PW, py1 = i1 / PW, px1 = i1 - py1 * PW;
+  const int o0 = py0 * (SBX + 2) + px0, o1 = py1 * (SBX + 2) + px1;
   const size_t r0 = (size_t)wrapi(y0 - 1 + py0, Ny) * Nx + wrapi(x0 - 1 + px0, Nx);
   const size_t r1 = (size_t)wrapi(y0 - 1 + py1, Ny) * Nx + wrapi(x0 - 1 + px1, Nx);
-  double v0 = 0.0, v1 = 0.0;
-  auto gload = [&](int zl) {
-    const double* pa;
-    const double* pp;
-    if (s.dist && zl < 0) {
-      pa = s.a_lo;
-      pp = s.p_lo;
-    } else if (s.dist && zl >= Nz) {
-      pa = s.a_hi;
-      pp = s.p_hi;
-    } else {
-      const size_t base = (size_t)wrapi(zl, Nz) * Ny * Nx;
-      pa = ain + base;
-      pp = pold + base;
+  // plane index pi = 0 .. TZ + 1 <-> level z0 - 1 + pi; one commit group per plane (possibly empty)
+  auto issue = [&](int pi) {
+    if (pi <= TZ + 1) {
+      const int zl = z0 - 1 + pi;
+      const double* pa;
+      const double* pp;
+      if (s.dist && zl < 0) {
+        pa = s.a_lo;
+        pp = s.p_lo;
+      } else if (s.dist && zl >= Nz) {
+        pa = s.a_hi;
+        pp = s.p_hi;
+      } else {
+        const size_t base = (size_t)wrapi(zl, Nz) * Ny * Nx;
+        pa = ain + base;
+        pp = pold + base;
+      }
+      double* d = ring[pi % kRing][0];
+      if (i0 < PN) cp_async8(d + o0, pa + r0);
+      if (i1 < PN) cp_async8(d + o1, pa + r1);
+      if (MODE == ST_PCG) {
+        double* dp = ring[pi % kRing][NA - 1];
+        if (i0 < PN) cp_async8(dp + o0, pp + r0);
+        if (i1 < PN) cp_async8(dp + o1, pp + r1);
+      }
     }
-    if (i0 < PN) {
-      v0 = __ldcs(pa + r0);
-      if (MODE == ST_PCG) v0 = fma(beta, pp[r0], v0);
-    }
-    if (i1 < PN) {
-      v1 = __ldcs(pa + r1);
-      if (MODE == ST_PCG) v1 = fma(beta, pp[r1], v1);
-    }
-  };
-  auto sstore = [&](int b) {
-    if (i0 < PN) planes[b][py0][px0] = v0;
-    if (i1 < PN) planes[b][py1][px1] = v1;
+    cp_async_commit_s();
   };
   double A0[3][3], A1[3][3];      // a at (x-1..x+1, y-1..y+1) of levels z and z+1
   double fp[4][3], fc[4][3];      // fluxes of the 4 corners at levels z-1 (fp) and z (fc)
   double red = 0.0;
-  auto read3 = [&](int b, double (&A)[3][3]) {
+  auto read3 = [&](int pi, double (&A)[3][3]) {
+    const double* pa = ring[pi % kRing][0];
+    const double* pp = ring[pi % kRing][NA - 1];
 #pragma unroll
     for (int dy = 0; dy < 3; ++dy)
 #pragma unroll
-      for (int dx = 0; dx < 3; ++dx) A[dy][dx] = planes[b][ty + dy][tx + dx];
+      for (int dx = 0; dx < 3; ++dx) {
+        const int o = (ty + dy) * (SBX + 2) + tx + dx;
+        A[dy][dx] = MODE == ST_PCG ? fma(beta, pp[o], pa[o]) : pa[o];
+      }
   };
   auto fluxes = [&](int zl, double (&F)[4][3]) {
     const uint8_t* pb = (s.dist && zl < 0) ? s.ph_lo : phase + (size_t)wrapi(zl, Nz) * Ny * Nx;
@@ -121,13 +145,9 @@ __global__ void __launch_bounds__(256, 2) k_stencil(SArgs s, const double* __res
     corner_flux(A0, A1, 0, 1, l01, ih, F[2]);   // corner (x-1, y)
     corner_flux(A0, A1, 1, 1, l11, ih, F[3]);   // corner (x,   y)
   };
-  // warm-up: planes z0-1 (buffer 0) and z0 (buffer 1); fluxes of level z0-1
-  gload(z0 - 1);
-  sstore(0);
-  gload(z0);
-  sstore(1);
+  for (int pi = 0; pi < kRing; ++pi) issue(pi);
+  cp_async_wait_s<kRing - 2>();       // planes 0 and 1 (levels z0 - 1, z0) have landed
   __syncthreads();
-  gload(z0 + 1);                      // prefetch for the first level
   if (act) {
     read3(0, A0);
     read3(1, A1);
@@ -135,16 +155,16 @@ __global__ void __launch_bounds__(256, 2) k_stencil(SArgs s, const double* __res
   }
   for (int zz = 0; zz < TZ; ++zz) {
     const int z = z0 + zz;
-    __syncthreads();                  // everyone is done reading buffer zz & 1 (plane z - 1)
-    sstore(zz & 1);                   // plane z + 1
+    __syncthreads();                  // all threads are done with the slot of plane zz
+    issue(zz + kRing);                // into that slot
+    cp_async_wait_s<kRing - 2>();     // plane zz + 2 (level z + 1) has landed
     __syncthreads();
-    if (zz + 1 < TZ) gload(z + 2);    // next plane in flight while this level computes
     if (act) {
 #pragma unroll
       for (int dy = 0; dy < 3; ++dy)
 #pragma unroll
         for (int dx = 0; dx < 3; ++dx) A0[dy][dx] = A1[dy][dx];
-      read3(zz & 1, A1);
+      read3(zz + 2, A1);
       fluxes(z, fc);
       // D^T gather: corner c = cx + 2 cy (cx = 1 - vx, cy = 1 - vy); level z (vz = 0) / z-1 (vz = 1)
       const double tx_ = (fc[0][0] - fc[1][0]) + (fc[2][0] - fc[3][0]) + (fp[0][0] - fp[1][0]) + (fp[2][0] - fp[3][0]);
@@ -164,6 +184,7 @@ __global__ void __launch_bounds__(256, 2) k_stencil(SArgs s, const double* __res
         for (int j = 0; j < 3; ++j) fp[c][j] = fc[c][j];
     }
   }
+  cp_async_wait_s<0>();
   if (MODE == ST_PCG) {
     double rr[1] = {red};
     reduce_finalize<1>(rr, partials, sc, red_op, red_slot);
@@ -184,7 +205,7 @@ fgd_status launch_stencil(fgd_ctx* c, int field, int mode, const double* a, cons
   s.Nz = c->nz_l;
   s.TX = std::min(SBX, s.Nx);
   s.TY = std::min(SBY, s.Ny);
-  s.TZ = std::min(16, s.Nz);
+  s.TZ = std::min(32, s.Nz);
   s.nvox = c->nvox;
   for (int j = 0; j < 3; ++j) s.ih[j] = 0.25 / c->h[j];
   for (int p = 0; p < kMaxPhases; ++p) s.lut[p] = (p < c->nphases) ? c->ell[field][p] * c->ell[field][p] : 0.0;

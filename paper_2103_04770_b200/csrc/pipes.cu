@@ -471,6 +471,95 @@ __global__ void __launch_bounds__(NC == 6 ? 96 : 128) __maxnreg__(NC == 6 ? 128 
 }
 
 // ---------------------------------------------------------------------------------------------
+// Y pass for Ny = 256 as a register four-step FFT (256 = 16 x 16), as the z pass below
+// ---------------------------------------------------------------------------------------------
+// Tile = (c, kx pair kx0 = kKB kb, TZ planes z0..): 2 TZ lines; warp w handles plane z0 + w, its
+// half warps the two kx of the pair, so that the loads / stores on the A side (kKB x Ny
+// contiguous per plane) are 512 B per warp instruction.  The B side (z fastest, runs of TZ x 16 B)
+// goes through the line buffers in shared memory (line l = kl TZ + zz, conflict-free pitch).
+//   fwd: global A -> registers -> DFT16, twiddle, 16 x 16 transpose (smem), DFT16 -> smem -> B
+//   inv: B -> smem (cp.async) -> registers -> DFT16, twiddle, transpose (smem), DFT16 -> A
+constexpr int kYLine = kZLine + 1;   // 273 slots: odd pitch between lines
+
+template <bool INV>
+__global__ void __launch_bounds__(256, 2) k_yreg256(YArgs a) {
+  extern __shared__ double2 sm[];
+  constexpr int N = 256;
+  const int TZ = a.TZ;                              // blockDim.x == 32 * TZ
+  double2* tw = sm + (size_t)2 * TZ * kYLine;       // W256^{t k2} at (k2 - 1) * 16 + t
+  for (int i = threadIdx.x; i < 240; i += blockDim.x) tw[i] = __ldg(&a.tw[(i & 15) * (1 + (i >> 4))]);
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int kl = lane >> 4, t = lane & 15, zz = w;
+  const int l = kl * TZ + zz;
+  double2* ls = sm + (size_t)l * kYLine;
+  const int nzt = a.Nz / TZ, nkb = a.HxA / kKB;
+  const int ntiles = a.ncomp * nkb * nzt;
+  __syncthreads();
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int zt = tile % nzt, r = tile / nzt, kb = r % nkb, c = r / nkb;
+    const int z0 = zt * TZ, kx0 = kb * kKB, kx = kx0 + kl;
+    double2* Arow = a.A + aidx(a.HxA, N, a.Nz, c, z0 + zz, 0, kx0) + kl;   // element y at Arow[kKB * y]
+    double2 v[16];
+    if (!INV) {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) v[j] = __ldcs(Arow + kKB * (t + 16 * j));
+      dft16<false>(v);
+#pragma unroll
+      for (int k2 = 1; k2 < 16; ++k2) v[k2] = cmul(v[k2], ld_tw(tw + (k2 - 1) * 16 + t));
+      __syncwarp();
+#pragma unroll
+      for (int k2 = 0; k2 < 16; ++k2) ls[k2 * kZRowPad + t] = v[k2];
+      __syncwarp();
+#pragma unroll
+      for (int n1 = 0; n1 < 16; ++n1) v[n1] = ls[t * kZRowPad + n1];
+      dft16<false>(v);                              // v[k1] = X[ky = t + 16 k1]
+      __syncwarp();
+#pragma unroll
+      for (int k1 = 0; k1 < 16; ++k1) ls[k1 * kZRowPad + t] = v[k1];
+      __syncthreads();
+      // B side: z fastest
+      for (int idx = threadIdx.x; idx < 2 * N * TZ; idx += blockDim.x) {
+        const int z2 = idx % TZ, ky = (idx / TZ) & (N - 1), k2l = idx / (TZ * N);
+        const int kxo = kx0 + k2l;
+        if (kxo < a.Hx)
+          a.B[s_index(a.L, a.ncomp, a.Hx, c, kxo, ky, z0 + z2)] = sm[(size_t)(k2l * TZ + z2) * kYLine + ky + (ky >> 4)];
+      }
+      __syncthreads();
+    } else {
+      for (int idx = threadIdx.x; idx < 2 * N * TZ; idx += blockDim.x) {
+        const int z2 = idx % TZ, ky = (idx / TZ) & (N - 1), k2l = idx / (TZ * N);
+        const int kxo = kx0 + k2l;
+        if (kxo < a.Hx)
+          cp_async16(&sm[(size_t)(k2l * TZ + z2) * kYLine + ky + (ky >> 4)], &a.B[s_index(a.L, a.ncomp, a.Hx, c, kxo, ky, z0 + z2)]);
+      }
+      cp_async_commit();
+      cp_async_wait<0>();
+      __syncthreads();
+#pragma unroll
+      for (int k1 = 0; k1 < 16; ++k1) v[k1] = ls[k1 * kZRowPad + t];   // X[ky = t + 16 k1]
+      dft16<true>(v);                               // v[n1] = U[k2 = t][n1]
+#pragma unroll
+      for (int n1 = 1; n1 < 16; ++n1) {
+        double2 wv = ld_tw(tw + (n1 - 1) * 16 + t);
+        wv.y = -wv.y;
+        v[n1] = cmul(v[n1], wv);
+      }
+#pragma unroll
+      for (int n1 = 0; n1 < 16; ++n1) ls[n1 * kZRowPad + t] = v[n1];
+      __syncwarp();
+#pragma unroll
+      for (int k2 = 0; k2 < 16; ++k2) v[k2] = ls[t * kZRowPad + k2];
+      dft16<true>(v);                               // v[n2] = y-line value at y = t + 16 n2
+      if (kx < a.Hx) {
+#pragma unroll
+        for (int n2 = 0; n2 < 16; ++n2) Arow[kKB * (t + 16 * n2)] = v[n2];
+      }
+      __syncthreads();                              // line buffers free for the next tile's loads
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
 // X passes, one component per tile
 // ---------------------------------------------------------------------------------------------
 struct XPArgs {
@@ -698,6 +787,18 @@ static SlabL slab_layout(const fgd_ctx* c) {
 
 fgd_status pipe_y(fgd_ctx* c, int ncomp, bool inv) {
   const int Ny = c->n[1], Nz = c->nz_l;
+  if (Ny == 256 && !std::getenv("FGD_NO_YREG")) {
+    const int TZ = std::min(8, std::min(Nz, c->n[2] / c->P));
+    const int thr = 32 * TZ;
+    const size_t smem = ((size_t)2 * TZ * kYLine + 240) * sizeof(double2);
+    const int ntiles = ncomp * (c->HxA / kKB) * (Nz / TZ);
+    YArgs a{c->specA, c->specB, Nz, c->Hx, c->HxA, TZ, kKB, ncomp, ilog2(TZ), ilog2(kKB), c->tabs.tw[ilog2(Ny)],
+            slab_layout(c)};
+    KTimer kt(c, inv ? (ncomp == 6 ? KC_YINV6 : KC_YINV1) : (ncomp == 6 ? KC_YFWD6 : KC_YFWD1));
+    if (inv) FGD_PLAUNCH(c, k_yreg256<true>, thr, smem, ntiles, a);
+    else FGD_PLAUNCH(c, k_yreg256<false>, thr, smem, ntiles, a);
+    return FGD_OK;
+  }
   const int TPL = fft_TPL(Ny, true);
   static const int nl_env = [] {
     const char* e = std::getenv("FGD_YL");
