@@ -10,6 +10,8 @@
 // memory, form the vertex fluxes f_j = l^2(P) (D_j a)(P) for the tile plus its low halo, and
 // gather L a.  The PCG variant builds p = z + beta p_old on the fly (halo included), writes p and
 // q = L p and reduces p.q.  HBM traffic: read a (8 B) + phase (1 B) + write (8 B) per voxel.
+#include <cstdlib>
+
 #include "reduce.cuh"
 
 namespace fgd {
@@ -64,35 +66,48 @@ __device__ __forceinline__ void cp_async_wait_s() {
 // Planes of `a` (and p_old for PCG) arrive in a ring of kRing shared-memory slots by cp.async, up
 // to kRing - 2 planes ahead of the level being computed, so that every SM keeps several planes of
 // loads in flight through the z march.
-constexpr int kRing = 6;
-constexpr int kPlane = (SBY + 2) * (SBX + 2);
+//
+// Each thread owns a column of RY voxels (x, y0' .. y0' + RY - 1) and keeps the (RY + 2) x 3
+// neighbourhood of levels z and z + 1 in registers.  Per level it forms the vertex fluxes of the
+// 2 x (RY + 1) vertices around its column ONCE (instead of 4 corners per voxel) and scatters them
+// with the D^T signs into two accumulators: the voxels of level z (complete after this level) and
+// of level z + 1 (seeded for the next level).  Vertex V(xv, yv, zl) sits at the far corner of voxel
+// (xv, yv, zl), uses a on {xv, xv+1} x {yv, yv+1} x {zl, zl+1} and l^2 of voxel (xv, yv, zl).
+constexpr int kRing = 5;
 
-template <int MODE>
+// phase ids of a plane: rows y0-1 .. y0+TY-1, 4-byte words covering x0-4 .. x0+TX+3 (aligned, so
+// that the periodic wrap never splits a word); byte of x at (x - x0 + 4)
+constexpr int kPhW = SBX + 8;
+template <int RY>
+constexpr size_t stencil_smem(int na) {
+  return (size_t)kRing * na * (SBX + 2) * (SBY * RY + 2) * sizeof(double) + (size_t)kRing * (SBY * RY + 1) * kPhW;
+}
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+
+template <int MODE, int RY>
 __global__ void __launch_bounds__(256, 2) k_stencil(SArgs s, const double* __restrict__ ain, const double* __restrict__ pold,
                                                      double* __restrict__ pout, double* __restrict__ q,
                                                      const uint8_t* __restrict__ phase, DevScalars* sc, double* partials,
                                                      int red_op, int red_slot) {
   constexpr int NA = MODE == ST_PCG ? 2 : 1;
-  __shared__ double ring[kRing][NA][kPlane];
+  constexpr int PX = SBX + 2, PY = SBY * RY + 2, PL = PX * PY, PHL = (SBY * RY + 1) * kPhW;
+  extern __shared__ double ring[];                 // [kRing][NA][PL], then phase ids [kRing][PHL]
+  uint8_t* phs = reinterpret_cast<uint8_t*>(ring + (size_t)kRing * NA * PL);
   __shared__ double lut[kMaxPhases];
-  const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * SBX + tx;
-  const int TX = s.TX, TY = s.TY, TZ = s.TZ;
+  const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * SBX + tx, nthr = SBX * blockDim.y;
+  const int TX = s.TX, TY = s.TY, TZ = s.TZ;      // TY = blockDim.y * RY
   const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY, z0 = blockIdx.z * TZ;
   const int Nx = s.Nx, Ny = s.Ny, Nz = s.Nz;
   const double beta = (MODE == ST_PCG) ? sc->beta : 0.0;
   if (tid < kMaxPhases) lut[tid] = s.lut[tid];
-  const bool act = (tx < TX) && (ty < TY);
-  const int gx = x0 + tx, gy = y0 + ty;
-  const int xm = wrapi(gx - 1, Nx), ym = wrapi(gy - 1, Ny);
-  const double ih[3] = {s.ih[0], s.ih[1], s.ih[2]};
-  // plane elements staged by this thread (at most 2 of (TY+2) x (TX+2) <= 340), stored at the
-  // fixed (SBY+2) x (SBX+2) pitch
+  const bool act = tx < TX;
+  const int gx = x0 + tx, gyb = y0 + ty * RY;
+  // D^T D carries 1/(4h_j) twice
+  const double w0 = s.ih[0] * s.ih[0], w1 = s.ih[1] * s.ih[1], w2 = s.ih[2] * s.ih[2];
   const int PW = TX + 2, PN = (TY + 2) * PW;
-  const int i0 = tid, i1 = tid + SBX * SBY;
-  const int py0 = i0 / PW, px0 = i0 - py0 * PW, py1 = i1 / PW, px1 = i1 - py1 * PW;
-  const int o0 = py0 * (SBX + 2) + px0, o1 = py1 * (SBX + 2) + px1;
-  const size_t r0 = (size_t)wrapi(y0 - 1 + py0, Ny) * Nx + wrapi(x0 - 1 + px0, Nx);
-  const size_t r1 = (size_t)wrapi(y0 - 1 + py1, Ny) * Nx + wrapi(x0 - 1 + px1, Nx);
   // plane index pi = 0 .. TZ + 1 <-> level z0 - 1 + pi; one commit group per plane (possibly empty)
   auto issue = [&](int pi) {
     if (pi <= TZ + 1) {
@@ -110,48 +125,75 @@ __global__ void __launch_bounds__(256, 2) k_stencil(SArgs s, const double* __res
         pa = ain + base;
         pp = pold + base;
       }
-      double* d = ring[pi % kRing][0];
-      if (i0 < PN) cp_async8(d + o0, pa + r0);
-      if (i1 < PN) cp_async8(d + o1, pa + r1);
-      if (MODE == ST_PCG) {
-        double* dp = ring[pi % kRing][NA - 1];
-        if (i0 < PN) cp_async8(dp + o0, pp + r0);
-        if (i1 < PN) cp_async8(dp + o1, pp + r1);
+      double* d = ring + (size_t)(pi % kRing) * NA * PL;
+      for (int e = tid; e < PN; e += nthr) {
+        const int py = e / PW, px = e - py * PW;
+        const size_t r = (size_t)wrapi(y0 - 1 + py, Ny) * Nx + wrapi(x0 - 1 + px, Nx);
+        cp_async8(d + py * PX + px, pa + r);
+        if (MODE == ST_PCG) cp_async8(d + PL + py * PX + px, pp + r);
+      }
+      const uint8_t* pb = (s.dist && zl < 0) ? s.ph_lo : phase + (size_t)wrapi(zl, Nz) * Ny * Nx;
+      uint8_t* dph = phs + (size_t)(pi % kRing) * PHL;
+      const int nw = (TX + 8) / 4;                 // words per row (TX is a multiple of 4)
+      for (int e = tid; e < (TY + 1) * nw; e += nthr) {
+        const int row = e / nw, wd = e - row * nw;
+        const size_t r = (size_t)wrapi(y0 - 1 + row, Ny) * Nx + wrapi(x0 - 4 + 4 * wd, Nx);
+        cp_async4(dph + row * kPhW + 4 * wd, pb + r);
       }
     }
     cp_async_commit_s();
   };
-  double A0[3][3], A1[3][3];      // a at (x-1..x+1, y-1..y+1) of levels z and z+1
-  double fp[4][3], fc[4][3];      // fluxes of the 4 corners at levels z-1 (fp) and z (fc)
-  double red = 0.0;
-  auto read3 = [&](int pi, double (&A)[3][3]) {
-    const double* pa = ring[pi % kRing][0];
-    const double* pp = ring[pi % kRing][NA - 1];
+  double Alo[RY + 2][3], Ahi[RY + 2][3];   // rows gyb-1 .. gyb+RY, columns x-1 .. x+1; levels z, z+1
+  auto readcol = [&](int pi, double (&A)[RY + 2][3]) {
+    const double* pa = ring + (size_t)(pi % kRing) * NA * PL;
 #pragma unroll
-    for (int dy = 0; dy < 3; ++dy)
+    for (int r = 0; r < RY + 2; ++r)
 #pragma unroll
       for (int dx = 0; dx < 3; ++dx) {
-        const int o = (ty + dy) * (SBX + 2) + tx + dx;
-        A[dy][dx] = MODE == ST_PCG ? fma(beta, pp[o], pa[o]) : pa[o];
+        const int o = (ty * RY + r) * PX + tx + dx;
+        A[r][dx] = MODE == ST_PCG ? fma(beta, pa[PL + o], pa[o]) : pa[o];
       }
   };
-  auto fluxes = [&](int zl, double (&F)[4][3]) {
-    const uint8_t* pb = (s.dist && zl < 0) ? s.ph_lo : phase + (size_t)wrapi(zl, Nz) * Ny * Nx;
-    const size_t row0 = (size_t)ym * Nx, row1 = (size_t)gy * Nx;
-    const double l00 = lut[__ldg(pb + row0 + xm)], l10 = lut[__ldg(pb + row0 + gx)];
-    const double l01 = lut[__ldg(pb + row1 + xm)], l11 = lut[__ldg(pb + row1 + gx)];
-    corner_flux(A0, A1, 0, 0, l00, ih, F[0]);   // corner (x-1, y-1)
-    corner_flux(A0, A1, 1, 0, l10, ih, F[1]);   // corner (x,   y-1)
-    corner_flux(A0, A1, 0, 1, l01, ih, F[2]);   // corner (x-1, y)
-    corner_flux(A0, A1, 1, 1, l11, ih, F[3]);   // corner (x,   y)
+  // fluxes of the vertices of level zl (between Alo = level zl and Ahi = level zl + 1):
+  // cur[k] += contribution to voxel (x, gyb + k, zl), nxt[k] += contribution to voxel (.., zl + 1)
+  auto vertices = [&](int pi, double* cur, double* nxt) {
+    const uint8_t* ph = phs + (size_t)(pi % kRing) * PHL + ty * RY * kPhW + tx + 3;
+#pragma unroll
+    for (int vr = 0; vr <= RY; ++vr) {            // vertex row yv = gyb - 1 + vr: A rows vr, vr + 1
+#pragma unroll
+      for (int cx = 0; cx < 2; ++cx) {            // xv = x - 1 + cx: A columns cx, cx + 1
+        const double l2 = lut[ph[vr * kPhW + cx]];
+        const double a000 = Alo[vr][cx], a100 = Alo[vr][cx + 1], a010 = Alo[vr + 1][cx], a110 = Alo[vr + 1][cx + 1];
+        const double a001 = Ahi[vr][cx], a101 = Ahi[vr][cx + 1], a011 = Ahi[vr + 1][cx], a111 = Ahi[vr + 1][cx + 1];
+        const double f0 = l2 * w0 * ((a100 - a000) + (a110 - a010) + (a101 - a001) + (a111 - a011));
+        const double f1 = l2 * w1 * ((a010 - a000) + (a110 - a100) + (a011 - a001) + (a111 - a101));
+        const double f2 = l2 * w2 * ((a001 - a000) + (a101 - a100) + (a011 - a010) + (a111 - a110));
+        const double ex = cx == 0 ? f0 : -f0;      // + from xv = x - 1, - from xv = x
+        if (vr < RY) {                             // voxel row yv + 1: + f1
+          cur[vr] += (ex + f1) - f2;
+          nxt[vr] += (ex + f1) + f2;
+        }
+        if (vr >= 1) {                             // voxel row yv: - f1
+          cur[vr - 1] += (ex - f1) - f2;
+          nxt[vr - 1] += (ex - f1) + f2;
+        }
+      }
+    }
   };
+  double cur[RY], nxt[RY];
+  double red = 0.0;
+#pragma unroll
+  for (int k = 0; k < RY; ++k) nxt[k] = 0.0;
   for (int pi = 0; pi < kRing; ++pi) issue(pi);
   cp_async_wait_s<kRing - 2>();       // planes 0 and 1 (levels z0 - 1, z0) have landed
   __syncthreads();
   if (act) {
-    read3(0, A0);
-    read3(1, A1);
-    fluxes(z0 - 1, fp);
+    readcol(0, Alo);
+    readcol(1, Ahi);
+    double scratch[RY];
+#pragma unroll
+    for (int k = 0; k < RY; ++k) scratch[k] = 0.0;
+    vertices(0, scratch, nxt);
   }
   for (int zz = 0; zz < TZ; ++zz) {
     const int z = z0 + zz;
@@ -161,27 +203,27 @@ __global__ void __launch_bounds__(256, 2) k_stencil(SArgs s, const double* __res
     __syncthreads();
     if (act) {
 #pragma unroll
-      for (int dy = 0; dy < 3; ++dy)
+      for (int r = 0; r < RY + 2; ++r)
 #pragma unroll
-        for (int dx = 0; dx < 3; ++dx) A0[dy][dx] = A1[dy][dx];
-      read3(zz + 2, A1);
-      fluxes(z, fc);
-      // D^T gather: corner c = cx + 2 cy (cx = 1 - vx, cy = 1 - vy); level z (vz = 0) / z-1 (vz = 1)
-      const double tx_ = (fc[0][0] - fc[1][0]) + (fc[2][0] - fc[3][0]) + (fp[0][0] - fp[1][0]) + (fp[2][0] - fp[3][0]);
-      const double ty_ = (fc[0][1] - fc[2][1]) + (fc[1][1] - fc[3][1]) + (fp[0][1] - fp[2][1]) + (fp[1][1] - fp[3][1]);
-      const double tz_ = (fp[0][2] - fc[0][2]) + (fp[1][2] - fc[1][2]) + (fp[2][2] - fc[2][2]) + (fp[3][2] - fc[3][2]);
-      const double ac = A0[1][1];
-      const double out = ac + tx_ * ih[0] + ty_ * ih[1] + tz_ * ih[2];
-      const size_t g = ((size_t)z * Ny + gy) * Nx + gx;
-      __stcs(q + g, out);
-      if (MODE == ST_PCG) {
-        __stcs(pout + g, ac);
-        red = fma(ac, out, red);
+        for (int dx = 0; dx < 3; ++dx) Alo[r][dx] = Ahi[r][dx];
+      readcol(zz + 2, Ahi);
+#pragma unroll
+      for (int k = 0; k < RY; ++k) {
+        cur[k] = nxt[k];
+        nxt[k] = 0.0;
       }
+      vertices(zz + 1, cur, nxt);                // vertex level z = plane zz + 1
 #pragma unroll
-      for (int c = 0; c < 4; ++c)
-#pragma unroll
-        for (int j = 0; j < 3; ++j) fp[c][j] = fc[c][j];
+      for (int k = 0; k < RY; ++k) {
+        const double ac = Alo[k + 1][1];
+        const double out = ac + cur[k];
+        const size_t g = ((size_t)z * Ny + gyb + k) * Nx + gx;
+        __stcs(q + g, out);
+        if (MODE == ST_PCG) {
+          __stcs(pout + g, ac);
+          red = fma(ac, out, red);
+        }
+      }
     }
   }
   cp_async_wait_s<0>();
@@ -203,14 +245,21 @@ fgd_status launch_stencil(fgd_ctx* c, int field, int mode, const double* a, cons
   s.Nx = c->n[0];
   s.Ny = c->n[1];
   s.Nz = c->nz_l;
+  // rows per thread: 4 when the tile can be 32 rows high, else 2 / 1
+  const int RY = s.Ny >= 4 * SBY ? 4 : (s.Ny >= 2 * SBY ? 2 : 1);
+  const int WY = std::min(SBY, s.Ny / RY);
   s.TX = std::min(SBX, s.Nx);
-  s.TY = std::min(SBY, s.Ny);
-  s.TZ = std::min(32, s.Nz);
+  s.TY = WY * RY;
+  static const int tz_env = [] {
+    const char* e = std::getenv("FGD_ST_TZ");
+    return e ? std::atoi(e) : 16;
+  }();
+  s.TZ = std::min(tz_env, s.Nz);
   s.nvox = c->nvox;
   for (int j = 0; j < 3; ++j) s.ih[j] = 0.25 / c->h[j];
   for (int p = 0; p < kMaxPhases; ++p) s.lut[p] = (p < c->nphases) ? c->ell[field][p] * c->ell[field][p] : 0.0;
   dim3 grid(s.Nx / s.TX, s.Ny / s.TY, s.Nz / s.TZ);
-  dim3 block(SBX, SBY);
+  dim3 block(SBX, WY);
   if (c->nranks > 1) {
     const size_t plane = (size_t)s.Nx * s.Ny;
     if (!c->halo && cudaMalloc((void**)&c->halo, 4 * plane * sizeof(double)) != cudaSuccess)
@@ -236,11 +285,25 @@ fgd_status launch_stencil(fgd_ctx* c, int field, int mode, const double* a, cons
   c->launches++;
   KTimer kt(c, KC_STENCIL);
   const int rop = red_op_for(c, red_op), rslot = red_slot_for(c, red_op, 0);
-  if (mode == ST_APPLY)
-    k_stencil<ST_APPLY><<<grid, block, 0, c->stream>>>(s, a, nullptr, nullptr, q, c->phase, c->sc, c->partials, rop, rslot);
-  else
-    k_stencil<ST_PCG><<<grid, block, 0, c->stream>>>(s, zin, pold, pout, q, c->phase, c->sc, c->partials, rop, rslot);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = cudaSuccess;
+#define STL(RYV)                                                                                                  \
+  {                                                                                                               \
+    const size_t smem = stencil_smem<RYV>(mode == ST_PCG ? 2 : 1);                                               \
+    if (mode == ST_APPLY) {                                                                                       \
+      e = cudaFuncSetAttribute(k_stencil<ST_APPLY, RYV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+      if (e == cudaSuccess)                                                                                       \
+        k_stencil<ST_APPLY, RYV><<<grid, block, smem, c->stream>>>(s, a, nullptr, nullptr, q, c->phase, c->sc,    \
+                                                                    c->partials, rop, rslot);                     \
+    } else {                                                                                                      \
+      e = cudaFuncSetAttribute(k_stencil<ST_PCG, RYV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);   \
+      if (e == cudaSuccess)                                                                                       \
+        k_stencil<ST_PCG, RYV><<<grid, block, smem, c->stream>>>(s, zin, pold, pout, q, c->phase, c->sc,          \
+                                                                  c->partials, rop, rslot);                       \
+    }                                                                                                             \
+  }
+  if (RY == 4) STL(4) else if (RY == 2) STL(2) else STL(1)
+#undef STL
+  if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return set_err(c, FGD_ECUDA, std::string("k_stencil: ") + cudaGetErrorString(e));
   return FGD_OK;
 }
