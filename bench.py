@@ -48,6 +48,7 @@ def args_():
     p.add_argument("--khelm", type=int, default=10)
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--no-cufft", action="store_true", help="skip the cuFFT comparison arm")
     return p.parse_args()
 
 
@@ -193,8 +194,8 @@ def peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-TRAFFIC_KERNEL = {"xfwd6": "k_xfwd<{n}, 6, 2>", "xinv6": "k_xipipe<{n}, 1>", "z6": "k_zpipe<{n}, 6, 0>",
-                  "yfwd6": "k_ypipe<{n}, 0>", "yinv6": "k_ypipe<{n}, 1>", "stencil": "k_stencil<1>"}
+TRAFFIC_KERNEL = {"xfwd6": "k_xtan<{n}, 2, 1>", "xinv6": "k_xipipe<{n}, 1>", "z6": "k_zreg256<6, 0>",
+                  "yfwd6": "k_yreg256<0>", "yinv6": "k_yreg256<1>", "stencil": "k_stencil<1, 4>"}
 
 
 def measured_traffic(cls, n):
@@ -228,6 +229,95 @@ def class_bytes(n, kcg, khelm, world=1):
     b["stencil"] = khelm * 33 * V
     b["constitutive"] = (48 + 48 + 8 + 8 + 8 + 1 + 48 + TB + 8) * V
     return b
+
+
+# ---------------------------------------------------------------------------------------------
+# measured comparison: the projected-tangent apply through cuFFT (torch.fft) + torch elementwise
+# ---------------------------------------------------------------------------------------------
+def cufft_comparison(ctx, n, dev, mask, reps=5):
+    """y = G*(C:x) built from library pieces -- torch.einsum for C:x, torch.fft.rfftn /
+    irfftn (cuFFT) for the transforms, torch elementwise ops for the Galerkin projection with the
+    Willot symbol (A-04) -- against the library's fused 5-pass apply on the same x and tangent.
+    A comparison arm only (north_star: "a cuFFT-based path is kept only as a measured comparison")."""
+    import torch
+    g = torch.Generator(device=dev)
+    g.manual_seed(77)
+    x = torch.randn((6, n, n, n), generator=g, dtype=torch.float64, device=dev) * 1e-3
+    Cp = torch.empty((21, n, n, n), dtype=torch.float64, device=dev)
+    ctx.get_field(5, Cp)                      # FGD_FIELD_TANGENT (packed upper triangle, Mandel)
+    y = torch.empty_like(x)
+
+    def timeit(fn):
+        fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps
+
+    t_ours = timeit(lambda: ctx.apply_projected_tangent(x, y))
+    pk = {}
+    t = 0
+    for i in range(6):
+        for j in range(i, 6):
+            pk[(i, j)] = pk[(j, i)] = t
+            t += 1
+    idx = torch.tensor([pk[(i, j)] for i in range(6) for j in range(6)], device=dev)
+    Cf = Cp.view(21, -1).index_select(0, idx).view(6, 6, -1)
+    del Cp
+    h = 1.0                                    # L = n, N = n
+    def cis(m):
+        # e^{2 pi i m / n} with the quarter points exact, so that the rotated-scheme null modes
+        # (1 + e^{i pi} = 0) are exactly zero as in the library's tables
+        th = 2 * math.pi * m.to(torch.float64) / n
+        c, s_ = torch.cos(th), torch.sin(th)
+        q = (4 * m) % n == 0
+        quarter = (4 * m) // n % 4
+        c = torch.where(q, torch.tensor([1.0, 0.0, -1.0, 0.0], dtype=torch.float64, device=dev)[quarter], c)
+        s_ = torch.where(q, torch.tensor([0.0, 1.0, 0.0, -1.0], dtype=torch.float64, device=dev)[quarter], s_)
+        return torch.complex(c, s_)
+
+    mm = torch.arange(n, device=dev)
+    ex = cis(mm[: n // 2 + 1]).view(1, 1, -1)
+    ey = cis(mm).view(1, -1, 1)
+    ez = cis(mm).view(-1, 1, 1)
+    k0 = (ex - 1) * (1 + ey) * (1 + ez) / (4 * h)
+    k1 = (1 + ex) * (ey - 1) * (1 + ez) / (4 * h)
+    k2 = (1 + ex) * (1 + ey) * (ez - 1) / (4 * h)
+    kk = (k0.abs() ** 2 + k1.abs() ** 2 + k2.abs() ** 2)
+    inv = torch.where(kk > 0, 1.0 / torch.where(kk > 0, kk, torch.ones_like(kk)), torch.zeros_like(kk))
+    r2 = math.sqrt(2.0)
+    mk = torch.tensor([float(m) for m in mask], device=dev, dtype=torch.float64)
+    yt = torch.empty_like(x)
+
+    def torch_apply():
+        tau = torch.einsum("ijv,jv->iv", Cf, x.view(6, -1)).view(6, n, n, n)
+        T = torch.fft.rfftn(tau, dim=(1, 2, 3))
+        dc = T[:, 0, 0, 0].clone()
+        T00, T11, T22, T12, T02, T01 = T[0], T[1], T[2], T[3] / r2, T[4] / r2, T[5] / r2
+        c0, c1, c2 = k0.conj(), k1.conj(), k2.conj()
+        t0 = T00 * c0 + T01 * c1 + T02 * c2
+        t1 = T01 * c0 + T11 * c1 + T12 * c2
+        t2 = T02 * c0 + T12 * c1 + T22 * c2
+        sv = c0 * t0 + c1 * t1 + c2 * t2
+        hs = sv * (0.5 * inv)
+        u0, u1, u2 = (t0 - k0 * hs) * (2 * inv), (t1 - k1 * hs) * (2 * inv), (t2 - k2 * hs) * (2 * inv)
+        out = torch.stack([u0 * k0, u1 * k1, u2 * k2, (u1 * k2 + k1 * u2) / r2, (u0 * k2 + k0 * u2) / r2,
+                           (u0 * k1 + k0 * u1) / r2])
+        out[:, 0, 0, 0] = dc * mk
+        yt.copy_(torch.fft.irfftn(out, s=(n, n, n), dim=(1, 2, 3)))
+
+    t_torch = timeit(torch_apply)
+    rel = float(torch.linalg.vector_norm(yt - y) / torch.linalg.vector_norm(y))
+    del Cf
+    torch.cuda.empty_cache()
+    return {"what": "projected-tangent apply y = G*(C:x) at %d^3: torch.einsum + torch.fft (cuFFT) + torch "
+                    "elementwise projection vs the fused 5-pass library apply, same x and tangent" % n,
+            "ms_per_apply_cufft_torch": t_torch, "ms_per_apply_ours": t_ours, "speedup": t_torch / t_ours,
+            "rel_diff": rel}
 
 
 def run_ours(a):
@@ -348,7 +438,18 @@ def run_ours(a):
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu:
         cpu = cpu_baseline(a.kcg, a.khelm)
+    cmp_cufft = None
+    if world == 1 and not a.no_cufft:
+        cmp_cufft = cufft_comparison(ctx, n, dev, synth.CONFIG1_MASK)
 
+    # per-solver rates inside the step (kernel-class times, this rank)
+    t_mech = sum(per_class[k]["ms_per_step"] for k in ("xfwd6", "yfwd6", "z6", "yinv6", "xinv6") if k in per_class)
+    t_helm = sum(per_class[k]["ms_per_step"] for k in ("xfwd1", "yfwd1", "z1", "yinv1", "xinv1", "stencil")
+                 if k in per_class)
+    rates = {"mech_cg_iter_per_s": 1e3 / ms * a.kcg,
+             "mech_apply_ms": t_mech / (a.kcg + 1) if t_mech else None,
+             "helm_pcg_iter_ms": t_helm / (a.khelm + 1) if t_helm else None,
+             "helm_pcg_voxel_iter_per_s": V * (a.khelm + 1) / (t_helm * 1e-3) if t_helm else None}
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
                 "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True,
@@ -360,7 +461,7 @@ def run_ours(a):
                            "l2": "no flush: every input field (>=134 MB) and the tangent (2.8 GB) exceed the 126 MB L2"},
                 "roofline": roof, "step_roofline": step_eff, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": launches, "clocks": clk, "kernels": per_class,
-                "rates": {"mech_cg_iter_per_s": 1e3 / ms * a.kcg}}
+                "rates": rates, "cufft_comparison": cmp_cufft}
         print(json.dumps(line), flush=True)
     ctx.close()
     if world > 1:

@@ -235,7 +235,7 @@ __device__ __forceinline__ void tangent_smem(const double* C, int v, int cs, con
 }
 
 template <int N, int MODE, bool CMP>
-__global__ void __launch_bounds__(128) k_xtan(XTArgs a) {
+__global__ void __launch_bounds__(256) k_xtan(XTArgs a) {
   constexpr int M = N / 2, Hx = M + 1;
   constexpr int LP = xline(M);
   constexpr int NOP = xt_rows<MODE, CMP>();
@@ -423,7 +423,9 @@ static fgd_status launch_xtan(fgd_ctx* c, int mode, const double* r, double* p, 
     const char* e = std::getenv("FGD_XT_CW");
     return e ? std::atoi(e) : 128;
   }();
-  const int CW = std::min(Nx, std::max(16, cw_env));
+  // N = 512: a row pair needs 24 line FFTs of 256 points -> 256 threads and 256-voxel chunks
+  const int CW = std::min(Nx, std::max(16, Nx >= 512 ? 256 : cw_env));
+  const int thr = Nx >= 512 ? 256 : 128;
   const int nop = (mode == XF_TANGENT_CG ? 18 : 6) + (cmp ? 9 : 21);
   const size_t stage = (size_t)nop * CW * 8;
   size_t fixed = 0;
@@ -448,7 +450,7 @@ static fgd_status launch_xtan(fgd_ctx* c, int mode, const double* r, double* p, 
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);          \
     if (e != cudaSuccess) return set_err(c, FGD_ECUDA, std::string("k_xtan smem attr: ") + cudaGetErrorString(e)); \
     int occ = 0;                                                                                      \
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 128, smem) != cudaSuccess || occ < 1) occ = 1; \
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, thr, smem) != cudaSuccess || occ < 1) occ = 1; \
     grid = std::max(1, std::min(ntiles, sm_count() * occ));                                           \
     if (red_op != RED_NONE) {                                                                         \
       fgd_status s_ = ensure_partials(c, (size_t)grid);                                               \
@@ -456,7 +458,7 @@ static fgd_status launch_xtan(fgd_ctx* c, int mode, const double* r, double* p, 
       a.partials = c->partials;                                                                       \
     }                                                                                                 \
     c->launches++;                                                                                    \
-    kern<<<grid, 128, smem, c->stream>>>(a);                                                          \
+    kern<<<grid, thr, smem, c->stream>>>(a);                                                          \
     e = cudaGetLastError();                                                                           \
     if (e != cudaSuccess) return set_err(c, FGD_ECUDA, std::string("k_xtan: ") + cudaGetErrorString(e));         \
   }

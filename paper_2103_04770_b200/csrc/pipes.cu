@@ -808,7 +808,8 @@ fgd_status pipe_y(fgd_ctx* c, int ncomp, bool inv) {
     const char* e = std::getenv("FGD_YTK");
     return e ? std::atoi(e) : kKB;
   }();
-  const int NL = p2floor(std::max(1, std::min(nl_env, 256) * 16 / TPL));   // lines per tile = TZ * TK
+  // lines per tile = TZ * TK; at least 8 so that both sides of the transpose move >= 64 B runs
+  const int NL = std::max(8, p2floor(std::max(1, std::min(nl_env, 256) * 16 / TPL)));
   int TK = p2floor(std::max(1, std::min(std::min(tk_env, NL), 4)));
   int TZ = std::min(NL / TK, std::min(Nz, c->n[2] / c->P));
   TK = std::min(NL / TZ, 4);

@@ -42,16 +42,23 @@ def launches(path):
 def full(path):
     out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     r = list(csv.reader(out.splitlines()))
-    h = r[0]
+    h, units = r[0], r[1]
+    scale = {"ns": 1e-6, "us": 1e-3, "usecond": 1e-3, "msecond": 1.0, "ms": 1.0, "nsecond": 1e-6, "s": 1e3,
+             "second": 1e3, "byte": 1e-9, "Kbyte": 1e-6, "Mbyte": 1e-3, "Gbyte": 1.0, "Tbyte": 1e3,
+             "KB": 1e-6, "MB": 1e-3, "GB": 1.0}
 
     def g(row, m):
         return row[h.index(m)] if m in h else ""
 
+    def gs(row, m):   # value converted to ms (times) or GB (bytes) using the units row
+        v = float(g(row, m).replace(",", ""))
+        return v * scale.get(units[h.index(m)], 1.0)
+
     recs = []
     for row in r[2:]:
         recs.append(dict(
-            kernel=short(g(row, "Kernel Name")), ms=float(g(row, "gpu__time_duration.sum")),
-            dram_GB=float(g(row, "dram__bytes_read.sum")) + float(g(row, "dram__bytes_write.sum")),
+            kernel=short(g(row, "Kernel Name")), ms=gs(row, "gpu__time_duration.sum"),
+            dram_GB=gs(row, "dram__bytes_read.sum") + gs(row, "dram__bytes_write.sum"),
             dram_pct=float(g(row, "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed")),
             l1tex_pct=float(g(row, "l1tex__throughput.avg.pct_of_peak_sustained_active")),
             fp64_pct=float(g(row, "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active")),
@@ -79,7 +86,7 @@ if __name__ == "__main__":
     open(os.path.join(HERE, f"{tag}_launches.md"), "w").write(
         f"# {tag}: ncu launch list (cold-cache, serialised; compare shares)\n\n"
         f"`ncu --metrics gpu__time_duration.sum --clock-control none` over the launches of "
-        f"`bench.py --n 256 --steps 2 --warmup 1` after set-up; total {s:.2f} ms.\n\n{lt}\n")
+        f"`bench.py --steps 2 --warmup 3 --no-cpu --no-e2e --no-cufft` (256^3) after set-up; total {s:.2f} ms.\n\n{lt}\n")
     ft, traffic = full(fpath)
     open(os.path.join(HERE, f"{tag}_ncu_full.md"), "w").write(
         f"# {tag}: `ncu --set full` capture of the hot kernels (256^3 sweep)\n\n{ft}\n")
