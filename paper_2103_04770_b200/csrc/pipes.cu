@@ -560,6 +560,177 @@ __global__ void __launch_bounds__(256, 2) k_yreg256(YArgs a) {
 }
 
 // ---------------------------------------------------------------------------------------------
+// 512-point lines as a register FFT 8 x 8 x 8: 64 threads per line, 8 points per thread, two
+// shared-memory exchanges.  n = t + 64 j, t = t1 + 8 t2; k = ka + 8 kb + 64 kc:
+//   S1 (thread t):           DFT8 over j -> ka, twiddle W512^{t ka}
+//   S2 (thread ka + 8 t1):   DFT8 over t2 -> kb, twiddle W64^{t1 kb}
+//   S3 (thread ka + 8 kb):   DFT8 over t1 -> kc        => thread t holds X[t + 64 kc]
+// The inverse is the same algorithm with conjugate twiddles, applied to that layout, and returns
+// thread t holding x[t + 64 m] -- the coalesced store layout.  Exchange slots (pitch 65, both
+// sides conflict free):  E1 (ka, t) -> ka * 65 + t;  E2 (kb, ka, t1) -> kb * 65 + ka + 8 t1.
+// Calls __syncthreads(): every thread of the CTA must call it.
+constexpr int k512Line = 8 * 65;
+
+template <bool INV>
+__device__ __forceinline__ void fft512_reg(double2 (&v)[8], int t, double2* ls, const double2* tw1,
+                                           const double2* tw2) {
+  dft8<INV>(v);
+#pragma unroll
+  for (int ka = 1; ka < 8; ++ka) {
+    double2 w = ld_tw(tw1 + (ka - 1) * 64 + t);
+    if (INV) w.y = -w.y;
+    v[ka] = cmul(v[ka], w);
+  }
+#pragma unroll
+  for (int ka = 0; ka < 8; ++ka) ls[ka * 65 + t] = v[ka];
+  __syncthreads();
+  const int ka = t & 7, hi = t >> 3;
+#pragma unroll
+  for (int t2 = 0; t2 < 8; ++t2) v[t2] = ls[ka * 65 + hi + 8 * t2];
+  __syncthreads();
+  dft8<INV>(v);
+#pragma unroll
+  for (int kb = 1; kb < 8; ++kb) {
+    double2 w = ld_tw(tw2 + (kb - 1) * 8 + hi);
+    if (INV) w.y = -w.y;
+    v[kb] = cmul(v[kb], w);
+  }
+#pragma unroll
+  for (int kb = 0; kb < 8; ++kb) ls[kb * 65 + ka + 8 * hi] = v[kb];
+  __syncthreads();
+#pragma unroll
+  for (int t1 = 0; t1 < 8; ++t1) v[t1] = ls[hi * 65 + ka + 8 * t1];
+  __syncthreads();
+  dft8<INV>(v);
+}
+
+// twiddle tables of fft512_reg in shared memory: tw1[(ka-1)*64 + t] = W512^{t ka}, tw2[(kb-1)*8 + t1] = W64^{t1 kb}
+__device__ __forceinline__ void fft512_tables(double2* tw1, double2* tw2, const double2* __restrict__ w512) {
+  for (int i = threadIdx.x; i < 448; i += blockDim.x) tw1[i] = __ldg(&w512[(i & 63) * (1 + (i >> 6))]);
+  for (int i = threadIdx.x; i < 56; i += blockDim.x) tw2[i] = __ldg(&w512[8 * (i & 7) * (1 + (i >> 3))]);
+}
+
+// Z pass, Nz = 512: one (kx, ky) per tile, NC lines of 64 threads.
+template <int NC, int MODE>
+__global__ void __launch_bounds__(NC * 64, NC == 6 ? 2 : 8) k_zreg512(ZPArgs a) {
+  extern __shared__ double2 sm[];
+  constexpr int N = 512;
+  double2* tw1 = sm + (size_t)NC * k512Line;
+  double2* tw2 = tw1 + 448;
+  double2* tws = tw2 + 56;                      // e^{-2 pi i m / 512} (symbol)
+  fft512_tables(tw1, tw2, a.twz);
+  load_table(tws, a.twz, N);
+  __syncthreads();
+  const int c = threadIdx.x >> 6, t = threadIdx.x & 63;
+  double2* ls = sm + (size_t)c * k512Line;
+  const int ntiles = a.Hx * a.Nyl;
+  const int BS = NC * a.Hx * a.SL.nys * a.SL.nzs, zm = a.SL.nzs - 1, lgz = a.SL.lg_nzs;
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int kx = tile / a.Nyl, kyl = tile % a.Nyl;
+    double2* Bl = a.B + r_index(a.SL, NC, a.Hx, c, kx, kyl, 0);
+    double2 v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int z = t + 64 * j;
+      v[j] = __ldcg(Bl + ((z >> lgz) * BS + (z & zm)));
+    }
+    fft512_reg<false>(v, t, ls, tw1, tw2);      // v[kc] = X[t + 64 kc]
+#pragma unroll
+    for (int kc = 0; kc < 8; ++kc) ls[kc * 65 + t] = v[kc];
+    __syncthreads();
+    const int ky = kyl + a.ky_off;
+    for (int kz = threadIdx.x; kz < N; kz += blockDim.x) {
+      double2 k[3];
+      zsymbol(a, N, kx, ky, kz, k, tws);
+      const int slot = (kz >> 6) * 65 + (kz & 63);
+      if (MODE == Z_PRECOND) {
+        const double k2 = k[0].x * k[0].x + k[0].y * k[0].y + k[1].x * k[1].x + k[1].y * k[1].y + k[2].x * k[2].x +
+                          k[2].y * k[2].y;
+        sm[slot] = cscale(sm[slot], a.scale / (1.0 + a.mean_ell2 * k2));
+      } else {
+        double2* pv[6];
+#pragma unroll
+        for (int cc = 0; cc < 6; ++cc) pv[cc] = &sm[(size_t)cc * k512Line + slot];
+        project6(a, pv, k, kx == 0 && ky == 0 && kz == 0);
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kc = 0; kc < 8; ++kc) v[kc] = ls[kc * 65 + t];
+    __syncthreads();
+    fft512_reg<true>(v, t, ls, tw1, tw2);       // v[m] = z[t + 64 m]
+#pragma unroll
+    for (int m = 0; m < 8; ++m) {
+      const int z = t + 64 * m;
+      Bl[(z >> lgz) * BS + (z & zm)] = v[m];
+    }
+  }
+}
+
+// Y pass, Ny = 512: tile (c, kx pair, TZ planes), 2 TZ lines of 64 threads.  Warp w carries 16
+// threads of each kx of the pair for plane zz = w / 4 (t = 16 (w % 4) + lane % 16), so that the
+// A-side loads / stores are 512 B per warp instruction.  Line l = kl TZ + zz at pitch k512Line + 1.
+constexpr int kY512Line = k512Line + 1;
+
+template <bool INV>
+__global__ void __launch_bounds__(512, 2) k_yreg512(YArgs a) {
+  extern __shared__ double2 sm[];
+  constexpr int N = 512;
+  const int TZ = a.TZ;                             // blockDim.x == 128 * TZ
+  double2* tw1 = sm + (size_t)2 * TZ * kY512Line;
+  double2* tw2 = tw1 + 448;
+  fft512_tables(tw1, tw2, a.tw);
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int kl = lane >> 4, t = 16 * (w & 3) + (lane & 15), zz = w >> 2;
+  const int l = kl * TZ + zz;
+  double2* ls = sm + (size_t)l * kY512Line;
+  const int nzt = a.Nz / TZ, nkb = a.HxA / kKB;
+  const int ntiles = a.ncomp * nkb * nzt;
+  __syncthreads();
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int zt = tile % nzt, r = tile / nzt, kb = r % nkb, c = r / nkb;
+    const int z0 = zt * TZ, kx0 = kb * kKB, kx = kx0 + kl;
+    double2* Arow = a.A + aidx(a.HxA, N, a.Nz, c, z0 + zz, 0, kx0) + kl;   // element y at Arow[kKB * y]
+    double2 v[8];
+    if (!INV) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = __ldcs(Arow + kKB * (t + 64 * j));
+      fft512_reg<false>(v, t, ls, tw1, tw2);     // v[kc] = X[ky = t + 64 kc]
+#pragma unroll
+      for (int kc = 0; kc < 8; ++kc) ls[kc * 65 + t] = v[kc];
+      __syncthreads();
+      for (int idx = threadIdx.x; idx < 2 * N * TZ; idx += blockDim.x) {
+        const int z2 = idx % TZ, ky = (idx / TZ) & (N - 1), k2l = idx / (TZ * N);
+        const int kxo = kx0 + k2l;
+        if (kxo < a.Hx)
+          a.B[s_index(a.L, a.ncomp, a.Hx, c, kxo, ky, z0 + z2)] =
+              sm[(size_t)(k2l * TZ + z2) * kY512Line + (ky >> 6) * 65 + (ky & 63)];
+      }
+      __syncthreads();
+    } else {
+      for (int idx = threadIdx.x; idx < 2 * N * TZ; idx += blockDim.x) {
+        const int z2 = idx % TZ, ky = (idx / TZ) & (N - 1), k2l = idx / (TZ * N);
+        const int kxo = kx0 + k2l;
+        if (kxo < a.Hx)
+          cp_async16(&sm[(size_t)(k2l * TZ + z2) * kY512Line + (ky >> 6) * 65 + (ky & 63)],
+                     &a.B[s_index(a.L, a.ncomp, a.Hx, c, kxo, ky, z0 + z2)]);
+      }
+      cp_async_commit();
+      cp_async_wait<0>();
+      __syncthreads();
+#pragma unroll
+      for (int kc = 0; kc < 8; ++kc) v[kc] = ls[kc * 65 + t];
+      __syncthreads();
+      fft512_reg<true>(v, t, ls, tw1, tw2);      // v[m] = y-line value at y = t + 64 m
+      if (kx < a.Hx) {
+#pragma unroll
+        for (int m = 0; m < 8; ++m) Arow[kKB * (t + 64 * m)] = v[m];
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
 // X passes, one component per tile
 // ---------------------------------------------------------------------------------------------
 struct XPArgs {
@@ -787,6 +958,18 @@ static SlabL slab_layout(const fgd_ctx* c) {
 
 fgd_status pipe_y(fgd_ctx* c, int ncomp, bool inv) {
   const int Ny = c->n[1], Nz = c->nz_l;
+  if (Ny == 512 && !std::getenv("FGD_NO_YREG")) {
+    const int TZ = std::min(4, std::min(Nz, c->n[2] / c->P));
+    const int thr = 128 * TZ;
+    const size_t smem = ((size_t)2 * TZ * kY512Line + 448 + 56) * sizeof(double2);
+    const int ntiles = ncomp * (c->HxA / kKB) * (Nz / TZ);
+    YArgs a{c->specA, c->specB, Nz, c->Hx, c->HxA, TZ, kKB, ncomp, ilog2(TZ), ilog2(kKB), c->tabs.tw[ilog2(Ny)],
+            slab_layout(c)};
+    KTimer kt(c, inv ? (ncomp == 6 ? KC_YINV6 : KC_YINV1) : (ncomp == 6 ? KC_YFWD6 : KC_YFWD1));
+    if (inv) FGD_PLAUNCH(c, k_yreg512<true>, thr, smem, ntiles, a);
+    else FGD_PLAUNCH(c, k_yreg512<false>, thr, smem, ntiles, a);
+    return FGD_OK;
+  }
   if (Ny == 256 && !std::getenv("FGD_NO_YREG")) {
     const int TZ = std::min(8, std::min(Nz, c->n[2] / c->P));
     const int thr = 32 * TZ;
@@ -865,6 +1048,14 @@ fgd_status pipe_z(fgd_ctx* c, int ncomp, int mode, double scale, const double* d
   a.twy = c->tabs.tw[ilog2(Ny)];
   a.twz = c->tabs.tw[ilog2(Nz)];
   KTimer kt(c, ncomp == 6 ? KC_Z6 : KC_Z1);
+  if (Nz == 512 && ((ncomp == 6 && mode == Z_PROJECT) || (ncomp == 1 && mode == Z_PRECOND))) {
+    const int thr_r = 64 * ncomp;
+    const size_t smem_r = ((size_t)ncomp * k512Line + 448 + 56 + 512) * sizeof(double2);
+    const int nt_r = c->Hx * Nyl;
+    if (ncomp == 6) FGD_PLAUNCH(c, (k_zreg512<6, Z_PROJECT>), thr_r, smem_r, nt_r, a);
+    else FGD_PLAUNCH(c, (k_zreg512<1, Z_PRECOND>), thr_r, smem_r, nt_r, a);
+    return FGD_OK;
+  }
   if (Nz == 256 && ((ncomp == 6 && mode == Z_PROJECT) || (ncomp == 1 && mode == Z_PRECOND))) {
     const int TLr = std::min(ncomp == 6 ? 1 : 8, Nyl);
     a.TL = TLr;
