@@ -185,12 +185,12 @@ __global__ void __launch_bounds__(kMaxThr, 2) k_xfwd(XArgs a, const double2* __r
 // buffer (12 lines: 6 components x 2 rows), and after the last chunk of the pair runs the R2C
 // line transforms and stores the half spectra as one contiguous block per component.
 struct XTArgs {
-  int Ny, Nz, HxA, CW, S;
+  int Ny, Nz, HxA, CW, S, R;   // chunk width, stages, rows per tile
   size_t nvox;
-  const double* r;     // CG: residual (in)
-  double* p;           // CG: direction (in/out); TANGENT: operand (in)
-  double* x;           // CG: solution (in/out, one step late)
-  const double* C;     // tangent, 9 (compact) or 21 (packed) rows of nvox
+  double* r;           // CG: residual (in)                      HELM: r (in/out)
+  double* p;           // CG: direction (in/out); TANGENT: operand  HELM: p (in)
+  double* x;           // CG: solution (in/out, one step late)    HELM: x (in/out)
+  const double* C;     // tangent, 9 (compact) or 21 (packed) rows  HELM: q (in)
   double2* spec;
   DevScalars* sc;
   double* partials;
@@ -199,11 +199,17 @@ struct XTArgs {
   const double2* twN;
 };
 
+template <int MODE>
+__host__ __device__ constexpr int xt_nc() { return MODE == XF_HELM_UPDATE ? 1 : 6; }
 template <int MODE, bool CMP>
-__host__ __device__ constexpr int xt_rows() { return (MODE == XF_TANGENT_CG ? 18 : 6) + (CMP ? 9 : 21); }
+__host__ __device__ constexpr int xt_rows() {
+  return MODE == XF_HELM_UPDATE ? 4 : (MODE == XF_TANGENT_CG ? 18 : 6) + (CMP ? 9 : 21);
+}
+// rows per tile: a pair for the 6-component passes (12 lines), 8 rows (4 if Ny = 4) for the
+// 1-component PCG pass
 template <int N>
-__host__ __device__ constexpr size_t xt_fixed_bytes() {
-  return 64 + (6 * kXR * (size_t)xline(N / 2) + N / 2 + N) * sizeof(double2);
+__host__ __device__ constexpr size_t xt_fixed_bytes(int nlines) {
+  return 64 + ((size_t)nlines * xline(N / 2) + N / 2 + N) * sizeof(double2);
 }
 
 // tau = C p with the tangent rows in shared memory (stride cs between rows)
@@ -234,21 +240,23 @@ __device__ __forceinline__ void tangent_smem(const double* C, int v, int cs, con
   }
 }
 
-template <int N, int MODE, bool CMP>
+template <int N, int MODE, bool CMP, int R>
 __global__ void __launch_bounds__(256) k_xtan(XTArgs a) {
   constexpr int M = N / 2, Hx = M + 1;
   constexpr int LP = xline(M);
+  constexpr int NC = xt_nc<MODE>();
   constexpr int NOP = xt_rows<MODE, CMP>();
   constexpr int C0 = MODE == XF_TANGENT_CG ? 18 : 6;   // first tangent row
+  // R: rows per tile; line l = c * R + row
   extern __shared__ __align__(16) unsigned char smraw[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smraw);                  // [S], S <= 8
-  double2* fb = reinterpret_cast<double2*>(smraw + 64);                // FFT buffer: 12 lines of LP
-  double2* twM = fb + 6 * kXR * LP;
+  double2* fb = reinterpret_cast<double2*>(smraw + 64);                // FFT buffer: NC * R lines of LP
+  double2* twM = fb + (size_t)NC * R * LP;
   double2* twN = twM + M;
   double* stg = reinterpret_cast<double*>(twN + N);                    // [S][NOP][CW]
   const int CW = a.CW, S = a.S;
   const int nch = N / CW;
-  const int ntiles = a.Nz * (a.Ny / kXR);
+  const int ntiles = a.Nz * (a.Ny / R);
   const size_t n = a.nvox;
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
@@ -258,11 +266,11 @@ __global__ void __launch_bounds__(256) k_xtan(XTArgs a) {
   load_table(twN, a.twN, N);
   __syncthreads();
   const int myrows = (int)blockIdx.x < ntiles ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
-  // chunk q: tile t = blockIdx.x + (q / (kXR nch)) gridDim.x, row rr = (q / nch) % kXR, part h = q % nch
-  const int nq = myrows * nch * kXR;
+  // chunk q: tile t = blockIdx.x + (q / (R nch)) gridDim.x, row rr = (q / nch) % R, part h = q % nch
+  const int nq = myrows * nch * R;
   auto issue = [&](int q) {      // warp 0
-    const int t = blockIdx.x + (q / (kXR * nch)) * gridDim.x, rr = (q / nch) % kXR, h = q % nch;
-    const size_t g0 = ((size_t)t * kXR + rr) * N + (size_t)h * CW;   // row z Ny + kXR yb + rr
+    const int t = blockIdx.x + (q / (R * nch)) * gridDim.x, rr = (q / nch) % R, h = q % nch;
+    const size_t g0 = ((size_t)t * R + rr) * N + (size_t)h * CW;   // row z Ny + R yb + rr
     double* dst = stg + (size_t)(q % S) * NOP * CW;
     uint64_t* bar = &bars[q % S];
     const unsigned bytes = CW * 8;
@@ -275,74 +283,88 @@ __global__ void __launch_bounds__(256) k_xtan(XTArgs a) {
       const double* src;
       if (MODE == XF_TANGENT_CG)
         src = i < 6 ? a.r + i * n : i < 12 ? a.p + (i - 6) * n : i < 18 ? a.x + (i - 12) * n : a.C + (i - 18) * n;
-      else
+      else if (MODE == XF_TANGENT)
         src = i < 6 ? a.p + i * n : a.C + (i - 6) * n;
+      else   // HELM: p, q, x, r
+        src = i == 0 ? a.p : i == 1 ? a.C : i == 2 ? a.x : a.r;
       bulk_g2s(dst + (size_t)i * CW, src + g0, bytes, bar);
     }
   };
   if (threadIdx.x < 32)
     for (int q = 0; q < S - 1 && q < nq; ++q) issue(q);
   double beta = 0.0, alpha = 0.0;
-  if (MODE == XF_TANGENT_CG) {
-    beta = a.sc->beta;
-    alpha = a.sc->alpha;
-  }
+  if (MODE == XF_TANGENT_CG) beta = a.sc->beta;
+  if (MODE == XF_TANGENT_CG || MODE == XF_HELM_UPDATE) alpha = a.sc->alpha;
   double red = 0.0;
   double* fbd = reinterpret_cast<double*>(fb);
   for (int q = 0; q < nq; ++q) {
     // refill the stage consumed at q - 1 (released by the barriers at the end of that iteration)
     if (threadIdx.x < 32 && q + S - 1 < nq) issue(q + S - 1);
     mbar_wait(&bars[q % S], (q / S) & 1);
-    const int t = blockIdx.x + (q / (kXR * nch)) * gridDim.x, rr = (q / nch) % kXR, h = q % nch;
+    const int t = blockIdx.x + (q / (R * nch)) * gridDim.x, rr = (q / nch) % R, h = q % nch;
     const double* st = stg + (size_t)(q % S) * NOP * CW;
     for (int v = threadIdx.x; v < CW; v += blockDim.x) {
       const int xg = h * CW + v;
-      const size_t g = ((size_t)t * kXR + rr) * N + xg;
-      double p[6], tau[6];
-      if (MODE == XF_TANGENT_CG) {
-        // CG with the solution update one step late (x += alpha_{k-1} p_{k-1}); see cg_mech
-#pragma unroll
-        for (int c = 0; c < 6; ++c) {
-          const double po = st[(6 + c) * CW + v];
-          a.x[c * n + g] = fma(alpha, po, st[(12 + c) * CW + v]);
-          p[c] = fma(beta, po, st[c * CW + v]);
-          a.p[c * n + g] = p[c];
-        }
+      const size_t g = ((size_t)t * R + rr) * N + xg;
+      double tau[NC];
+      if (MODE == XF_HELM_UPDATE) {
+        // PCG update (real space, A-10 / R-PCG): x += alpha p, r -= alpha q; tau = r; r.r
+        a.x[g] = fma(alpha, st[v], st[2 * CW + v]);
+        const double rn = fma(-alpha, st[CW + v], st[3 * CW + v]);
+        a.r[g] = rn;
+        tau[0] = rn;
+        red = fma(rn, rn, red);
       } else {
+        double p[6], tv[6];
+        if (MODE == XF_TANGENT_CG) {
+          // CG with the solution update one step late (x += alpha_{k-1} p_{k-1}); see cg_mech
 #pragma unroll
-        for (int c = 0; c < 6; ++c) p[c] = st[c * CW + v];
+          for (int c = 0; c < 6; ++c) {
+            const double po = st[(6 + c) * CW + v];
+            a.x[c * n + g] = fma(alpha, po, st[(12 + c) * CW + v]);
+            p[c] = fma(beta, po, st[c * CW + v]);
+            a.p[c * n + g] = p[c];
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < 6; ++c) p[c] = st[c * CW + v];
+        }
+        tangent_smem<CMP>(st + C0 * CW, v, CW, p, tv);
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+          tau[c] = tv[c];
+          if (MODE == XF_TANGENT_CG) red = fma(p[c], tv[c], red);
+        }
       }
-      tangent_smem<CMP>(st + C0 * CW, v, CW, p, tau);
 #pragma unroll
-      for (int c = 0; c < 6; ++c) {
-        if (MODE == XF_TANGENT_CG) red = fma(p[c], tau[c], red);
-        const int l = c * kXR + rr;
+      for (int c = 0; c < NC; ++c) {
+        const int l = c * R + rr;
         fbd[(size_t)(l * LP + SWZ(l, xg >> 1)) * 2 + (xg & 1)] = tau[c];
       }
     }
     __syncthreads();
-    if (rr == kXR - 1 && h == nch - 1) {
-      fft_lines<M, false>(fb, 6 * kXR, LP, twM);
+    if (rr == R - 1 && h == nch - 1) {
+      fft_lines<M, false>(fb, NC * R, LP, twM);
       __syncthreads();
-      for (int idx = threadIdx.x; idx < 6 * kXR * (M / 2 + 1); idx += blockDim.x) {
+      for (int idx = threadIdx.x; idx < NC * R * (M / 2 + 1); idx += blockDim.x) {
         const int k = idx % (M / 2 + 1), l = idx / (M / 2 + 1);
         r2c_post<N>(fb + (size_t)l * LP, l, k, twN);
       }
       __syncthreads();
-      const int z = t / (a.Ny / kXR), yb = t % (a.Ny / kXR);
+      const int z = t / (a.Ny / R), y0 = (t % (a.Ny / R)) * R;
       constexpr int NB = (Hx + kKB - 1) / kKB;   // kx blocks holding data
-      for (int idx = threadIdx.x; idx < 6 * NB * kXR * kKB; idx += blockDim.x) {
-        // order (kx % kKB, row, kx / kKB, c): runs of kXR * kKB contiguous elements
-        const int kl = idx % kKB, r2 = (idx / kKB) % kXR, kb = (idx / (kKB * kXR)) % NB, c = idx / (kKB * kXR * NB);
-        const int kx = kb * kKB + kl, l = c * kXR + r2;
-        if (kx < Hx) a.spec[aidx(a.HxA, a.Ny, a.Nz, c, z, yb * kXR + r2, kx)] = fb[l * LP + SWZ(l, kx)];
+      for (int idx = threadIdx.x; idx < NC * NB * R * kKB; idx += blockDim.x) {
+        // order (kx % kKB, row, kx / kKB, c): runs of R * kKB contiguous elements
+        const int kl = idx % kKB, r2 = (idx / kKB) % R, kb = (idx / (kKB * R)) % NB, c = idx / (kKB * R * NB);
+        const int kx = kb * kKB + kl, l = c * R + r2;
+        if (kx < Hx) a.spec[aidx(a.HxA, a.Ny, a.Nz, c, z, y0 + r2, kx)] = fb[l * LP + SWZ(l, kx)];
       }
       __syncthreads();
     }
   }
-  if (MODE == XF_TANGENT_CG) {
-    double rr[1] = {red};
-    reduce_finalize<1>(rr, a.partials, a.sc, a.red_op, a.red_slot);
+  if (MODE == XF_TANGENT_CG || MODE == XF_HELM_UPDATE) {
+    double rr2[1] = {red};
+    reduce_finalize<1>(rr2, a.partials, a.sc, a.red_op, a.red_slot);
   }
 }
 
@@ -411,25 +433,29 @@ static int sm_count() {
   return s;
 }
 
-// returns FGD_OK and *done = false when the bulk-copy path does not apply (alignment, N > 512)
-static fgd_status launch_xtan(fgd_ctx* c, int mode, const double* r, double* p, double* x, const double* Cp,
+// returns FGD_OK and *done = false when the bulk-copy path does not apply (alignment)
+// operands: CG (r, p, x, C); TANGENT (-, p, -, C); HELM (r, p, x, q in C)
+static fgd_status launch_xtan(fgd_ctx* c, int mode, double* r, double* p, double* x, const double* Cp,
                               int red_op, int red_slot, bool* done) {
   *done = false;
-  const int Nx = c->n[0];
-  const bool cmp = Cp == c->Cc;
+  const int Nx = c->n[0], Ny = c->n[1];
+  const bool cmp = mode != XF_HELM_UPDATE && Cp == c->Cc;
   auto al = [](const void* q) { return ((uintptr_t)q & 15) == 0; };
-  if (!al(p) || !al(Cp) || (mode == XF_TANGENT_CG && (!al(r) || !al(x)))) return FGD_OK;
+  if (!al(p) || !al(Cp) || (mode != XF_TANGENT && (!al(r) || !al(x)))) return FGD_OK;
   static const int cw_env = [] {
     const char* e = std::getenv("FGD_XT_CW");
     return e ? std::atoi(e) : 128;
   }();
-  // N = 512: a row pair needs 24 line FFTs of 256 points -> 256 threads and 256-voxel chunks
-  const int CW = std::min(Nx, std::max(16, Nx >= 512 ? 256 : cw_env));
-  const int thr = Nx >= 512 ? 256 : 128;
-  const int nop = (mode == XF_TANGENT_CG ? 18 : 6) + (cmp ? 9 : 21);
+  const bool helm = mode == XF_HELM_UPDATE;
+  // N = 512 (6 components): a row pair needs 24 line FFTs of 256 points -> 256 threads, 256-voxel chunks
+  const int CW = helm ? Nx : std::min(Nx, std::max(16, Nx >= 512 ? 256 : cw_env));
+  const int thr = (!helm && Nx >= 512) ? 256 : 128;
+  const int R = helm ? std::min(Ny, 8) : kXR;
+  const int nc = helm ? 1 : 6;
+  const int nop = helm ? 4 : (mode == XF_TANGENT_CG ? 18 : 6) + (cmp ? 9 : 21);
   const size_t stage = (size_t)nop * CW * 8;
   size_t fixed = 0;
-#define XTF(NN) fixed = xt_fixed_bytes<NN>();
+#define XTF(NN) fixed = xt_fixed_bytes<NN>(nc * R);
   FGD_DISPATCH_N(Nx, XTF)
 #undef XTF
   // as many stages (2..4) as leave room for two CTAs per SM
@@ -438,15 +464,16 @@ static fgd_status launch_xtan(fgd_ctx* c, int mode, const double* r, double* p, 
   if (S < 2) S = 2;
   const size_t smem = fixed + S * stage;
   if (smem > 227 * 1024) return FGD_OK;
-  XTArgs a{c->n[1], c->nz_l, c->HxA, CW, S, c->nvox, r, p, x, Cp, c->specA, c->sc, c->partials, red_op, red_slot,
+  XTArgs a{Ny, c->nz_l, c->HxA, CW, S, R, c->nvox, r, p, x, Cp, c->specA, c->sc, c->partials, red_op, red_slot,
            c->tabs.tw[ilog2(Nx / 2)], c->tabs.tw[ilog2(Nx)]};
-  const int ntiles = (c->n[1] / kXR) * c->nz_l;
-  KTimer kt(c, KC_XFWD6);
+  const int ntiles = (Ny / R) * c->nz_l;
+  KTimer kt(c, helm ? KC_XFWD1 : KC_XFWD6);
   int grid = 1;
 #define XTL(NN)                                                                                       \
   {                                                                                                   \
-    auto kern = mode == XF_TANGENT_CG ? (cmp ? k_xtan<NN, XF_TANGENT_CG, true> : k_xtan<NN, XF_TANGENT_CG, false>) \
-                                      : (cmp ? k_xtan<NN, XF_TANGENT, true> : k_xtan<NN, XF_TANGENT, false>);     \
+    auto kern = mode == XF_TANGENT_CG ? (cmp ? k_xtan<NN, XF_TANGENT_CG, true, kXR> : k_xtan<NN, XF_TANGENT_CG, false, kXR>) \
+              : mode == XF_TANGENT    ? (cmp ? k_xtan<NN, XF_TANGENT, true, kXR> : k_xtan<NN, XF_TANGENT, false, kXR>)       \
+              : R == 8                ? k_xtan<NN, XF_HELM_UPDATE, false, 8> : k_xtan<NN, XF_HELM_UPDATE, false, 4>;    \
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);          \
     if (e != cudaSuccess) return set_err(c, FGD_ECUDA, std::string("k_xtan smem attr: ") + cudaGetErrorString(e)); \
     int occ = 0;                                                                                      \
@@ -476,11 +503,16 @@ fgd_status launch_xfwd(fgd_ctx* c, int ncomp, int mode, const double* in0, const
 fgd_status launch_xfwd_io(fgd_ctx* c, int ncomp, int mode, const double* in0, const double* in1, double* out0,
                           double* io1, const double* Cp, int red_op, int red_slot) {
   if (mode == XF_PLAIN && ((uintptr_t)in0 & 15) == 0) return pipe_xfwd_plain(c, ncomp, in0);
-  if (ncomp == 6 && (mode == XF_TANGENT || mode == XF_TANGENT_CG) && !std::getenv("FGD_NO_XTAN")) {
+  if (((ncomp == 6 && (mode == XF_TANGENT || mode == XF_TANGENT_CG)) || (ncomp == 1 && mode == XF_HELM_UPDATE)) &&
+      !std::getenv("FGD_NO_XTAN")) {
     bool done = false;
-    fgd_status s = mode == XF_TANGENT_CG ? launch_xtan(c, mode, in0, out0, io1, Cp, red_op, red_slot, &done)
-                                         : launch_xtan(c, mode, nullptr, const_cast<double*>(in0), nullptr, Cp,
-                                                       red_op, red_slot, &done);
+    fgd_status s;
+    if (mode == XF_TANGENT_CG)
+      s = launch_xtan(c, mode, const_cast<double*>(in0), out0, io1, Cp, red_op, red_slot, &done);
+    else if (mode == XF_TANGENT)
+      s = launch_xtan(c, mode, nullptr, const_cast<double*>(in0), nullptr, Cp, red_op, red_slot, &done);
+    else   // HELM: x(out0) += alpha p(in0); r(io1) -= alpha q(in1)
+      s = launch_xtan(c, mode, io1, const_cast<double*>(in0), out0, in1, red_op, red_slot, &done);
     if (s != FGD_OK || done) return s;
   }
   const int Nx = c->n[0], Ny = c->n[1], Nz = c->nz_l;

@@ -774,7 +774,7 @@ __device__ __forceinline__ void xi_issue(const XPArgs& a, int t, double2* buf, d
 }
 
 template <int N, int MODE>
-__global__ void __launch_bounds__(128, 4) k_xipipe(XPArgs a) {
+__global__ void __launch_bounds__(256, 2) k_xipipe(XPArgs a) {
   extern __shared__ double2 sm[];
   constexpr int M = N / 2;
   constexpr int LP = xline(M);
@@ -1098,8 +1098,12 @@ static int choose_TYp(int N, int Ny) {
 fgd_status pipe_xinv(fgd_ctx* c, int ncomp, int mode, double* out0, double* io1, double* io2, const double* in1,
                      int red_op, int red_slot) {
   const int Nx = c->n[0], Ny = c->n[1], Nz = c->nz_l;
-  const int TY = choose_TYp(Nx, Ny);
-  const int thr = std::min(128, r32(TY * fft_TPL(Nx / 2)));
+  static const int ty_env = [] {
+    const char* e = std::getenv("FGD_XI_TY");
+    return e ? std::atoi(e) : 0;
+  }();
+  const int TY = ty_env > 0 ? std::min(Ny, ty_env) : choose_TYp(Nx, Ny);
+  const int thr = std::min(256, r32(TY * fft_TPL(Nx / 2)));
   const bool pre = mode == XI_MECH_CG || mode == XI_HELM_Z;
   const size_t smem = (2 * (size_t)TY * xline(Nx / 2) + Nx / 2 + Nx) * sizeof(double2) +
                       (pre ? 2 * (size_t)TY * Nx * sizeof(double) : 0);
