@@ -481,26 +481,52 @@ __global__ void __launch_bounds__(NC == 6 ? 96 : 128) __maxnreg__(NC == 6 ? 128 
 //   inv: B -> smem (cp.async) -> registers -> DFT16, twiddle, transpose (smem), DFT16 -> A
 constexpr int kYLine = kZLine + 1;   // 273 slots: odd pitch between lines
 
+// fwd: A rows go straight from HBM into registers (512 B per warp instruction); the line buffers
+//      hold the exchange and the B-side output staging.
+// inv: the NEXT tile's B-side input is staged by cp.async (double buffer, stage[b][l][slot(ky)])
+//      while the current tile is transformed; the current stage buffer doubles as the exchange
+//      buffer once its column has been read into registers.
+__device__ __forceinline__ void y256_issue_inv(const YArgs& a, int tile, double2* buf) {
+  constexpr int N = 256;
+  const int TZ = a.TZ;
+  const int nzt = a.Nz / TZ, nkb = a.HxA / kKB;
+  const int zt = tile % nzt, r = tile / nzt, kb = r % nkb, c = r / nkb;
+  const int z0 = zt * TZ, kx0 = kb * kKB;
+  for (int idx = threadIdx.x; idx < 2 * N * TZ; idx += blockDim.x) {
+    const int z2 = idx % TZ, ky = (idx / TZ) & (N - 1), k2l = idx / (TZ * N);
+    const int kxo = kx0 + k2l;
+    if (kxo < a.Hx)
+      cp_async16(&buf[(size_t)(k2l * TZ + z2) * kYLine + ky + (ky >> 4)],
+                 &a.B[s_index(a.L, a.ncomp, a.Hx, c, kxo, ky, z0 + z2)]);
+  }
+}
+
 template <bool INV>
 __global__ void __launch_bounds__(256, 2) k_yreg256(YArgs a) {
   extern __shared__ double2 sm[];
   constexpr int N = 256;
   const int TZ = a.TZ;                              // blockDim.x == 32 * TZ
-  double2* tw = sm + (size_t)2 * TZ * kYLine;       // W256^{t k2} at (k2 - 1) * 16 + t
+  const size_t buf_sz = (size_t)2 * TZ * kYLine;    // fwd: one line buffer; inv: two stage buffers
+  double2* tw = sm + (INV ? 2 : 1) * buf_sz;        // W256^{t k2} at (k2 - 1) * 16 + t
   for (int i = threadIdx.x; i < 240; i += blockDim.x) tw[i] = __ldg(&a.tw[(i & 15) * (1 + (i >> 4))]);
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int kl = lane >> 4, t = lane & 15, zz = w;
   const int l = kl * TZ + zz;
-  double2* ls = sm + (size_t)l * kYLine;
   const int nzt = a.Nz / TZ, nkb = a.HxA / kKB;
   const int ntiles = a.ncomp * nkb * nzt;
+  int tile = blockIdx.x;
+  if (INV) {
+    if (tile < ntiles) y256_issue_inv(a, tile, sm);
+    cp_async_commit();
+  }
   __syncthreads();
-  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  for (int i = 0; tile < ntiles; ++i, tile += gridDim.x) {
     const int zt = tile % nzt, r = tile / nzt, kb = r % nkb, c = r / nkb;
     const int z0 = zt * TZ, kx0 = kb * kKB, kx = kx0 + kl;
     double2* Arow = a.A + aidx(a.HxA, N, a.Nz, c, z0 + zz, 0, kx0) + kl;   // element y at Arow[kKB * y]
     double2 v[16];
     if (!INV) {
+      double2* ls = sm + (size_t)l * kYLine;
 #pragma unroll
       for (int j = 0; j < 16; ++j) v[j] = __ldcs(Arow + kKB * (t + 16 * j));
       dft16<false>(v);
@@ -526,15 +552,12 @@ __global__ void __launch_bounds__(256, 2) k_yreg256(YArgs a) {
       }
       __syncthreads();
     } else {
-      for (int idx = threadIdx.x; idx < 2 * N * TZ; idx += blockDim.x) {
-        const int z2 = idx % TZ, ky = (idx / TZ) & (N - 1), k2l = idx / (TZ * N);
-        const int kxo = kx0 + k2l;
-        if (kxo < a.Hx)
-          cp_async16(&sm[(size_t)(k2l * TZ + z2) * kYLine + ky + (ky >> 4)], &a.B[s_index(a.L, a.ncomp, a.Hx, c, kxo, ky, z0 + z2)]);
-      }
+      const int tn = tile + gridDim.x;
+      if (tn < ntiles) y256_issue_inv(a, tn, sm + ((i + 1) & 1) * buf_sz);
       cp_async_commit();
-      cp_async_wait<0>();
+      cp_async_wait<1>();
       __syncthreads();
+      double2* ls = sm + (i & 1) * buf_sz + (size_t)l * kYLine;
 #pragma unroll
       for (int k1 = 0; k1 < 16; ++k1) v[k1] = ls[k1 * kZRowPad + t];   // X[ky = t + 16 k1]
       dft16<true>(v);                               // v[n1] = U[k2 = t][n1]
@@ -554,9 +577,10 @@ __global__ void __launch_bounds__(256, 2) k_yreg256(YArgs a) {
 #pragma unroll
         for (int n2 = 0; n2 < 16; ++n2) Arow[kKB * (t + 16 * n2)] = v[n2];
       }
-      __syncthreads();                              // line buffers free for the next tile's loads
+      __syncthreads();                              // stage buffer free for the next issue
     }
   }
+  if (INV) cp_async_wait<0>();
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -971,9 +995,10 @@ fgd_status pipe_y(fgd_ctx* c, int ncomp, bool inv) {
     return FGD_OK;
   }
   if (Ny == 256 && !std::getenv("FGD_NO_YREG")) {
-    const int TZ = std::min(8, std::min(Nz, c->n[2] / c->P));
+    // fwd: 8 planes per tile (128 B runs on the B side); inv: 4 planes, double-buffered staging
+    const int TZ = std::min(inv ? 4 : 8, std::min(Nz, c->n[2] / c->P));
     const int thr = 32 * TZ;
-    const size_t smem = ((size_t)2 * TZ * kYLine + 240) * sizeof(double2);
+    const size_t smem = ((inv ? 2 : 1) * (size_t)2 * TZ * kYLine + 240) * sizeof(double2);
     const int ntiles = ncomp * (c->HxA / kKB) * (Nz / TZ);
     YArgs a{c->specA, c->specB, Nz, c->Hx, c->HxA, TZ, kKB, ncomp, ilog2(TZ), ilog2(kKB), c->tabs.tw[ilog2(Ny)],
             slab_layout(c)};

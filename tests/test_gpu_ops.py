@@ -198,7 +198,76 @@ def test_full_size_operators_256(n):
     assert rel(za, apply_precond(g, a, e2)) <= TOL_APPLY
 
 
-@pytest.mark.parametrize("n", [(16, 8, 16), (8, 8, 256)])
+def _dft_sample(f, kx, ky, kz, n):
+    """F(f)(xi) of a (C, Nz, Ny, Nx) device field at one frequency (explicit separable DFT sums)."""
+    idx = torch.arange(n, device="cuda", dtype=torch.float64)
+    ex = torch.exp(-2j * np.pi * kx * idx / n)
+    ey = torch.exp(-2j * np.pi * ky * idx / n)
+    ez = torch.exp(-2j * np.pi * kz * idx / n)
+    out = []
+    for c in range(f.shape[0]):
+        out.append(torch.einsum("zyx,x,y,z->", f[c].to(torch.complex128), ex, ey, ez).item())
+    return np.array(out)
+
+
+def test_full_size_operators_512():
+    """BASELINE's 512^3 metric size, in the launch configuration bench.py --size 512 times (bulk-copy
+    tangent pass with 256-thread CTAs, 8x8x8 register y/z FFTs).  At sampled frequencies the oracle's
+    per-frequency operators are checked against explicit DFT sums of the GPU input and output:
+    projected tangent F(y) = G^*(xi) F(C:x); preconditioner F(z) = F(r) / (1 + <l^2>|k|^2) (P:731-737);
+    Helmholtz apply with uniform l: F(L a) = (1 + l^2 |k|^2) F(a) (c6 closed form)."""
+    import synth
+    from oracle.projection import project_spectrum
+    from oracle.mech import PACKED21
+    n = 512
+    g = Grid((n, n, n), (float(n),) * 3)
+    ctx = Context((n, n, n), (float(n),) * 3)
+    mask = synth.CONFIG1_MASK
+    ctx.set_control(mask)
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(11)
+    Cd = synth.random_spd_tangent_torch(g.nvox, 5, device="cuda")
+    ctx.set_tangent(Cd)
+    x = torch.randn((6,) + g.shape, generator=gen, dtype=torch.float64, device="cuda") * 1e-3
+    y = ctx.apply_projected_tangent(x)
+    tau = torch.zeros_like(x)
+    for t, (i, j) in enumerate(PACKED21):
+        cij = Cd[t].reshape(g.shape)
+        tau[i] += cij * x[j]
+        if i != j:
+            tau[j] += cij * x[i]
+    del Cd
+    ks = g.symbol(half=True)
+    rng = np.random.default_rng(5)
+    samples = [(0, 0, 0), (n // 2, 0, 0), (0, n // 2, n // 2), (3, 1, 2)] + \
+              [tuple(int(v) for v in rng.integers(0, (n // 2 + 1, n, n))) for _ in range(3)]
+    for (kx, ky, kz) in samples:
+        ft = _dft_sample(tau, kx, ky, kz, n)
+        fy = _dft_sample(y, kx, ky, kz, n)
+        if (kx, ky, kz) == (0, 0, 0):
+            ref = np.asarray(mask) * ft
+        else:
+            k = ks[:, kz, ky, kx]
+            ref = project_spectrum(np.stack([np.zeros(6), ft], 1), np.stack([np.zeros(3), k], 1), mask,
+                                   dc_index=(0,))[:, 1]
+        assert np.linalg.norm(fy - ref) <= 1e-10 * max(np.linalg.norm(ft), 1e-300), (kx, ky, kz)
+    del tau, y
+    # Helmholtz: one phase, l = 3 (uniform) -> diagonal symbols
+    ell = 3.0
+    ctx.set_phases(torch.zeros(g.shape, dtype=torch.uint8, device="cuda"), 2)
+    ctx.set_nonlocal(np.array([[ell, ell]]), [0])
+    a = x[0].contiguous()
+    ya = ctx.apply_helmholtz(0, a)
+    za = ctx.apply_helmholtz_precond(0, a)
+    for (kx, ky, kz) in samples:
+        fa = _dft_sample(a[None], kx, ky, kz, n)[0]
+        k = ks[:, kz, ky, kx]
+        sym = 1.0 + ell * ell * float(np.sum(np.abs(k) ** 2))
+        assert abs(_dft_sample(ya[None], kx, ky, kz, n)[0] - sym * fa) <= 1e-10 * max(abs(fa) * sym, 1e-300)
+        assert abs(_dft_sample(za[None], kx, ky, kz, n)[0] - fa / sym) <= 1e-10 * max(abs(fa), 1e-300)
+
+
+@pytest.mark.parametrize("n", [(16, 8, 16), (8, 8, 256), (4, 512, 8), (4, 8, 512)])
 @pytest.mark.parametrize("P", [2, 4])
 def test_emulated_slab_layout(P, n, monkeypatch):
     """Multi-GPU transposition layout (S[r][s] -> R[s][r] block all-to-all, y-slab z pass)
