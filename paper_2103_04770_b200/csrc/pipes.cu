@@ -806,8 +806,11 @@ __global__ void __launch_bounds__(256, 2) k_xipipe(XPArgs a) {
   double2* twM = sm + 2 * TY * LP;
   double2* twN = twM + M;
   double* ebuf = reinterpret_cast<double*>(twN + N);   // [2][TY * N] epilogue operand (xi_prefetch)
+  double2* tw128 = reinterpret_cast<double2*>(ebuf + (xi_prefetch<MODE>() ? 2 * TY * N : 0));   // M = 128 only
   build_pass_tables<M>(twM, a.twM);
   load_table(twN, a.twN, N);
+  if constexpr (M == 128)
+    for (int k = threadIdx.x; k < 120; k += blockDim.x) tw128[k] = __ldg(&a.twM[(k & 7) * (1 + (k >> 3))]);
   const int ntiles = a.ncomp * a.Nz * nyt;
   const size_t n = a.nvox;
   double red[1] = {0.0};
@@ -828,12 +831,68 @@ __global__ void __launch_bounds__(256, 2) k_xipipe(XPArgs a) {
       c2r_pre_p<N>(buf + (size_t)l * LP, l, k, twN);
     }
     __syncthreads();
-    fft_lines<M, true>(buf, TY, LP, twM);
-    __syncthreads();
     const int yt = t % nyt, r = t / nyt, z = r % a.Nz, c = r / a.Nz;
     const int y0 = yt * TY;
-    const double* bd = reinterpret_cast<const double*>(buf);
     const double* eb = ebuf + (i & 1) * TY * N;
+    if constexpr (M == 128) {
+      // register FFT 128 = 16 x 8 (8 threads per line, 16 points each, one exchange), epilogue
+      // straight from the registers: thread (yy, tt) ends with z[n], n = tt + 16 k1 and tt + 8 + 16 k1,
+      // z[n] = x[2n] + i x[2n+1]
+      if (threadIdx.x < TY * 8) {
+        const int yy = threadIdx.x >> 3, tt = threadIdx.x & 7;
+        double2* ln = buf + (size_t)yy * LP;
+        double2 v[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] = ln[SWZ(yy, tt + 8 * j)];
+        dft16<true>(v);
+#pragma unroll
+        for (int k2 = 1; k2 < 16; ++k2) {
+          double2 w = ld_tw(tw128 + (k2 - 1) * 8 + tt);
+          w.y = -w.y;
+          v[k2] = cmul(v[k2], w);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int k2 = 0; k2 < 16; ++k2) ln[k2 * 9 + tt] = v[k2];
+        __syncwarp();
+        double2 u0[8], u1[8];
+#pragma unroll
+        for (int n1 = 0; n1 < 8; ++n1) {
+          u0[n1] = ln[tt * 9 + n1];
+          u1[n1] = ln[(tt + 8) * 9 + n1];
+        }
+        dft8<true>(u0);
+        dft8<true>(u1);
+        const size_t grow = (size_t)c * n + ((size_t)z * a.Ny + y0 + yy) * N;
+#pragma unroll
+        for (int h = 0; h < 16; ++h) {
+          const int nn = (h < 8 ? tt : tt + 8) + 16 * (h & 7);
+          const double2 q2 = h < 8 ? u0[h & 7] : u1[h & 7];
+          const int x = 2 * nn;
+          double2* o2;
+          if (MODE == XI_MECH_CG) {
+            const double2 ro = *reinterpret_cast<const double2*>(eb + yy * N + x);
+            const double2 rn = make_double2(fma(-alpha, q2.x, ro.x), fma(-alpha, q2.y, ro.y));
+            o2 = reinterpret_cast<double2*>(a.io2 + grow + x);
+            *o2 = rn;
+            red[0] = fma(rn.x, rn.x, fma(rn.y, rn.y, red[0]));
+          } else {
+            o2 = reinterpret_cast<double2*>(a.out0 + grow + x);
+            *o2 = q2;
+            if (MODE == XI_STORE_RR) red[0] = fma(q2.x, q2.x, fma(q2.y, q2.y, red[0]));
+            if (MODE == XI_HELM_Z) {
+              const double2 ro = *reinterpret_cast<const double2*>(eb + yy * N + x);
+              red[0] = fma(ro.x, q2.x, fma(ro.y, q2.y, red[0]));
+            }
+          }
+        }
+      }
+      __syncthreads();
+      continue;
+    }
+    fft_lines<M, true>(buf, TY, LP, twM);
+    __syncthreads();
+    const double* bd = reinterpret_cast<const double*>(buf);
 #pragma unroll 4
     for (int idx = threadIdx.x; idx < TY * N; idx += blockDim.x) {
       const int yy = idx / N, x = idx % N;
@@ -1130,7 +1189,7 @@ fgd_status pipe_xinv(fgd_ctx* c, int ncomp, int mode, double* out0, double* io1,
   const int TY = ty_env > 0 ? std::min(Ny, ty_env) : choose_TYp(Nx, Ny);
   const int thr = std::min(256, r32(TY * fft_TPL(Nx / 2)));
   const bool pre = mode == XI_MECH_CG || mode == XI_HELM_Z;
-  const size_t smem = (2 * (size_t)TY * xline(Nx / 2) + Nx / 2 + Nx) * sizeof(double2) +
+  const size_t smem = (2 * (size_t)TY * xline(Nx / 2) + Nx / 2 + Nx + (Nx == 256 ? 120 : 0)) * sizeof(double2) +
                       (pre ? 2 * (size_t)TY * Nx * sizeof(double) : 0);
   const double* eop = mode == XI_MECH_CG ? io2 : in1;
   if (pre && ((uintptr_t)eop & 15) != 0) return set_err(c, FGD_EINVAL, "xinv: epilogue operand not 16 B aligned");
