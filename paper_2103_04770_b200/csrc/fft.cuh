@@ -284,4 +284,68 @@ __device__ __forceinline__ void fft_lines(double2* buf, int nl, int ldl, const d
 }
 
 
+// ---------------------------------------------------------------------------------------------
+// Register FFTs of one 128- or 256-point line held in shared memory (natural padded order SWZ in
+// and out), for the x passes.  M = 16 x T (T = 8 or 16 threads per line, all in one warp, 16
+// points per thread): thread tt loads z[tt + T j], DFT16 over j, twiddle W_M^{tt k2}, one exchange
+// (rows of T + 1 slots), DFT_T over n1 for k2 = tt (+ 8 when T = 8: two DFT8), written back in
+// natural order.  Two shared-memory accesses per point for the exchange instead of two per radix
+// pass.  twR[(k2 - 1) T + tt] = W_M^{tt k2}; the inverse uses the conjugates.
+template <int M>
+__host__ __device__ constexpr bool fft_reg_ok() { return M == 128 || M == 256; }
+template <int M>
+__host__ __device__ constexpr int fft_reg_tpl() { return M / 16; }
+
+template <int M>
+__device__ __forceinline__ void fft_reg_tables(double2* twR, const double2* __restrict__ twM) {
+  constexpr int T = M / 16;
+  const int nt = blockDim.x * blockDim.y * blockDim.z;
+  const int tid = threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z);
+  for (int k = tid; k < 15 * T; k += nt) twR[k] = __ldg(&twM[(k % T) * (1 + k / T)]);
+}
+
+template <int M, bool INV>
+__device__ __forceinline__ void fft_reg_inplace(double2* ln, int l, int tt, const double2* twR) {
+  constexpr int T = M / 16;
+  constexpr int RP = T + 1;   // exchange row pitch
+  double2 v[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) v[j] = ln[SWZ(l, tt + T * j)];
+  dft16<INV>(v);
+#pragma unroll
+  for (int k2 = 1; k2 < 16; ++k2) {
+    double2 w = ld_tw(twR + (k2 - 1) * T + tt);
+    if (INV) w.y = -w.y;
+    v[k2] = cmul(v[k2], w);
+  }
+  __syncwarp();
+#pragma unroll
+  for (int k2 = 0; k2 < 16; ++k2) ln[k2 * RP + tt] = v[k2];
+  __syncwarp();
+  if constexpr (T == 16) {
+#pragma unroll
+    for (int n1 = 0; n1 < 16; ++n1) v[n1] = ln[tt * RP + n1];
+    dft16<INV>(v);
+    __syncwarp();
+#pragma unroll
+    for (int k1 = 0; k1 < 16; ++k1) ln[SWZ(l, tt + 16 * k1)] = v[k1];
+  } else {
+    double2 u0[8], u1[8];
+#pragma unroll
+    for (int n1 = 0; n1 < 8; ++n1) {
+      u0[n1] = ln[tt * RP + n1];
+      u1[n1] = ln[(tt + 8) * RP + n1];
+    }
+    dft<8, INV>(u0);
+    dft<8, INV>(u1);
+    __syncwarp();
+#pragma unroll
+    for (int k1 = 0; k1 < 8; ++k1) {
+      ln[SWZ(l, tt + 16 * k1)] = u0[k1];
+      ln[SWZ(l, tt + 8 + 16 * k1)] = u1[k1];
+    }
+  }
+}
+
+
 }  // namespace fgd

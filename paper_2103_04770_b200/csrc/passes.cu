@@ -209,7 +209,7 @@ __host__ __device__ constexpr int xt_rows() {
 // 1-component PCG pass
 template <int N>
 __host__ __device__ constexpr size_t xt_fixed_bytes(int nlines) {
-  return 64 + ((size_t)nlines * xline(N / 2) + N / 2 + N + 120) * sizeof(double2);
+  return 64 + ((size_t)nlines * xline(N / 2) + N / 2 + N + 240) * sizeof(double2);
 }
 
 // tau = C p with the tangent rows in shared memory (stride cs between rows)
@@ -240,37 +240,6 @@ __device__ __forceinline__ void tangent_smem(const double* C, int v, int cs, con
   }
 }
 
-// In-place forward FFT of one 128-point line in shared memory (natural padded order SWZ in and
-// out) by 8 threads (tt = 0..7, all in one warp): 128 = 16 x 8, thread tt loads z[tt + 8 j],
-// DFT16 over j, twiddle W128^{tt k2}, one exchange (rows of 9), two DFT8 -> X[k2 + 16 k1] for
-// k2 = tt, tt + 8, written back in natural order.  tw128[(k2 - 1) * 8 + tt] = W128^{tt k2}.
-__device__ __forceinline__ void fft128_reg_fwd(double2* ln, int l, int tt, const double2* tw128) {
-  double2 v[16];
-#pragma unroll
-  for (int j = 0; j < 16; ++j) v[j] = ln[SWZ(l, tt + 8 * j)];
-  dft16<false>(v);
-#pragma unroll
-  for (int k2 = 1; k2 < 16; ++k2) v[k2] = cmul(v[k2], ld_tw(tw128 + (k2 - 1) * 8 + tt));
-  __syncwarp();
-#pragma unroll
-  for (int k2 = 0; k2 < 16; ++k2) ln[k2 * 9 + tt] = v[k2];
-  __syncwarp();
-  double2 u0[8], u1[8];
-#pragma unroll
-  for (int n1 = 0; n1 < 8; ++n1) {
-    u0[n1] = ln[tt * 9 + n1];
-    u1[n1] = ln[(tt + 8) * 9 + n1];
-  }
-  dft8<false>(u0);
-  dft8<false>(u1);
-  __syncwarp();
-#pragma unroll
-  for (int k1 = 0; k1 < 8; ++k1) {
-    ln[SWZ(l, tt + 16 * k1)] = u0[k1];
-    ln[SWZ(l, tt + 8 + 16 * k1)] = u1[k1];
-  }
-}
-
 template <int N, int MODE, bool CMP, int R>
 __global__ void __launch_bounds__(256) k_xtan(XTArgs a) {
   constexpr int M = N / 2, Hx = M + 1;
@@ -284,8 +253,8 @@ __global__ void __launch_bounds__(256) k_xtan(XTArgs a) {
   double2* fb = reinterpret_cast<double2*>(smraw + 64);                // FFT buffer: NC * R lines of LP
   double2* twM = fb + (size_t)NC * R * LP;
   double2* twN = twM + M;
-  double2* tw128 = twN + N;                                            // [120], N = 256 only
-  double* stg = reinterpret_cast<double*>(tw128 + 120);                // [S][NOP][CW]
+  double2* twR = twN + N;                                              // [240] register-FFT twiddles
+  double* stg = reinterpret_cast<double*>(twR + 240);                  // [S][NOP][CW]
   const int CW = a.CW, S = a.S;
   const int nch = N / CW;
   const int ntiles = a.Nz * (a.Ny / R);
@@ -296,8 +265,7 @@ __global__ void __launch_bounds__(256) k_xtan(XTArgs a) {
   }
   build_pass_tables<M>(twM, a.twM);
   load_table(twN, a.twN, N);
-  if constexpr (M == 128)
-    for (int k = threadIdx.x; k < 120; k += blockDim.x) tw128[k] = __ldg(&a.twM[(k & 7) * (1 + (k >> 3))]);
+  if constexpr (fft_reg_ok<M>()) fft_reg_tables<M>(twR, a.twM);
   __syncthreads();
   const int myrows = (int)blockIdx.x < ntiles ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
   // chunk q: tile t = blockIdx.x + (q / (R nch)) gridDim.x, row rr = (q / nch) % R, part h = q % nch
@@ -378,10 +346,11 @@ __global__ void __launch_bounds__(256) k_xtan(XTArgs a) {
     }
     __syncthreads();
     if (rr == R - 1 && h == nch - 1) {
-      if constexpr (M == 128) {
-        for (int base = 0; base < NC * R * 8; base += blockDim.x) {
+      if constexpr (fft_reg_ok<M>()) {
+        constexpr int TPT = fft_reg_tpl<M>();
+        for (int base = 0; base < NC * R * TPT; base += blockDim.x) {
           const int id = base + threadIdx.x;
-          if (id < NC * R * 8) fft128_reg_fwd(fb + (size_t)(id >> 3) * LP, id >> 3, id & 7, tw128);
+          if (id < NC * R * TPT) fft_reg_inplace<M, false>(fb + (size_t)(id / TPT) * LP, id / TPT, id % TPT, twR);
         }
       } else {
         fft_lines<M, false>(fb, NC * R, LP, twM);
