@@ -195,10 +195,12 @@ __global__ void __launch_bounds__(256, 2) k_stencil(SArgs s, const double* __res
     for (int k = 0; k < RY; ++k) scratch[k] = 0.0;
     vertices(0, scratch, nxt);
   }
+  __syncthreads();                    // planes 0 and 1 have been read by every thread
   for (int zz = 0; zz < TZ; ++zz) {
     const int z = z0 + zz;
-    __syncthreads();                  // all threads are done with the slot of plane zz
-    issue(zz + kRing);                // into that slot
+    // the slot of plane zz was last read at iteration zz - 2 (or in the prologue): every thread has
+    // passed the barrier of iteration zz - 1 (or the one above) since, so it can be refilled
+    issue(zz + kRing);
     cp_async_wait_s<kRing - 2>();     // plane zz + 2 (level z + 1) has landed
     __syncthreads();
     if (act) {
