@@ -101,8 +101,10 @@ __global__ void __launch_bounds__(256, 2) k_stencil(SArgs s, const double* __res
   const int TX = s.TX, TY = s.TY, TZ = s.TZ;      // TY = blockDim.y * RY
   const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY, z0 = blockIdx.z * TZ;
   const int Nx = s.Nx, Ny = s.Ny, Nz = s.Nz;
-  const double beta = (MODE == ST_PCG) ? sc->beta : 0.0;
+  pdl_trigger();
   if (tid < kMaxPhases) lut[tid] = s.lut[tid];
+  pdl_wait();
+  const double beta = (MODE == ST_PCG) ? sc->beta : 0.0;
   const bool act = tx < TX;
   const int gx = x0 + tx, gyb = y0 + ty * RY;
   // D^T D carries 1/(4h_j) twice
@@ -294,13 +296,13 @@ fgd_status launch_stencil(fgd_ctx* c, int field, int mode, const double* a, cons
     if (mode == ST_APPLY) {                                                                                       \
       e = cudaFuncSetAttribute(k_stencil<ST_APPLY, RYV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
       if (e == cudaSuccess)                                                                                       \
-        k_stencil<ST_APPLY, RYV><<<grid, block, smem, c->stream>>>(s, a, nullptr, nullptr, q, c->phase, c->sc,    \
-                                                                    c->partials, rop, rslot);                     \
+        e = launch_pdl(k_stencil<ST_APPLY, RYV>, grid, block, smem, c->stream, s, a, (const double*)nullptr,     \
+                       (double*)nullptr, q, (const uint8_t*)c->phase, c->sc, c->partials, rop, rslot);           \
     } else {                                                                                                      \
       e = cudaFuncSetAttribute(k_stencil<ST_PCG, RYV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);   \
       if (e == cudaSuccess)                                                                                       \
-        k_stencil<ST_PCG, RYV><<<grid, block, smem, c->stream>>>(s, zin, pold, pout, q, c->phase, c->sc,          \
-                                                                  c->partials, rop, rslot);                       \
+        e = launch_pdl(k_stencil<ST_PCG, RYV>, grid, block, smem, c->stream, s, zin, pold, pout, q,              \
+                       (const uint8_t*)c->phase, c->sc, c->partials, rop, rslot);                                \
     }                                                                                                             \
   }
   if (RY == 4) STL(4) else if (RY == 2) STL(2) else STL(1)

@@ -259,6 +259,7 @@ __global__ void __launch_bounds__(256) k_xtan(XTArgs a) {
   const int nch = N / CW;
   const int ntiles = a.Nz * (a.Ny / R);
   const size_t n = a.nvox;
+  pdl_trigger();
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
     fence_mbar_init();
@@ -267,6 +268,7 @@ __global__ void __launch_bounds__(256) k_xtan(XTArgs a) {
   load_table(twN, a.twN, N);
   if constexpr (fft_reg_ok<M>()) fft_reg_tables<M>(twR, a.twM);
   __syncthreads();
+  pdl_wait();
   const int myrows = (int)blockIdx.x < ntiles ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
   // chunk q: tile t = blockIdx.x + (q / (R nch)) gridDim.x, row rr = (q / nch) % R, part h = q % nch
   const int nq = myrows * nch * R;
@@ -495,8 +497,8 @@ static fgd_status launch_xtan(fgd_ctx* c, int mode, double* r, double* p, double
       a.partials = c->partials;                                                                       \
     }                                                                                                 \
     c->launches++;                                                                                    \
-    kern<<<grid, thr, smem, c->stream>>>(a);                                                          \
-    e = cudaGetLastError();                                                                           \
+    e = launch_pdl(kern, dim3(grid), dim3(thr), smem, c->stream, a);                                  \
+    if (e == cudaSuccess) e = cudaGetLastError();                                                     \
     if (e != cudaSuccess) return set_err(c, FGD_ECUDA, std::string("k_xtan: ") + cudaGetErrorString(e));         \
   }
   FGD_DISPATCH_N(Nx, XTL)

@@ -131,10 +131,12 @@ __global__ void __launch_bounds__(256, 2) k_ypipe(YArgs a) {
   extern __shared__ double2 sm[];
   constexpr int LP = cline(N);
   const int NL = a.TZ * a.TK;
+  pdl_trigger();
   double2* tws = sm + 2 * NL * LP;
   build_pass_tables<N, true>(tws, a.tw);
   const int ntiles = a.ncomp * (a.HxA / a.TK) * (a.Nz / a.TZ);
   int t = blockIdx.x;
+  pdl_wait();
   if (t < ntiles) y_issue<N, INV>(a, t, sm);
   cp_async_commit();
   for (int i = 0; t < ntiles; ++i, t += gridDim.x) {
@@ -300,11 +302,13 @@ __global__ void __launch_bounds__(192, 3) k_zpipe(ZPArgs a) {
   const int TL = a.TL;
   double2* tws = sm + 2 * NC * TL * LP;    // e^{-2 pi i m/N} (symbol)
   double2* tpz = tws + N;                    // per-pass FFT twiddles
+  pdl_trigger();
   load_table(tws, a.twz, N);
   build_pass_tables<N>(tpz, a.twz);
   const int nyt = a.Nyl / TL;
   const int ntiles = a.Hx * nyt;
   int t = blockIdx.x;
+  pdl_wait();
   if (t < ntiles) z_issue<N, NC>(a, t, sm);
   cp_async_commit();
   for (int i = 0; t < ntiles; ++i, t += gridDim.x) {
@@ -373,9 +377,11 @@ __global__ void __launch_bounds__(NC == 6 ? 96 : 128) __maxnreg__(NC == 6 ? 128 
   const int nl = NC * TL;                       // blockDim.x == 16 * nl
   double2* tw = sm + (size_t)nl * kZLine;       // W256^{t k2} at (k2 - 1) * 16 + t
   double2* tws = tw + 240;                      // e^{-2 pi i m / 256} (symbol)
+  pdl_trigger();
   for (int i = threadIdx.x; i < 240; i += blockDim.x) tw[i] = __ldg(&a.twz[(i & 15) * (1 + (i >> 4))]);
   load_table(tws, a.twz, N);
   __syncthreads();
+  pdl_wait();
   const int line = threadIdx.x >> 4, t = threadIdx.x & 15;
   const int c = line >> a.lgTL, ll = line & (TL - 1);
   double2* ls = sm + (size_t)line * kZLine;
@@ -508,7 +514,9 @@ __global__ void __launch_bounds__(256, 2) k_yreg256(YArgs a) {
   const int TZ = a.TZ;                              // blockDim.x == 32 * TZ
   const size_t buf_sz = (size_t)2 * TZ * kYLine;    // fwd: one line buffer; inv: two stage buffers
   double2* tw = sm + (INV ? 2 : 1) * buf_sz;        // W256^{t k2} at (k2 - 1) * 16 + t
+  pdl_trigger();
   for (int i = threadIdx.x; i < 240; i += blockDim.x) tw[i] = __ldg(&a.tw[(i & 15) * (1 + (i >> 4))]);
+  pdl_wait();
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int kl = lane >> 4, t = lane & 15, zz = w;
   const int l = kl * TZ + zz;
@@ -642,9 +650,11 @@ __global__ void __launch_bounds__(NC * 64, NC == 6 ? 2 : 8) k_zreg512(ZPArgs a) 
   double2* tw1 = sm + (size_t)NC * k512Line;
   double2* tw2 = tw1 + 448;
   double2* tws = tw2 + 56;                      // e^{-2 pi i m / 512} (symbol)
+  pdl_trigger();
   fft512_tables(tw1, tw2, a.twz);
   load_table(tws, a.twz, N);
   __syncthreads();
+  pdl_wait();
   const int c = threadIdx.x >> 6, t = threadIdx.x & 63;
   double2* ls = sm + (size_t)c * k512Line;
   const int ntiles = a.Hx * a.Nyl;
@@ -703,7 +713,9 @@ __global__ void __launch_bounds__(512, 2) k_yreg512(YArgs a) {
   const int TZ = a.TZ;                             // blockDim.x == 128 * TZ
   double2* tw1 = sm + (size_t)2 * TZ * kY512Line;
   double2* tw2 = tw1 + 448;
+  pdl_trigger();
   fft512_tables(tw1, tw2, a.tw);
+  pdl_wait();
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int kl = lane >> 4, t = 16 * (w & 3) + (lane & 15), zz = w >> 2;
   const int l = kl * TZ + zz;
@@ -800,6 +812,7 @@ __device__ __forceinline__ void xi_issue(const XPArgs& a, int t, double2* buf, d
 template <int N, int MODE>
 __global__ void __launch_bounds__(256, 2) k_xipipe(XPArgs a) {
   extern __shared__ double2 sm[];
+  pdl_trigger();
   constexpr int M = N / 2;
   constexpr int LP = xline(M);
   const int TY = a.TY, nyt = a.Ny / TY;
@@ -815,6 +828,7 @@ __global__ void __launch_bounds__(256, 2) k_xipipe(XPArgs a) {
   const size_t n = a.nvox;
   double red[1] = {0.0};
   double alpha = 0.0;
+  pdl_wait();
   if (MODE == XI_MECH_CG) alpha = a.sc->alpha;
   int t = blockIdx.x;
   if (t < ntiles) xi_issue<N, MODE>(a, t, sm, ebuf);
@@ -940,10 +954,12 @@ __global__ void __launch_bounds__(128, 4) k_xfpipe(XPArgs a) {
   const int TY = a.TY, nyt = a.Ny / TY;
   double2* twM = sm + 2 * TY * LP;
   double2* twN = twM + M;
+  pdl_trigger();
   build_pass_tables<M>(twM, a.twM);
   load_table(twN, a.twN, N);
   const int ntiles = a.ncomp * a.Nz * nyt;
   int t = blockIdx.x;
+  pdl_wait();
   if (t < ntiles) xf_issue<N>(a, t, sm);
   cp_async_commit();
   for (int i = 0; t < ntiles; ++i, t += gridDim.x) {
@@ -1011,8 +1027,8 @@ static fgd_status launch_persistent(fgd_ctx* c, K kernel, int threads, size_t sm
     fgd_status st_ = launch_persistent(ctx, kern, thr, smem, ntiles, &grid_, #kern);                     \
     if (st_ != FGD_OK) return st_;                                                                      \
     (ctx)->launches++;                                                                                  \
-    kern<<<grid_, thr, smem, (ctx)->stream>>>(__VA_ARGS__);                                              \
-    cudaError_t e_ = cudaGetLastError();                                                                \
+    cudaError_t e_ = launch_pdl(kern, dim3(grid_), dim3(thr), smem, (ctx)->stream, __VA_ARGS__);          \
+    if (e_ == cudaSuccess) e_ = cudaGetLastError();                                                     \
     if (e_ != cudaSuccess) return set_err(ctx, FGD_ECUDA, std::string(#kern) + ": " + cudaGetErrorString(e_)); \
   } while (0)
 
