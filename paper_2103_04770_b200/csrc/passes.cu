@@ -474,6 +474,12 @@ static fgd_status launch_xtan(fgd_ctx* c, int mode, double* r, double* p, double
   const size_t budget = 112 * 1024;
   int S = (int)std::min<size_t>(4, budget > fixed ? (budget - fixed) / stage : 0);
   if (S < 2) S = 2;
+  static const int s_env = [] {
+    const char* e = std::getenv("FGD_XT_S");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (helm) S = 3;   // measured: 3 stages of 8 KB beat 4 for the 1-component PCG pass (256^3)
+  if (s_env >= 2 && s_env <= 8) S = s_env;
   const size_t smem = fixed + S * stage;
   if (smem > 227 * 1024) return FGD_OK;
   XTArgs a{Ny, c->nz_l, c->HxA, CW, S, R, c->nvox, r, p, x, Cp, c->specA, c->sc, c->partials, red_op, red_slot,
