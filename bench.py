@@ -194,7 +194,7 @@ def peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-TRAFFIC_KERNEL = {"xfwd6": "k_xtan<{n}, 2, 1>", "xinv6": "k_xipipe<{n}, 1>", "z6": "k_zreg256<6, 0>",
+TRAFFIC_KERNEL = {"xfwd6": "k_xtan<{n}, 2, 1, 2>", "xinv6": "k_xipipe<{n}, 1>", "z6": "k_zreg256<6, 0>",
                   "yfwd6": "k_yreg256<0>", "yinv6": "k_yreg256<1>", "stencil": "k_stencil<1, 4>"}
 
 
