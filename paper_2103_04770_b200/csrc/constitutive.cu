@@ -263,10 +263,16 @@ __global__ void k_phase_count(size_t n, const uint8_t* ph, unsigned long long* c
   __shared__ unsigned long long s[kMaxPhases];
   if (threadIdx.x < kMaxPhases) s[threadIdx.x] = 0;
   __syncthreads();
-  for (size_t g = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g < n; g += (size_t)gridDim.x * blockDim.x) {
-    const int q = ph[g];
+  // warp-aggregated: one shared atomic per distinct phase id per warp and element round
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  const size_t g0 = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  const size_t nround = (n + stride - 1) / stride;
+  for (size_t k = 0; k < nround; ++k) {
+    const size_t g = g0 + k * stride;
+    const int q = g < n ? (int)ph[g] : -1;
     if (q >= nph) atomicExch(bad, 1);
-    else atomicAdd(&s[q], 1ull);
+    const unsigned same = __match_any_sync(0xffffffffu, q);
+    if (q >= 0 && q < nph && (threadIdx.x & 31) == __ffs(same) - 1) atomicAdd(&s[q], (unsigned long long)__popc(same));
   }
   __syncthreads();
   if (threadIdx.x < nph) atomicAdd(&cnt[threadIdx.x], s[threadIdx.x]);

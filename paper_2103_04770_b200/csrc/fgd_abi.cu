@@ -227,11 +227,7 @@ static fgd_status op_projection(fgd_ctx* c, const double* tau, const double* S, 
 static fgd_status op_precond(fgd_ctx* c, int field, const double* r, double* z, int red_op) {
   TRY(ensure_spectral(c));
   TRY(launch_xfwd(c, 1, XF_PLAIN, r, nullptr, nullptr, nullptr, RED_NONE, 0));
-  TRY(launch_yfwd(c, 1));
-  TRY(exchange(c, 1, true));
-  TRY(launch_z(c, 1, Z_PRECOND, inv_nvox(c), nullptr, mean_ell2(c, field)));
-  TRY(exchange(c, 1, false));
-  TRY(launch_yinv(c, 1));
+  TRY(launch_precond_yz(c, inv_nvox(c), mean_ell2(c, field)));
   if (red_op == RED_NONE) return launch_xinv(c, 1, XI_STORE, z, nullptr, nullptr, nullptr, RED_NONE, 0);
   TRY(launch_xinv(c, 1, XI_HELM_Z, z, nullptr, nullptr, r, RED(red_op)));
   return post_reduce(c, red_op);
@@ -314,11 +310,7 @@ static fgd_status pcg_helmholtz(fgd_ctx* c, int field, const double* b, double* 
         rel = std::sqrt(rn2 / bb);
         if (rel < tol) break;
       }
-      TRY(launch_yfwd(c, 1));
-      TRY(exchange(c, 1, true));
-      TRY(launch_z(c, 1, Z_PRECOND, inv_nvox(c), nullptr, mean_ell2(c, field)));
-      TRY(exchange(c, 1, false));
-      TRY(launch_yinv(c, 1));
+      TRY(launch_precond_yz(c, inv_nvox(c), mean_ell2(c, field)));
       TRY(launch_xinv(c, 1, XI_HELM_Z, z, nullptr, nullptr, r, RED(RED_HELM_RZ)));
       TRY(post_reduce(c, RED_HELM_RZ));
     }

@@ -219,6 +219,7 @@ fgd_status pipe_z(fgd_ctx* c, int ncomp, int mode, double scale, const double* d
 fgd_status pipe_xinv(fgd_ctx* c, int ncomp, int mode, double* out0, double* io1, double* io2, const double* in1,
                      int red_op, int red_slot);
 fgd_status pipe_xfwd_plain(fgd_ctx* c, int ncomp, const double* in0);
+fgd_status launch_precond_yz(fgd_ctx* c, double scale, double mean_ell2);
 fgd_status ensure_partials(fgd_ctx* c, size_t nblocks);
 
 // dist.cu
