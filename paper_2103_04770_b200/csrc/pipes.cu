@@ -440,11 +440,33 @@ __global__ void __launch_bounds__(NC == 6 ? 96 : 128) __maxnreg__(NC == 6 ? 128 
 #pragma unroll
       for (int k1 = 0; k1 < 16; ++k1) ls[k1 * kZRowPad + t] = v[k1];
       __syncthreads();
+      // Willot symbol with the (kx, ky) factors hoisted (one ky per tile when TL = 1):
+      // k0 = [(e^{ith1}-1)(1+e^{ith2}) qh0] (1+e^{ith3}), k1 = [(1+e^{ith1})(e^{ith2}-1) qh1] (1+e^{ith3}),
+      // k2 = [(1+e^{ith1})(1+e^{ith2}) qh2] (e^{ith3}-1)
+      double2 P0 = make_double2(0.0, 0.0), P1 = P0, P2 = P0;
+      const bool hoist = a.scheme == 1 && TL == 1;
+      if (hoist) {
+        const double2 wx = __ldg(&a.twx[kx]), wy = __ldg(&a.twy[ky0 + a.ky_off]);
+        const double2 ex = make_double2(wx.x, -wx.y), ey = make_double2(wy.x, -wy.y);
+        const double2 dx = make_double2(ex.x - 1.0, ex.y), dy = make_double2(ey.x - 1.0, ey.y);
+        const double2 cx = make_double2(ex.x + 1.0, ex.y), cy = make_double2(ey.x + 1.0, ey.y);
+        P0 = cscale(cmul(dx, cy), a.qh[0]);
+        P1 = cscale(cmul(cx, dy), a.qh[1]);
+        P2 = cscale(cmul(cx, cy), a.qh[2]);
+      }
       for (int idx = threadIdx.x; idx < TL * N; idx += blockDim.x) {
         const int kz = idx & (N - 1), l2 = idx >> 8;
         const int kyg = ky0 + l2 + a.ky_off;
         double2 k[3];
-        zsymbol(a, N, kx, kyg, kz, k, tws);
+        if (hoist) {
+          const double2 wz = tws[kz];
+          const double2 cz = make_double2(wz.x + 1.0, -wz.y), dz = make_double2(wz.x - 1.0, -wz.y);
+          k[0] = cmul(P0, cz);
+          k[1] = cmul(P1, cz);
+          k[2] = cmul(P2, dz);
+        } else {
+          zsymbol(a, N, kx, kyg, kz, k, tws);
+        }
         double2* pv[6];
 #pragma unroll
         for (int cc = 0; cc < 6; ++cc) pv[cc] = &sm[(size_t)(cc * TL + l2) * kZLine + kz + (kz >> 4)];
