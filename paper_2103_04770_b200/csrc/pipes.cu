@@ -963,8 +963,9 @@ struct XPArgs {
 
 // Modes whose epilogue reads one real operand row per output row (MECH_CG: r, HELM_Z: r of the
 // PCG): that operand is staged by cp.async together with the spectrum of the tile.
-template <int MODE>
-__host__ __device__ constexpr bool xi_prefetch() { return MODE == XI_MECH_CG || MODE == XI_HELM_Z; }
+// (N = 256 loads its epilogue operand into registers ahead of the FFT instead; see k_xipipe)
+template <int N, int MODE>
+__host__ __device__ constexpr bool xi_prefetch() { return (MODE == XI_MECH_CG || MODE == XI_HELM_Z) && N != 256; }
 
 template <int N, int MODE>
 __device__ __forceinline__ void xi_issue(const XPArgs& a, int t, double2* buf, double* ebuf) {
@@ -979,7 +980,7 @@ __device__ __forceinline__ void xi_issue(const XPArgs& a, int t, double2* buf, d
     const int kl = idx % kKB, yy = (idx / kKB) & (TY - 1), kx = (idx / kKB >> a.lgTY) * kKB + kl;
     if (kx < Hx) cp_async16(&buf[yy * LP + SWZ(yy, kx)], &a.spec[aidx(a.HxA, a.Ny, a.Nz, c, z, y0 + yy, kx)]);
   }
-  if constexpr (xi_prefetch<MODE>()) {
+  if constexpr (xi_prefetch<N, MODE>()) {
     // rows y0 .. y0 + TY - 1 of plane z are contiguous: TY * N doubles
     const double* src = (MODE == XI_MECH_CG ? a.io2 : a.in0) + (size_t)c * a.nvox + ((size_t)z * a.Ny + y0) * N;
     for (int idx = threadIdx.x; idx < TY * N / 2; idx += blockDim.x) cp_async16(ebuf + 2 * idx, src + 2 * idx);
@@ -987,7 +988,7 @@ __device__ __forceinline__ void xi_issue(const XPArgs& a, int t, double2* buf, d
 }
 
 template <int N, int MODE>
-__global__ void __launch_bounds__(256, 2) k_xipipe(XPArgs a) {
+__global__ void __launch_bounds__(N == 256 ? 128 : 256, N == 256 ? 3 : 2) k_xipipe(XPArgs a) {
   extern __shared__ double2 sm[];
   pdl_trigger();
   constexpr int M = N / 2;
@@ -996,7 +997,7 @@ __global__ void __launch_bounds__(256, 2) k_xipipe(XPArgs a) {
   double2* twM = sm + 2 * TY * LP;
   double2* twN = twM + M;
   double* ebuf = reinterpret_cast<double*>(twN + N);   // [2][TY * N] epilogue operand (xi_prefetch)
-  double2* tw128 = reinterpret_cast<double2*>(ebuf + (xi_prefetch<MODE>() ? 2 * TY * N : 0));   // M = 128 only
+  double2* tw128 = reinterpret_cast<double2*>(ebuf + (xi_prefetch<N, MODE>() ? 2 * TY * N : 0));   // M = 128 only
   build_pass_tables<M>(twM, a.twM);
   load_table(twN, a.twN, N);
   if constexpr (M == 128)
@@ -1032,6 +1033,17 @@ __global__ void __launch_bounds__(256, 2) k_xipipe(XPArgs a) {
       if (threadIdx.x < TY * 8) {
         const int yy = threadIdx.x >> 3, tt = threadIdx.x & 7;
         double2* ln = buf + (size_t)yy * LP;
+        const size_t grow = (size_t)c * n + ((size_t)z * a.Ny + y0 + yy) * N;
+        // epilogue operand (r) of this thread's 16 output pairs, in flight during the FFT
+        double2 ro[16];
+        if (MODE == XI_MECH_CG || MODE == XI_HELM_Z) {
+          const double* rs = (MODE == XI_MECH_CG ? a.io2 : a.in0) + grow;
+#pragma unroll
+          for (int h = 0; h < 16; ++h) {
+            const int nn = (h < 8 ? tt : tt + 8) + 16 * (h & 7);
+            ro[h] = __ldcs(reinterpret_cast<const double2*>(rs + 2 * nn));
+          }
+        }
         double2 v[16];
 #pragma unroll
         for (int j = 0; j < 16; ++j) v[j] = ln[SWZ(yy, tt + 8 * j)];
@@ -1054,7 +1066,6 @@ __global__ void __launch_bounds__(256, 2) k_xipipe(XPArgs a) {
         }
         dft8<true>(u0);
         dft8<true>(u1);
-        const size_t grow = (size_t)c * n + ((size_t)z * a.Ny + y0 + yy) * N;
 #pragma unroll
         for (int h = 0; h < 16; ++h) {
           const int nn = (h < 8 ? tt : tt + 8) + 16 * (h & 7);
@@ -1062,8 +1073,7 @@ __global__ void __launch_bounds__(256, 2) k_xipipe(XPArgs a) {
           const int x = 2 * nn;
           double2* o2;
           if (MODE == XI_MECH_CG) {
-            const double2 ro = *reinterpret_cast<const double2*>(eb + yy * N + x);
-            const double2 rn = make_double2(fma(-alpha, q2.x, ro.x), fma(-alpha, q2.y, ro.y));
+            const double2 rn = make_double2(fma(-alpha, q2.x, ro[h].x), fma(-alpha, q2.y, ro[h].y));
             o2 = reinterpret_cast<double2*>(a.io2 + grow + x);
             *o2 = rn;
             red[0] = fma(rn.x, rn.x, fma(rn.y, rn.y, red[0]));
@@ -1071,10 +1081,7 @@ __global__ void __launch_bounds__(256, 2) k_xipipe(XPArgs a) {
             o2 = reinterpret_cast<double2*>(a.out0 + grow + x);
             *o2 = q2;
             if (MODE == XI_STORE_RR) red[0] = fma(q2.x, q2.x, fma(q2.y, q2.y, red[0]));
-            if (MODE == XI_HELM_Z) {
-              const double2 ro = *reinterpret_cast<const double2*>(eb + yy * N + x);
-              red[0] = fma(ro.x, q2.x, fma(ro.y, q2.y, red[0]));
-            }
+            if (MODE == XI_HELM_Z) red[0] = fma(ro[h].x, q2.x, fma(ro[h].y, q2.y, red[0]));
           }
         }
       }
@@ -1381,7 +1388,7 @@ fgd_status pipe_xinv(fgd_ctx* c, int ncomp, int mode, double* out0, double* io1,
   }();
   const int TY = ty_env > 0 ? std::min(Ny, ty_env) : choose_TYp(Nx, Ny);
   const int thr = std::min(256, r32(TY * fft_TPL(Nx / 2)));
-  const bool pre = mode == XI_MECH_CG || mode == XI_HELM_Z;
+  const bool pre = (mode == XI_MECH_CG || mode == XI_HELM_Z) && Nx != 256;
   const size_t smem = (2 * (size_t)TY * xline(Nx / 2) + Nx / 2 + Nx + (Nx == 256 ? 120 : 0)) * sizeof(double2) +
                       (pre ? 2 * (size_t)TY * Nx * sizeof(double) : 0);
   const double* eop = mode == XI_MECH_CG ? io2 : in1;
