@@ -551,15 +551,24 @@ __global__ void __launch_bounds__(256, 2) k_yreg256(YArgs a) {
     cp_async_commit();
   }
   __syncthreads();
+  double2 v[16];
+  // fwd: the A-side loads of the next tile are issued into v as soon as v is dead (before the
+  // B-side stores of the current tile), so they are in flight while the stores drain
+  auto arow_of = [&](int tl) {
+    const int zt = tl % nzt, r = tl / nzt, kb = r % nkb, c = r / nkb;
+    return a.A + aidx(a.HxA, N, a.Nz, c, zt * TZ + zz, 0, kb * kKB) + kl;
+  };
+  if (!INV && tile < ntiles) {
+    const double2* A0 = arow_of(tile);
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] = __ldcs(A0 + kKB * (t + 16 * j));
+  }
   for (int i = 0; tile < ntiles; ++i, tile += gridDim.x) {
     const int zt = tile % nzt, r = tile / nzt, kb = r % nkb, c = r / nkb;
     const int z0 = zt * TZ, kx0 = kb * kKB, kx = kx0 + kl;
     double2* Arow = a.A + aidx(a.HxA, N, a.Nz, c, z0 + zz, 0, kx0) + kl;   // element y at Arow[kKB * y]
-    double2 v[16];
     if (!INV) {
       double2* ls = sm + (size_t)l * kYLine;
-#pragma unroll
-      for (int j = 0; j < 16; ++j) v[j] = __ldcs(Arow + kKB * (t + 16 * j));
       dft16<false>(v);
 #pragma unroll
       for (int k2 = 1; k2 < 16; ++k2) v[k2] = cmul(v[k2], ld_tw(tw + (k2 - 1) * 16 + t));
@@ -574,6 +583,12 @@ __global__ void __launch_bounds__(256, 2) k_yreg256(YArgs a) {
 #pragma unroll
       for (int k1 = 0; k1 < 16; ++k1) ls[k1 * kZRowPad + t] = v[k1];
       __syncthreads();
+      const int tn = tile + gridDim.x;
+      if (tn < ntiles) {
+        const double2* An = arow_of(tn);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] = __ldcs(An + kKB * (t + 16 * j));
+      }
       // B side: z fastest
       for (int idx = threadIdx.x; idx < 2 * N * TZ; idx += blockDim.x) {
         const int z2 = idx % TZ, ky = (idx / TZ) & (N - 1), k2l = idx / (TZ * N);
