@@ -761,18 +761,31 @@ __global__ void __launch_bounds__(512, 2) k_yreg512(YArgs a) {
   const int nzt = a.Nz / TZ, nkb = a.HxA / kKB;
   const int ntiles = a.ncomp * nkb * nzt;
   __syncthreads();
+  double2 v[8];
+  auto arow_of = [&](int tl) {
+    const int zt = tl % nzt, r = tl / nzt, kb = r % nkb, c = r / nkb;
+    return a.A + aidx(a.HxA, N, a.Nz, c, zt * TZ + zz, 0, kb * kKB) + kl;
+  };
+  if (!INV && (int)blockIdx.x < ntiles) {
+    const double2* A0 = arow_of(blockIdx.x);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = __ldcs(A0 + kKB * (t + 64 * j));
+  }
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int zt = tile % nzt, r = tile / nzt, kb = r % nkb, c = r / nkb;
     const int z0 = zt * TZ, kx0 = kb * kKB, kx = kx0 + kl;
     double2* Arow = a.A + aidx(a.HxA, N, a.Nz, c, z0 + zz, 0, kx0) + kl;   // element y at Arow[kKB * y]
-    double2 v[8];
     if (!INV) {
-#pragma unroll
-      for (int j = 0; j < 8; ++j) v[j] = __ldcs(Arow + kKB * (t + 64 * j));
       fft512_reg<false>(v, t, ls, tw1, tw2);     // v[kc] = X[ky = t + 64 kc]
 #pragma unroll
       for (int kc = 0; kc < 8; ++kc) ls[kc * 65 + t] = v[kc];
       __syncthreads();
+      const int tn = tile + gridDim.x;           // next tile's A rows in flight during the stores
+      if (tn < ntiles) {
+        const double2* An = arow_of(tn);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = __ldcs(An + kKB * (t + 64 * j));
+      }
       for (int idx = threadIdx.x; idx < 2 * N * TZ; idx += blockDim.x) {
         const int z2 = idx % TZ, ky = (idx / TZ) & (N - 1), k2l = idx / (TZ * N);
         const int kxo = kx0 + k2l;
