@@ -333,10 +333,13 @@ static fgd_status cg_mech(fgd_ctx* c, const double* b, double* x_out, double tol
   TRY(ensure_cg(c));
   TRY(ensure_spectral(c));
   const size_t n6 = 6 * c->nvox;
-  FGD_CUDA(c, cudaMemsetAsync(c->cg_x, 0, n6 * 8, c->stream));
-  FGD_CUDA(c, cudaMemsetAsync(c->cg_p, 0, n6 * 8, c->stream));
-  FGD_CUDA(c, cudaMemcpyAsync(c->cg_r, b, n6 * 8, cudaMemcpyDeviceToDevice, c->stream));
-  TRY(launch_dot(c, n6, c->cg_r, c->cg_r, RED(RED_MECH_INIT)));
+  // r_0 = b is never copied: the first tangent pass reads b as r (p_1 = b, x_1 = 0, no memsets)
+  // and the first inverse pass writes r_1 = b - alpha q into cg_r.
+  if (((uintptr_t)b & 15) != 0) {
+    FGD_CUDA(c, cudaMemcpyAsync(c->cg_r, b, n6 * 8, cudaMemcpyDeviceToDevice, c->stream));
+    b = c->cg_r;
+  }
+  TRY(launch_dot(c, n6, b, b, RED(RED_MECH_INIT)));
   TRY(post_reduce(c, RED_MECH_INIT));
   double bb = 0.0;
   TRY(sync_read(c, &c->sc->bb, 8, &bb));
@@ -345,15 +348,16 @@ static fgd_status cg_mech(fgd_ctx* c, const double* b, double* x_out, double tol
   if (bb > 0.0) {
     rel = 1.0;
     while (it < maxit) {
-      TRY(launch_xfwd_io(c, 6, XF_TANGENT_CG, c->cg_r, nullptr, c->cg_p, c->cg_x, c->compact ? c->Cc : c->C,
-                         RED(RED_MECH_PQ)));
+      const bool first = it == 0;
+      TRY(launch_xfwd_io(c, 6, XF_TANGENT_CG, first ? b : c->cg_r, nullptr, c->cg_p, c->cg_x,
+                         c->compact ? c->Cc : c->C, RED(RED_MECH_PQ), first ? 1 : 0));
       TRY(launch_yfwd(c, 6));
       TRY(exchange(c, 6, true));
       TRY(launch_z(c, 6, Z_PROJECT, inv_nvox(c), nullptr, 0.0));
       TRY(exchange(c, 6, false));
       TRY(post_reduce(c, RED_MECH_PQ));
       TRY(launch_yinv(c, 6));
-      TRY(launch_xinv(c, 6, XI_MECH_CG, nullptr, nullptr, c->cg_r, nullptr, RED(RED_MECH_RR)));
+      TRY(launch_xinv(c, 6, XI_MECH_CG, nullptr, nullptr, c->cg_r, first ? b : c->cg_r, RED(RED_MECH_RR)));
       TRY(post_reduce(c, RED_MECH_RR));
       ++it;
       if (tol > 0.0) {
@@ -370,6 +374,7 @@ static fgd_status cg_mech(fgd_ctx* c, const double* b, double* x_out, double tol
     }
     if (it > 0) TRY(launch_axpy_alpha(c, n6, c->cg_x, c->cg_p));   // x += alpha_last p_last
   }
+  if (it == 0) FGD_CUDA(c, cudaMemsetAsync(c->cg_x, 0, n6 * 8, c->stream));   // b = 0 or maxit = 0
   if (x_out) FGD_CUDA(c, cudaMemcpyAsync(x_out, c->cg_x, n6 * 8, cudaMemcpyDeviceToDevice, c->stream));
   if (iters) *iters = it;
   if (relres) *relres = rel;

@@ -206,7 +206,7 @@ struct KTimer {
 fgd_status launch_xfwd(fgd_ctx* c, int ncomp, int mode, const double* in0, const double* in1, double* out0,
                        const double* Cp, int red_op, int red_slot);
 fgd_status launch_xfwd_io(fgd_ctx* c, int ncomp, int mode, const double* in0, const double* in1, double* out0,
-                          double* io1, const double* Cp, int red_op, int red_slot);
+                          double* io1, const double* Cp, int red_op, int red_slot, int first = 0);
 fgd_status launch_yfwd(fgd_ctx* c, int ncomp);
 fgd_status launch_z(fgd_ctx* c, int ncomp, int mode, double scale, const double* dc_shift, double mean_ell2);
 fgd_status launch_yinv(fgd_ctx* c, int ncomp);
@@ -262,7 +262,8 @@ enum XFwdMode : int {
 enum ZMode : int { Z_PROJECT = 0, Z_PRECOND = 1 };
 enum XInvMode : int {
   XI_STORE = 0,        // out0 = q
-  XI_MECH_CG = 1,      // r(io2) -= alpha q ; reduce r.r   (x is updated one step late, in XF_TANGENT_CG)
+  XI_MECH_CG = 1,      // r(io2) = r_old(in1) - alpha q ; reduce r.r  (x is updated one step late, in
+                       // XF_TANGENT_CG; in1 = b on the first step, = io2 afterwards)
   XI_HELM_Z = 2,       // z(out0) = q ; reduce r(in3).q
   XI_STORE_RR = 3,     // out0 = q ; reduce q.q
 };

@@ -186,6 +186,7 @@ __global__ void __launch_bounds__(kMaxThr, 2) k_xfwd(XArgs a, const double2* __r
 // line transforms and stores the half spectra as one contiguous block per component.
 struct XTArgs {
   int Ny, Nz, HxA, CW, S, R;   // chunk width, stages, rows per tile
+  int first;                   // CG step 1: p = r, x = 0 (p_old and x are neither read nor needed)
   size_t nvox;
   double* r;           // CG: residual (in)                      HELM: r (in/out)
   double* p;           // CG: direction (in/out); TANGENT: operand  HELM: p (in)
@@ -278,12 +279,14 @@ __global__ void __launch_bounds__(256) k_xtan(XTArgs a) {
     double* dst = stg + (size_t)(q % S) * NOP * CW;
     uint64_t* bar = &bars[q % S];
     const unsigned bytes = CW * 8;
+    const bool skip_px = MODE == XF_TANGENT_CG && a.first;   // rows 6..17 (p_old, x) not needed
     if (threadIdx.x == 0) {
       fence_proxy_async();
-      mbar_arrive_expect_tx(bar, bytes * NOP);
+      mbar_arrive_expect_tx(bar, bytes * (skip_px ? NOP - 12 : NOP));
     }
     __syncwarp();
     for (int i = threadIdx.x; i < NOP; i += 32) {
+      if (skip_px && i >= 6 && i < 18) continue;
       const double* src;
       if (MODE == XF_TANGENT_CG)
         src = i < 6 ? a.r + i * n : i < 12 ? a.p + (i - 6) * n : i < 18 ? a.x + (i - 12) * n : a.C + (i - 18) * n;
@@ -322,12 +325,21 @@ __global__ void __launch_bounds__(256) k_xtan(XTArgs a) {
         double p[6], tv[6];
         if (MODE == XF_TANGENT_CG) {
           // CG with the solution update one step late (x += alpha_{k-1} p_{k-1}); see cg_mech
+          if (a.first) {
 #pragma unroll
-          for (int c = 0; c < 6; ++c) {
-            const double po = st[(6 + c) * CW + v];
-            a.x[c * n + g] = fma(alpha, po, st[(12 + c) * CW + v]);
-            p[c] = fma(beta, po, st[c * CW + v]);
-            a.p[c * n + g] = p[c];
+            for (int c = 0; c < 6; ++c) {
+              a.x[c * n + g] = 0.0;
+              p[c] = st[c * CW + v];
+              a.p[c * n + g] = p[c];
+            }
+          } else {
+#pragma unroll
+            for (int c = 0; c < 6; ++c) {
+              const double po = st[(6 + c) * CW + v];
+              a.x[c * n + g] = fma(alpha, po, st[(12 + c) * CW + v]);
+              p[c] = fma(beta, po, st[c * CW + v]);
+              a.p[c * n + g] = p[c];
+            }
           }
         } else {
 #pragma unroll
@@ -448,7 +460,7 @@ static int sm_count() {
 // returns FGD_OK and *done = false when the bulk-copy path does not apply (alignment)
 // operands: CG (r, p, x, C); TANGENT (-, p, -, C); HELM (r, p, x, q in C)
 static fgd_status launch_xtan(fgd_ctx* c, int mode, double* r, double* p, double* x, const double* Cp,
-                              int red_op, int red_slot, bool* done) {
+                              int red_op, int red_slot, bool* done, int first) {
   *done = false;
   const int Nx = c->n[0], Ny = c->n[1];
   const bool cmp = mode != XF_HELM_UPDATE && Cp == c->Cc;
@@ -482,7 +494,7 @@ static fgd_status launch_xtan(fgd_ctx* c, int mode, double* r, double* p, double
   if (s_env >= 2 && s_env <= 8) S = s_env;
   const size_t smem = fixed + S * stage;
   if (smem > 227 * 1024) return FGD_OK;
-  XTArgs a{Ny, c->nz_l, c->HxA, CW, S, R, c->nvox, r, p, x, Cp, c->specA, c->sc, c->partials, red_op, red_slot,
+  XTArgs a{Ny, c->nz_l, c->HxA, CW, S, R, first, c->nvox, r, p, x, Cp, c->specA, c->sc, c->partials, red_op, red_slot,
            c->tabs.tw[ilog2(Nx / 2)], c->tabs.tw[ilog2(Nx)]};
   const int ntiles = (Ny / R) * c->nz_l;
   KTimer kt(c, helm ? KC_XFWD1 : KC_XFWD6);
@@ -519,19 +531,24 @@ fgd_status launch_xfwd(fgd_ctx* c, int ncomp, int mode, const double* in0, const
 }
 
 fgd_status launch_xfwd_io(fgd_ctx* c, int ncomp, int mode, const double* in0, const double* in1, double* out0,
-                          double* io1, const double* Cp, int red_op, int red_slot) {
+                          double* io1, const double* Cp, int red_op, int red_slot, int first) {
   if (mode == XF_PLAIN && ((uintptr_t)in0 & 15) == 0) return pipe_xfwd_plain(c, ncomp, in0);
   if (((ncomp == 6 && (mode == XF_TANGENT || mode == XF_TANGENT_CG)) || (ncomp == 1 && mode == XF_HELM_UPDATE)) &&
       !std::getenv("FGD_NO_XTAN")) {
     bool done = false;
     fgd_status s;
     if (mode == XF_TANGENT_CG)
-      s = launch_xtan(c, mode, const_cast<double*>(in0), out0, io1, Cp, red_op, red_slot, &done);
+      s = launch_xtan(c, mode, const_cast<double*>(in0), out0, io1, Cp, red_op, red_slot, &done, first);
     else if (mode == XF_TANGENT)
-      s = launch_xtan(c, mode, nullptr, const_cast<double*>(in0), nullptr, Cp, red_op, red_slot, &done);
+      s = launch_xtan(c, mode, nullptr, const_cast<double*>(in0), nullptr, Cp, red_op, red_slot, &done, 0);
     else   // HELM: x(out0) += alpha p(in0); r(io1) -= alpha q(in1)
-      s = launch_xtan(c, mode, io1, const_cast<double*>(in0), out0, in1, red_op, red_slot, &done);
+      s = launch_xtan(c, mode, io1, const_cast<double*>(in0), out0, in1, red_op, red_slot, &done, 0);
     if (s != FGD_OK || done) return s;
+  }
+  if (first && mode == XF_TANGENT_CG) {
+    // generic path: p_old = x = 0 make the update exact (alpha = beta = 0 after RED_MECH_INIT)
+    FGD_CUDA(c, cudaMemsetAsync(out0, 0, 6 * c->nvox * sizeof(double), c->stream));
+    FGD_CUDA(c, cudaMemsetAsync(io1, 0, 6 * c->nvox * sizeof(double), c->stream));
   }
   const int Nx = c->n[0], Ny = c->n[1], Nz = c->nz_l;
   const int TY = choose_TY(Nx, ncomp, Ny);

@@ -1010,7 +1010,7 @@ __device__ __forceinline__ void xi_issue(const XPArgs& a, int t, double2* buf, d
   }
   if constexpr (xi_prefetch<N, MODE>()) {
     // rows y0 .. y0 + TY - 1 of plane z are contiguous: TY * N doubles
-    const double* src = (MODE == XI_MECH_CG ? a.io2 : a.in0) + (size_t)c * a.nvox + ((size_t)z * a.Ny + y0) * N;
+    const double* src = a.in0 + (size_t)c * a.nvox + ((size_t)z * a.Ny + y0) * N;
     for (int idx = threadIdx.x; idx < TY * N / 2; idx += blockDim.x) cp_async16(ebuf + 2 * idx, src + 2 * idx);
   }
 }
@@ -1065,7 +1065,7 @@ __global__ void __launch_bounds__(N == 256 ? 128 : 256, N == 256 ? 3 : 2) k_xipi
         // epilogue operand (r) of this thread's 16 output pairs, in flight during the FFT
         double2 ro[16];
         if (MODE == XI_MECH_CG || MODE == XI_HELM_Z) {
-          const double* rs = (MODE == XI_MECH_CG ? a.io2 : a.in0) + grow;
+          const double* rs = a.in0 + grow;
 #pragma unroll
           for (int h = 0; h < 16; ++h) {
             const int nn = (h < 8 ? tt : tt + 8) + 16 * (h & 7);
@@ -1419,7 +1419,7 @@ fgd_status pipe_xinv(fgd_ctx* c, int ncomp, int mode, double* out0, double* io1,
   const bool pre = (mode == XI_MECH_CG || mode == XI_HELM_Z) && Nx != 256;
   const size_t smem = (2 * (size_t)TY * xline(Nx / 2) + Nx / 2 + Nx + (Nx == 256 ? 120 : 0)) * sizeof(double2) +
                       (pre ? 2 * (size_t)TY * Nx * sizeof(double) : 0);
-  const double* eop = mode == XI_MECH_CG ? io2 : in1;
+  const double* eop = in1;
   if (pre && ((uintptr_t)eop & 15) != 0) return set_err(c, FGD_EINVAL, "xinv: epilogue operand not 16 B aligned");
   const int ntiles = ncomp * Nz * (Ny / TY);
   XPArgs a{Ny, Nz, TY, ncomp, ilog2(TY), c->HxA, c->nvox, c->specA, in1, out0, io1, io2, c->sc, nullptr, red_op, red_slot,
