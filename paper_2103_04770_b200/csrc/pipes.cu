@@ -1282,8 +1282,10 @@ fgd_status pipe_y(fgd_ctx* c, int ncomp, bool inv) {
     return FGD_OK;
   }
   if (Ny == 256 && !std::getenv("FGD_NO_YREG")) {
-    // fwd: 8 planes per tile (128 B runs on the B side); inv: 4 planes, double-buffered staging
-    const int TZ = std::min(inv ? 4 : 8, std::min(Nz, c->n[2] / c->P));
+    // fwd: 8 planes per tile (128 B runs on the B side); inv: 4 planes, double-buffered staging.
+    // One component: 4 planes in both directions (2112 tiles of 8 planes would leave the
+    // persistent grid 7.1 tiles per CTA, i.e. a 11 % tail)
+    const int TZ = std::min((inv || ncomp == 1) ? 4 : 8, std::min(Nz, c->n[2] / c->P));
     const int thr = 32 * TZ;
     const size_t smem = ((inv ? 2 : 1) * (size_t)2 * TZ * kYLine + 240) * sizeof(double2);
     const int ntiles = ncomp * (c->HxA / kKB) * (Nz / TZ);
