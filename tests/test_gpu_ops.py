@@ -124,6 +124,35 @@ def test_mech_cg(n):
     assert it7 == 7 and rel(out.cpu().numpy(), ref7) <= 1e-10
 
 
+@pytest.mark.parametrize("n", [(256, 8, 8), (512, 4, 8), (8, 256, 256), (4, 512, 8), (4, 8, 512)])
+def test_krylov_iterates_specialised_sizes(n):
+    """Fixed-iteration CG and PCG iterates at sizes that select the 256/512-point specialisations:
+    bulk-copy tangent/PCG x passes with register FFTs (N1 = 256, 512), register y/z FFTs (N2, N3 =
+    256 or 512), the register x-inverse epilogue (N1 = 256), the first-step CG path (no r = b copy)."""
+    ctx, g = make_ctx(n)
+    mask = (1, 1, 0, 1, 1, 1)
+    ctx.set_control(mask)
+    Cp = random_spd_tangent(g.nvox, 8)
+    ctx.set_tangent(dev(Cp))
+    C = unpack21(Cp).reshape((6, 6) + g.shape)
+    b = apply_projection(g, gaussian_field(6, g.shape, 1.0, 9), mask)
+    out = torch.empty((6,) + g.shape, dtype=torch.float64, device="cuda")
+    for k in (1, 2, 6):
+        it, _ = ctx.solve_tangent_cg(dev(b), out, tol=0.0, maxit=k)
+        ref, _, _ = cg(g, C, b, mask, tol=0.0, maxit=k)
+        assert it == k and rel(out.cpu().numpy(), ref) <= 1e-10, k
+    ph = bernoulli_phases(g.shape, 0.25, 3)
+    ctx.set_phases(dev(ph), 2)
+    ell = [0.05, 0.001]
+    ctx.set_nonlocal(np.array([ell]), [0])
+    e2 = ell2_field(ph, ell)
+    src = np.random.default_rng(8).random(g.shape)
+    o = torch.empty(g.shape, dtype=torch.float64, device="cuda")
+    it, _ = ctx.solve_helmholtz(0, dev(src), o, tol=0.0, maxit=4)
+    ref4, _, _ = solve_helmholtz(g, src, e2, tol=0.0, maxit=4)
+    assert it == 4 and rel(o.cpu().numpy(), ref4) <= 1e-10
+
+
 def test_errors_and_edge_cases():
     from paper_2103_04770_b200 import FgdError
     with pytest.raises(FgdError):
