@@ -106,10 +106,30 @@ struct Stage {
     cudaError_t e = cudaMallocAsync(&d, count * sizeof(T) + 16, c->stream);
     if (e != cudaSuccess) return set_err(c, FGD_ENOMEM, std::string("staging: ") + cudaGetErrorString(e));
     bufs.push_back(d);
-    e = cudaMemcpyAsync(d, p, count * sizeof(T), cudaMemcpyHostToDevice, c->stream);
+    e = h2d(d, p, count * sizeof(T));
     if (e != cudaSuccess) return set_err(c, FGD_ECUDA, std::string("H2D: ") + cudaGetErrorString(e));
     *out = (const T*)d;
     return FGD_OK;
+  }
+  // Large host->device copies are split in two halves on two streams (the context stream and an
+  // auxiliary one ordered by events), so that two copy engines share the PCIe link.
+  cudaError_t h2d(void* d, const void* p, size_t bytes) {
+    if (bytes < ((size_t)64 << 20)) return cudaMemcpyAsync(d, p, bytes, cudaMemcpyHostToDevice, c->stream);
+    cudaError_t e = cudaSuccess;
+    if (!c->aux) {
+      e = cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->aux_ev[0], cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->aux_ev[1], cudaEventDisableTiming);
+      if (e != cudaSuccess) return e;
+    }
+    const size_t h = (bytes / 2 + 255) & ~(size_t)255;
+    if ((e = cudaEventRecord(c->aux_ev[0], c->stream)) != cudaSuccess) return e;
+    if ((e = cudaStreamWaitEvent(c->aux, c->aux_ev[0], 0)) != cudaSuccess) return e;
+    if ((e = cudaMemcpyAsync((char*)d + h, (const char*)p + h, bytes - h, cudaMemcpyHostToDevice, c->aux)) != cudaSuccess)
+      return e;
+    if ((e = cudaEventRecord(c->aux_ev[1], c->aux)) != cudaSuccess) return e;
+    if ((e = cudaMemcpyAsync(d, p, h, cudaMemcpyHostToDevice, c->stream)) != cudaSuccess) return e;
+    return cudaStreamWaitEvent(c->stream, c->aux_ev[1], 0);
   }
   // out(): device destination for a result that must end in p (copied back by finish()).
   struct Pending {
@@ -471,6 +491,9 @@ void fgd_destroy(fgd_ctx* c) {
   if (c->pinned) cudaFreeHost(c->pinned);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+  if (c->aux) cudaStreamDestroy(c->aux);
+  for (cudaEvent_t e : c->aux_ev)
+    if (e) cudaEventDestroy(e);
   dist_destroy(c);
   if (c->specC) cudaFree(c->specC);
   if (c->halo) cudaFree(c->halo);

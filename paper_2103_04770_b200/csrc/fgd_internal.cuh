@@ -114,6 +114,8 @@ struct fgd_ctx {
   size_t nspecA = 0;           // HxA * Ny * Nz
   int device = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t aux = nullptr;           // second copy stream for split host<->device staging
+  cudaEvent_t aux_ev[2] = {nullptr, nullptr};
   bool own_stream = false;
   std::string err;
   unsigned long long launches = 0;
