@@ -500,6 +500,191 @@ __global__ void __launch_bounds__(NC == 6 ? 96 : 128) __maxnreg__(NC == 6 ? 128 
 }
 
 // ---------------------------------------------------------------------------------------------
+// Z pass with the Galerkin projection for the Willot scheme, Nz = 256: factorised form
+// ---------------------------------------------------------------------------------------------
+// Along a z line (fixed kx, ky) the rotated symbol factors as k_j(kz) = A_j m_j(kz) with per-line
+// constants A_0 = (e^{ith1}-1)(1+e^{ith2})/(4h1), A_1 = (1+e^{ith1})(e^{ith2}-1)/(4h2),
+// A_2 = (1+e^{ith1})(1+e^{ith2})/(4h3) and m_0 = m_1 = 1 + e^{ith3}, m_2 = e^{ith3} - 1 (A-04).
+// Multiplying by e^{+ith3} is a shift z -> z+1, by e^{-ith3} a shift z -> z-1.  G^* needs tau only
+// through t = tau^ conj(k) and returns sym(u (x) k):
+//   t_i = F_z[d_i],   d_i(z) = sum_j conj(A_j) (tau_ij(z) + tau_ij(z-1))   (j = 0, 1)
+//                                      + conj(A_2) (tau_i2(z-1) - tau_i2(z))
+//   u_i = (2/|k|^2)(t_i - k_i s / (2|k|^2)),  s = conj(k) . t          (per kz)
+//   U_i = F_z^{-1}[u_i],  eps_ij(z) = (A_j (U_i * m_j)(z) + A_i (U_j * m_i)(z)) / 2
+//   with (U * m_0)(z) = U(z) + U(z+1), (U * m_2)(z) = U(z+1) - U(z).
+// So each line transforms 3 components each way instead of 6 (exactly the same operator; only the
+// association order of the sums changes).  Opt-in (FGD_ZFAC=1), see pipe_z.  The zero frequency (line kx = ky = 0, kz = 0) takes the
+// mask branch: eps_c += mask_c (sum_z tau_c - N shift_c) scale on every z of that line.
+__global__ void __launch_bounds__(96, 5) k_zfac256(ZPArgs a) {
+  extern __shared__ double2 sm[];
+  constexpr int N = 256;
+  constexpr double HS2 = 0.70710678118654752440;   // sqrt(2)/2 = 1/sqrt(2)
+  double2* tw = sm + 6 * kZLine;                    // W256^{t k2} at (k2 - 1) * 16 + t
+  double2* tws = tw + 240;                          // e^{-2 pi i m / 256}
+  pdl_trigger();
+  for (int i = threadIdx.x; i < 240; i += blockDim.x) tw[i] = __ldg(&a.twz[(i & 15) * (1 + (i >> 4))]);
+  load_table(tws, a.twz, N);
+  __syncthreads();
+  pdl_wait();
+  const int line = threadIdx.x >> 4, t = threadIdx.x & 15;   // line = Mandel component in phases A, B, G
+  double2* ls = sm + (size_t)line * kZLine;
+  const int ntiles = a.Hx * a.Nyl;
+  const int BS = 6 * a.Hx * a.SL.nys * a.SL.nzs, zm = a.SL.nzs - 1, lgz = a.SL.lg_nzs;
+  auto slot = [](int z) { return z + (z >> 4); };
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int kx = tile / a.Nyl, kyl = tile % a.Nyl;
+    const int ky = kyl + a.ky_off;
+    double2* Bl = a.B + r_index(a.SL, 6, a.Hx, line, kx, kyl, 0);
+    // per-line symbol factors
+    const double2 wx = __ldg(&a.twx[kx]), wy = __ldg(&a.twy[ky]);
+    const double2 ex = make_double2(wx.x, -wx.y), ey = make_double2(wy.x, -wy.y);
+    const double2 A0 = cscale(cmul(make_double2(ex.x - 1.0, ex.y), make_double2(ey.x + 1.0, ey.y)), a.qh[0]);
+    const double2 A1 = cscale(cmul(make_double2(ex.x + 1.0, ex.y), make_double2(ey.x - 1.0, ey.y)), a.qh[1]);
+    const double2 A2 = cscale(cmul(make_double2(ex.x + 1.0, ex.y), make_double2(ey.x + 1.0, ey.y)), a.qh[2]);
+    // ---- A: load tau_c(z), z = t + 16 j; B: to shared memory (natural z) ----
+    double2 v[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int z = t + 16 * j;
+      v[j] = __ldcg(Bl + ((z >> lgz) * BS + (z & zm)));
+    }
+    double2 tsum = make_double2(0.0, 0.0);
+    const bool dcline = kx == 0 && ky == 0;
+    if (dcline) {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) tsum = cadd(tsum, v[j]);
+#pragma unroll
+      for (int o = 8; o >= 1; o >>= 1) {
+        tsum.x += __shfl_xor_sync(0xffffffffu, tsum.x, o, 16);
+        tsum.y += __shfl_xor_sync(0xffffffffu, tsum.y, o, 16);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 16; ++j) ls[slot(t + 16 * j)] = v[j];
+    __syncthreads();
+    // ---- C: d_i(z) for i = line < 3 ----
+    const int i = line;
+    if (i < 3) {
+      // tensor row i in Mandel storage: (comp, factor) of tau_i0, tau_i1, tau_i2
+      const int c0 = i == 0 ? 0 : i == 1 ? 5 : 4;
+      const int c1 = i == 0 ? 5 : i == 1 ? 1 : 3;
+      const int c2 = i == 0 ? 4 : i == 1 ? 3 : 2;
+      const double f0 = i == 0 ? 1.0 : HS2, f1 = i == 1 ? 1.0 : HS2, f2 = i == 2 ? 1.0 : HS2;
+      const double2 B0 = cscale(conjg(A0), f0), B1 = cscale(conjg(A1), f1), B2 = cscale(conjg(A2), f2);
+      const double2* L0 = sm + (size_t)c0 * kZLine;
+      const double2* L1 = sm + (size_t)c1 * kZLine;
+      const double2* L2 = sm + (size_t)c2 * kZLine;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int z = t + 16 * j, zp = (z - 1) & (N - 1);
+        const double2 g0 = cadd(L0[slot(z)], L0[slot(zp)]);
+        const double2 g1 = cadd(L1[slot(z)], L1[slot(zp)]);
+        const double2 g2 = csub(L2[slot(zp)], L2[slot(z)]);
+        v[j] = cadd(cadd(cmul(B0, g0), cmul(B1, g1)), cmul(B2, g2));
+      }
+    }
+    __syncthreads();
+    // ---- D: forward z FFT of d_i (lines 0..2) -> t_i(kz = t + 16 k1) ----
+    if (i < 3) {
+      dft16<false>(v);
+#pragma unroll
+      for (int k2 = 1; k2 < 16; ++k2) v[k2] = cmul(v[k2], ld_tw(tw + (k2 - 1) * 16 + t));
+#pragma unroll
+      for (int k2 = 0; k2 < 16; ++k2) ls[k2 * kZRowPad + t] = v[k2];
+      __syncwarp(0x0000ffffu << (16 * (threadIdx.x >> 4 & 1)));
+#pragma unroll
+      for (int n1 = 0; n1 < 16; ++n1) v[n1] = ls[t * kZRowPad + n1];
+      dft16<false>(v);
+      __syncwarp(0x0000ffffu << (16 * (threadIdx.x >> 4 & 1)));
+#pragma unroll
+      for (int k1 = 0; k1 < 16; ++k1) ls[slot(t + 16 * k1)] = v[k1];
+    }
+    __syncthreads();
+    // ---- E: per kz: u = (2/|k|^2)(t - k s/(2|k|^2)) scale, in place on lines 0..2 ----
+    for (int kz = threadIdx.x; kz < N; kz += blockDim.x) {
+      const double2 wz = tws[kz];
+      const double2 cz = make_double2(wz.x + 1.0, -wz.y), dz = make_double2(wz.x - 1.0, -wz.y);
+      const double2 k0 = cmul(A0, cz), k1 = cmul(A1, cz), k2 = cmul(A2, dz);
+      const double kk = k0.x * k0.x + k0.y * k0.y + k1.x * k1.x + k1.y * k1.y + k2.x * k2.x + k2.y * k2.y;
+      double2* p0 = sm + slot(kz);
+      double2* p1 = p0 + kZLine;
+      double2* p2 = p1 + kZLine;
+      if (kk == 0.0) {
+        *p0 = *p1 = *p2 = make_double2(0.0, 0.0);
+      } else {
+        const double2 t0 = *p0, t1 = *p1, t2 = *p2;
+        const double2 sv = cadd(cadd(cmul(conjg(k0), t0), cmul(conjg(k1), t1)), cmul(conjg(k2), t2));
+        const double inv = 1.0 / kk;
+        const double2 hs = cscale(sv, 0.5 * inv);
+        const double f = 2.0 * inv * a.scale;
+        *p0 = cscale(csub(t0, cmul(k0, hs)), f);
+        *p1 = cscale(csub(t1, cmul(k1, hs)), f);
+        *p2 = cscale(csub(t2, cmul(k2, hs)), f);
+      }
+    }
+    __syncthreads();
+    // ---- F: inverse z FFT of u_i -> U_i(z), back to shared memory (natural z) ----
+    if (i < 3) {
+#pragma unroll
+      for (int k1 = 0; k1 < 16; ++k1) v[k1] = ls[slot(t + 16 * k1)];
+      dft16<true>(v);
+#pragma unroll
+      for (int n1 = 1; n1 < 16; ++n1) {
+        double2 wv = ld_tw(tw + (n1 - 1) * 16 + t);
+        wv.y = -wv.y;
+        v[n1] = cmul(v[n1], wv);
+      }
+      __syncwarp(0x0000ffffu << (16 * (threadIdx.x >> 4 & 1)));
+#pragma unroll
+      for (int n1 = 0; n1 < 16; ++n1) ls[n1 * kZRowPad + t] = v[n1];
+      __syncwarp(0x0000ffffu << (16 * (threadIdx.x >> 4 & 1)));
+#pragma unroll
+      for (int k2 = 0; k2 < 16; ++k2) v[k2] = ls[t * kZRowPad + k2];
+      dft16<true>(v);                               // v[n2] = U_i(z = t + 16 n2)
+      __syncwarp(0x0000ffffu << (16 * (threadIdx.x >> 4 & 1)));
+#pragma unroll
+      for (int n2 = 0; n2 < 16; ++n2) ls[slot(t + 16 * n2)] = v[n2];
+    }
+    __syncthreads();
+    // ---- G: eps_c(z) from U (and the zero frequency on the kx = ky = 0 line), store ----
+    {
+      const int c = line;
+      const double2* U0 = sm;
+      const double2* U1 = sm + kZLine;
+      const double2* U2 = sm + 2 * kZLine;
+      double2 dcv = make_double2(0.0, 0.0);
+      if (dcline && a.mask[c]) dcv = cscale(make_double2(tsum.x - a.shift[c], tsum.y), a.scale);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int z = t + 16 * j, zn = (z + 1) & (N - 1);
+        const int s0 = slot(z), s1 = slot(zn);
+        double2 e;
+        if (c == 0) {
+          e = cmul(A0, cadd(U0[s0], U0[s1]));
+        } else if (c == 1) {
+          e = cmul(A1, cadd(U1[s0], U1[s1]));
+        } else if (c == 2) {
+          e = cmul(A2, csub(U2[s1], U2[s0]));
+        } else if (c == 3) {   // sqrt2 eps_12 = (A2 (U1 * m2) + A1 (U2 * m1)) / sqrt2
+          e = cscale(cadd(cmul(A2, csub(U1[s1], U1[s0])), cmul(A1, cadd(U2[s0], U2[s1]))), HS2);
+        } else if (c == 4) {   // sqrt2 eps_02
+          e = cscale(cadd(cmul(A2, csub(U0[s1], U0[s0])), cmul(A0, cadd(U2[s0], U2[s1]))), HS2);
+        } else {               // sqrt2 eps_01
+          e = cscale(cadd(cmul(A1, cadd(U0[s0], U0[s1])), cmul(A0, cadd(U1[s0], U1[s1]))), HS2);
+        }
+        v[j] = cadd(e, dcv);
+      }
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int z = t + 16 * j;
+        Bl[(z >> lgz) * BS + (z & zm)] = v[j];
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
 // Y pass for Ny = 256 as a register four-step FFT (256 = 16 x 16), as the z pass below
 // ---------------------------------------------------------------------------------------------
 // Tile = (c, kx pair kx0 = kKB kb, TZ planes z0..): 2 TZ lines; warp w handles plane z0 + w, its
@@ -1377,7 +1562,12 @@ fgd_status pipe_z(fgd_ctx* c, int ncomp, int mode, double scale, const double* d
     const int thr_r = 16 * ncomp * TLr;
     const size_t smem_r = ((size_t)ncomp * TLr * kZLine + 240 + 256) * sizeof(double2);
     const int nt_r = c->Hx * (Nyl / TLr);
-    if (ncomp == 6) FGD_PLAUNCH(c, (k_zreg256<6, Z_PROJECT>), thr_r, smem_r, nt_r, a);
+    // factorised form (3 transformed components each way) is opt-in: measured 7.66 vs 4.72 ms per
+    // 256^3 sweep -- its serial phases leave half of the CTA idle and spill; the FP64 saving does
+    // not pay for that at this occupancy
+    if (ncomp == 6 && c->scheme == 1 && TLr == 1 && std::getenv("FGD_ZFAC"))
+      FGD_PLAUNCH(c, k_zfac256, 96, smem_r, nt_r, a);
+    else if (ncomp == 6) FGD_PLAUNCH(c, (k_zreg256<6, Z_PROJECT>), thr_r, smem_r, nt_r, a);
     else FGD_PLAUNCH(c, (k_zreg256<1, Z_PRECOND>), thr_r, smem_r, nt_r, a);
     return FGD_OK;
   }

@@ -351,3 +351,22 @@ def test_cluster_fused_precond(scheme, monkeypatch):
         ctx.solve_helmholtz(0, dev(np.abs(a)), o, tol=0.0, maxit=4)
         ref, _, _ = solve_helmholtz(g, np.abs(a), e2, tol=0.0, maxit=4)
         assert rel(o.cpu().numpy(), ref) <= 1e-10
+
+
+@pytest.mark.parametrize("n", [(8, 16, 256), (4, 8, 256)])
+def test_factorised_z_projection(n, monkeypatch):
+    """Opt-in factorised z pass (FGD_ZFAC=1: Willot symbol k_j = A_j m_j(kz), 3 transformed components
+    each way): projection with a stress-mask DC and projected tangent against the oracle."""
+    monkeypatch.setenv("FGD_ZFAC", "1")
+    for mask in [(1, 1, 0, 1, 1, 1), (0, 1, 0, 0, 0, 1)]:
+        ctx, g = make_ctx(n)
+        ctx.set_control(mask)
+        tau = gaussian_field(6, g.shape, 1.0, 31)
+        S = np.array([0.3, -0.2, 0.1, 0.05, 0.0, -0.4])
+        y = ctx.apply_projection(dev(tau), S).cpu().numpy()
+        assert rel(y, apply_projection(g, tau, mask, dc_mean_shift=S)) <= TOL_APPLY
+        Cp = random_spd_tangent(g.nvox, 2)
+        ctx.set_tangent(dev(Cp))
+        x = gaussian_field(6, g.shape, 1e-3, 32)
+        yt = ctx.apply_projected_tangent(dev(x)).cpu().numpy()
+        assert rel(yt, apply_projected_tangent(g, unpack21(Cp).reshape((6, 6) + g.shape), x, mask)) <= TOL_APPLY
