@@ -693,7 +693,11 @@ __global__ void __launch_bounds__(96, 5) k_zfac256(ZPArgs a) {
 // goes through the line buffers in shared memory (line l = kl TZ + zz, conflict-free pitch).
 //   fwd: global A -> registers -> DFT16, twiddle, 16 x 16 transpose (smem), DFT16 -> smem -> B
 //   inv: B -> smem (cp.async) -> registers -> DFT16, twiddle, transpose (smem), DFT16 -> A
-constexpr int kYLine = kZLine + 1;   // 273 slots: odd pitch between lines
+constexpr int kYLine = kZLine + 2;   // max pitch between lines (see ypitch)
+// Line pitch of the y-pass line buffers: the B-side loops walk (z2 fastest, then ky), so 8
+// consecutive threads touch TZ lines x 8/TZ consecutive ky: pitch = 1 mod 8 for TZ = 8 and
+// 2 mod 8 for TZ = 4 keep those 8 16-B accesses in distinct bank groups.
+__host__ __device__ constexpr int ypitch(int base, int TZ) { return base + (TZ >= 8 ? 1 : 2); }
 
 // fwd: A rows go straight from HBM into registers (512 B per warp instruction); the line buffers
 //      hold the exchange and the B-side output staging.
@@ -710,7 +714,7 @@ __device__ __forceinline__ void y256_issue_inv(const YArgs& a, int tile, double2
     const int z2 = idx % TZ, ky = (idx / TZ) & (N - 1), k2l = idx / (TZ * N);
     const int kxo = kx0 + k2l;
     if (kxo < a.Hx)
-      cp_async16(&buf[(size_t)(k2l * TZ + z2) * kYLine + ky + (ky >> 4)],
+      cp_async16(&buf[(size_t)(k2l * TZ + z2) * ypitch(kZLine, TZ) + ky + (ky >> 4)],
                  &a.B[s_index(a.L, a.ncomp, a.Hx, c, kxo, ky, z0 + z2)]);
   }
 }
@@ -720,7 +724,8 @@ __global__ void __launch_bounds__(256, 2) k_yreg256(YArgs a) {
   extern __shared__ double2 sm[];
   constexpr int N = 256;
   const int TZ = a.TZ;                              // blockDim.x == 32 * TZ
-  const size_t buf_sz = (size_t)2 * TZ * kYLine;    // fwd: one line buffer; inv: two stage buffers
+  const int LPY = ypitch(kZLine, TZ);
+  const size_t buf_sz = (size_t)2 * TZ * LPY;       // fwd: one line buffer; inv: two stage buffers
   double2* tw = sm + (INV ? 2 : 1) * buf_sz;        // W256^{t k2} at (k2 - 1) * 16 + t
   pdl_trigger();
   for (int i = threadIdx.x; i < 240; i += blockDim.x) tw[i] = __ldg(&a.tw[(i & 15) * (1 + (i >> 4))]);
@@ -753,7 +758,7 @@ __global__ void __launch_bounds__(256, 2) k_yreg256(YArgs a) {
     const int z0 = zt * TZ, kx0 = kb * kKB, kx = kx0 + kl;
     double2* Arow = a.A + aidx(a.HxA, N, a.Nz, c, z0 + zz, 0, kx0) + kl;   // element y at Arow[kKB * y]
     if (!INV) {
-      double2* ls = sm + (size_t)l * kYLine;
+      double2* ls = sm + (size_t)l * LPY;
       dft16<false>(v);
 #pragma unroll
       for (int k2 = 1; k2 < 16; ++k2) v[k2] = cmul(v[k2], ld_tw(tw + (k2 - 1) * 16 + t));
@@ -779,7 +784,7 @@ __global__ void __launch_bounds__(256, 2) k_yreg256(YArgs a) {
         const int z2 = idx % TZ, ky = (idx / TZ) & (N - 1), k2l = idx / (TZ * N);
         const int kxo = kx0 + k2l;
         if (kxo < a.Hx)
-          a.B[s_index(a.L, a.ncomp, a.Hx, c, kxo, ky, z0 + z2)] = sm[(size_t)(k2l * TZ + z2) * kYLine + ky + (ky >> 4)];
+          a.B[s_index(a.L, a.ncomp, a.Hx, c, kxo, ky, z0 + z2)] = sm[(size_t)(k2l * TZ + z2) * LPY + ky + (ky >> 4)];
       }
       __syncthreads();
     } else {
@@ -788,7 +793,7 @@ __global__ void __launch_bounds__(256, 2) k_yreg256(YArgs a) {
       cp_async_commit();
       cp_async_wait<1>();
       __syncthreads();
-      double2* ls = sm + (i & 1) * buf_sz + (size_t)l * kYLine;
+      double2* ls = sm + (i & 1) * buf_sz + (size_t)l * LPY;
 #pragma unroll
       for (int k1 = 0; k1 < 16; ++k1) v[k1] = ls[k1 * kZRowPad + t];   // X[ky = t + 16 k1]
       dft16<true>(v);                               // v[n1] = U[k2 = t][n1]
@@ -927,14 +932,15 @@ __global__ void __launch_bounds__(NC * 64, NC == 6 ? 2 : 8) k_zreg512(ZPArgs a) 
 // Y pass, Ny = 512: tile (c, kx pair, TZ planes), 2 TZ lines of 64 threads.  Warp w carries 16
 // threads of each kx of the pair for plane zz = w / 4 (t = 16 (w % 4) + lane % 16), so that the
 // A-side loads / stores are 512 B per warp instruction.  Line l = kl TZ + zz at pitch k512Line + 1.
-constexpr int kY512Line = k512Line + 1;
+constexpr int kY512Line = k512Line + 2;   // max pitch (see ypitch)
 
 template <bool INV>
 __global__ void __launch_bounds__(512, 2) k_yreg512(YArgs a) {
   extern __shared__ double2 sm[];
   constexpr int N = 512;
   const int TZ = a.TZ;                             // blockDim.x == 128 * TZ
-  double2* tw1 = sm + (size_t)2 * TZ * kY512Line;
+  const int LPY = ypitch(k512Line, TZ);
+  double2* tw1 = sm + (size_t)2 * TZ * LPY;
   double2* tw2 = tw1 + 448;
   pdl_trigger();
   fft512_tables(tw1, tw2, a.tw);
@@ -942,7 +948,7 @@ __global__ void __launch_bounds__(512, 2) k_yreg512(YArgs a) {
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int kl = lane >> 4, t = 16 * (w & 3) + (lane & 15), zz = w >> 2;
   const int l = kl * TZ + zz;
-  double2* ls = sm + (size_t)l * kY512Line;
+  double2* ls = sm + (size_t)l * LPY;
   const int nzt = a.Nz / TZ, nkb = a.HxA / kKB;
   const int ntiles = a.ncomp * nkb * nzt;
   __syncthreads();
@@ -976,7 +982,7 @@ __global__ void __launch_bounds__(512, 2) k_yreg512(YArgs a) {
         const int kxo = kx0 + k2l;
         if (kxo < a.Hx)
           a.B[s_index(a.L, a.ncomp, a.Hx, c, kxo, ky, z0 + z2)] =
-              sm[(size_t)(k2l * TZ + z2) * kY512Line + (ky >> 6) * 65 + (ky & 63)];
+              sm[(size_t)(k2l * TZ + z2) * LPY + (ky >> 6) * 65 + (ky & 63)];
       }
       __syncthreads();
     } else {
@@ -984,7 +990,7 @@ __global__ void __launch_bounds__(512, 2) k_yreg512(YArgs a) {
         const int z2 = idx % TZ, ky = (idx / TZ) & (N - 1), k2l = idx / (TZ * N);
         const int kxo = kx0 + k2l;
         if (kxo < a.Hx)
-          cp_async16(&sm[(size_t)(k2l * TZ + z2) * kY512Line + (ky >> 6) * 65 + (ky & 63)],
+          cp_async16(&sm[(size_t)(k2l * TZ + z2) * LPY + (ky >> 6) * 65 + (ky & 63)],
                      &a.B[s_index(a.L, a.ncomp, a.Hx, c, kxo, ky, z0 + z2)]);
       }
       cp_async_commit();
