@@ -454,6 +454,17 @@ def run_ours(a):
     if world == 1 and not a.no_cufft:
         cmp_cufft = cufft_comparison(ctx, n, dev, synth.CONFIG1_MASK)
 
+    # multi-GPU: share and achieved bandwidth of the slab transposes; every operator
+    # apply moves (P-1)/P of the rank's spectrum twice (before and after the z pass)
+    comm = None
+    if world > 1 and "comm" in per_class:
+        S_loc = 16 * (n // 2 + 1) * n * n // world
+        a2a_bytes = 2 * (world - 1) / world * S_loc * (6 * (a.kcg + 1) + (a.khelm + 1))
+        cms = per_class["comm"]["ms_per_step"]
+        comm = {"ms_per_step": cms, "share": cms / ms, "alltoall_bytes_sent_per_gpu_per_step": a2a_bytes,
+                "alltoall_GBs_per_gpu": a2a_bytes / (cms * 1e-3) / 1e9 if cms else None,
+                "nvlink_GBs_per_direction": 900.0,
+                "note": "comm = NCCL all-to-all transposes + stencil z-halos + Krylov allreduces (event-timed)"}
     # per-solver rates inside the step (kernel-class times, this rank)
     t_mech = sum(per_class[k]["ms_per_step"] for k in ("xfwd6", "yfwd6", "z6", "yinv6", "xinv6") if k in per_class)
     t_helm = sum(per_class[k]["ms_per_step"] for k in ("xfwd1", "yfwd1", "z1", "yinv1", "xinv1", "stencil")
@@ -473,7 +484,7 @@ def run_ours(a):
                            "l2": "no flush: every input field (>=134 MB) and the tangent (2.8 GB) exceed the 126 MB L2"},
                 "roofline": roof, "step_roofline": step_eff, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": launches, "clocks": clk, "kernels": per_class,
-                "rates": rates, "cufft_comparison": cmp_cufft}
+                "rates": rates, "cufft_comparison": cmp_cufft, "comm": comm}
         print(json.dumps(line), flush=True)
     ctx.close()
     if world > 1:

@@ -178,8 +178,10 @@ fgd_status fgd_macro_stress(fgd_ctx* ctx, double out[6]);
  * the stream and returns, per class, the summed duration in ms and the launch count.
  * Classes: 0 x-fwd (6 comps), 1 y-fwd (6), 2 z (6), 3 y-inv (6), 4 x-inv (6), 5 x-fwd (1),
  * 6 y-fwd (1), 7 z (1), 8 y-inv (1), 9 x-inv (1), 10 Helmholtz stencil, 11 constitutive,
- * 12 other (dots, axpy, commit, error norms). */
-#define FGD_NUM_KCLASS 13
+ * 12 other (dots, axpy, commit, error norms), 13 communication (slab all-to-all transposes,
+ * stencil z-halos and Krylov allreduces when nranks > 1; the block copies of the single-GPU slab
+ * emulation). */
+#define FGD_NUM_KCLASS 14
 fgd_status fgd_set_timing(fgd_ctx* ctx, int enable);
 fgd_status fgd_kernel_times(fgd_ctx* ctx, double* ms, unsigned long long* count, int n);
 

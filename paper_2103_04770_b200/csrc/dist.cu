@@ -66,7 +66,7 @@ fgd_status exchange(fgd_ctx* c, int ncomp, bool fwd) {
   const size_t blk = (size_t)ncomp * c->Hx * (c->n[1] / P) * (c->n[2] / P);
   double2* src = fwd ? c->specB : c->specC;
   double2* dst = fwd ? c->specC : c->specB;
-  KTimer kt(c, KC_OTHER);
+  KTimer kt(c, KC_COMM);
   if (c->nranks == 1) {
     // emulated: every (r, s) block is local; S[r][s] -> R[s][r] (the map is an involution)
     for (int r = 0; r < P; ++r)
@@ -86,12 +86,14 @@ fgd_status exchange(fgd_ctx* c, int ncomp, bool fwd) {
 
 fgd_status allreduce_sum(fgd_ctx* c, double* dev, int count) {
   if (c->nranks == 1) return FGD_OK;
+  KTimer kt(c, KC_COMM);
   FGD_NCCL(c, ncclAllReduce(dev, dev, count, ncclDouble, ncclSum, comm_of(c), c->stream));
   return FGD_OK;
 }
 
 fgd_status allreduce_max_u64(fgd_ctx* c, unsigned long long* dev) {
   if (c->nranks == 1) return FGD_OK;
+  KTimer kt(c, KC_COMM);
   FGD_NCCL(c, ncclAllReduce(dev, dev, 1, ncclUint64, ncclMax, comm_of(c), c->stream));
   return FGD_OK;
 }
@@ -123,6 +125,7 @@ fgd_status halo_exchange(fgd_ctx* c, const void* field, size_t plane_bytes, void
   const int up = (c->rank + 1) % c->nranks, dn = (c->rank + c->nranks - 1) % c->nranks;
   const char* f = static_cast<const char*>(field);
   const char* last = f + (size_t)(c->nz_l - 1) * plane_bytes;
+  KTimer kt(c, KC_COMM);
   FGD_NCCL(c, ncclGroupStart());
   // order matters when up == dn (P = 2): first the plane sent up / received from below
   FGD_NCCL(c, ncclSend(last, plane_bytes, ncclChar, up, comm_of(c), c->stream));

@@ -196,7 +196,7 @@ fgd_status set_err(fgd_ctx* c, fgd_status s, const std::string& m);
 
 // scoped event timer around one kernel launch (no-op unless ctx->timing)
 enum KClass : int { KC_XFWD6 = 0, KC_YFWD6, KC_Z6, KC_YINV6, KC_XINV6, KC_XFWD1, KC_YFWD1, KC_Z1, KC_YINV1, KC_XINV1,
-                    KC_STENCIL, KC_CONST, KC_OTHER };
+                    KC_STENCIL, KC_CONST, KC_OTHER, KC_COMM };
 struct KTimer {
   fgd_ctx* c;
   int cls, e0 = -1;
