@@ -195,7 +195,7 @@ def peaks():
 
 
 TRAFFIC_KERNEL = {"xfwd6": "k_xtan<{n}, 2, 1, 2>", "xinv6": "k_xipipe<{n}, 1>", "z6": "k_zreg256<6, 0>",
-                  "yfwd6": "k_yreg256<0>", "yinv6": "k_yreg256<1>", "stencil": "k_stencil<1, 4>"}
+                  "yfwd6": "k_yreg256<0>", "yinv6": "k_yreg256<1>", "stencil": "k_stencil<1, 2>"}
 
 
 def measured_traffic(cls, n):

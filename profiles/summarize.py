@@ -87,7 +87,12 @@ if __name__ == "__main__":
         f"# {tag}: ncu launch list (cold-cache, serialised; compare shares)\n\n"
         f"`ncu --metrics gpu__time_duration.sum --clock-control none` over the launches of "
         f"`bench.py --steps 2 --warmup 3 --no-cpu --no-e2e --no-cufft` (256^3) after set-up; total {s:.2f} ms.\n\n{lt}\n")
-    ft, traffic = full(fpath)
+    # several reports (comma-separated) are concatenated in order
+    ft, traffic = "", {}
+    for k, fp in enumerate(fpath.split(",")):
+        t_k, tr_k = full(fp)
+        ft = t_k if k == 0 else ft + "\n" + "\n".join(t_k.splitlines()[2:])
+        traffic.update({key: val for key, val in tr_k.items() if key not in traffic})
     open(os.path.join(HERE, f"{tag}_ncu_full.md"), "w").write(
         f"# {tag}: `ncu --set full` capture of the hot kernels (256^3 sweep)\n\n{ft}\n")
     json.dump(traffic, open(os.path.join(HERE, f"{tag}_traffic.json"), "w"), indent=1)
