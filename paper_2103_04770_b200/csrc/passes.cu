@@ -362,6 +362,8 @@ __global__ void __launch_bounds__(256) k_xtan(XTArgs a) {
     if (rr == R - 1 && h == nch - 1) {
       if constexpr (fft_reg_ok<M>()) {
         constexpr int TPT = fft_reg_tpl<M>();
+        // fft_reg_inplace synchronises with full-warp __syncwarp(): whole warps must take part
+        static_assert((NC * R * TPT) % 32 == 0, "register x FFT needs whole warps of lines");
         for (int base = 0; base < NC * R * TPT; base += blockDim.x) {
           const int id = base + threadIdx.x;
           if (id < NC * R * TPT) fft_reg_inplace<M, false>(fb + (size_t)(id / TPT) * LP, id / TPT, id % TPT, twR);
