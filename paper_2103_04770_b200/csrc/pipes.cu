@@ -1184,7 +1184,9 @@ struct XPArgs {
 // PCG): that operand is staged by cp.async together with the spectrum of the tile.
 // (N = 256 loads its epilogue operand into registers ahead of the FFT instead; see k_xipipe)
 template <int N, int MODE>
-__host__ __device__ constexpr bool xi_prefetch() { return (MODE == XI_MECH_CG || MODE == XI_HELM_Z) && N != 256; }
+__host__ __device__ constexpr bool xi_prefetch() {
+  return (MODE == XI_MECH_CG || MODE == XI_HELM_Z) && N != 256 && N != 512;
+}
 
 template <int N, int MODE>
 __device__ __forceinline__ void xi_issue(const XPArgs& a, int t, double2* buf, double* ebuf) {
@@ -1207,7 +1209,7 @@ __device__ __forceinline__ void xi_issue(const XPArgs& a, int t, double2* buf, d
 }
 
 template <int N, int MODE>
-__global__ void __launch_bounds__(N == 256 ? 128 : 256, N == 256 ? 3 : 2) k_xipipe(XPArgs a) {
+__global__ void __launch_bounds__((N == 256 || N == 512) ? 128 : 256, (N == 256 || N == 512) ? 3 : 2) k_xipipe(XPArgs a) {
   extern __shared__ double2 sm[];
   pdl_trigger();
   constexpr int M = N / 2;
@@ -1221,6 +1223,7 @@ __global__ void __launch_bounds__(N == 256 ? 128 : 256, N == 256 ? 3 : 2) k_xipi
   load_table(twN, a.twN, N);
   if constexpr (M == 128)
     for (int k = threadIdx.x; k < 120; k += blockDim.x) tw128[k] = __ldg(&a.twM[(k & 7) * (1 + (k >> 3))]);
+  if constexpr (M == 256) fft_reg_tables<M>(tw128, a.twM);   // W256^{t k2} at (k2 - 1) * 16 + t
   const int ntiles = a.ncomp * a.Nz * nyt;
   const size_t n = a.nvox;
   double red[1] = {0.0};
@@ -1299,6 +1302,54 @@ __global__ void __launch_bounds__(N == 256 ? 128 : 256, N == 256 ? 3 : 2) k_xipi
           } else {
             o2 = reinterpret_cast<double2*>(a.out0 + grow + x);
             *o2 = q2;
+            if (MODE == XI_STORE_RR) red[0] = fma(q2.x, q2.x, fma(q2.y, q2.y, red[0]));
+            if (MODE == XI_HELM_Z) red[0] = fma(ro[h].x, q2.x, fma(ro[h].y, q2.y, red[0]));
+          }
+        }
+      }
+      __syncthreads();
+      continue;
+    }
+    if constexpr (M == 256) {
+      // register FFT 256 = 16 x 16 (16 threads per line, one exchange), epilogue from registers:
+      // thread (yy, tt) ends with z[n], n = tt + 16 k1, z[n] = x[2n] + i x[2n+1]
+      if (threadIdx.x < TY * 16) {
+        const int yy = threadIdx.x >> 4, tt = threadIdx.x & 15;
+        double2* ln = buf + (size_t)yy * LP;
+        const size_t grow = (size_t)c * n + ((size_t)z * a.Ny + y0 + yy) * N;
+        double2 ro[16];
+        if (MODE == XI_MECH_CG || MODE == XI_HELM_Z) {
+          const double* rs = a.in0 + grow;
+#pragma unroll
+          for (int h = 0; h < 16; ++h) ro[h] = __ldcs(reinterpret_cast<const double2*>(rs + 2 * (tt + 16 * h)));
+        }
+        double2 v[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] = ln[SWZ(yy, tt + 16 * j)];
+        dft16<true>(v);
+#pragma unroll
+        for (int k2 = 1; k2 < 16; ++k2) {
+          double2 w = ld_tw(tw128 + (k2 - 1) * 16 + tt);
+          w.y = -w.y;
+          v[k2] = cmul(v[k2], w);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int k2 = 0; k2 < 16; ++k2) ln[k2 * 17 + tt] = v[k2];
+        __syncwarp();
+#pragma unroll
+        for (int n1 = 0; n1 < 16; ++n1) v[n1] = ln[tt * 17 + n1];
+        dft16<true>(v);
+#pragma unroll
+        for (int h = 0; h < 16; ++h) {
+          const int x = 2 * (tt + 16 * h);
+          const double2 q2 = v[h];
+          if (MODE == XI_MECH_CG) {
+            const double2 rn = make_double2(fma(-alpha, q2.x, ro[h].x), fma(-alpha, q2.y, ro[h].y));
+            *reinterpret_cast<double2*>(a.io2 + grow + x) = rn;
+            red[0] = fma(rn.x, rn.x, fma(rn.y, rn.y, red[0]));
+          } else {
+            *reinterpret_cast<double2*>(a.out0 + grow + x) = q2;
             if (MODE == XI_STORE_RR) red[0] = fma(q2.x, q2.x, fma(q2.y, q2.y, red[0]));
             if (MODE == XI_HELM_Z) red[0] = fma(ro[h].x, q2.x, fma(ro[h].y, q2.y, red[0]));
           }
@@ -1617,8 +1668,8 @@ fgd_status pipe_xinv(fgd_ctx* c, int ncomp, int mode, double* out0, double* io1,
   }();
   const int TY = ty_env > 0 ? std::min(Ny, ty_env) : choose_TYp(Nx, Ny);
   const int thr = std::min(256, r32(TY * fft_TPL(Nx / 2)));
-  const bool pre = (mode == XI_MECH_CG || mode == XI_HELM_Z) && Nx != 256;
-  const size_t smem = (2 * (size_t)TY * xline(Nx / 2) + Nx / 2 + Nx + (Nx == 256 ? 120 : 0)) * sizeof(double2) +
+  const bool pre = (mode == XI_MECH_CG || mode == XI_HELM_Z) && Nx != 256 && Nx != 512;
+  const size_t smem = (2 * (size_t)TY * xline(Nx / 2) + Nx / 2 + Nx + (Nx == 256 ? 120 : Nx == 512 ? 240 : 0)) * sizeof(double2) +
                       (pre ? 2 * (size_t)TY * Nx * sizeof(double) : 0);
   const double* eop = in1;
   if (pre && ((uintptr_t)eop & 15) != 0) return set_err(c, FGD_EINVAL, "xinv: epilogue operand not 16 B aligned");
