@@ -1,0 +1,117 @@
+"""Full loading runs through the library's increment solver (fgd_solve_increment): the staggered
+Alg. 1 per increment, fixed strain increments with deterministic halving on non-convergence
+(A-21: up to 6 halvings), the BASELINE configurations 0, 2 and 3 from `synth`.
+
+    python -m paper_2103_04770_b200.run --config 3 [--n 128] [--incr 60] [--tight]
+
+prints one JSON line: the macroscopic stress-strain curve (load component), the peak, the strain
+at 50 % post-peak drop (A-26), the increment / staggered / Newton / CG / PCG counts and the wall
+time.  Default solver tolerances are the performance-run values of SURVEY 8(c) (1e-4 staggered,
+1e-6 Newton, 1e-8 CG, 1e-6 PCG); --tight uses the parity-run values.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+
+def _context(cfg):
+    import torch
+
+    from . import Context, Material
+    ctx = Context(cfg.n, cfg.L)
+    ctx.set_phases(torch.from_numpy(np.ascontiguousarray(cfg.phases)).cuda(), len(cfg.materials))
+    for q, m in enumerate(cfg.materials):
+        ctx.set_material(q, Material(m.model, m.E, m.nu, m.sigma_y, m.H, m.eps_c, m.eps_r, m.d_max, m.kappa0,
+                                     m.kappa_f))
+    ctx.set_nonlocal(np.asarray(cfg.ell), cfg.source_phase)
+    ctx.set_control(cfg.stress_mask)
+    return ctx
+
+
+def run_config(cfg, n_incr=None, tol=(1e-4, 1e-6, 1e-8, 1e-6), max_halvings=6, max_cg=5000, max_helm=5000):
+    """Load the cell along cfg.load_comp in n_incr steps of cfg.dE; returns a result dict."""
+    import torch
+
+    from . import _fgd
+    n_incr = cfg.n_incr if n_incr is None else n_incr
+    ctx = _context(cfg)
+    tol_stag, tol_newton, tol_cg, tol_helm = tol
+    E_done = 0.0
+    curve = [(0.0, 0.0)]
+    counts = dict(increments=0, substeps=0, stag=0, newton=0, cg=0, helm=0, failed=0)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for i in range(1, n_incr + 1):
+        E_goal = i * cfg.dE
+        step = cfg.dE
+        halvings = 0
+        while E_done < E_goal - 1e-15:
+            E_try = min(E_done + step, E_goal)
+            Et = np.zeros(6)
+            Et[cfg.load_comp] = E_try
+            st, rep = ctx.solve_increment(Et, np.zeros(6), tol_stag, tol_newton, tol_cg, tol_helm,
+                                          max_cg=max_cg, max_helm=max_helm)
+            counts["stag"] += rep["stag"]
+            counts["newton"] += rep["newton"]
+            counts["cg"] += rep["cg"]
+            counts["helm"] += rep["helm"]
+            if st == 0:
+                E_done = E_try
+                counts["substeps"] += 1
+                curve.append((E_try, float(rep["macro_stress"][cfg.load_comp])))
+            elif st == _fgd.ENOCONV and halvings < max_halvings:
+                step *= 0.5
+                halvings += 1
+            else:
+                counts["failed"] = 1
+                break
+        if counts["failed"]:
+            break
+        counts["increments"] += 1
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    ctx.close()
+    e = np.array([c[0] for c in curve])
+    s = np.array([c[1] for c in curve])
+    ip = int(np.argmax(s))
+    fail = None
+    for k in range(ip + 1, len(s)):          # first crossing of 50 % of the peak, linear (A-26)
+        if s[k] < 0.5 * s[ip]:
+            f = (s[k - 1] - 0.5 * s[ip]) / (s[k - 1] - s[k])
+            fail = float(e[k - 1] + f * (e[k] - e[k - 1]))
+            break
+    return dict(config=cfg.name, n=list(cfg.n), load_comp=cfg.load_comp, dE=cfg.dE, wall_s=wall,
+                peak_stress=float(s[ip]), strain_at_peak=float(e[ip]), strain_at_failure=fail,
+                curve=[[float(a), float(b)] for a, b in curve], tolerances=list(tol), max_cg=max_cg,
+                max_halvings=max_halvings, **counts)
+
+
+def main(argv=None):
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import synth
+    p = argparse.ArgumentParser()
+    p.add_argument("--config", type=int, default=0, choices=[0, 2, 3])
+    p.add_argument("--n", type=int, default=None)
+    p.add_argument("--incr", type=int, default=None)
+    p.add_argument("--tight", action="store_true")
+    p.add_argument("--max-cg", type=int, default=5000)
+    p.add_argument("--halvings", type=int, default=6)
+    a = p.parse_args(argv)
+    if a.config == 0:
+        cfg = synth.config0(a.n or 32)
+    elif a.config == 2:
+        cfg = synth.config2(a.n or 256)
+    else:
+        cfg = synth.config3(n=a.n or 128)
+    tol = (1e-8, 1e-10, 1e-11, 1e-11) if a.tight else (1e-4, 1e-6, 1e-8, 1e-6)
+    print(json.dumps(run_config(cfg, a.incr, tol, a.halvings, a.max_cg, a.max_cg)), flush=True)
+
+
+if __name__ == "__main__":
+    main()
