@@ -246,6 +246,12 @@ __global__ void k_axpy(size_t n, double* y, const double* x, double s) {
     y[g] = fma(s, x[g], y[g]);
 }
 
+__global__ void k_guard_init(DevScalars* sc, double tol2) {
+  sc->tol2 = tol2;
+  sc->done = 0;
+  sc->iters = 0;
+}
+
 // y += alpha x with alpha the device-resident Krylov step (final deferred CG solution update)
 __global__ void k_axpy_alpha(size_t n, double* y, const double* x, const DevScalars* sc) {
   const double s = sc->alpha;
@@ -361,6 +367,13 @@ fgd_status launch_axpy(fgd_ctx* c, size_t n, double* y, const double* x, double 
   KTimer kt(c, KC_OTHER);
   k_axpy<<<ew_blocks(c, n), 256, 0, c->stream>>>(n, y, x, s);
   FGD_CHECK_LAUNCH(c, "k_axpy");
+  return FGD_OK;
+}
+
+fgd_status launch_guard_init(fgd_ctx* c, double tol2) {
+  c->launches++;
+  k_guard_init<<<1, 1, 0, c->stream>>>(c->sc, tol2);
+  FGD_CHECK_LAUNCH(c, "k_guard_init");
   return FGD_OK;
 }
 

@@ -294,6 +294,16 @@ static fgd_status ensure_state(fgd_ctx* c) {
 }
 
 // Algorithm 2 in real space (equivalent to the Fourier-space PCG: F is unitary up to N).
+// Krylov loops with tol > 0 on one GPU launch iterations in growing batches (4, 8, .. 32) and
+// read the device convergence flag once per batch; the hot kernels skip themselves once the
+// finalise of the monitored norm has set it (guard_done), so the returned iterate and iteration
+// count are those of the converged iteration.  With nranks > 1 the host checks every iteration.
+struct GuardScope {
+  fgd_ctx* c;
+  GuardScope(fgd_ctx* cc, bool on) : c(cc) { c->guard = on; }
+  ~GuardScope() { c->guard = false; }
+};
+
 static fgd_status pcg_helmholtz(fgd_ctx* c, int field, const double* b, double* x_out, double tol, int maxit,
                                 int* iters, double* relres) {
   TRY(ensure_helm(c));
@@ -307,6 +317,8 @@ static fgd_status pcg_helmholtz(fgd_ctx* c, int field, const double* b, double* 
   FGD_CUDA(c, cudaMemsetAsync(x, 0, n * 8, c->stream));
   FGD_CUDA(c, cudaMemsetAsync(P[0], 0, n * 8, c->stream));
   FGD_CUDA(c, cudaMemcpyAsync(r, b, n * 8, cudaMemcpyDeviceToDevice, c->stream));
+  const bool batched = tol > 0.0 && c->nranks == 1;
+  TRY(launch_guard_init(c, tol > 0.0 ? tol * tol : 0.0));
   TRY(launch_dot(c, n, r, r, RED(RED_BB)));
   TRY(post_reduce(c, RED_BB));
   double bb = 0.0;
@@ -317,28 +329,47 @@ static fgd_status pcg_helmholtz(fgd_ctx* c, int field, const double* b, double* 
     TRY(op_precond(c, field, r, z, RED_HELM_INIT));
     int cur = 0;
     rel = 1.0;
-    while (it < maxit) {
-      TRY(launch_stencil(c, field, 1, nullptr, z, P[cur], P[cur ^ 1], q, RED_HELM_PQ));
-      TRY(post_reduce(c, RED_HELM_PQ));
-      cur ^= 1;
-      TRY(launch_xfwd_io(c, 1, XF_HELM_UPDATE, P[cur], q, x, r, nullptr, RED(RED_HELM_RN)));
-      TRY(post_reduce(c, RED_HELM_RN));
-      ++it;
-      if (tol > 0.0) {
-        double rn2;
-        TRY(sync_read(c, &c->sc->rn2, 8, &rn2));
-        rel = std::sqrt(rn2 / bb);
-        if (rel < tol) break;
+    GuardScope gs(c, batched);
+    int launched = 0, batch = 4;
+    bool done = false;
+    while (launched < maxit && !done) {
+      const int nb = batched ? std::min(batch, maxit - launched) : 1;
+      for (int k = 0; k < nb; ++k, ++launched) {
+        TRY(launch_stencil(c, field, 1, nullptr, z, P[cur], P[cur ^ 1], q, RED_HELM_PQ));
+        TRY(post_reduce(c, RED_HELM_PQ));
+        cur ^= 1;
+        TRY(launch_xfwd_io(c, 1, XF_HELM_UPDATE, P[cur], q, x, r, nullptr, RED(RED_HELM_RN)));
+        TRY(post_reduce(c, RED_HELM_RN));
+        if (!batched && tol > 0.0) {
+          double rn2;
+          TRY(sync_read(c, &c->sc->rn2, 8, &rn2));
+          if (std::sqrt(rn2 / bb) < tol) {
+            done = true;
+            ++launched;
+            break;
+          }
+        }
+        TRY(launch_precond_yz(c, inv_nvox(c), mean_ell2(c, field)));
+        TRY(launch_xinv(c, 1, XI_HELM_Z, z, nullptr, nullptr, r, RED(RED_HELM_RZ)));
+        TRY(post_reduce(c, RED_HELM_RZ));
       }
-      TRY(launch_precond_yz(c, inv_nvox(c), mean_ell2(c, field)));
-      TRY(launch_xinv(c, 1, XI_HELM_Z, z, nullptr, nullptr, r, RED(RED_HELM_RZ)));
-      TRY(post_reduce(c, RED_HELM_RZ));
+      if (batched) {
+        int flags[2];   // done, iters
+        TRY(sync_read(c, &c->sc->done, sizeof(flags), flags));
+        done = flags[0] != 0;
+        batch = std::min(2 * batch, 32);
+      }
     }
-    if (tol <= 0.0) {
-      double rn2;
-      TRY(sync_read(c, &c->sc->rn2, 8, &rn2));
-      rel = std::sqrt(rn2 / bb);
+    if (batched) {
+      int flags[2];
+      TRY(sync_read(c, &c->sc->done, sizeof(flags), flags));
+      it = flags[1];
+    } else {
+      it = launched;
     }
+    double rn2;
+    TRY(sync_read(c, &c->sc->rn2, 8, &rn2));
+    rel = std::sqrt(rn2 / bb);
   }
   if (x_out) FGD_CUDA(c, cudaMemcpyAsync(x_out, x, n * 8, cudaMemcpyDeviceToDevice, c->stream));
   if (iters) *iters = it;
@@ -359,6 +390,8 @@ static fgd_status cg_mech(fgd_ctx* c, const double* b, double* x_out, double tol
     FGD_CUDA(c, cudaMemcpyAsync(c->cg_r, b, n6 * 8, cudaMemcpyDeviceToDevice, c->stream));
     b = c->cg_r;
   }
+  const bool batched = tol > 0.0 && c->nranks == 1;
+  TRY(launch_guard_init(c, tol > 0.0 ? tol * tol : 0.0));
   TRY(launch_dot(c, n6, b, b, RED(RED_MECH_INIT)));
   TRY(post_reduce(c, RED_MECH_INIT));
   double bb = 0.0;
@@ -367,31 +400,45 @@ static fgd_status cg_mech(fgd_ctx* c, const double* b, double* x_out, double tol
   double rel = 0.0;
   if (bb > 0.0) {
     rel = 1.0;
-    while (it < maxit) {
-      const bool first = it == 0;
-      TRY(launch_xfwd_io(c, 6, XF_TANGENT_CG, first ? b : c->cg_r, nullptr, c->cg_p, c->cg_x,
-                         c->compact ? c->Cc : c->C, RED(RED_MECH_PQ), first ? 1 : 0));
-      TRY(launch_yfwd(c, 6));
-      TRY(exchange(c, 6, true));
-      TRY(launch_z(c, 6, Z_PROJECT, inv_nvox(c), nullptr, 0.0));
-      TRY(exchange(c, 6, false));
-      TRY(post_reduce(c, RED_MECH_PQ));
-      TRY(launch_yinv(c, 6));
-      TRY(launch_xinv(c, 6, XI_MECH_CG, nullptr, nullptr, c->cg_r, first ? b : c->cg_r, RED(RED_MECH_RR)));
-      TRY(post_reduce(c, RED_MECH_RR));
-      ++it;
-      if (tol > 0.0) {
+    GuardScope gs(c, batched);
+    int launched = 0, batch = 4;
+    bool done = false;
+    while (launched < maxit && !done) {
+      const int nb = batched ? std::min(batch, maxit - launched) : 1;
+      for (int k = 0; k < nb; ++k, ++launched) {
+        const bool first = launched == 0;
+        TRY(launch_xfwd_io(c, 6, XF_TANGENT_CG, first ? b : c->cg_r, nullptr, c->cg_p, c->cg_x,
+                           c->compact ? c->Cc : c->C, RED(RED_MECH_PQ), first ? 1 : 0));
+        TRY(launch_yfwd(c, 6));
+        TRY(exchange(c, 6, true));
+        TRY(launch_z(c, 6, Z_PROJECT, inv_nvox(c), nullptr, 0.0));
+        TRY(exchange(c, 6, false));
+        TRY(post_reduce(c, RED_MECH_PQ));
+        TRY(launch_yinv(c, 6));
+        TRY(launch_xinv(c, 6, XI_MECH_CG, nullptr, nullptr, c->cg_r, first ? b : c->cg_r, RED(RED_MECH_RR)));
+        TRY(post_reduce(c, RED_MECH_RR));
+      }
+      if (batched) {
+        int flags[2];   // done, iters
+        TRY(sync_read(c, &c->sc->done, sizeof(flags), flags));
+        done = flags[0] != 0;
+        batch = std::min(2 * batch, 32);
+      } else if (tol > 0.0) {
         double rr;
         TRY(sync_read(c, &c->sc->rr, 8, &rr));
-        rel = std::sqrt(rr / bb);
-        if (rel < tol) break;
+        done = std::sqrt(rr / bb) < tol;
       }
     }
-    if (tol <= 0.0) {
-      double rr;
-      TRY(sync_read(c, &c->sc->rr, 8, &rr));
-      rel = std::sqrt(rr / bb);
+    if (batched) {
+      int flags[2];
+      TRY(sync_read(c, &c->sc->done, sizeof(flags), flags));
+      it = flags[1];
+    } else {
+      it = launched;
     }
+    double rr;
+    TRY(sync_read(c, &c->sc->rr, 8, &rr));
+    rel = std::sqrt(rr / bb);
     if (it > 0) TRY(launch_axpy_alpha(c, n6, c->cg_x, c->cg_p));   // x += alpha_last p_last
   }
   if (it == 0) FGD_CUDA(c, cudaMemsetAsync(c->cg_x, 0, n6 * 8, c->stream));   // b = 0 or maxit = 0

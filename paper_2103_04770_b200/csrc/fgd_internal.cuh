@@ -47,6 +47,13 @@ inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
   return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
 }
 
+struct DevScalars;
+// Device-side convergence guard of the Krylov loops: with tol > 0 the host launches iterations in
+// batches and reads the flag once per batch; every kernel of an iteration returns immediately
+// (uniformly, before any shared-memory work) once the finalise of the monitored reduction has
+// set sc->done, so the iterate is exactly the one of the converged iteration.
+__device__ __forceinline__ bool guard_done(const DevScalars* g);
+
 struct DevScalars {
   double rr;        // mech: r.r        | helm: r.z
   double pq;        // mech: p.C p      | helm: p.L p
@@ -54,10 +61,17 @@ struct DevScalars {
   double beta;
   double bb;        // |b|^2 (stopping reference)
   double rn2;       // helm: r.r after the update
+  double tol2;      // convergence threshold on the monitored square norm (tol^2 |b|^2)
+  int done;         // set by the finalise once the monitored norm is below tol2
+  int iters;        // Krylov iterations completed (device count)
   double red[kRedSlots];   // generic reduction results
   unsigned int counter[8];
   unsigned long long maxbits;
 };
+
+__device__ __forceinline__ bool guard_done(const DevScalars* g) {
+  return g != nullptr && *(volatile const int*)&g->done != 0;
+}
 
 enum RedOp : int {
   RED_NONE = 0,
@@ -114,6 +128,7 @@ struct fgd_ctx {
   size_t nspecA = 0;           // HxA * Ny * Nz
   int device = 0;
   cudaStream_t stream = nullptr;
+  bool guard = false;                   // Krylov loop in flight: hot kernels skip once sc->done
   cudaStream_t aux = nullptr;           // second copy stream for split host<->device staging
   cudaEvent_t aux_ev[2] = {nullptr, nullptr};
   bool own_stream = false;
@@ -248,6 +263,7 @@ fgd_status launch_err(fgd_ctx* c, const double* eps, const double* eps_prev, con
 fgd_status launch_dot(fgd_ctx* c, size_t n, const double* a, const double* b, int op, int slot);
 fgd_status launch_axpy(fgd_ctx* c, size_t n, double* y, const double* x, double s);
 fgd_status launch_axpy_alpha(fgd_ctx* c, size_t n, double* y, const double* x);   // y += sc->alpha x
+fgd_status launch_guard_init(fgd_ctx* c, double tol2);   // sc->tol2 = tol^2, done = iters = 0
 fgd_status launch_init_iterate(fgd_ctx* c, const double* eps_n, double* eps, const double* dE6_dev);
 fgd_status launch_phase_count(fgd_ctx* c, const uint8_t* ph, unsigned long long* cnt, int nph, int* bad);
 fgd_status launch_expand_tangent(fgd_ctx* c, const double* Cc, double* Cp);

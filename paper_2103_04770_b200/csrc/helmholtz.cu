@@ -17,6 +17,7 @@
 namespace fgd {
 
 struct SArgs {
+  const DevScalars* guard;
   int Nx, Ny, Nz, TX, TY, TZ;   // Nz: local planes
   size_t nvox;
   double ih[3];          // 1 / (4 h_j)
@@ -92,6 +93,7 @@ __global__ void __launch_bounds__(256, 2) k_stencil(SArgs s, const double* __res
                                                      double* __restrict__ pout, double* __restrict__ q,
                                                      const uint8_t* __restrict__ phase, DevScalars* sc, double* partials,
                                                      int red_op, int red_slot) {
+  if (guard_done(s.guard)) return;   // converged Krylov loop: skip
   constexpr int NA = MODE == ST_PCG ? 2 : 1;
   constexpr int PX = SBX + 2, PY = SBY * RY + 2, PL = PX * PY, PHL = (SBY * RY + 1) * kPhW;
   extern __shared__ double ring[];                 // [kRing][NA][PL], then phase ids [kRing][PHL]
@@ -246,6 +248,7 @@ double mean_ell2(const fgd_ctx* c, int field) {
 fgd_status launch_stencil(fgd_ctx* c, int field, int mode, const double* a, const double* zin, const double* pold,
                           double* pout, double* q, int red_op) {
   SArgs s{};
+  s.guard = c->guard ? c->sc : nullptr;
   s.Nx = c->n[0];
   s.Ny = c->n[1];
   s.Nz = c->nz_l;

@@ -23,6 +23,7 @@ namespace fgd {
 constexpr int kMaxThr = 384;
 
 struct XArgs {
+  const DevScalars* guard;
   int Ny, Nz, TY, HxA;   // HxA: kx stride of layout A
   size_t nvox;
   const double* in0;
@@ -96,6 +97,7 @@ __device__ __forceinline__ void tangent_apply_c(const double* __restrict__ Cc, s
 template <int N, int NC, int MODE>
 __global__ void __launch_bounds__(kMaxThr, 2) k_xfwd(XArgs a, const double2* __restrict__ twM,
                                                       const double2* __restrict__ twN) {
+  if (guard_done(a.guard)) return;   // converged Krylov loop: skip
   extern __shared__ double2 sm[];
   constexpr int M = N / 2;
   constexpr int LP = xline(M);
@@ -185,6 +187,7 @@ __global__ void __launch_bounds__(kMaxThr, 2) k_xfwd(XArgs a, const double2* __r
 // buffer (12 lines: 6 components x 2 rows), and after the last chunk of the pair runs the R2C
 // line transforms and stores the half spectra as one contiguous block per component.
 struct XTArgs {
+  const DevScalars* guard;
   int Ny, Nz, HxA, CW, S, R;   // chunk width, stages, rows per tile
   int first;                   // CG step 1: p = r, x = 0 (p_old and x are neither read nor needed)
   size_t nvox;
@@ -243,6 +246,7 @@ __device__ __forceinline__ void tangent_smem(const double* C, int v, int cs, con
 
 template <int N, int MODE, bool CMP, int R>
 __global__ void __launch_bounds__(256) k_xtan(XTArgs a) {
+  if (guard_done(a.guard)) return;   // converged Krylov loop: skip
   constexpr int M = N / 2, Hx = M + 1;
   constexpr int LP = xline(M);
   constexpr int NC = xt_nc<MODE>();
@@ -496,7 +500,7 @@ static fgd_status launch_xtan(fgd_ctx* c, int mode, double* r, double* p, double
   if (s_env >= 2 && s_env <= 8) S = s_env;
   const size_t smem = fixed + S * stage;
   if (smem > 227 * 1024) return FGD_OK;
-  XTArgs a{Ny, c->nz_l, c->HxA, CW, S, R, first, c->nvox, r, p, x, Cp, c->specA, c->sc, c->partials, red_op, red_slot,
+  XTArgs a{c->guard ? c->sc : nullptr, Ny, c->nz_l, c->HxA, CW, S, R, first, c->nvox, r, p, x, Cp, c->specA, c->sc, c->partials, red_op, red_slot,
            c->tabs.tw[ilog2(Nx / 2)], c->tabs.tw[ilog2(Nx)]};
   const int ntiles = (Ny / R) * c->nz_l;
   KTimer kt(c, helm ? KC_XFWD1 : KC_XFWD6);
@@ -558,7 +562,7 @@ fgd_status launch_xfwd_io(fgd_ctx* c, int ncomp, int mode, const double* in0, co
   const int thr = std::min(kMaxThr, std::max(64, round32(nl * fft_TPL(Nx / 2))));
   const size_t smem = ((size_t)nl * xline(Nx / 2) + Nx / 2) * sizeof(double2);
   dim3 grid(Ny / TY, Nz);
-  XArgs a{Ny, Nz, TY, c->HxA, c->nvox, in0, in1, out0, io1, nullptr, Cp, c->specA, c->sc, c->partials, red_op, red_slot,
+  XArgs a{c->guard ? c->sc : nullptr, Ny, Nz, TY, c->HxA, c->nvox, in0, in1, out0, io1, nullptr, Cp, c->specA, c->sc, c->partials, red_op, red_slot,
           (Cp != nullptr && Cp == c->Cc) ? 1 : 0};
   if (red_op != RED_NONE) {
     fgd_status s = ensure_partials(c, (size_t)grid.x * grid.y);

@@ -89,6 +89,7 @@ __device__ __forceinline__ size_t r_index(const SlabL& L, int C, int Hx, int c, 
 // z (runs of TZ * 16 B in B, z fastest); line l = zz * TK + kk.  kx >= Hx (padding of the last kx
 // block, HxA = Hx rounded up to 4) is neither loaded nor stored.
 struct YArgs {
+  const DevScalars* guard;   // non-null inside a guarded Krylov loop
   double2* A;
   double2* B;
   int Nz, Hx, HxA, TZ, TK, ncomp, lgTZ, lgTK;
@@ -129,6 +130,7 @@ __device__ __forceinline__ void y_issue(const YArgs& a, int t, double2* buf) {
 
 template <int N, bool INV>
 __global__ void __launch_bounds__(256, 2) k_ypipe(YArgs a) {
+  if (guard_done(a.guard)) return;   // converged Krylov loop: skip
   extern __shared__ double2 sm[];
   constexpr int LP = cline(N);
   const int NL = a.TZ * a.TK;
@@ -173,6 +175,7 @@ __global__ void __launch_bounds__(256, 2) k_ypipe(YArgs a) {
 // Z pass with the spectral multiply
 // ---------------------------------------------------------------------------------------------
 struct ZPArgs {
+  const DevScalars* guard;
   double2* B;
   SlabL SL;
   int ky_off;          // global index of the first local ky (distributed y-slab)
@@ -298,6 +301,7 @@ __device__ __forceinline__ void z_issue(const ZPArgs& a, int t, double2* buf) {
 
 template <int N, int NC, int MODE>
 __global__ void __launch_bounds__(192, 3) k_zpipe(ZPArgs a) {
+  if (guard_done(a.guard)) return;   // converged Krylov loop: skip
   extern __shared__ double2 sm[];
   constexpr int LP = cline(N);
   const int TL = a.TL;
@@ -372,6 +376,7 @@ constexpr int kZLine = 16 * kZRowPad;
 
 template <int NC, int MODE>
 __global__ void __launch_bounds__(NC == 6 ? 96 : 128) __maxnreg__(NC == 6 ? 128 : 128) k_zreg256(ZPArgs a) {
+  if (guard_done(a.guard)) return;   // converged Krylov loop: skip
   extern __shared__ double2 sm[];
   constexpr int N = 256;
   const int TL = a.TL;
@@ -516,6 +521,7 @@ __global__ void __launch_bounds__(NC == 6 ? 96 : 128) __maxnreg__(NC == 6 ? 128 
 // association order of the sums changes).  Opt-in (FGD_ZFAC=1), see pipe_z.  The zero frequency (line kx = ky = 0, kz = 0) takes the
 // mask branch: eps_c += mask_c (sum_z tau_c - N shift_c) scale on every z of that line.
 __global__ void __launch_bounds__(96, 5) k_zfac256(ZPArgs a) {
+  if (guard_done(a.guard)) return;   // converged Krylov loop: skip
   extern __shared__ double2 sm[];
   constexpr int N = 256;
   constexpr double HS2 = 0.70710678118654752440;   // sqrt(2)/2 = 1/sqrt(2)
@@ -721,6 +727,7 @@ __device__ __forceinline__ void y256_issue_inv(const YArgs& a, int tile, double2
 
 template <bool INV>
 __global__ void __launch_bounds__(256, 2) k_yreg256(YArgs a) {
+  if (guard_done(a.guard)) return;   // converged Krylov loop: skip
   extern __shared__ double2 sm[];
   constexpr int N = 256;
   const int TZ = a.TZ;                              // blockDim.x == 32 * TZ
@@ -873,6 +880,7 @@ __device__ __forceinline__ void fft512_tables(double2* tw1, double2* tw2, const 
 // Z pass, Nz = 512: one (kx, ky) per tile, NC lines of 64 threads.
 template <int NC, int MODE>
 __global__ void __launch_bounds__(NC * 64, NC == 6 ? 2 : 8) k_zreg512(ZPArgs a) {
+  if (guard_done(a.guard)) return;   // converged Krylov loop: skip
   extern __shared__ double2 sm[];
   constexpr int N = 512;
   double2* tw1 = sm + (size_t)NC * k512Line;
@@ -936,6 +944,7 @@ constexpr int kY512Line = k512Line + 2;   // max pitch (see ypitch)
 
 template <bool INV>
 __global__ void __launch_bounds__(512, 2) k_yreg512(YArgs a) {
+  if (guard_done(a.guard)) return;   // converged Krylov loop: skip
   extern __shared__ double2 sm[];
   constexpr int N = 512;
   const int TZ = a.TZ;                             // blockDim.x == 128 * TZ
@@ -1042,6 +1051,7 @@ __device__ __forceinline__ double rcp_pos(double x) {
 }
 
 __global__ void __cluster_dims__(kYZCl, 1, 1) __launch_bounds__(512, 1) k_yzy256(YZArgs a) {
+  if (guard_done(a.z.guard)) return;   // converged Krylov loop: skip
   extern __shared__ double2 sm[];
   constexpr int N = 256;
   cg::cluster_group cluster = cg::this_cluster();
@@ -1166,6 +1176,7 @@ __global__ void __cluster_dims__(kYZCl, 1, 1) __launch_bounds__(512, 1) k_yzy256
 // X passes, one component per tile
 // ---------------------------------------------------------------------------------------------
 struct XPArgs {
+  const DevScalars* guard;
   int Ny, Nz, TY, ncomp, lgTY, HxA;
   size_t nvox;
   double2* spec;
@@ -1210,6 +1221,7 @@ __device__ __forceinline__ void xi_issue(const XPArgs& a, int t, double2* buf, d
 
 template <int N, int MODE>
 __global__ void __launch_bounds__((N == 256 || N == 512) ? 128 : 256, (N == 256 || N == 512) ? 3 : 2) k_xipipe(XPArgs a) {
+  if (guard_done(a.guard)) return;   // converged Krylov loop: skip
   extern __shared__ double2 sm[];
   pdl_trigger();
   constexpr int M = N / 2;
@@ -1402,6 +1414,7 @@ __device__ __forceinline__ void xf_issue(const XPArgs& a, int t, double2* buf) {
 
 template <int N>
 __global__ void __launch_bounds__(128, 4) k_xfpipe(XPArgs a) {
+  if (guard_done(a.guard)) return;   // converged Krylov loop: skip
   extern __shared__ double2 sm[];
   constexpr int M = N / 2, Hx = M + 1;
   constexpr int LP = xline(M);
@@ -1516,7 +1529,7 @@ fgd_status pipe_y(fgd_ctx* c, int ncomp, bool inv) {
     const int thr = 128 * TZ;
     const size_t smem = ((size_t)2 * TZ * kY512Line + 448 + 56) * sizeof(double2);
     const int ntiles = ncomp * (c->HxA / kKB) * (Nz / TZ);
-    YArgs a{c->specA, c->specB, Nz, c->Hx, c->HxA, TZ, kKB, ncomp, ilog2(TZ), ilog2(kKB), c->tabs.tw[ilog2(Ny)],
+    YArgs a{c->guard ? c->sc : nullptr, c->specA, c->specB, Nz, c->Hx, c->HxA, TZ, kKB, ncomp, ilog2(TZ), ilog2(kKB), c->tabs.tw[ilog2(Ny)],
             slab_layout(c)};
     KTimer kt(c, inv ? (ncomp == 6 ? KC_YINV6 : KC_YINV1) : (ncomp == 6 ? KC_YFWD6 : KC_YFWD1));
     if (inv) FGD_PLAUNCH(c, k_yreg512<true>, thr, smem, ntiles, a);
@@ -1534,7 +1547,7 @@ fgd_status pipe_y(fgd_ctx* c, int ncomp, bool inv) {
     const int thr = 32 * TZ;
     const size_t smem = ((inv ? 2 : 1) * (size_t)2 * TZ * kYLine + 240) * sizeof(double2);
     const int ntiles = ncomp * (c->HxA / kKB) * (Nz / TZ);
-    YArgs a{c->specA, c->specB, Nz, c->Hx, c->HxA, TZ, kKB, ncomp, ilog2(TZ), ilog2(kKB), c->tabs.tw[ilog2(Ny)],
+    YArgs a{c->guard ? c->sc : nullptr, c->specA, c->specB, Nz, c->Hx, c->HxA, TZ, kKB, ncomp, ilog2(TZ), ilog2(kKB), c->tabs.tw[ilog2(Ny)],
             slab_layout(c)};
     KTimer kt(c, inv ? (ncomp == 6 ? KC_YINV6 : KC_YINV1) : (ncomp == 6 ? KC_YFWD6 : KC_YFWD1));
     if (inv) FGD_PLAUNCH(c, k_yreg256<true>, thr, smem, ntiles, a);
@@ -1558,7 +1571,7 @@ fgd_status pipe_y(fgd_ctx* c, int ncomp, bool inv) {
   const int thr = std::min(256, r32(TZ * TK * TPL));
   const size_t smem = (2 * (size_t)TZ * TK * cline(Ny) + Ny) * sizeof(double2);
   const int ntiles = ncomp * (c->HxA / TK) * (Nz / TZ);
-  YArgs a{c->specA, c->specB, Nz, c->Hx, c->HxA, TZ, TK, ncomp, ilog2(TZ), ilog2(TK), c->tabs.tw[ilog2(Ny)],
+  YArgs a{c->guard ? c->sc : nullptr, c->specA, c->specB, Nz, c->Hx, c->HxA, TZ, TK, ncomp, ilog2(TZ), ilog2(TK), c->tabs.tw[ilog2(Ny)],
           slab_layout(c)};
   KTimer kt(c, inv ? (ncomp == 6 ? KC_YINV6 : KC_YINV1) : (ncomp == 6 ? KC_YFWD6 : KC_YFWD1));
 #define YPP(NN)                                                                  \
@@ -1580,6 +1593,7 @@ fgd_status pipe_z(fgd_ctx* c, int ncomp, int mode, double scale, const double* d
   const size_t smem = (2 * (size_t)ncomp * TL * cline(Nz) + 2 * Nz) * sizeof(double2);
   const int ntiles = c->Hx * (Nyl / TL);
   ZPArgs a{};
+  a.guard = c->guard ? c->sc : nullptr;
   a.B = c->P > 1 ? c->specC : c->specB;
   a.SL = slab_layout(c);
   a.ky_off = c->nranks > 1 ? c->rank * (Ny / c->P) : 0;
@@ -1674,7 +1688,7 @@ fgd_status pipe_xinv(fgd_ctx* c, int ncomp, int mode, double* out0, double* io1,
   const double* eop = in1;
   if (pre && ((uintptr_t)eop & 15) != 0) return set_err(c, FGD_EINVAL, "xinv: epilogue operand not 16 B aligned");
   const int ntiles = ncomp * Nz * (Ny / TY);
-  XPArgs a{Ny, Nz, TY, ncomp, ilog2(TY), c->HxA, c->nvox, c->specA, in1, out0, io1, io2, c->sc, nullptr, red_op, red_slot,
+  XPArgs a{c->guard ? c->sc : nullptr, Ny, Nz, TY, ncomp, ilog2(TY), c->HxA, c->nvox, c->specA, in1, out0, io1, io2, c->sc, nullptr, red_op, red_slot,
            c->tabs.tw[ilog2(Nx / 2)], c->tabs.tw[ilog2(Nx)]};
   if (mode != XI_STORE) {
     fgd_status s = ensure_partials(c, (size_t)num_sms() * 8);
@@ -1699,7 +1713,7 @@ fgd_status pipe_xfwd_plain(fgd_ctx* c, int ncomp, const double* in0) {
   const int thr = std::min(128, r32(TY * fft_TPL(Nx / 2)));
   const size_t smem = (2 * (size_t)TY * xline(Nx / 2) + Nx / 2 + Nx) * sizeof(double2);
   const int ntiles = ncomp * Nz * (Ny / TY);
-  XPArgs a{Ny, Nz, TY, ncomp, ilog2(TY), c->HxA, c->nvox, c->specA, in0, nullptr, nullptr, nullptr, c->sc, nullptr, RED_NONE, 0,
+  XPArgs a{c->guard ? c->sc : nullptr, Ny, Nz, TY, ncomp, ilog2(TY), c->HxA, c->nvox, c->specA, in0, nullptr, nullptr, nullptr, c->sc, nullptr, RED_NONE, 0,
            c->tabs.tw[ilog2(Nx / 2)], c->tabs.tw[ilog2(Nx)]};
   KTimer kt(c, ncomp == 6 ? KC_XFWD6 : KC_XFWD1);
 #define XFP(NN) FGD_PLAUNCH(c, (k_xfpipe<NN>), thr, smem, ntiles, a);
@@ -1717,6 +1731,7 @@ fgd_status launch_precond_yz(fgd_ctx* c, double scale, double mean_ell2) {
   const bool yzy = std::getenv("FGD_YZY") != nullptr;
   if (yzy && Ny == 256 && Nz == 256 && c->P == 1) {
     YZArgs a{};
+    a.z.guard = c->guard ? c->sc : nullptr;
     a.A = c->specA;
     a.Nz = c->nz_l;
     a.Hx = c->Hx;

@@ -44,6 +44,9 @@ __device__ __forceinline__ void finalize(DevScalars* sc, int op, int slot, const
       sc->bb = t[0];
       sc->beta = 0.0;
       sc->alpha = 0.0;
+      sc->tol2 *= t[0];   // the host stored tol^2
+      sc->done = 0;
+      sc->iters = 0;
       break;
     case RED_MECH_PQ:
     case RED_HELM_PQ:
@@ -51,6 +54,11 @@ __device__ __forceinline__ void finalize(DevScalars* sc, int op, int slot, const
       sc->alpha = sc->rr / t[0];
       break;
     case RED_MECH_RR:
+      sc->beta = t[0] / sc->rr;
+      sc->rr = t[0];
+      sc->iters += 1;
+      if (t[0] < sc->tol2) sc->done = 1;
+      break;
     case RED_HELM_RZ:
       sc->beta = t[0] / sc->rr;
       sc->rr = t[0];
@@ -61,9 +69,14 @@ __device__ __forceinline__ void finalize(DevScalars* sc, int op, int slot, const
       break;
     case RED_HELM_RN:
       sc->rn2 = t[0];
+      sc->iters += 1;
+      if (t[0] < sc->tol2) sc->done = 1;
       break;
     case RED_BB:
       sc->bb = t[0];
+      sc->tol2 *= t[0];   // the host stored tol^2
+      sc->done = 0;
+      sc->iters = 0;
       break;
     default:
       break;
