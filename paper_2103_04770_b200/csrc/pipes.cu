@@ -840,7 +840,9 @@ constexpr int k512Line = 8 * 65;
 
 template <bool INV>
 __device__ __forceinline__ void fft512_reg(double2 (&v)[8], int t, double2* ls, const double2* tw1,
-                                           const double2* tw2) {
+                                           const double2* tw2, int bar, int nbar) {
+  // the exchanges only involve the warps that carry this line: named barrier `bar` over `nbar` threads
+  auto sync = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(nbar) : "memory"); };
   dft8<INV>(v);
 #pragma unroll
   for (int ka = 1; ka < 8; ++ka) {
@@ -850,11 +852,11 @@ __device__ __forceinline__ void fft512_reg(double2 (&v)[8], int t, double2* ls, 
   }
 #pragma unroll
   for (int ka = 0; ka < 8; ++ka) ls[ka * 65 + t] = v[ka];
-  __syncthreads();
+  sync();
   const int ka = t & 7, hi = t >> 3;
 #pragma unroll
   for (int t2 = 0; t2 < 8; ++t2) v[t2] = ls[ka * 65 + hi + 8 * t2];
-  __syncthreads();
+  sync();
   dft8<INV>(v);
 #pragma unroll
   for (int kb = 1; kb < 8; ++kb) {
@@ -864,10 +866,10 @@ __device__ __forceinline__ void fft512_reg(double2 (&v)[8], int t, double2* ls, 
   }
 #pragma unroll
   for (int kb = 0; kb < 8; ++kb) ls[kb * 65 + ka + 8 * hi] = v[kb];
-  __syncthreads();
+  sync();
 #pragma unroll
   for (int t1 = 0; t1 < 8; ++t1) v[t1] = ls[hi * 65 + ka + 8 * t1];
-  __syncthreads();
+  sync();
   dft8<INV>(v);
 }
 
@@ -904,7 +906,7 @@ __global__ void __launch_bounds__(NC * 64, NC == 6 ? 2 : 8) k_zreg512(ZPArgs a) 
       const int z = t + 64 * j;
       v[j] = __ldcg(Bl + ((z >> lgz) * BS + (z & zm)));
     }
-    fft512_reg<false>(v, t, ls, tw1, tw2);      // v[kc] = X[t + 64 kc]
+    fft512_reg<false>(v, t, ls, tw1, tw2, 1 + c, 64);   // v[kc] = X[t + 64 kc]
 #pragma unroll
     for (int kc = 0; kc < 8; ++kc) ls[kc * 65 + t] = v[kc];
     __syncthreads();
@@ -928,7 +930,7 @@ __global__ void __launch_bounds__(NC * 64, NC == 6 ? 2 : 8) k_zreg512(ZPArgs a) 
 #pragma unroll
     for (int kc = 0; kc < 8; ++kc) v[kc] = ls[kc * 65 + t];
     __syncthreads();
-    fft512_reg<true>(v, t, ls, tw1, tw2);       // v[m] = z[t + 64 m]
+    fft512_reg<true>(v, t, ls, tw1, tw2, 1 + c, 64);    // v[m] = z[t + 64 m]
 #pragma unroll
     for (int m = 0; m < 8; ++m) {
       const int z = t + 64 * m;
@@ -976,7 +978,7 @@ __global__ void __launch_bounds__(512, 2) k_yreg512(YArgs a) {
     const int z0 = zt * TZ, kx0 = kb * kKB, kx = kx0 + kl;
     double2* Arow = a.A + aidx(a.HxA, N, a.Nz, c, z0 + zz, 0, kx0) + kl;   // element y at Arow[kKB * y]
     if (!INV) {
-      fft512_reg<false>(v, t, ls, tw1, tw2);     // v[kc] = X[ky = t + 64 kc]
+      fft512_reg<false>(v, t, ls, tw1, tw2, 1 + zz, 128);   // v[kc] = X[ky = t + 64 kc]
 #pragma unroll
       for (int kc = 0; kc < 8; ++kc) ls[kc * 65 + t] = v[kc];
       __syncthreads();
@@ -1008,7 +1010,7 @@ __global__ void __launch_bounds__(512, 2) k_yreg512(YArgs a) {
 #pragma unroll
       for (int kc = 0; kc < 8; ++kc) v[kc] = ls[kc * 65 + t];
       __syncthreads();
-      fft512_reg<true>(v, t, ls, tw1, tw2);      // v[m] = y-line value at y = t + 64 m
+      fft512_reg<true>(v, t, ls, tw1, tw2, 1 + zz, 128);    // v[m] = y-line value at y = t + 64 m
       if (kx < a.Hx) {
 #pragma unroll
         for (int m = 0; m < 8; ++m) Arow[kKB * (t + 64 * m)] = v[m];
