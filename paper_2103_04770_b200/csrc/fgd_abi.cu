@@ -304,6 +304,60 @@ struct GuardScope {
   ~GuardScope() { c->guard = false; }
 };
 
+// Launch-bound small grids: a block of `reps` standard Krylov iterations is captured once per solve
+// into a CUDA graph (on a private capture stream) and replayed on the context stream, one graph
+// launch per block instead of ~8 kernel launches per iteration.  Used on one GPU for grids of at
+// most 2^21 voxels and with per-launch timing off; the captured pointers are context buffers.
+struct KGraph {
+  cudaGraphExec_t exec = nullptr;
+  long long launches = 0;   // kernels per replay (launch accounting)
+  ~KGraph() {
+    if (exec) cudaGraphExecDestroy(exec);
+  }
+};
+
+static bool use_graphs(const fgd_ctx* c) {
+  static const bool off = std::getenv("FGD_NO_GRAPHS") != nullptr;
+  return !off && c->nranks == 1 && !c->timing && c->nvox <= ((size_t)1 << 21);
+}
+
+// Captures `reps` calls of body(); on any failure the capture is dropped (g->exec stays null, the
+// CUDA error state is cleared) and the caller keeps launching kernels directly.
+template <typename F>
+static void capture_graph(fgd_ctx* c, int reps, F body, KGraph* g) {
+  if (!c->cap && cudaStreamCreateWithFlags(&c->cap, cudaStreamNonBlocking) != cudaSuccess) {
+    (void)cudaGetLastError();
+    c->cap = nullptr;
+    return;
+  }
+  cudaStream_t saved = c->stream;
+  const long long l0 = c->launches;
+  const std::string err0 = c->err;
+  c->stream = c->cap;
+  cudaError_t e = cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal);
+  fgd_status st = FGD_OK;
+  for (int k = 0; k < reps && st == FGD_OK && e == cudaSuccess; ++k) st = body();
+  cudaGraph_t graph = nullptr;
+  if (e == cudaSuccess) e = cudaStreamEndCapture(c->stream, &graph);
+  c->stream = saved;
+  g->launches = c->launches - l0;
+  c->launches = l0;
+  if (st == FGD_OK && e == cudaSuccess && graph) e = cudaGraphInstantiate(&g->exec, graph, 0);
+  if (graph) cudaGraphDestroy(graph);
+  if (st != FGD_OK || e != cudaSuccess) {
+    if (g->exec) cudaGraphExecDestroy(g->exec);
+    g->exec = nullptr;
+    (void)cudaGetLastError();
+    c->err = err0;
+  }
+}
+
+static fgd_status replay_graph(fgd_ctx* c, const KGraph& g) {
+  c->launches += g.launches;
+  FGD_CUDA(c, cudaGraphLaunch(g.exec, c->stream));
+  return FGD_OK;
+}
+
 static fgd_status pcg_helmholtz(fgd_ctx* c, int field, const double* b, double* x_out, double tol, int maxit,
                                 int* iters, double* relres) {
   TRY(ensure_helm(c));
@@ -332,8 +386,40 @@ static fgd_status pcg_helmholtz(fgd_ctx* c, int field, const double* b, double* 
     GuardScope gs(c, batched);
     int launched = 0, batch = 4;
     bool done = false;
-    while (launched < maxit && !done) {
-      const int nb = batched ? std::min(batch, maxit - launched) : 1;
+    // batched mode: one PCG iteration (stencil, update, preconditioner, inverse pass); P[] alternates,
+    // so a captured block has an even number of iterations
+    auto iteration = [&]() -> fgd_status {
+      TRY(launch_stencil(c, field, 1, nullptr, z, P[cur], P[cur ^ 1], q, RED_HELM_PQ));
+      TRY(post_reduce(c, RED_HELM_PQ));
+      cur ^= 1;
+      TRY(launch_xfwd_io(c, 1, XF_HELM_UPDATE, P[cur], q, x, r, nullptr, RED(RED_HELM_RN)));
+      TRY(post_reduce(c, RED_HELM_RN));
+      TRY(launch_precond_yz(c, inv_nvox(c), mean_ell2(c, field)));
+      TRY(launch_xinv(c, 1, XI_HELM_Z, z, nullptr, nullptr, r, RED(RED_HELM_RZ)));
+      TRY(post_reduce(c, RED_HELM_RZ));
+      return FGD_OK;
+    };
+    constexpr int kG = 4;
+    KGraph graph;
+    int gcur = 0;
+    const bool graphs = batched && use_graphs(c) && maxit > 2 * kG;
+    while (batched && launched < maxit && !done) {
+      const int nb = std::min(batch, maxit - launched);
+      int k = 0;
+      if (graphs && !graph.exec && nb >= kG) {
+        gcur = cur;
+        capture_graph(c, kG, iteration, &graph);
+        cur = gcur;   // the capture only recorded the launches
+      }
+      for (; graph.exec && cur == gcur && k + kG <= nb; k += kG, launched += kG) TRY(replay_graph(c, graph));
+      for (; k < nb; ++k, ++launched) TRY(iteration());
+      int flags[2];   // done, iters
+      TRY(sync_read(c, &c->sc->done, sizeof(flags), flags));
+      done = flags[0] != 0;
+      batch = std::min(2 * batch, 32);
+    }
+    while (!batched && launched < maxit && !done) {
+      const int nb = 1;
       for (int k = 0; k < nb; ++k, ++launched) {
         TRY(launch_stencil(c, field, 1, nullptr, z, P[cur], P[cur ^ 1], q, RED_HELM_PQ));
         TRY(post_reduce(c, RED_HELM_PQ));
@@ -403,21 +489,33 @@ static fgd_status cg_mech(fgd_ctx* c, const double* b, double* x_out, double tol
     GuardScope gs(c, batched);
     int launched = 0, batch = 4;
     bool done = false;
+    auto iteration = [&](bool first) -> fgd_status {
+      TRY(launch_xfwd_io(c, 6, XF_TANGENT_CG, first ? b : c->cg_r, nullptr, c->cg_p, c->cg_x,
+                         c->compact ? c->Cc : c->C, RED(RED_MECH_PQ), first ? 1 : 0));
+      TRY(launch_yfwd(c, 6));
+      TRY(exchange(c, 6, true));
+      TRY(launch_z(c, 6, Z_PROJECT, inv_nvox(c), nullptr, 0.0));
+      TRY(exchange(c, 6, false));
+      TRY(post_reduce(c, RED_MECH_PQ));
+      TRY(launch_yinv(c, 6));
+      TRY(launch_xinv(c, 6, XI_MECH_CG, nullptr, nullptr, c->cg_r, first ? b : c->cg_r, RED(RED_MECH_RR)));
+      TRY(post_reduce(c, RED_MECH_RR));
+      return FGD_OK;
+    };
+    constexpr int kG = 4;   // iterations per graph replay
+    KGraph graph;
+    const bool graphs = batched && use_graphs(c) && maxit > 2 * kG;
     while (launched < maxit && !done) {
       const int nb = batched ? std::min(batch, maxit - launched) : 1;
-      for (int k = 0; k < nb; ++k, ++launched) {
-        const bool first = launched == 0;
-        TRY(launch_xfwd_io(c, 6, XF_TANGENT_CG, first ? b : c->cg_r, nullptr, c->cg_p, c->cg_x,
-                           c->compact ? c->Cc : c->C, RED(RED_MECH_PQ), first ? 1 : 0));
-        TRY(launch_yfwd(c, 6));
-        TRY(exchange(c, 6, true));
-        TRY(launch_z(c, 6, Z_PROJECT, inv_nvox(c), nullptr, 0.0));
-        TRY(exchange(c, 6, false));
-        TRY(post_reduce(c, RED_MECH_PQ));
-        TRY(launch_yinv(c, 6));
-        TRY(launch_xinv(c, 6, XI_MECH_CG, nullptr, nullptr, c->cg_r, first ? b : c->cg_r, RED(RED_MECH_RR)));
-        TRY(post_reduce(c, RED_MECH_RR));
+      int k = 0;
+      if (launched == 0) {
+        TRY(iteration(true));
+        ++k;
+        ++launched;
       }
+      if (graphs && !graph.exec && nb - k >= kG) capture_graph(c, kG, [&]() { return iteration(false); }, &graph);
+      for (; graph.exec && k + kG <= nb; k += kG, launched += kG) TRY(replay_graph(c, graph));
+      for (; k < nb; ++k, ++launched) TRY(iteration(false));
       if (batched) {
         int flags[2];   // done, iters
         TRY(sync_read(c, &c->sc->done, sizeof(flags), flags));
@@ -539,6 +637,7 @@ void fgd_destroy(fgd_ctx* c) {
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   if (c->aux) cudaStreamDestroy(c->aux);
+  if (c->cap) cudaStreamDestroy(c->cap);
   for (cudaEvent_t e : c->aux_ev)
     if (e) cudaEventDestroy(e);
   dist_destroy(c);

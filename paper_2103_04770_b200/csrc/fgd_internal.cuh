@@ -130,6 +130,7 @@ struct fgd_ctx {
   cudaStream_t stream = nullptr;
   bool guard = false;                   // Krylov loop in flight: hot kernels skip once sc->done
   cudaStream_t aux = nullptr;           // second copy stream for split host<->device staging
+  cudaStream_t cap = nullptr;           // stream used to capture Krylov iterations into CUDA graphs
   cudaEvent_t aux_ev[2] = {nullptr, nullptr};
   bool own_stream = false;
   std::string err;
