@@ -89,7 +89,7 @@ __device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
 }
 
 template <int MODE, int RY>
-__global__ void __launch_bounds__(256, 2) k_stencil(SArgs s, const double* __restrict__ ain, const double* __restrict__ pold,
+__global__ void __launch_bounds__(256, RY == 4 ? 2 : 3) k_stencil(SArgs s, const double* __restrict__ ain, const double* __restrict__ pold,
                                                      double* __restrict__ pout, double* __restrict__ q,
                                                      const uint8_t* __restrict__ phase, DevScalars* sc, double* partials,
                                                      int red_op, int red_slot) {
@@ -202,11 +202,11 @@ __global__ void __launch_bounds__(256, 2) k_stencil(SArgs s, const double* __res
   __syncthreads();                    // planes 0 and 1 have been read by every thread
   for (int zz = 0; zz < TZ; ++zz) {
     const int z = z0 + zz;
-    // the slot of plane zz was last read at iteration zz - 2 (or in the prologue): every thread has
-    // passed the barrier of iteration zz - 1 (or the one above) since, so it can be refilled
-    issue(zz + kRing);
-    cp_async_wait_s<kRing - 2>();     // plane zz + 2 (level z + 1) has landed
+    cp_async_wait_s<kRing - 3>();     // plane zz + 2 (level z + 1) has landed
     __syncthreads();
+    // the slot of plane zz was last read at iteration zz - 1 (its phase ids, by vertices(zz)) or in
+    // the prologue: every thread has passed the barrier above since, so it can be refilled now
+    issue(zz + kRing);
     if (act) {
 #pragma unroll
       for (int r = 0; r < RY + 2; ++r)
