@@ -34,6 +34,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
+from . import gtn as gtn_
 from . import material as mat_
 from .helmholtz import ell2_field, solve_helmholtz
 from .mech import cg
@@ -113,7 +114,25 @@ def frozen_damage(cell: Cell, state: State, abar: np.ndarray) -> np.ndarray:
             if j is not None:
                 kap = np.maximum(kap, abar[j].reshape(-1)[sel])
             D[sel] = mat_.brittle_damage(kap, m.kappa0, m.kappa_f, m.d_max)
+        elif m.model == 3:
+            D[sel] = gtn_porosity(cell, q, state, abar)[sel]
     return D
+
+
+def gtn_porosity(cell: Cell, q: int, state: State, abar: np.ndarray) -> np.ndarray:
+    """Frozen porosity f of a GTN phase q (A-30): fields j (ebar0) and j + 1 (trbar) are the
+    phase's two non-local fields; f = porosity(f_n, abar^(k), abar_n) per voxel (n,)."""
+    j = cell.field_of_phase(q)
+    if j is None or j + 1 >= cell.J or cell.source_phase[j + 1] != q:
+        raise ValueError("a GTN phase needs two consecutive non-local fields (eps0p, tr eps^p)")
+    m = cell.materials[q]
+    e0, e0n = abar[j].reshape(-1), state.abar[j].reshape(-1)
+    t, tn = abar[j + 1].reshape(-1), state.abar[j + 1].reshape(-1)
+    return np.array([gtn_.porosity(state.hist[v], e0[v], e0n[v], t[v], tn[v], m) for v in range(e0.shape[0])])
+
+
+class ReturnMapFailure(Exception):
+    """A GTN return mapping did not converge (the increment is rolled back and cut)."""
 
 
 def evaluate(cell: Cell, eps: np.ndarray, state: State, D: np.ndarray):
@@ -145,6 +164,14 @@ def evaluate(cell: Cell, eps: np.ndarray, state: State, D: np.ndarray):
             s, c, eq = mat_.brittle(e[:, sel], D[sel], m)
             if j is not None:
                 alpha[j, sel] = eq
+        elif m.model == 3:
+            s, c, pp, pe, ok = gtn_.gtn(e[:, sel], state.epsp[:, sel], state.ep[sel], D[sel], m)
+            if not np.all(ok):
+                raise ReturnMapFailure()
+            epsp[:, sel] = pp
+            ep[sel] = pe
+            alpha[j, sel] = pe                         # ebar0 source: eps0p
+            alpha[j + 1, sel] = pp[0] + pp[1] + pp[2]  # trbar source: tr eps^p
         else:
             raise ValueError(m.model)
         sigma[:, sel] = s
@@ -196,7 +223,11 @@ def solve_increment(cell: Cell, state: State, E_target, S_target, tol: Tolerance
         eps_prev = eps.copy()
         newton_ok = False
         for r in range(tol.max_newton + 1):
-            sigma, C, alpha, epsp, ep = evaluate(cell, eps, state, D)
+            try:
+                sigma, C, alpha, epsp, ep = evaluate(cell, eps, state, D)
+            except ReturnMapFailure:
+                return state, Report(np.zeros(6), eps.reshape(6, n).mean(axis=1), np.inf, k + 1, newton_total,
+                                     cg_total, helm_total, False, err_hist)
             b = -apply_projection(g, sigma, mask, backend, dc_mean_shift=S_bar)
             smean = sigma.reshape(6, n).mean(axis=1)
             rms = np.sqrt(np.sum(b * b) / n)
@@ -246,6 +277,10 @@ def solve_increment(cell: Cell, state: State, E_target, S_target, tol: Tolerance
                 np.maximum(0.0, abar[j].reshape(-1)[sel]), m.eps_c, m.eps_r, m.d_max))
         elif m.model == 2:
             new.hist[sel] = np.maximum(state.hist[sel], abar[j].reshape(-1)[sel])
+        elif m.model == 3:
+            # f_{n+1} from the converged non-local fields (App. A); eps^p, eps0p are those
+            # of the last mechanical solve (f frozen at abar^(k)), A-30
+            new.hist[sel] = gtn_porosity(cell, q, state, abar)[sel]
     rep = Report(smean, eps.reshape(6, n).mean(axis=1), err, k + 1, newton_total, cg_total,
                  helm_total, True, err_hist, sigma)
     return new, rep

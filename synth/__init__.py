@@ -149,7 +149,7 @@ def random_spd_tangent_torch(nvox: int, seed: int, device="cuda", lo: float = 1.
 # ----------------------------------------------------------------------------------------------
 @dataclass
 class Material:
-    model: int            # 0 elastic, 1 j2_lemaitre, 2 elastic_brittle
+    model: int            # 0 elastic, 1 j2_lemaitre, 2 elastic_brittle, 3 gtn
     E: float
     nu: float
     sigma_y: float = 0.0
@@ -159,6 +159,17 @@ class Material:
     d_max: float = 0.99
     kappa0: float = 0.0
     kappa_f: float = 1.0
+    # GTN (model 3, paper Sec. 2.1.1; defaults = the Sec. 4.1 values, cap P:837)
+    q1: float = 1.5
+    q2: float = 1.0
+    q3: float = 2.25
+    f_c: float = 0.15
+    f_f: float = 0.25
+    f_n: float = 0.04
+    eps_n: float = 0.3
+    s_n: float = 0.1
+    n_hard: float = 0.1
+    fstar_max: float = 0.6
 
 
 MATRIX_J2 = Material(model=1, E=70.0e3, nu=0.3, sigma_y=300.0, H=500.0, eps_c=0.005, eps_r=0.025, d_max=0.99)

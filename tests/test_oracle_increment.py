@@ -137,3 +137,54 @@ def test_elastic_path_independence_and_two_staggered_iterations():
         st, rb = solve_increment(cell, st, Et, np.zeros(6), TOL)
     assert np.max(np.abs(a.eps - st.eps)) < 1e-12
     assert np.allclose(ra.macro_stress, rb.macro_stress, rtol=1e-10, atol=1e-9)
+
+
+def gtn_point_driver(mat, mask, load_comp, Es):
+    """1-voxel mixed-control Newton + staggered fixed point for GTN (homogeneous cell: the
+    Helmholtz solution of a uniform source is the source, so abar = (eps0p, tr eps^p))."""
+    from oracle import gtn as GT
+    mask = np.array(mask, bool)
+    epsp_n, e0_n, f_n, eb_n, tb_n = np.zeros(6), 0.0, 0.0, 0.0, 0.0
+    eps = np.zeros(6)
+    out = []
+    for E in Es:
+        eps = eps.copy(); eps[load_comp] = E
+        eb, tb = eb_n, tb_n
+        for _ in range(200):
+            f = GT.porosity(f_n, eb, eb_n, tb, tb_n, mat)
+            for _ in range(60):
+                r = GT.gtn_point(eps, epsp_n, e0_n, f, mat)
+                res = r["sigma"][mask]
+                if np.linalg.norm(res) < 1e-13 * max(1.0, np.linalg.norm(r["sigma"])):
+                    break
+                eps[mask] -= np.linalg.solve(r["C"][np.ix_(mask, mask)], res)
+            eb_new, tb_new = r["e0"], r["epsp"][:3].sum()
+            done = abs(eb_new - eb) + abs(tb_new - tb) < 1e-15
+            eb, tb = eb_new, tb_new
+            if done:
+                break
+        f_n = GT.porosity(f_n, eb, eb_n, tb, tb_n, mat)
+        epsp_n, e0_n, eb_n, tb_n = r["epsp"], r["e0"], eb, tb
+        out.append((r["sigma"].copy(), f_n))
+    return out
+
+
+def test_homogeneous_gtn_cell_equals_material_point():
+    # nucleation moved into the loading range so that porosity grows within a few increments
+    mat = Material(model=3, E=300e3, nu=0.3, sigma_y=1000.0, eps_n=0.02, s_n=0.01, f_n=0.04)
+    g = Grid((4, 4, 4))
+    mask = (1, 1, 0, 1, 1, 1)
+    cell = Cell(g, np.zeros(g.shape, np.uint8), [mat], np.array([[0.1], [0.1]]), [0, 0], mask)
+    st = State.zero(cell)
+    Es = [4e-3 * i for i in range(1, 9)]
+    ref = gtn_point_driver(mat, mask, 2, Es)
+    for i, E in enumerate(Es):
+        Et = np.zeros(6); Et[2] = E
+        st, rep = solve_increment(cell, st, Et, np.zeros(6), TOL)
+        assert rep.converged
+        e = st.eps.reshape(6, -1)
+        assert np.max(e.max(axis=1) - e.min(axis=1)) <= 1e-13 * max(1e-3, np.abs(e).max())
+        assert np.allclose(rep.macro_stress, ref[i][0], rtol=1e-9, atol=1e-7)
+        assert np.allclose(st.hist, ref[i][1], rtol=1e-9, atol=1e-15)
+    assert st.hist.max() > 0.01          # porosity grew (nucleation + dilatant growth)
+    assert np.all(st.epsp[:3].sum(axis=0) > 0)
