@@ -350,8 +350,7 @@ def run_ours(a):
     ctx.set_phases(ph, 2)
     m0, m1 = synth.MATRIX_J2, synth.INCLUSION_EL
     for q, m in enumerate((m0, m1)):
-        ctx.set_material(q, Material(m.model, m.E, m.nu, m.sigma_y, m.H, m.eps_c, m.eps_r, m.d_max, m.kappa0,
-                                     m.kappa_f))
+        ctx.set_material(q, Material.of(m))
     ctx.set_nonlocal(synth.CONFIG1_ELL, [0])
     ctx.set_control(synth.CONFIG1_MASK)
     zero6 = np.zeros(6)

@@ -79,13 +79,22 @@ unsigned long long fgd_launch_count(const fgd_ctx* ctx);
 /* Phase map (Omega = U Omega_q): one uint8 per voxel, values < nphases <= 16. */
 fgd_status fgd_set_phases(fgd_ctx* ctx, const uint8_t* phase, int nphases);
 
-/* Per-phase material (A-17, A-18).
+/* Per-phase material (A-17, A-18, A-30..A-33).
  * model 0 elastic (E, nu); 1 J2-Lemaitre with linear hardening sigma_0 = sigma_y + H eps_p and
  * damage D(ebar) = clamp((ebar - eps_c)/(eps_r - eps_c), 0, d_max); 2 elastic-brittle particle
- * with d = clamp((kappa - kappa0)/(kappa_f - kappa0), 0, d_max).  E > 0, -1 < nu < 0.5. */
+ * with d = clamp((kappa - kappa0)/(kappa_f - kappa0), 0, d_max); 3 non-local GTN (Sec. 2.1.1
+ * P:89-166, Sec. 2.2.2, App. A): yield
+ * (q/sigma_0)^2 + 2 f* q1 cosh(-3 q2 p/(2 sigma_0)) - (1 + q3 f*^2), Aravas hardening
+ * sigma_0/sigma_y = (sigma_0/sigma_y + 3 mu eps0p/sigma_y)^n_hard, f* law with
+ * f_c, f_f capped at fstar_max, Chu-Needleman nucleation f_n, eps_n, s_n
+ * (P:151-155).  A GTN phase q needs two consecutive non-local fields j, j+1 with
+ * source_phase = q: field j regularises eps0p, field j+1 tr eps^p; its porosity is
+ * frozen from them during the mechanics (App. A).  E > 0, -1 < nu < 0.5.  The GTN fields
+ * are ignored by the other models. */
 typedef struct {
   int model;
   double E, nu, sigma_y, H, eps_c, eps_r, d_max, kappa0, kappa_f;
+  double q1, q2, q3, f_c, f_f, f_n, eps_n, s_n, n_hard, fstar_max;
 } fgd_material;
 fgd_status fgd_set_material(fgd_ctx* ctx, int phase, const fgd_material* m);
 
@@ -161,12 +170,15 @@ enum {
   FGD_FIELD_STRESS = 0,     /* 6 comps, last mechanical solve (get only) */
   FGD_FIELD_STRAIN = 1,     /* 6 comps, committed strain eps_n */
   FGD_FIELD_EPS_P = 2,      /* 6 comps, committed plastic strain */
-  FGD_FIELD_EQPS = 3,       /* 1 comp, committed equivalent plastic strain */
-  FGD_FIELD_HIST = 4,       /* 1 comp, committed damage history (D_n / kappa_n) */
+  FGD_FIELD_EQPS = 3,       /* 1 comp, committed equivalent plastic strain (GTN: matrix eps0p) */
+  FGD_FIELD_HIST = 4,       /* 1 comp, committed history: D_n (J2), kappa_n (brittle), porosity f_n (GTN) */
   FGD_FIELD_TANGENT = 5,    /* 21 comps, packed tangent in use (get only) */
   FGD_FIELD_NONLOCAL = 16,  /* + j: 1 comp, non-local field abar_j */
   FGD_FIELD_SOURCE = 32,    /* + j: 1 comp, local source alpha_j of the last constitutive call (get only) */
-  FGD_FIELD_ITERATE = 48    /* 6 comps, current strain iterate */
+  FGD_FIELD_ITERATE = 48,   /* 6 comps, current strain iterate */
+  FGD_FIELD_NONLOCAL_ITERATE = 64  /* + j: 1 comp, the current (staggered-iterate) abar_j the next
+                                      fgd_constitutive is frozen at; FGD_FIELD_NONLOCAL sets both it
+                                      and the committed abar_j,n (GTN porosity increments, A-30) */
 };
 fgd_status fgd_get_field(fgd_ctx* ctx, int which, double* out);
 fgd_status fgd_set_field(fgd_ctx* ctx, int which, const double* in);

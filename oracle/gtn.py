@@ -32,8 +32,8 @@ u = (a, b, x):
   R2 = Q^2 + 2 f* q1 cosh(xi) - 1 - q3 f*^2       [= phi]
   R3 = (1 - f)(eps0p(x) - eps0p_n) + P a - Q b   [work identity / sigma_0]
 with P = p/sigma_0, Q = q/sigma_0, xi = (3/2) q2 P, sigma_0 = sigma_Y x.  Newton from
-(0, 0, x_n) with step halving on R1^2 + R2^2 + R3^2 (and x >= 1), until the scaled step is at
-round-off; elastic if phi(p_tr, q_tr, sigma_0(eps0p_n)) <= 0.
+(0, 0, x_n) with step halving on R1^2 + R2^2 + R3^2 (and x >= 1), until the Newton step is at
+round-off (|da| + |db| <= 1e-13 (|a| + |b|) + 1e-14 sigma_Y/(3 mu), |dx| <= 1e-13 x); elastic if phi(p_tr, q_tr, sigma_0(eps0p_n)) <= 0.
 
 Consistent tangent: linearise R(u; p_tr, q_tr) = 0 -> du = M (dp_tr, dq_tr), M = -J^-1 dR/d(p_tr, q_tr),
 dp_tr = -K 1:de, dq_tr = 2 mu n:de, dn = (3 mu/q_tr)(I_dev - (2/3) n(x)n) de, so
@@ -187,8 +187,11 @@ def return_map(ptr, qtr, e0n, f, fs, m, K, mu, max_it=50):
     for it in range(1, max_it + 1):
         J, _ = _jacobians(u, ptr, qtr, f, fs, m, K, mu)
         du = -np.linalg.solve(J, R)
-        if abs(du[0]) + abs(du[1]) <= 1e-13 * (abs(u[0]) + abs(u[1])) and abs(du[2]) <= 1e-13 * u[2]:
-            return u + du, it, True           # Newton step at round-off: done
+        # Newton step at round-off: done.  The absolute floor (strain units) is ~50x the rounding
+        # of eps0p(x) = sigma_Y (x^(1/N) - x)/(3 mu) near x = 1, which bounds how well a, b resolve.
+        if (abs(du[0]) + abs(du[1]) <= 1e-13 * (abs(u[0]) + abs(u[1])) + 1e-14 * m.sigma_y / (3.0 * mu)
+                and abs(du[2]) <= 1e-13 * u[2]):
+            return u + du, it, True
         psi = float(R @ R)
         t = 1.0
         for _ in range(30):                   # halve until R^2 decreases (x projected onto x >= 1)

@@ -23,7 +23,7 @@ OK, EINVAL, ESHAPE, ECUDA, ENCCL, ENOMEM, ENOCONV, ESTATE = 0, -1, -2, -3, -4, -
 STATUS = {0: "FGD_OK", -1: "FGD_EINVAL", -2: "FGD_ESHAPE", -3: "FGD_ECUDA", -4: "FGD_ENCCL",
           -5: "FGD_ENOMEM", -6: "FGD_ENOCONV", -7: "FGD_ESTATE"}
 FIELD_STRESS, FIELD_STRAIN, FIELD_EPS_P, FIELD_EQPS, FIELD_HIST, FIELD_TANGENT = 0, 1, 2, 3, 4, 5
-FIELD_NONLOCAL, FIELD_SOURCE, FIELD_ITERATE = 16, 32, 48
+FIELD_NONLOCAL, FIELD_SOURCE, FIELD_ITERATE, FIELD_NONLOCAL_ITERATE = 16, 32, 48, 64
 
 
 class fgd_grid(C.Structure):
@@ -35,9 +35,12 @@ class fgd_dist(C.Structure):
                 ("nccl_id", C.c_void_p), ("stream", C.c_void_p)]
 
 
+MATERIAL_KEYS = ("E", "nu", "sigma_y", "H", "eps_c", "eps_r", "d_max", "kappa0", "kappa_f",
+                 "q1", "q2", "q3", "f_c", "f_f", "f_n", "eps_n", "s_n", "n_hard", "fstar_max")
+
+
 class fgd_material(C.Structure):
-    _fields_ = [("model", C.c_int)] + [(k, C.c_double) for k in
-                                       ("E", "nu", "sigma_y", "H", "eps_c", "eps_r", "d_max", "kappa0", "kappa_f")]
+    _fields_ = [("model", C.c_int)] + [(k, C.c_double) for k in MATERIAL_KEYS]
 
 
 class fgd_increment(C.Structure):

@@ -19,10 +19,21 @@ __all__ = ["Context", "FgdError", "Material", "nccl_id"]
 
 
 class Material:
+    """fgd_material: model 0 elastic, 1 J2-Lemaitre, 2 elastic-brittle, 3 non-local GTN (the GTN
+    defaults are the paper's Sec. 4.1 values, with the f* cap 0.6 of P:837)."""
+
     def __init__(self, model, E, nu, sigma_y=0.0, H=0.0, eps_c=0.0, eps_r=1.0, d_max=0.99, kappa0=0.0,
-                 kappa_f=1.0):
+                 kappa_f=1.0, q1=1.5, q2=1.0, q3=2.25, f_c=0.15, f_f=0.25, f_n=0.04, eps_n=0.3, s_n=0.1,
+                 n_hard=0.1, fstar_max=0.6):
         self.model, self.E, self.nu, self.sigma_y, self.H = model, E, nu, sigma_y, H
         self.eps_c, self.eps_r, self.d_max, self.kappa0, self.kappa_f = eps_c, eps_r, d_max, kappa0, kappa_f
+        self.q1, self.q2, self.q3, self.f_c, self.f_f = q1, q2, q3, f_c, f_f
+        self.f_n, self.eps_n, self.s_n, self.n_hard, self.fstar_max = f_n, eps_n, s_n, n_hard, fstar_max
+
+    @classmethod
+    def of(cls, m):
+        """From any object carrying the fgd_material attributes (e.g. synth.Material)."""
+        return cls(int(m.model), *[float(getattr(m, k)) for k in _fgd.MATERIAL_KEYS])
 
 
 def _like(x, shape=None):
@@ -103,8 +114,7 @@ class Context:
         self._chk(_fgd.fgd_set_phases(self.h, ptr(phases, np.uint8), int(nphases)))
 
     def set_material(self, phase: int, m):
-        mm = _fgd.fgd_material(int(m.model), *[float(getattr(m, k)) for k in
-                                              ("E", "nu", "sigma_y", "H", "eps_c", "eps_r", "d_max", "kappa0", "kappa_f")])
+        mm = _fgd.fgd_material(int(m.model), *[float(getattr(m, k)) for k in _fgd.MATERIAL_KEYS])
         self._chk(_fgd.fgd_set_material(self.h, int(phase), C.byref(mm)))
 
     def set_nonlocal(self, ell, source_phase):

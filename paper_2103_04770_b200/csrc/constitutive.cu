@@ -39,6 +39,8 @@ struct PointOut {
   double epsp[6];
   double ep;
   double alpha;
+  double alpha2;    // GTN: source of the phase's second field (tr eps^p)
+  int fail;         // GTN: return mapping did not converge
 };
 
 __device__ __forceinline__ void elastic_C(double K, double mu, double f, PointOut& o) {
@@ -49,15 +51,221 @@ __device__ __forceinline__ void elastic_C(double K, double mu, double f, PointOu
   for (int i = 0; i < 6; ++i) o.n[i] = 0.0;
 }
 
+
+// ---------------------------------------------------------------------------------------------
+// Non-local GTN (model 3): Sec. 2.1.1, Sec. 2.2.2, App. A P:1100-1129.
+// Mandel vectors; q = Mises stress (the paper's s), p = -tr(sigma)/3, sigma_0 = sigma_y x.
+// Frozen porosity (App. A P:1119 with the non-local fields of the staggered iterate, A-30):
+//   f = (f_n + A_N(ebar0) (ebar0 - ebar0_n) + (trbar - trbar_n)) / (1 + trbar - trbar_n) in [0, 1]
+// Return mapping in u = (a, b, x): d eps^p = (a/3) 1 + b n, n = 1.5 s_tr/q_tr, p = p_tr + K a,
+// q = q_tr - 3 mu b, residuals (scaled)
+//   R1 = a Q + b c sinh(xi)                         (normality with dlam eliminated)
+//   R2 = Q^2 + 2 f* q1 cosh(xi) - 1 - q3 f*^2       (yield)
+//   R3 = (1 - f)(e(x) - e_n) + P a - Q b            (plastic work P:125-131 over sigma_0)
+// P = p/sigma_0, Q = q/sigma_0, xi = 1.5 q2 P, c = 1.5 f* q1 q2, e(x) = sigma_y (x^(1/N) - x)/(3 mu)
+// (Aravas P:826-829 solved for eps0p).  Newton from (0, 0, x_n) with step halving on |R|^2 and
+// x >= 1; converged when the Newton step is at round-off (relative 1e-13, plus an absolute
+// 1e-14 sigma_y/(3 mu) on a, b: the rounding floor of e(x) near x = 1); 50 iterations max.
+// Tangent: du = -J^-1 dR/d(p_tr, q_tr) (dp_tr, dq_tr), dp_tr = -K 1:de, dq_tr = 2 mu n:de, giving
+//   C = 2 mu theta I_dev + K a_pp 1x1 - 2 mu a_pq 1xn - (2/3) K a_qp nx1 + (4/3) mu (a_qq - theta) nxn,
+// used symmetrised (A-32): ca 1x1 + cb I - cc nxn + cd (1xn + nx1) with cb = 2 mu theta,
+// ca = K a_pp - cb/3, cc = (4/3) mu (theta - a_qq), cd = -mu a_pq - K a_qp/3 (cd := 0 where
+// |cc| < 1e-6 cb, A-33), and folded into the compact form with m = n - (cd/cc) 1:
+//   ca 1x1 - cc nxn + cd (1xn + nx1) = (ca + cd^2/cc) 1x1 - cc m x m.
+__device__ __forceinline__ double gtn_fstar(double f, const Material& m) {
+  const double fv = (m.q1 + sqrt(m.q1 * m.q1 - m.q3)) / m.q3;
+  double fs = f < m.f_c ? f : (f < m.f_f ? m.f_c + (fv - m.f_c) / (m.f_f - m.f_c) * (f - m.f_c) : fv);
+  return fs < m.fstar_max ? fs : m.fstar_max;
+}
+
+__device__ __forceinline__ double gtn_porosity(double fn, double e0, double e0n, double t, double tn,
+                                               const Material& m) {
+  const double z = (e0 - m.eps_n) / m.s_n;
+  const double AN = m.f_n / (m.s_n * 2.50662827463100050242) * exp(-0.5 * z * z);   // sqrt(2 pi)
+  const double dt = t - tn;
+  double f = (fn + AN * (e0 - e0n) + dt) / (1.0 + dt);
+  f = f < 0.0 ? 0.0 : f;
+  return f > 1.0 ? 1.0 : f;
+}
+
+// x = sigma_0/sigma_y at eps0p = e: Newton on x^(1/N) - x - 3 mu e/sigma_y from x = 1
+__device__ double gtn_aravas_x(double e, const Material& m, double mu) {
+  const double c = 3.0 * mu * e / m.sigma_y;
+  if (!(c > 0.0)) return 1.0;
+  const double iN = 1.0 / m.n_hard;
+  double x = 1.0;
+  for (int it = 0; it < 100; ++it) {
+    const double xp = pow(x, iN - 1.0);
+    const double dx = (xp * x - x - c) / (iN * xp - 1.0);
+    x -= dx;
+    if (fabs(dx) <= 1e-15 * x) break;
+  }
+  return x;
+}
+
+struct GtnCtx {
+  double ptr, qtr, e0n, f, fs, K, mu;
+};
+
+__device__ void gtn_eval(const Material& m, const GtnCtx& g, const double u[3], double R[3], double J[3][3],
+                         double B[3][2]) {
+  const double a = u[0], b = u[1], x = u[2];
+  const double s0 = m.sigma_y * x, is0 = 1.0 / s0;
+  const double P = (g.ptr + g.K * a) * is0, Q = (g.qtr - 3.0 * g.mu * b) * is0;
+  const double k = 1.5 * m.q2, xi = k * P;
+  const double c = 1.5 * g.fs * m.q1 * m.q2;
+  const double ch = cosh(xi), sh = sinh(xi);
+  const double iN = 1.0 / m.n_hard;
+  const double xp = pow(x, iN - 1.0);
+  const double ex = m.sigma_y * (xp * x - x) / (3.0 * g.mu);
+  R[0] = a * Q + b * c * sh;
+  R[1] = Q * Q + 2.0 * g.fs * m.q1 * ch - 1.0 - m.q3 * g.fs * g.fs;
+  R[2] = (1.0 - g.f) * (ex - g.e0n) + P * a - Q * b;
+  if (J) {
+    const double dPa = g.K * is0, dPx = -P / x, dQb = -3.0 * g.mu * is0, dQx = -Q / x;
+    const double dex = m.sigma_y * (iN * xp - 1.0) / (3.0 * g.mu);
+    const double tq = 2.0 * g.fs * m.q1 * sh * k;   // d(2 f* q1 cosh xi)/dP
+    J[0][0] = Q + b * c * ch * k * dPa;
+    J[0][1] = a * dQb + c * sh;
+    J[0][2] = a * dQx + b * c * ch * k * dPx;
+    J[1][0] = tq * dPa;
+    J[1][1] = 2.0 * Q * dQb;
+    J[1][2] = 2.0 * Q * dQx + tq * dPx;
+    J[2][0] = P + a * dPa;
+    J[2][1] = -Q - b * dQb;
+    J[2][2] = (1.0 - g.f) * dex + a * dPx - b * dQx;
+    B[0][0] = b * c * ch * k * is0;
+    B[0][1] = a * is0;
+    B[1][0] = tq * is0;
+    B[1][1] = 2.0 * Q * is0;
+    B[2][0] = a * is0;
+    B[2][1] = -b * is0;
+  }
+}
+
+// x = A^-1 r (Cramer)
+__device__ __forceinline__ void solve3(const double A[3][3], const double r[3], double x[3]) {
+  const double c00 = A[1][1] * A[2][2] - A[1][2] * A[2][1];
+  const double c01 = A[1][2] * A[2][0] - A[1][0] * A[2][2];
+  const double c02 = A[1][0] * A[2][1] - A[1][1] * A[2][0];
+  const double id = 1.0 / (A[0][0] * c00 + A[0][1] * c01 + A[0][2] * c02);
+  const double c10 = A[0][2] * A[2][1] - A[0][1] * A[2][2];
+  const double c11 = A[0][0] * A[2][2] - A[0][2] * A[2][0];
+  const double c12 = A[0][1] * A[2][0] - A[0][0] * A[2][1];
+  const double c20 = A[0][1] * A[1][2] - A[0][2] * A[1][1];
+  const double c21 = A[0][2] * A[1][0] - A[0][0] * A[1][2];
+  const double c22 = A[0][0] * A[1][1] - A[0][1] * A[1][0];
+  x[0] = (c00 * r[0] + c10 * r[1] + c20 * r[2]) * id;
+  x[1] = (c01 * r[0] + c11 * r[1] + c21 * r[2]) * id;
+  x[2] = (c02 * r[0] + c12 * r[1] + c22 * r[2]) * id;
+}
+
+__device__ __forceinline__ void gtn_update(const Material& m, double K, double mu, const double* e, const double* epsp_n,
+                                        double e0n, double f, PointOut& o) {
+  double ee[6];
+  for (int i = 0; i < 6; ++i) ee[i] = e[i] - epsp_n[i];
+  const double tr = ee[0] + ee[1] + ee[2];
+  double s_tr[6], ss = 0.0;
+  for (int i = 0; i < 6; ++i) {
+    s_tr[i] = 2.0 * mu * (ee[i] - (i < 3 ? tr / 3.0 : 0.0));
+    ss += s_tr[i] * s_tr[i];
+  }
+  GtnCtx g{-K * tr, sqrt(1.5 * ss), e0n, f, gtn_fstar(f, m), K, mu};
+  const double xn = gtn_aravas_x(e0n, m, mu);
+  const double Ptr = g.ptr / (m.sigma_y * xn), Qtr = g.qtr / (m.sigma_y * xn);
+  const double phi_tr = Qtr * Qtr + 2.0 * g.fs * m.q1 * cosh(1.5 * m.q2 * Ptr) - 1.0 - m.q3 * g.fs * g.fs;
+  o.fail = 0;
+  o.ep = e0n;
+  for (int i = 0; i < 6; ++i) o.epsp[i] = epsp_n[i];
+  if (!(phi_tr > 0.0)) {   // elastic
+    for (int i = 0; i < 6; ++i) o.sig[i] = s_tr[i] + (i < 3 ? K * tr : 0.0);
+    elastic_C(K, mu, 1.0, o);
+    o.alpha = e0n;
+    o.alpha2 = o.epsp[0] + o.epsp[1] + o.epsp[2];
+    return;
+  }
+  const bool tiny = g.qtr <= 1e-12 * m.sigma_y;
+  double n[6];
+  for (int i = 0; i < 6; ++i) n[i] = tiny ? 0.0 : 1.5 * s_tr[i] / g.qtr;
+  double u[3] = {0.0, 0.0, xn}, R[3], J[3][3], B[3][2];
+  gtn_eval(m, g, u, R, nullptr, nullptr);
+  bool conv = false;
+  for (int it = 0; it < 50 && !conv; ++it) {
+    gtn_eval(m, g, u, R, J, B);
+    double du[3];
+    solve3(J, R, du);
+    for (int i = 0; i < 3; ++i) du[i] = -du[i];
+    if (fabs(du[0]) + fabs(du[1]) <= 1e-13 * (fabs(u[0]) + fabs(u[1])) + 1e-14 * m.sigma_y / (3.0 * mu) &&
+        fabs(du[2]) <= 1e-13 * u[2]) {
+      for (int i = 0; i < 3; ++i) u[i] += du[i];
+      conv = true;
+      break;
+    }
+    const double psi = R[0] * R[0] + R[1] * R[1] + R[2] * R[2];
+    double t = 1.0, un[3], Rn[3];
+    for (int ls = 0; ls < 30; ++ls) {
+      for (int i = 0; i < 3; ++i) un[i] = u[i] + t * du[i];
+      un[2] = un[2] > 1.0 ? un[2] : 1.0;
+      gtn_eval(m, g, un, Rn, nullptr, nullptr);
+      if (Rn[0] * Rn[0] + Rn[1] * Rn[1] + Rn[2] * Rn[2] < psi) break;
+      t *= 0.5;
+    }
+    for (int i = 0; i < 3; ++i) u[i] = un[i];
+  }
+  o.fail = conv ? 0 : 1;
+  const double a = u[0], b = u[1], x = u[2];
+  const double p = g.ptr + K * a, q = g.qtr - 3.0 * mu * b;
+  for (int i = 0; i < 6; ++i) {
+    o.sig[i] = (2.0 / 3.0) * q * n[i] - (i < 3 ? p : 0.0);
+    o.epsp[i] = epsp_n[i] + b * n[i] + (i < 3 ? a / 3.0 : 0.0);
+  }
+  o.ep = m.sigma_y * (pow(x, 1.0 / m.n_hard) - x) / (3.0 * mu);
+  o.alpha = o.ep;
+  o.alpha2 = o.epsp[0] + o.epsp[1] + o.epsp[2];
+  // consistent tangent
+  gtn_eval(m, g, u, R, J, B);
+  double Mc[3][2];
+  for (int col = 0; col < 2; ++col) {
+    const double rhs[3] = {B[0][col], B[1][col], B[2][col]};
+    double sol[3];
+    solve3(J, rhs, sol);
+    for (int i = 0; i < 3; ++i) Mc[i][col] = -sol[i];
+  }
+  const double a_pp = 1.0 + K * Mc[0][0], a_pq = K * Mc[0][1];
+  const double a_qp = -3.0 * mu * Mc[1][0], a_qq = 1.0 - 3.0 * mu * Mc[1][1];
+  const double theta = tiny ? 1.0 : q / g.qtr;
+  const double cb = 2.0 * mu * theta;
+  double ca = K * a_pp - cb / 3.0;
+  const double cc = (4.0 / 3.0) * mu * (theta - a_qq);
+  double cd = -mu * a_pq - K * a_qp / 3.0;
+  if (fabs(cc) < 1e-6 * cb) cd = 0.0;
+  const double gam = cd != 0.0 ? cd / cc : 0.0;
+  ca += cd * gam;
+  o.ca = ca;
+  o.cb = cb;
+  o.cc = cc;
+  for (int i = 0; i < 6; ++i) o.n[i] = n[i] - (i < 3 ? gam : 0.0);
+}
+
+// gf: the frozen porosity of a GTN phase (unused by the other models)
+template <bool GTN>
 __device__ void point_update(const Material& m, int has_field, const double* e, const double* epsp_n, double ep_n,
-                             double hist, double abar, double D_override, PointOut& o) {
+                             double hist, double abar, double D_override, double gf, PointOut& o) {
   const double K = m.E / (3.0 * (1.0 - 2.0 * m.nu));
   const double mu = m.E / (2.0 * (1.0 + m.nu));
   const double tr = e[0] + e[1] + e[2];
   const double de[6] = {e[0] - tr / 3.0, e[1] - tr / 3.0, e[2] - tr / 3.0, e[3], e[4], e[5]};
   o.alpha = 0.0;
+  o.alpha2 = 0.0;
+  o.fail = 0;
   o.ep = ep_n;
   for (int i = 0; i < 6; ++i) o.epsp[i] = epsp_n[i];
+  if constexpr (GTN) {
+    if (m.model == 3) {
+      gtn_update(m, K, mu, e, epsp_n, ep_n, gf, o);
+      return;
+    }
+  }
   if (m.model == 0) {
     elastic_C(K, mu, 1.0, o);
     for (int i = 0; i < 6; ++i) o.sig[i] = 2.0 * mu * de[i] + (i < 3 ? K * tr : 0.0);
@@ -121,7 +329,8 @@ struct KArgs {
   const double* epsp_n;
   const double* ep_n;
   const double* hist;
-  const double* abar;   // J * nvox
+  const double* abar;   // J * nvox: non-local fields the mechanics is frozen at
+  const double* abar_n; // J * nvox: committed non-local fields (GTN porosity increments)
   const uint8_t* phase;
   double* sig;
   double* C;
@@ -130,8 +339,19 @@ struct KArgs {
   double* partials;
 };
 
+// frozen porosity of GTN voxel g from the fields (j: ebar0, j + 1: trbar) at ab against the committed ones
+__device__ __forceinline__ double gtn_frozen_f(const Material& m, const double* ab, const double* abn, double fn,
+                                               int j, size_t n, size_t g) {
+  return gtn_porosity(fn, ab[(size_t)j * n + g], abn[(size_t)j * n + g], ab[(size_t)(j + 1) * n + g],
+                      abn[(size_t)(j + 1) * n + g], m);
+}
+
+template <bool GTN>
 __global__ void __launch_bounds__(256) k_constitutive(KArgs a, MatTable mt) {
-  double red[6] = {0, 0, 0, 0, 0, 0};
+  constexpr int NR = GTN ? 7 : 6;   // <sigma> sums (+ GTN return-mapping failures)
+  double red[NR];
+#pragma unroll
+  for (int i = 0; i < NR; ++i) red[i] = 0.0;
   const size_t n = a.nvox;
   for (size_t g = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g < n; g += (size_t)gridDim.x * blockDim.x) {
     const int q = a.phase[g];
@@ -143,8 +363,12 @@ __global__ void __launch_bounds__(256) k_constitutive(KArgs a, MatTable mt) {
       ep6[i] = a.epsp_n[i * n + g];
     }
     const double abar = (j >= 0) ? a.abar[(size_t)j * n + g] : 0.0;
+    double gf = 0.0;
+    const bool gtn = GTN && m.model == 3;
+    if (gtn) gf = gtn_frozen_f(m, a.abar, a.abar_n, a.hist[g], j, n, g);
     PointOut o;
-    point_update(m, j >= 0, e, ep6, a.ep_n[g], a.hist[g], abar, -1.0, o);
+    point_update<GTN>(m, j >= 0, e, ep6, a.ep_n[g], a.hist[g], abar, -1.0, gf, o);
+    if constexpr (GTN) red[NR - 1] += (double)o.fail;
     for (int i = 0; i < 6; ++i) {
       a.sig[i * n + g] = o.sig[i];
       red[i] += o.sig[i];
@@ -153,14 +377,18 @@ __global__ void __launch_bounds__(256) k_constitutive(KArgs a, MatTable mt) {
     a.C[6 * n + g] = o.ca;
     a.C[7 * n + g] = o.cb;
     a.C[8 * n + g] = o.cc;
-    for (int f = 0; f < mt.nfields; ++f) a.alpha[(size_t)f * n + g] = (f == j) ? o.alpha : 0.0;
+    for (int f = 0; f < mt.nfields; ++f)
+      a.alpha[(size_t)f * n + g] = (f == j) ? o.alpha : ((gtn && f == j + 1) ? o.alpha2 : 0.0);
   }
-  reduce_finalize<6>(red, a.partials, a.sc, RED_STORE, 0);
+  reduce_finalize<NR>(red, a.partials, a.sc, RED_STORE, 0);
 }
 
-// commit: recompute eps^p, eps_p at the converged strain; D_n <- max(D_n, D(abar)), kappa_n <- max
-__global__ void __launch_bounds__(256) k_commit(KArgs a, MatTable mt, double* epsp_out, double* ep_out,
-                                                double* hist_out) {
+// commit: recompute eps^p, eps_p at the converged strain with the non-local fields the last
+// mechanics was frozen at (a.abar); history from the accepted new fields abar_new:
+// D_n <- max(D_n, D(abar_new)), kappa_n <- max(kappa_n, abar_new), GTN f_n <- f(abar_new) (A-30)
+template <bool GTN>
+__global__ void __launch_bounds__(256) k_commit(KArgs a, MatTable mt, const double* abar_new, double* epsp_out,
+                                                double* ep_out, double* hist_out) {
   const size_t n = a.nvox;
   for (size_t g = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g < n; g += (size_t)gridDim.x * blockDim.x) {
     const int q = a.phase[g];
@@ -172,18 +400,23 @@ __global__ void __launch_bounds__(256) k_commit(KArgs a, MatTable mt, double* ep
       ep6[i] = a.epsp_n[i * n + g];
     }
     const double abar = (j >= 0) ? a.abar[(size_t)j * n + g] : 0.0;
+    const bool gtn = GTN && m.model == 3;
+    const double gf = gtn ? gtn_frozen_f(m, a.abar, a.abar_n, a.hist[g], j, n, g) : 0.0;
     PointOut o;
-    point_update(m, j >= 0, e, ep6, a.ep_n[g], a.hist[g], abar, 0.0, o);
+    point_update<GTN>(m, j >= 0, e, ep6, a.ep_n[g], a.hist[g], abar, 0.0, gf, o);
     for (int i = 0; i < 6; ++i) epsp_out[i * n + g] = o.epsp[i];
     ep_out[g] = o.ep;
     double h = a.hist[g];
     if (j >= 0) {
+      const double an = abar_new[(size_t)j * n + g];
       if (m.model == 1) {
-        const double ab = abar > 0.0 ? abar : 0.0;
+        const double ab = an > 0.0 ? an : 0.0;
         const double D = clamp01cap((ab - m.eps_c) / (m.eps_r - m.eps_c), m.d_max);
         h = D > h ? D : h;
       } else if (m.model == 2) {
-        h = abar > h ? abar : h;
+        h = an > h ? an : h;
+      } else if (gtn) {
+        h = gtn_frozen_f(m, abar_new, a.abar_n, a.hist[g], j, n, g);
       }
     }
     hist_out[g] = h;
@@ -303,7 +536,7 @@ static MatTable make_table(const fgd_ctx* c) {
     t.m[q] = c->mat[q];
     t.field_of[q] = -1;
   }
-  for (int j = 0; j < c->nfields; ++j) t.field_of[c->source_phase[j]] = j;
+  for (int j = c->nfields - 1; j >= 0; --j) t.field_of[c->source_phase[j]] = j;   // first field of the phase
   t.nfields = c->nfields;
   return t;
 }
@@ -314,26 +547,56 @@ static MatTable make_table(const fgd_ctx* c) {
     if (e_ != cudaSuccess) return set_err(ctx, FGD_ECUDA, std::string(name) + ": " + cudaGetErrorString(e_)); \
   } while (0)
 
+bool has_gtn(const fgd_ctx* c) {
+  for (int q = 0; q < c->nphases; ++q)
+    if (c->mat[q].model == 3) return true;
+  return false;
+}
+
+// every GTN phase needs two consecutive fields (eps0p, tr eps^p) sourced by it
+static fgd_status check_gtn_fields(fgd_ctx* c, const MatTable& t) {
+  for (int q = 0; q < c->nphases; ++q) {
+    if (c->mat[q].model != 3) continue;
+    const int j = t.field_of[q];
+    if (j < 0 || j + 1 >= c->nfields || c->source_phase[j + 1] != q)
+      return set_err(c, FGD_ESTATE, "GTN phase " + std::to_string(q) +
+                                        " needs two consecutive non-local fields with source_phase = " +
+                                        std::to_string(q) + " (eps0p, tr eps^p)");
+  }
+  return FGD_OK;
+}
+
 fgd_status launch_constitutive(fgd_ctx* c, const double* eps) {
   const int nb = ew_blocks(c, c->nvox);
   fgd_status s = ensure_partials(c, nb);
   if (s != FGD_OK) return s;
-  KArgs a{c->nvox, eps, c->st_epsp, c->st_ep, c->st_hist, c->w_abar, c->phase, c->w_sig, c->Cc, c->w_alpha, c->sc,
-          c->partials};
+  const MatTable t = make_table(c);
+  const bool gtn = has_gtn(c);
+  if (gtn && (s = check_gtn_fields(c, t)) != FGD_OK) return s;
+  KArgs a{c->nvox, eps, c->st_epsp, c->st_ep, c->st_hist, c->w_abar, c->st_abar, c->phase, c->w_sig, c->Cc,
+          c->w_alpha, c->sc, c->partials};
   c->launches++;
   KTimer kt(c, KC_CONST);
-  k_constitutive<<<nb, 256, 0, c->stream>>>(a, make_table(c));
+  if (gtn) {
+    k_constitutive<true><<<nb, 256, 0, c->stream>>>(a, t);
+  } else {
+    k_constitutive<false><<<nb, 256, 0, c->stream>>>(a, t);
+  }
   FGD_CHECK_LAUNCH(c, "k_constitutive");
   return FGD_OK;
 }
 
-fgd_status launch_commit(fgd_ctx* c, const double* eps, double* epsp_out, double* ep_out, double* hist_out) {
+fgd_status launch_commit(fgd_ctx* c, const double* eps, const double* abar_new, double* epsp_out, double* ep_out,
+                         double* hist_out) {
   const int nb = ew_blocks(c, c->nvox);
-  KArgs a{c->nvox, eps, c->st_epsp, c->st_ep, c->st_hist, c->w_abar, c->phase, nullptr, nullptr, nullptr, c->sc,
-          nullptr};
+  KArgs a{c->nvox, eps, c->st_epsp, c->st_ep, c->st_hist, c->w_abar, c->st_abar, c->phase, nullptr, nullptr, nullptr,
+          c->sc, nullptr};
   c->launches++;
   KTimer kt(c, KC_OTHER);
-  k_commit<<<nb, 256, 0, c->stream>>>(a, make_table(c), epsp_out, ep_out, hist_out);
+  if (has_gtn(c))
+    k_commit<true><<<nb, 256, 0, c->stream>>>(a, make_table(c), abar_new, epsp_out, ep_out, hist_out);
+  else
+    k_commit<false><<<nb, 256, 0, c->stream>>>(a, make_table(c), abar_new, epsp_out, ep_out, hist_out);
   FGD_CHECK_LAUNCH(c, "k_commit");
   return FGD_OK;
 }

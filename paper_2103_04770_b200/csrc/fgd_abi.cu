@@ -698,11 +698,22 @@ fgd_status fgd_set_phases(fgd_ctx* c, const uint8_t* phase, int nphases) {
 fgd_status fgd_set_material(fgd_ctx* c, int phase, const fgd_material* m) {
   if (!c || !m) return set_err(c, FGD_EINVAL, "null argument");
   if (phase < 0 || phase >= kMaxPhases) return set_err(c, FGD_EINVAL, "phase out of range");
-  if (m->model < 0 || m->model > 2) return set_err(c, FGD_EINVAL, "unknown material model");
+  if (m->model < 0 || m->model > 3) return set_err(c, FGD_EINVAL, "unknown material model");
   if (!(m->E > 0.0) || !(m->nu > -1.0 && m->nu < 0.5)) return set_err(c, FGD_EINVAL, "E > 0 and -1 < nu < 0.5 required");
   if (m->model == 1 && !(m->eps_r > m->eps_c)) return set_err(c, FGD_EINVAL, "eps_r must exceed eps_c");
   if (m->model == 2 && !(m->kappa_f > m->kappa0)) return set_err(c, FGD_EINVAL, "kappa_f must exceed kappa0");
-  c->mat[phase] = Material{m->model, m->E, m->nu, m->sigma_y, m->H, m->eps_c, m->eps_r, m->d_max, m->kappa0, m->kappa_f};
+  if (m->model == 3) {
+    const bool ok = m->sigma_y > 0.0 && m->q1 > 0.0 && m->q3 > 0.0 && m->q1 * m->q1 >= m->q3 && m->f_c > 0.0 &&
+                    m->f_f > m->f_c && m->s_n > 0.0 && m->n_hard > 0.0 && m->n_hard < 1.0 && m->fstar_max > 0.0 &&
+                    m->fstar_max < (m->q1 + std::sqrt(m->q1 * m->q1 - m->q3)) / m->q3;
+    if (!ok)
+      return set_err(c, FGD_EINVAL,
+                     "GTN needs sigma_y, q1, q3, s_n > 0, q1^2 >= q3, 0 < f_c < f_f, 0 < n_hard < 1, "
+                     "0 < fstar_max < f_V*");
+  }
+  c->mat[phase] = Material{m->model, m->E, m->nu, m->sigma_y, m->H, m->eps_c, m->eps_r, m->d_max, m->kappa0,
+                           m->kappa_f, m->q1, m->q2, m->q3, m->f_c, m->f_f, m->f_n, m->eps_n, m->s_n, m->n_hard,
+                           m->fstar_max};
   c->mat_set[phase] = true;
   return FGD_OK;
 }
@@ -863,7 +874,8 @@ fgd_status fgd_constitutive(fgd_ctx* c, const double* eps, double* sigma_out, do
       FGD_CUDA(c, cudaMemcpyAsync(c->w_eps, de, 6 * c->nvox * 8, cudaMemcpyDeviceToDevice, c->stream));
   }
   TRY(launch_constitutive(c, c->w_eps));
-  TRY(allreduce_sum(c, &c->sc->red[0], 6));
+  const bool gtn = has_gtn(c);   // red[6]: GTN return mappings that did not converge
+  TRY(allreduce_sum(c, &c->sc->red[0], gtn ? 7 : 6));
   c->tangent_set = true;
   c->compact = 1;
   c->have_sigma = true;
@@ -872,11 +884,15 @@ fgd_status fgd_constitutive(fgd_ctx* c, const double* eps, double* sigma_out, do
     TRY(st.out(sigma_out, 6 * c->nvox, &ds));
     FGD_CUDA(c, cudaMemcpyAsync(ds, c->w_sig, 6 * c->nvox * 8, cudaMemcpyDeviceToDevice, c->stream));
   }
-  double m[6];
-  TRY(sync_read(c, c->sc->red, 48, m));
+  double m[7] = {0, 0, 0, 0, 0, 0, 0};
+  TRY(sync_read(c, c->sc->red, gtn ? 56 : 48, m));
   for (int i = 0; i < 6; ++i) c->last_macro[i] = m[i] / (double)c->nvox_g;
   if (macro)
     for (int i = 0; i < 6; ++i) macro[i] = c->last_macro[i];
+  if (m[6] > 0.0) {
+    st.finish();
+    return set_err(c, FGD_ENOCONV, std::to_string((long long)m[6]) + " GTN return mappings did not converge");
+  }
   return st.finish();
 }
 
@@ -913,7 +929,7 @@ static fgd_status err_reduce(fgd_ctx* c, const double* eps, const double* eps_pr
 static double sigma_ref(const fgd_ctx* c) {
   double s = 0.0, e = 0.0;
   for (int q = 0; q < c->nphases; ++q) {
-    s = std::max(s, c->mat[q].model == 1 ? c->mat[q].sigma_y : 0.0);
+    s = std::max(s, (c->mat[q].model == 1 || c->mat[q].model == 3) ? c->mat[q].sigma_y : 0.0);
     e = std::max(e, c->mat[q].E);
   }
   return s > 0.0 ? s : e * 1e-3;
@@ -953,7 +969,9 @@ fgd_status fgd_solve_increment(fgd_ctx* c, const fgd_increment* inc, fgd_report*
     FGD_CUDA(c, cudaMemcpyAsync(c->w_eps_prev, c->w_eps, 6 * n * 8, cudaMemcpyDeviceToDevice, c->stream));
     bool newton_ok = false;
     for (int r = 0; r <= inc->max_newton; ++r) {
-      TRY(fgd_constitutive(c, nullptr, nullptr, macro));
+      const fgd_status cs = fgd_constitutive(c, nullptr, nullptr, macro);
+      if (cs == FGD_ENOCONV) break;   // a GTN return mapping failed: roll back, the caller cuts back
+      if (cs != FGD_OK) return cs;
       double rms;
       TRY(fgd_mech_residual(c, S, nullptr, &rms));
       const double nm = std::sqrt(macro[0] * macro[0] + macro[1] * macro[1] + macro[2] * macro[2] + macro[3] * macro[3] +
@@ -998,11 +1016,11 @@ fgd_status fgd_solve_increment(fgd_ctx* c, const fgd_increment* inc, fgd_report*
       const double dn = std::sqrt(red[7 + 2 * j]), nm = std::sqrt(red[6 + 2 * j]);
       err = std::max(err, dn > 1e-12 ? nm / dn : nm);
     }
-    if (J > 0) FGD_CUDA(c, cudaMemcpyAsync(c->w_abar, c->w_D, (size_t)J * n * 8, cudaMemcpyDeviceToDevice, c->stream));
-    if (err < inc->tol_stag) {
+    if (err < inc->tol_stag) {   // w_abar = abar^(k) (frozen in the mechanics), w_D = abar^(k+1)
       converged = true;
       break;
     }
+    if (J > 0) FGD_CUDA(c, cudaMemcpyAsync(c->w_abar, c->w_D, (size_t)J * n * 8, cudaMemcpyDeviceToDevice, c->stream));
   }
   if (rep) {
     for (int i = 0; i < 6; ++i) rep->macro_stress[i] = macro[i];
@@ -1019,8 +1037,10 @@ fgd_status fgd_solve_increment(fgd_ctx* c, const fgd_increment* inc, fgd_report*
     FGD_CUDA(c, cudaStreamSynchronize(c->stream));
     return set_err(c, FGD_ENOCONV, "increment did not converge");
   }
-  // 3. commit (A-16): eps^p, eps_p recomputed at the converged strain; history max-updated
-  TRY(launch_commit(c, c->w_eps, c->cm_epsp, c->cm_ep, c->cm_hist));
+  // 3. commit (A-16, A-30): eps^p, eps_p recomputed at the converged strain with the fields the last
+  // mechanics was frozen at; history from the accepted abar^(k+1)
+  TRY(launch_commit(c, c->w_eps, J > 0 ? c->w_D : c->w_abar, c->cm_epsp, c->cm_ep, c->cm_hist));
+  if (J > 0) FGD_CUDA(c, cudaMemcpyAsync(c->w_abar, c->w_D, (size_t)J * n * 8, cudaMemcpyDeviceToDevice, c->stream));
   std::swap(c->st_epsp, c->cm_epsp);
   std::swap(c->st_ep, c->cm_ep);
   std::swap(c->st_hist, c->cm_hist);
@@ -1060,6 +1080,8 @@ fgd_status fgd_get_field(fgd_ctx* c, int which, double* out) {
     src = c->w_abar + (size_t)(which - FGD_FIELD_NONLOCAL) * n;
   else if (which >= FGD_FIELD_SOURCE && which < FGD_FIELD_SOURCE + c->nfields)
     src = c->w_alpha + (size_t)(which - FGD_FIELD_SOURCE) * n;
+  else if (which >= FGD_FIELD_NONLOCAL_ITERATE && which < FGD_FIELD_NONLOCAL_ITERATE + c->nfields)
+    src = c->w_abar + (size_t)(which - FGD_FIELD_NONLOCAL_ITERATE) * n;
   else return set_err(c, FGD_EINVAL, "unknown field");
   Stage st(c);
   double* d;
@@ -1082,6 +1104,8 @@ fgd_status fgd_set_field(fgd_ctx* c, int which, const double* in) {
   else if (which == FGD_FIELD_ITERATE) dst[0] = c->w_eps, cnt = 6 * n;
   else if (which >= FGD_FIELD_NONLOCAL && which < FGD_FIELD_NONLOCAL + c->nfields)
     dst[0] = c->st_abar + (size_t)(which - FGD_FIELD_NONLOCAL) * n, dst[1] = c->w_abar + (size_t)(which - FGD_FIELD_NONLOCAL) * n;
+  else if (which >= FGD_FIELD_NONLOCAL_ITERATE && which < FGD_FIELD_NONLOCAL_ITERATE + c->nfields)
+    dst[0] = c->w_abar + (size_t)(which - FGD_FIELD_NONLOCAL_ITERATE) * n;
   else return set_err(c, FGD_EINVAL, "unknown or read-only field");
   Stage st(c);
   const double* d;

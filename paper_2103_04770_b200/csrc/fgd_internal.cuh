@@ -89,6 +89,7 @@ enum RedOp : int {
 struct Material {
   int model;
   double E, nu, sigma_y, H, eps_c, eps_r, d_max, kappa0, kappa_f;
+  double q1, q2, q3, f_c, f_f, f_n, eps_n, s_n, n_hard, fstar_max;   // GTN (model 3)
 };
 
 struct ConstTables {
@@ -258,7 +259,9 @@ double mean_ell2(const fgd_ctx* c, int field);
 
 // constitutive.cu
 fgd_status launch_constitutive(fgd_ctx* c, const double* eps);
-fgd_status launch_commit(fgd_ctx* c, const double* eps, double* epsp_out, double* ep_out, double* hist_out);
+fgd_status launch_commit(fgd_ctx* c, const double* eps, const double* abar_new, double* epsp_out, double* ep_out,
+                         double* hist_out);
+bool has_gtn(const fgd_ctx* c);
 fgd_status launch_err(fgd_ctx* c, const double* eps, const double* eps_prev, const double* abar_new,
                       const double* abar_old, unsigned long long* maxbits);
 fgd_status launch_dot(fgd_ctx* c, size_t n, const double* a, const double* b, int op, int slot);

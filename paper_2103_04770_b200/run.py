@@ -27,8 +27,7 @@ def _context(cfg):
     ctx = Context(cfg.n, cfg.L)
     ctx.set_phases(torch.from_numpy(np.ascontiguousarray(cfg.phases)).cuda(), len(cfg.materials))
     for q, m in enumerate(cfg.materials):
-        ctx.set_material(q, Material(m.model, m.E, m.nu, m.sigma_y, m.H, m.eps_c, m.eps_r, m.d_max, m.kappa0,
-                                     m.kappa_f))
+        ctx.set_material(q, Material.of(m))
     ctx.set_nonlocal(np.asarray(cfg.ell), cfg.source_phase)
     ctx.set_control(cfg.stress_mask)
     return ctx

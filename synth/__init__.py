@@ -229,6 +229,45 @@ def config3(n: int = 128, n_spheres: int = 30, phi: float = 0.20, seed: int = 3)
                       extra={"centres": centres, "radius": r})
 
 
+# GTN matrices of the paper (model 3): Sec. 4.1 (2D) and Sec. 4.2 (3D)
+MATRIX_GTN_2D = Material(model=3, E=300.0e3, nu=0.3, sigma_y=1000.0, q1=1.5, q2=1.0, q3=2.25, f_c=0.15, f_f=0.25,
+                         f_n=0.04, eps_n=0.3, s_n=0.1, n_hard=0.1, fstar_max=0.6)
+INCLUSION_EL_2D = Material(model=0, E=900.0e3, nu=0.3)
+MATRIX_GTN_3D = Material(model=3, E=70.0e3, nu=0.33, sigma_y=200.0, q1=1.5, q2=1.0, q3=2.25, f_c=0.15, f_f=0.25,
+                         f_n=0.04, eps_n=0.1, s_n=0.05, n_hard=0.1, fstar_max=0.6)
+
+
+def config_gtn2d(n: int = 32, ell_over_L: float = 0.05) -> CellConfig:
+    """Non-local GTN in 2D (paper Sec. 4.1): the centred disc r = 0.2 L of config 0,
+    GTN matrix (E = 300 GPa, nu = 0.3, sigma_Y = 1 GPa, q1 = 1.5, q2 = 1, q3 = 2.25, f_C = 0.15,
+    f_F = 0.25, f_N = 0.04, eps_N = 0.3, s_N = 0.1, Aravas N = 0.1, f* <= 0.6), elastic inclusion
+    (E = 900 GPa, nu = 0.3); two non-local fields of the matrix (eps0p, tr eps^p) with
+    ell_M = 0.05 L, ell_I = 0.001 L (P:843); plane strain E11 ramp (the paper reaches E11 = 0.5;
+    fixed increments here, A-21), mask (0,1,0,0,0,1)."""
+    L = 1.0
+    ph = disc_phases(n, 0.2 * L, L)
+    ellM = ell_over_L * L
+    row = [ellM, 0.001 * L]
+    return CellConfig(name=f"gtn2d_{n}", n=(n, n, 1), L=(L, L, L / n), phases=ph,
+                      materials=[MATRIX_GTN_2D, INCLUSION_EL_2D], ell=np.array([row, row]), source_phase=[0, 0],
+                      stress_mask=(0, 1, 0, 0, 0, 1), load_comp=0, dE=2.5e-3, n_incr=200)
+
+
+def config_gtn3d(n: int = 32, n_spheres: int = 30, phi: float = 0.20, seed: int = 3) -> CellConfig:
+    """Non-local GTN in 3D (paper Sec. 4.2): the RSA sphere cell of config 3 with
+    elastic particles (E = 400 GPa, nu = 0.2) in a GTN matrix (E = 70 GPa, nu = 0.33, sigma_Y =
+    200 MPa, eps_N = 0.1, s_N = 0.05, other GTN values as in 2D); ell_M = 0.05 L, ell_I = 0.001 L
+    for both fields; E_zz ramp, other stresses zero (mask (1,1,0,1,1,1))."""
+    L = 1.0
+    centres, r = rsa_centres(n_spheres, phi, seed, L)
+    ph = sphere_phases(n, centres, r, L)
+    row = [0.05 * L, 0.001 * L]
+    return CellConfig(name=f"gtn3d_{n}", n=(n, n, n), L=(L, L, L), phases=ph,
+                      materials=[MATRIX_GTN_3D, INCLUSION_EL], ell=np.array([row, row]), source_phase=[0, 0],
+                      stress_mask=(1, 1, 0, 1, 1, 1), load_comp=2, dE=1.0e-3, n_incr=600,
+                      extra={"centres": centres, "radius": r})
+
+
 def config1_phases(n: int, seed: int = 0) -> np.ndarray:
     """BJ config 1: phases rng(seed).random(N^3) < 0.2."""
     return bernoulli_phases((n, n, n), 0.2, seed)
