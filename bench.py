@@ -49,6 +49,7 @@ def args_():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--no-cufft", action="store_true", help="skip the cuFFT comparison arm")
+    p.add_argument("--no-gtn", action="store_true", help="skip the GTN constitutive measurement")
     return p.parse_args()
 
 
@@ -320,6 +321,69 @@ def cufft_comparison(ctx, n, dev, mask, reps=5):
             "rel_diff": rel}
 
 
+GTN_BYTES_PER_VOXEL = (48 + 48 + 8 + 8 + 1 + 16 + 16) + (48 + 72 + 16)   # K1 reads + writes (GTN)
+
+
+def gtn_measurement(n, dev, peak, reps=5):
+    """The non-local GTN constitutive update (material model 3) at the bench
+    size: config-1 phases with the Sec. 4.2 GTN matrix, a random committed state that puts most
+    matrix voxels on the yield surface across all f* branches, timed by the library's event pair
+    around the kernel."""
+    import numpy as np
+    import torch
+
+    import synth
+    from paper_2103_04770_b200 import Context, Material
+    from paper_2103_04770_b200 import _fgd
+    V = n ** 3
+    f64 = torch.float64
+    ctx = Context((n, n, n), (1.0, 1.0, 1.0), device=dev.index)
+    ctx.set_phases(torch.from_numpy(synth.config1_phases(n, 0)).to(dev), 2)
+    mg = synth.MATRIX_GTN_3D
+    ctx.set_material(0, Material.of(mg))
+    ctx.set_material(1, Material.of(synth.INCLUSION_EL))
+    ctx.set_nonlocal(np.array([[0.05, 0.001], [0.05, 0.001]]), [0, 0])
+    ctx.set_control(synth.CONFIG1_MASK)
+    g = torch.Generator(device=dev)
+    g.manual_seed(4321)
+    ey = mg.sigma_y / mg.E
+    eps = torch.randn((6, n, n, n), generator=g, dtype=f64, device=dev) * (2.5 * ey)
+    epsp = torch.randn((6, n, n, n), generator=g, dtype=f64, device=dev) * (0.5 * ey)
+    ctx.set_field(_fgd.FIELD_EPS_P, epsp)
+    ctx.set_field(_fgd.FIELD_EQPS, torch.randn((n, n, n), generator=g, dtype=f64, device=dev).abs() * (2 * ey))
+    ctx.set_field(_fgd.FIELD_HIST, torch.rand((n, n, n), generator=g, dtype=f64, device=dev) * 0.3)
+    for j in range(2):
+        ab = torch.randn((n, n, n), generator=g, dtype=f64, device=dev).abs() * (2 * ey)
+        ctx.set_field(_fgd.FIELD_NONLOCAL + j, ab)
+        ctx.set_field(_fgd.FIELD_NONLOCAL_ITERATE + j,
+                      ab + torch.randn((n, n, n), generator=g, dtype=f64, device=dev).abs() * (0.5 * ey))
+    sig = torch.empty_like(eps)
+    ctx.constitutive(eps, sig)
+    ctx.set_timing(True)
+    for _ in range(reps):
+        ctx.constitutive(eps)
+    kt = ctx.kernel_times()
+    ctx.set_timing(False)
+    ms = kt["constitutive"][0] / kt["constitutive"][1]
+    # plastic voxels: the stress differs from the elastic trial
+    K, mu = mg.E / (3 * (1 - 2 * mg.nu)), mg.E / (2 * (1 + mg.nu))
+    ee = eps - epsp
+    tr = ee[:3].sum(0)
+    trial = 2 * mu * ee
+    trial[:3] += (K - 2 * mu / 3) * tr
+    matrix = torch.from_numpy(synth.config1_phases(n, 0) == 0).to(dev)
+    plastic = ((sig - trial).abs().amax(0) > 1e-8 * trial.abs().amax(0)) & matrix
+    gbs = GTN_BYTES_PER_VOXEL * V / (ms * 1e-3) / 1e9
+    ctx.close()
+    return {"workload": f"config-1 phases at {n}^3, Sec. 4.2 GTN matrix (model 3) + elastic inclusion, random "
+                        "committed state (porosity U[0, 0.3], non-local fields and increments ~|N|)",
+            "ms_per_update": ms, "voxels_per_s": V / (ms * 1e-3),
+            "plastic_fraction": float(plastic.sum().item()) / V,
+            "bytes_per_voxel": GTN_BYTES_PER_VOXEL, "GBs": gbs, "frac_hbm": gbs / peak,
+            "note": "K1 with the GTN return mapping (3-unknown Newton with cosh/sinh and pow per plastic "
+                    "voxel); FP64-ALU bound on plastic voxels, see profiles/ for the ncu pipe utilisation"}
+
+
 def run_ours(a):
     import numpy as np
     import torch
@@ -452,6 +516,11 @@ def run_ours(a):
     cmp_cufft = None
     if world == 1 and not a.no_cufft:
         cmp_cufft = cufft_comparison(ctx, n, dev, synth.CONFIG1_MASK)
+    gtn = None
+    if world == 1 and not a.no_gtn:
+        gtn = gtn_measurement(n, dev, peak)
+        if "constitutive" in per_class:
+            gtn["j2_ms_per_update"] = per_class["constitutive"]["ms_per_step"]
 
     # multi-GPU: share and achieved bandwidth of the slab transposes; every operator
     # apply moves (P-1)/P of the rank's spectrum twice (before and after the z pass)
@@ -483,7 +552,7 @@ def run_ours(a):
                            "l2": "no flush: every input field (>=134 MB) and the tangent (2.8 GB) exceed the 126 MB L2"},
                 "roofline": roof, "step_roofline": step_eff, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": launches, "clocks": clk, "kernels": per_class,
-                "rates": rates, "cufft_comparison": cmp_cufft, "comm": comm}
+                "rates": rates, "cufft_comparison": cmp_cufft, "gtn_constitutive": gtn, "comm": comm}
         print(json.dumps(line), flush=True)
     ctx.close()
     if world > 1:

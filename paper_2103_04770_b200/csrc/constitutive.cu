@@ -114,13 +114,14 @@ __device__ void gtn_eval(const Material& m, const GtnCtx& g, const double u[3], 
   const double P = (g.ptr + g.K * a) * is0, Q = (g.qtr - 3.0 * g.mu * b) * is0;
   const double k = 1.5 * m.q2, xi = k * P;
   const double c = 1.5 * g.fs * m.q1 * m.q2;
-  const double ch = cosh(xi), sh = sinh(xi);
+  const double ex = exp(xi), iex = 1.0 / ex;   // cosh and sinh from one exponential
+  const double ch = 0.5 * (ex + iex), sh = 0.5 * (ex - iex);
   const double iN = 1.0 / m.n_hard;
   const double xp = pow(x, iN - 1.0);
-  const double ex = m.sigma_y * (xp * x - x) / (3.0 * g.mu);
+  const double e0 = m.sigma_y * (xp * x - x) / (3.0 * g.mu);
   R[0] = a * Q + b * c * sh;
   R[1] = Q * Q + 2.0 * g.fs * m.q1 * ch - 1.0 - m.q3 * g.fs * g.fs;
-  R[2] = (1.0 - g.f) * (ex - g.e0n) + P * a - Q * b;
+  R[2] = (1.0 - g.f) * (e0 - g.e0n) + P * a - Q * b;
   if (J) {
     const double dPa = g.K * is0, dPx = -P / x, dQb = -3.0 * g.mu * is0, dQx = -Q / x;
     const double dex = m.sigma_y * (iN * xp - 1.0) / (3.0 * g.mu);
@@ -187,11 +188,12 @@ __device__ __forceinline__ void gtn_update(const Material& m, double K, double m
   const bool tiny = g.qtr <= 1e-12 * m.sigma_y;
   double n[6];
   for (int i = 0; i < 6; ++i) n[i] = tiny ? 0.0 : 1.5 * s_tr[i] / g.qtr;
+  // J, B always hold the Jacobians at u: the line-search candidates are evaluated with them
+  // (J at u is dead once du is known), so an accepted step needs no second evaluation
   double u[3] = {0.0, 0.0, xn}, R[3], J[3][3], B[3][2];
-  gtn_eval(m, g, u, R, nullptr, nullptr);
+  gtn_eval(m, g, u, R, J, B);
   bool conv = false;
   for (int it = 0; it < 50 && !conv; ++it) {
-    gtn_eval(m, g, u, R, J, B);
     double du[3];
     solve3(J, R, du);
     for (int i = 0; i < 3; ++i) du[i] = -du[i];
@@ -202,12 +204,12 @@ __device__ __forceinline__ void gtn_update(const Material& m, double K, double m
       break;
     }
     const double psi = R[0] * R[0] + R[1] * R[1] + R[2] * R[2];
-    double t = 1.0, un[3], Rn[3];
+    double t = 1.0, un[3];
     for (int ls = 0; ls < 30; ++ls) {
       for (int i = 0; i < 3; ++i) un[i] = u[i] + t * du[i];
       un[2] = un[2] > 1.0 ? un[2] : 1.0;
-      gtn_eval(m, g, un, Rn, nullptr, nullptr);
-      if (Rn[0] * Rn[0] + Rn[1] * Rn[1] + Rn[2] * Rn[2] < psi) break;
+      gtn_eval(m, g, un, R, J, B);
+      if (R[0] * R[0] + R[1] * R[1] + R[2] * R[2] < psi) break;
       t *= 0.5;
     }
     for (int i = 0; i < 3; ++i) u[i] = un[i];
@@ -347,7 +349,7 @@ __device__ __forceinline__ double gtn_frozen_f(const Material& m, const double* 
 }
 
 template <bool GTN>
-__global__ void __launch_bounds__(256) k_constitutive(KArgs a, MatTable mt) {
+__global__ void __launch_bounds__(256, GTN ? 2 : 1) k_constitutive(KArgs a, MatTable mt) {
   constexpr int NR = GTN ? 7 : 6;   // <sigma> sums (+ GTN return-mapping failures)
   double red[NR];
 #pragma unroll
