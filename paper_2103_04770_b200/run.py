@@ -1,8 +1,10 @@
 """Full loading runs through the library's increment solver (fgd_solve_increment): the staggered
 Alg. 1 per increment, fixed strain increments with deterministic halving on non-convergence
-(A-21: up to 6 halvings), the BASELINE configurations 0, 2 and 3 from `synth`.
+(A-21: up to 6 halvings), the BASELINE configurations 0, 2 and 3 and the non-local GTN cells of the paper's Sec. 4.1 / 4.2
+(`synth.config_gtn2d`, `synth.config_gtn3d`) from `synth`.
 
     python -m paper_2103_04770_b200.run --config 3 [--n 128] [--incr 60] [--tight]
+    python -m paper_2103_04770_b200.run --config gtn2d [--n 64] [--de 2.5e-3] [--incr 200]
 
 prints one JSON line: the macroscopic stress-strain curve (load component), the peak, the strain
 at 50 % post-peak drop (A-26), the increment / staggered / Newton / CG / PCG counts and the wall
@@ -33,8 +35,37 @@ def _context(cfg):
     return ctx
 
 
-def run_config(cfg, n_incr=None, tol=(1e-4, 1e-6, 1e-8, 1e-6), max_halvings=6, max_cg=5000, max_helm=5000):
-    """Load the cell along cfg.load_comp in n_incr steps of cfg.dE; returns a result dict."""
+def adaptive_schedule(solve, E_end, dE0, dE_max=None, dE_min=1e-5, grow=1.5, grow_after=2):
+    """Adaptive incrementation (the paper's "variable strain increment",
+    P:990, rule A-34 of DESIGN.md): try dE = min(step, E_end - E); on failure halve the step and
+    retry from the last converged state; after `grow_after` consecutive first-try successes
+    multiply the step by `grow` (at most dE_max = dE0 by default).  Stops with failure when the
+    step falls below dE_min.  `solve(E) -> bool` runs one increment to macroscopic strain E (and
+    commits it on success).  Returns (accepted strains, number of cutbacks, reached E_end)."""
+    dE_max = dE0 if dE_max is None else dE_max
+    E, step, streak, cuts, accepted = 0.0, dE0, 0, 0, []
+    while E < E_end - 1e-15:
+        dE = min(step, E_end - E)
+        if solve(E + dE):
+            E += dE
+            accepted.append(E)
+            streak += 1
+            if streak >= grow_after:
+                step = min(step * grow, dE_max)
+                streak = 0
+        else:
+            cuts += 1
+            streak = 0
+            step *= 0.5
+            if step < dE_min:
+                return accepted, cuts, False
+    return accepted, cuts, True
+
+
+def run_config(cfg, n_incr=None, tol=(1e-4, 1e-6, 1e-8, 1e-6), max_halvings=6, max_cg=5000, max_helm=5000,
+               adaptive=False, de_min=1e-5):
+    """Load the cell along cfg.load_comp to n_incr * cfg.dE: fixed increments with deterministic
+    halving (A-21), or the adaptive schedule (A-34); returns a result dict."""
     import torch
 
     from . import _fgd
@@ -46,6 +77,26 @@ def run_config(cfg, n_incr=None, tol=(1e-4, 1e-6, 1e-8, 1e-6), max_halvings=6, m
     counts = dict(increments=0, substeps=0, stag=0, newton=0, cg=0, helm=0, failed=0)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
+
+    def solve(E_try):
+        Et = np.zeros(6)
+        Et[cfg.load_comp] = E_try
+        st, rep = ctx.solve_increment(Et, np.zeros(6), tol_stag, tol_newton, tol_cg, tol_helm,
+                                      max_cg=max_cg, max_helm=max_helm)
+        for k in ("stag", "newton", "cg", "helm"):
+            counts[k] += rep[k]
+        if st == 0:
+            counts["substeps"] += 1
+            curve.append((E_try, float(rep["macro_stress"][cfg.load_comp])))
+            return True
+        if st != _fgd.ENOCONV:
+            raise RuntimeError(f"solve_increment failed with status {st}")
+        return False
+
+    if adaptive:
+        acc, cuts, ok = adaptive_schedule(solve, n_incr * cfg.dE, cfg.dE, dE_min=de_min)
+        counts.update(increments=len(acc), cutbacks=cuts, failed=int(not ok))
+        n_incr = 0
     for i in range(1, n_incr + 1):
         E_goal = i * cfg.dE
         step = cfg.dE
@@ -88,28 +139,36 @@ def run_config(cfg, n_incr=None, tol=(1e-4, 1e-6, 1e-8, 1e-6), max_halvings=6, m
     return dict(config=cfg.name, n=list(cfg.n), load_comp=cfg.load_comp, dE=cfg.dE, wall_s=wall,
                 peak_stress=float(s[ip]), strain_at_peak=float(e[ip]), strain_at_failure=fail,
                 curve=[[float(a), float(b)] for a, b in curve], tolerances=list(tol), max_cg=max_cg,
-                max_halvings=max_halvings, **counts)
+                max_halvings=max_halvings, adaptive=adaptive, **counts)
 
 
 def main(argv=None):
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     import synth
     p = argparse.ArgumentParser()
-    p.add_argument("--config", type=int, default=0, choices=[0, 2, 3])
+    p.add_argument("--config", default="0", choices=["0", "2", "3", "gtn2d", "gtn3d"])
+    p.add_argument("--de", type=float, default=None, help="override the fixed strain increment")
     p.add_argument("--n", type=int, default=None)
     p.add_argument("--incr", type=int, default=None)
     p.add_argument("--tight", action="store_true")
     p.add_argument("--max-cg", type=int, default=5000)
     p.add_argument("--halvings", type=int, default=6)
+    p.add_argument("--adaptive", action="store_true", help="adaptive increments (A-34) instead of fixed + halving")
     a = p.parse_args(argv)
-    if a.config == 0:
+    if a.config == "0":
         cfg = synth.config0(a.n or 32)
-    elif a.config == 2:
+    elif a.config == "2":
         cfg = synth.config2(a.n or 256)
-    else:
+    elif a.config == "3":
         cfg = synth.config3(n=a.n or 128)
+    elif a.config == "gtn2d":
+        cfg = synth.config_gtn2d(a.n or 64)
+    else:
+        cfg = synth.config_gtn3d(a.n or 32)
+    if a.de:
+        cfg.dE = a.de
     tol = (1e-8, 1e-10, 1e-11, 1e-11) if a.tight else (1e-4, 1e-6, 1e-8, 1e-6)
-    print(json.dumps(run_config(cfg, a.incr, tol, a.halvings, a.max_cg, a.max_cg)), flush=True)
+    print(json.dumps(run_config(cfg, a.incr, tol, a.halvings, a.max_cg, a.max_cg, adaptive=a.adaptive)), flush=True)
 
 
 if __name__ == "__main__":
