@@ -161,8 +161,10 @@ __device__ __forceinline__ void solve3(const double A[3][3], const double r[3], 
   x[2] = (c02 * r[0] + c12 * r[1] + c22 * r[2]) * id;
 }
 
-__device__ __forceinline__ void gtn_update(const Material& m, double K, double mu, const double* e, const double* epsp_n,
-                                        double e0n, double f, PointOut& o) {
+// trial state; returns true if the trial violates the yield condition (plastic)
+__device__ __forceinline__ bool gtn_setup(const Material& m, double K, double mu, const double* e,
+                                          const double* epsp_n, double e0n, double f, GtnCtx& g, double* n,
+                                          double& xn, bool& tiny, double* sig_el) {
   double ee[6];
   for (int i = 0; i < 6; ++i) ee[i] = e[i] - epsp_n[i];
   const double tr = ee[0] + ee[1] + ee[2];
@@ -171,49 +173,62 @@ __device__ __forceinline__ void gtn_update(const Material& m, double K, double m
     s_tr[i] = 2.0 * mu * (ee[i] - (i < 3 ? tr / 3.0 : 0.0));
     ss += s_tr[i] * s_tr[i];
   }
-  GtnCtx g{-K * tr, sqrt(1.5 * ss), e0n, f, gtn_fstar(f, m), K, mu};
-  const double xn = gtn_aravas_x(e0n, m, mu);
+  g = GtnCtx{-K * tr, sqrt(1.5 * ss), e0n, f, gtn_fstar(f, m), K, mu};
+  xn = gtn_aravas_x(e0n, m, mu);
   const double Ptr = g.ptr / (m.sigma_y * xn), Qtr = g.qtr / (m.sigma_y * xn);
   const double phi_tr = Qtr * Qtr + 2.0 * g.fs * m.q1 * cosh(1.5 * m.q2 * Ptr) - 1.0 - m.q3 * g.fs * g.fs;
-  o.fail = 0;
+  tiny = g.qtr <= 1e-12 * m.sigma_y;
+  for (int i = 0; i < 6; ++i) {
+    n[i] = tiny ? 0.0 : 1.5 * s_tr[i] / g.qtr;
+    sig_el[i] = s_tr[i] + (i < 3 ? K * tr : 0.0);
+  }
+  return phi_tr > 0.0;
+}
+
+__device__ __forceinline__ void gtn_elastic_out(double K, double mu, const double* sig_el, const double* epsp_n,
+                                                double e0n, PointOut& o) {
+  for (int i = 0; i < 6; ++i) {
+    o.sig[i] = sig_el[i];
+    o.epsp[i] = epsp_n[i];
+  }
+  elastic_C(K, mu, 1.0, o);
   o.ep = e0n;
-  for (int i = 0; i < 6; ++i) o.epsp[i] = epsp_n[i];
-  if (!(phi_tr > 0.0)) {   // elastic
-    for (int i = 0; i < 6; ++i) o.sig[i] = s_tr[i] + (i < 3 ? K * tr : 0.0);
-    elastic_C(K, mu, 1.0, o);
-    o.alpha = e0n;
-    o.alpha2 = o.epsp[0] + o.epsp[1] + o.epsp[2];
-    return;
+  o.alpha = e0n;
+  o.alpha2 = epsp_n[0] + epsp_n[1] + epsp_n[2];
+  o.fail = 0;
+}
+
+// One Newton step of the return mapping at u (R, J, B at u on entry, at the new u on exit).
+// J, B always hold the Jacobians at u: the line-search candidates are evaluated with them
+// (J at u is dead once du is known), so an accepted step needs no second evaluation.
+// Returns true when the step was at round-off (u then holds the converged point).
+__device__ __forceinline__ bool gtn_newton_step(const Material& m, const GtnCtx& g, double* u, double* R,
+                                                double (&J)[3][3], double (&B)[3][2]) {
+  double du[3];
+  solve3(J, R, du);
+  for (int i = 0; i < 3; ++i) du[i] = -du[i];
+  if (fabs(du[0]) + fabs(du[1]) <= 1e-13 * (fabs(u[0]) + fabs(u[1])) + 1e-14 * m.sigma_y / (3.0 * g.mu) &&
+      fabs(du[2]) <= 1e-13 * u[2]) {
+    for (int i = 0; i < 3; ++i) u[i] += du[i];
+    return true;
   }
-  const bool tiny = g.qtr <= 1e-12 * m.sigma_y;
-  double n[6];
-  for (int i = 0; i < 6; ++i) n[i] = tiny ? 0.0 : 1.5 * s_tr[i] / g.qtr;
-  // J, B always hold the Jacobians at u: the line-search candidates are evaluated with them
-  // (J at u is dead once du is known), so an accepted step needs no second evaluation
-  double u[3] = {0.0, 0.0, xn}, R[3], J[3][3], B[3][2];
-  gtn_eval(m, g, u, R, J, B);
-  bool conv = false;
-  for (int it = 0; it < 50 && !conv; ++it) {
-    double du[3];
-    solve3(J, R, du);
-    for (int i = 0; i < 3; ++i) du[i] = -du[i];
-    if (fabs(du[0]) + fabs(du[1]) <= 1e-13 * (fabs(u[0]) + fabs(u[1])) + 1e-14 * m.sigma_y / (3.0 * mu) &&
-        fabs(du[2]) <= 1e-13 * u[2]) {
-      for (int i = 0; i < 3; ++i) u[i] += du[i];
-      conv = true;
-      break;
-    }
-    const double psi = R[0] * R[0] + R[1] * R[1] + R[2] * R[2];
-    double t = 1.0, un[3];
-    for (int ls = 0; ls < 30; ++ls) {
-      for (int i = 0; i < 3; ++i) un[i] = u[i] + t * du[i];
-      un[2] = un[2] > 1.0 ? un[2] : 1.0;
-      gtn_eval(m, g, un, R, J, B);
-      if (R[0] * R[0] + R[1] * R[1] + R[2] * R[2] < psi) break;
-      t *= 0.5;
-    }
-    for (int i = 0; i < 3; ++i) u[i] = un[i];
+  const double psi = R[0] * R[0] + R[1] * R[1] + R[2] * R[2];
+  double t = 1.0, un[3];
+  for (int ls = 0; ls < 30; ++ls) {
+    for (int i = 0; i < 3; ++i) un[i] = u[i] + t * du[i];
+    un[2] = un[2] > 1.0 ? un[2] : 1.0;
+    gtn_eval(m, g, un, R, J, B);
+    if (R[0] * R[0] + R[1] * R[1] + R[2] * R[2] < psi) break;
+    t *= 0.5;
   }
+  for (int i = 0; i < 3; ++i) u[i] = un[i];
+  return false;
+}
+
+// stress, plastic state, sources and the compact consistent tangent at the returned point u
+__device__ __forceinline__ void gtn_finish(const Material& m, const GtnCtx& g, const double* u, const double* n,
+                                           bool tiny, const double* epsp_n, bool conv, PointOut& o) {
+  const double K = g.K, mu = g.mu;
   o.fail = conv ? 0 : 1;
   const double a = u[0], b = u[1], x = u[2];
   const double p = g.ptr + K * a, q = g.qtr - 3.0 * mu * b;
@@ -224,7 +239,7 @@ __device__ __forceinline__ void gtn_update(const Material& m, double K, double m
   o.ep = m.sigma_y * (pow(x, 1.0 / m.n_hard) - x) / (3.0 * mu);
   o.alpha = o.ep;
   o.alpha2 = o.epsp[0] + o.epsp[1] + o.epsp[2];
-  // consistent tangent
+  double R[3], J[3][3], B[3][2];
   gtn_eval(m, g, u, R, J, B);
   double Mc[3][2];
   for (int col = 0; col < 2; ++col) {
@@ -247,6 +262,22 @@ __device__ __forceinline__ void gtn_update(const Material& m, double K, double m
   o.cb = cb;
   o.cc = cc;
   for (int i = 0; i < 6; ++i) o.n[i] = n[i] - (i < 3 ? gam : 0.0);
+}
+
+__device__ __forceinline__ void gtn_update(const Material& m, double K, double mu, const double* e, const double* epsp_n,
+                                           double e0n, double f, PointOut& o) {
+  GtnCtx g;
+  double n[6], sig_el[6], xn;
+  bool tiny;
+  if (!gtn_setup(m, K, mu, e, epsp_n, e0n, f, g, n, xn, tiny, sig_el)) {
+    gtn_elastic_out(K, mu, sig_el, epsp_n, e0n, o);
+    return;
+  }
+  double u[3] = {0.0, 0.0, xn}, R[3], J[3][3], B[3][2];
+  gtn_eval(m, g, u, R, J, B);
+  bool conv = false;
+  for (int it = 0; it < 50 && !conv; ++it) conv = gtn_newton_step(m, g, u, R, J, B);
+  gtn_finish(m, g, u, n, tiny, epsp_n, conv, o);
 }
 
 // gf: the frozen porosity of a GTN phase (unused by the other models)
@@ -383,6 +414,102 @@ __global__ void __launch_bounds__(256, GTN ? 2 : 1) k_constitutive(KArgs a, MatT
       a.alpha[(size_t)f * n + g] = (f == j) ? o.alpha : ((gtn && f == j + 1) ? o.alpha2 : 0.0);
   }
   reduce_finalize<NR>(red, a.partials, a.sc, RED_STORE, 0);
+}
+
+__device__ __forceinline__ void write_point(const KArgs& a, const MatTable& mt, size_t g, int j, bool gtn,
+                                            const PointOut& o, double (&red)[7]) {
+  const size_t n = a.nvox;
+  for (int i = 0; i < 6; ++i) {
+    a.sig[i * n + g] = o.sig[i];
+    red[i] += o.sig[i];
+  }
+  red[6] += (double)o.fail;
+  for (int i = 0; i < 6; ++i) a.C[(size_t)i * n + g] = o.n[i];
+  a.C[6 * n + g] = o.ca;
+  a.C[7 * n + g] = o.cb;
+  a.C[8 * n + g] = o.cc;
+  for (int f = 0; f < mt.nfields; ++f)
+    a.alpha[(size_t)f * n + g] = (f == j) ? o.alpha : ((gtn && f == j + 1) ? o.alpha2 : 0.0);
+}
+
+// K1 with GTN phases, per-warp lane refill.  The return mappings of neighbouring voxels take
+// different numbers of Newton steps (and elastic voxels none), so a thread-per-voxel loop idles
+// most lanes of a warp.  Here every warp walks a static chunk of voxels (deterministic: the
+// assignment depends only on the data); lanes without a plastic GTN point in flight pull the
+// next voxels of the chunk (elastic and non-GTN voxels are finished on the spot), then every
+// busy lane runs one Newton step; converged lanes write their point and refill.  Same per-point
+// arithmetic as gtn_update().
+constexpr int kGtnChunk = 1024;
+__global__ void __launch_bounds__(256, 2) k_constitutive_gtn(KArgs a, MatTable mt) {
+  double red[7] = {0, 0, 0, 0, 0, 0, 0};
+  const int lane = threadIdx.x & 31;
+  const size_t n = a.nvox;
+  const size_t wid = (blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5;
+  const size_t nw = ((size_t)gridDim.x * blockDim.x) >> 5;
+  for (size_t c0 = wid * kGtnChunk; c0 < n; c0 += nw * kGtnChunk) {
+    const size_t cend = c0 + kGtnChunk < n ? c0 + kGtnChunk : n;
+    size_t next = c0;       // warp-uniform
+    bool busy = false;
+    size_t g = 0;
+    int q = 0, it = 0;
+    bool tiny = false;
+    GtnCtx gc;
+    double nn[6], u[3], R[3], J[3][3], B[3][2];
+    while (true) {
+      while (true) {        // refill
+        const unsigned need = __ballot_sync(0xffffffffu, !busy);
+        if (need == 0 || next >= cend) break;
+        const size_t idx = next + __popc(need & ((1u << lane) - 1u));
+        next += __popc(need);
+        if (!busy && idx < cend) {
+          g = idx;
+          q = a.phase[g];
+          const Material& m = mt.m[q];
+          const int j = mt.field_of[q];
+          double e[6], ep6[6];
+          for (int i = 0; i < 6; ++i) {
+            e[i] = a.eps[i * n + g];
+            ep6[i] = a.epsp_n[i * n + g];
+          }
+          PointOut o;
+          if (m.model == 3) {
+            const double K = m.E / (3.0 * (1.0 - 2.0 * m.nu)), mu = m.E / (2.0 * (1.0 + m.nu));
+            const double gf = gtn_frozen_f(m, a.abar, a.abar_n, a.hist[g], j, n, g);
+            double sig_el[6], xn;
+            if (gtn_setup(m, K, mu, e, ep6, a.ep_n[g], gf, gc, nn, xn, tiny, sig_el)) {
+              u[0] = 0.0;
+              u[1] = 0.0;
+              u[2] = xn;
+              gtn_eval(m, gc, u, R, J, B);
+              it = 0;
+              busy = true;
+            } else {
+              gtn_elastic_out(K, mu, sig_el, ep6, a.ep_n[g], o);
+              write_point(a, mt, g, j, true, o, red);
+            }
+          } else {
+            const double abar = (j >= 0) ? a.abar[(size_t)j * n + g] : 0.0;
+            point_update<false>(m, j >= 0, e, ep6, a.ep_n[g], a.hist[g], abar, -1.0, 0.0, o);
+            write_point(a, mt, g, j, false, o, red);
+          }
+        }
+      }
+      if (__ballot_sync(0xffffffffu, busy) == 0) break;   // chunk exhausted and drained
+      if (busy) {
+        const Material& m = mt.m[q];
+        const bool conv = gtn_newton_step(m, gc, u, R, J, B);
+        if (conv || ++it >= 50) {
+          double ep6[6];
+          for (int i = 0; i < 6; ++i) ep6[i] = a.epsp_n[i * n + g];
+          PointOut o;
+          gtn_finish(m, gc, u, nn, tiny, ep6, conv, o);
+          write_point(a, mt, g, mt.field_of[q], true, o, red);
+          busy = false;
+        }
+      }
+    }
+  }
+  reduce_finalize<7>(red, a.partials, a.sc, RED_STORE, 0);
 }
 
 // commit: recompute eps^p, eps_p at the converged strain with the non-local fields the last
@@ -580,7 +707,11 @@ fgd_status launch_constitutive(fgd_ctx* c, const double* eps) {
   c->launches++;
   KTimer kt(c, KC_CONST);
   if (gtn) {
-    k_constitutive<true><<<nb, 256, 0, c->stream>>>(a, t);
+    static const bool plain = getenv("FGD_GTN_PLAIN") != nullptr;   // A/B: thread-per-voxel loop
+    if (plain)
+      k_constitutive<true><<<nb, 256, 0, c->stream>>>(a, t);
+    else
+      k_constitutive_gtn<<<std::min(nb, 148 * 2), 256, 0, c->stream>>>(a, t);
   } else {
     k_constitutive<false><<<nb, 256, 0, c->stream>>>(a, t);
   }
