@@ -416,101 +416,6 @@ __global__ void __launch_bounds__(256, GTN ? 2 : 1) k_constitutive(KArgs a, MatT
   reduce_finalize<NR>(red, a.partials, a.sc, RED_STORE, 0);
 }
 
-__device__ __forceinline__ void write_point(const KArgs& a, const MatTable& mt, size_t g, int j, bool gtn,
-                                            const PointOut& o, double (&red)[7]) {
-  const size_t n = a.nvox;
-  for (int i = 0; i < 6; ++i) {
-    a.sig[i * n + g] = o.sig[i];
-    red[i] += o.sig[i];
-  }
-  red[6] += (double)o.fail;
-  for (int i = 0; i < 6; ++i) a.C[(size_t)i * n + g] = o.n[i];
-  a.C[6 * n + g] = o.ca;
-  a.C[7 * n + g] = o.cb;
-  a.C[8 * n + g] = o.cc;
-  for (int f = 0; f < mt.nfields; ++f)
-    a.alpha[(size_t)f * n + g] = (f == j) ? o.alpha : ((gtn && f == j + 1) ? o.alpha2 : 0.0);
-}
-
-// K1 with GTN phases, per-warp lane refill.  The return mappings of neighbouring voxels take
-// different numbers of Newton steps (and elastic voxels none), so a thread-per-voxel loop idles
-// most lanes of a warp.  Here every warp walks a static chunk of voxels (deterministic: the
-// assignment depends only on the data); lanes without a plastic GTN point in flight pull the
-// next voxels of the chunk (elastic and non-GTN voxels are finished on the spot), then every
-// busy lane runs one Newton step; converged lanes write their point and refill.  Same per-point
-// arithmetic as gtn_update().
-constexpr int kGtnChunk = 1024;
-__global__ void __launch_bounds__(256, 2) k_constitutive_gtn(KArgs a, MatTable mt) {
-  double red[7] = {0, 0, 0, 0, 0, 0, 0};
-  const int lane = threadIdx.x & 31;
-  const size_t n = a.nvox;
-  const size_t wid = (blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5;
-  const size_t nw = ((size_t)gridDim.x * blockDim.x) >> 5;
-  for (size_t c0 = wid * kGtnChunk; c0 < n; c0 += nw * kGtnChunk) {
-    const size_t cend = c0 + kGtnChunk < n ? c0 + kGtnChunk : n;
-    size_t next = c0;       // warp-uniform
-    bool busy = false;
-    size_t g = 0;
-    int q = 0, it = 0;
-    bool tiny = false;
-    GtnCtx gc;
-    double nn[6], u[3], R[3], J[3][3], B[3][2];
-    while (true) {
-      while (true) {        // refill
-        const unsigned need = __ballot_sync(0xffffffffu, !busy);
-        if (need == 0 || next >= cend) break;
-        const size_t idx = next + __popc(need & ((1u << lane) - 1u));
-        next += __popc(need);
-        if (!busy && idx < cend) {
-          g = idx;
-          q = a.phase[g];
-          const Material& m = mt.m[q];
-          const int j = mt.field_of[q];
-          double e[6], ep6[6];
-          for (int i = 0; i < 6; ++i) {
-            e[i] = a.eps[i * n + g];
-            ep6[i] = a.epsp_n[i * n + g];
-          }
-          PointOut o;
-          if (m.model == 3) {
-            const double K = m.E / (3.0 * (1.0 - 2.0 * m.nu)), mu = m.E / (2.0 * (1.0 + m.nu));
-            const double gf = gtn_frozen_f(m, a.abar, a.abar_n, a.hist[g], j, n, g);
-            double sig_el[6], xn;
-            if (gtn_setup(m, K, mu, e, ep6, a.ep_n[g], gf, gc, nn, xn, tiny, sig_el)) {
-              u[0] = 0.0;
-              u[1] = 0.0;
-              u[2] = xn;
-              gtn_eval(m, gc, u, R, J, B);
-              it = 0;
-              busy = true;
-            } else {
-              gtn_elastic_out(K, mu, sig_el, ep6, a.ep_n[g], o);
-              write_point(a, mt, g, j, true, o, red);
-            }
-          } else {
-            const double abar = (j >= 0) ? a.abar[(size_t)j * n + g] : 0.0;
-            point_update<false>(m, j >= 0, e, ep6, a.ep_n[g], a.hist[g], abar, -1.0, 0.0, o);
-            write_point(a, mt, g, j, false, o, red);
-          }
-        }
-      }
-      if (__ballot_sync(0xffffffffu, busy) == 0) break;   // chunk exhausted and drained
-      if (busy) {
-        const Material& m = mt.m[q];
-        const bool conv = gtn_newton_step(m, gc, u, R, J, B);
-        if (conv || ++it >= 50) {
-          double ep6[6];
-          for (int i = 0; i < 6; ++i) ep6[i] = a.epsp_n[i * n + g];
-          PointOut o;
-          gtn_finish(m, gc, u, nn, tiny, ep6, conv, o);
-          write_point(a, mt, g, mt.field_of[q], true, o, red);
-          busy = false;
-        }
-      }
-    }
-  }
-  reduce_finalize<7>(red, a.partials, a.sc, RED_STORE, 0);
-}
 
 // commit: recompute eps^p, eps_p at the converged strain with the non-local fields the last
 // mechanics was frozen at (a.abar); history from the accepted new fields abar_new:
@@ -707,11 +612,7 @@ fgd_status launch_constitutive(fgd_ctx* c, const double* eps) {
   c->launches++;
   KTimer kt(c, KC_CONST);
   if (gtn) {
-    static const bool plain = getenv("FGD_GTN_PLAIN") != nullptr;   // A/B: thread-per-voxel loop
-    if (plain)
-      k_constitutive<true><<<nb, 256, 0, c->stream>>>(a, t);
-    else
-      k_constitutive_gtn<<<std::min(nb, 148 * 2), 256, 0, c->stream>>>(a, t);
+    k_constitutive<true><<<nb, 256, 0, c->stream>>>(a, t);
   } else {
     k_constitutive<false><<<nb, 256, 0, c->stream>>>(a, t);
   }
