@@ -911,9 +911,30 @@ __global__ void __launch_bounds__(NC * 64, NC == 6 ? 2 : 8) k_zreg512(ZPArgs a) 
     for (int kc = 0; kc < 8; ++kc) ls[kc * 65 + t] = v[kc];
     __syncthreads();
     const int ky = kyl + a.ky_off;
+    // Willot symbol with the (kx, ky) factors hoisted out of the kz loop (one line per tile):
+    // k0 = P0 (1+e^{ith3}), k1 = P1 (1+e^{ith3}), k2 = P2 (e^{ith3}-1)
+    const bool hoist = a.scheme == 1;
+    double2 P0 = make_double2(0.0, 0.0), P1 = P0, P2 = P0;
+    if (hoist) {
+      const double2 wx = __ldg(&a.twx[kx]), wy = __ldg(&a.twy[ky]);
+      const double2 ex = make_double2(wx.x, -wx.y), ey = make_double2(wy.x, -wy.y);
+      const double2 dx = make_double2(ex.x - 1.0, ex.y), dy = make_double2(ey.x - 1.0, ey.y);
+      const double2 cx = make_double2(ex.x + 1.0, ex.y), cy = make_double2(ey.x + 1.0, ey.y);
+      P0 = cscale(cmul(dx, cy), a.qh[0]);
+      P1 = cscale(cmul(cx, dy), a.qh[1]);
+      P2 = cscale(cmul(cx, cy), a.qh[2]);
+    }
     for (int kz = threadIdx.x; kz < N; kz += blockDim.x) {
       double2 k[3];
-      zsymbol(a, N, kx, ky, kz, k, tws);
+      if (hoist) {
+        const double2 wz = tws[kz];
+        const double2 cz = make_double2(wz.x + 1.0, -wz.y), dz = make_double2(wz.x - 1.0, -wz.y);
+        k[0] = cmul(P0, cz);
+        k[1] = cmul(P1, cz);
+        k[2] = cmul(P2, dz);
+      } else {
+        zsymbol(a, N, kx, ky, kz, k, tws);
+      }
       const int slot = (kz >> 6) * 65 + (kz & 63);
       if (MODE == Z_PRECOND) {
         const double k2 = k[0].x * k[0].x + k[0].y * k[0].y + k[1].x * k[1].x + k[1].y * k[1].y + k[2].x * k[2].x +
