@@ -130,3 +130,26 @@ def test_increment_parity_3d_two_fields():
     out, ctx, st = run_both(cfg, 4)
     for i, (ref, got, rep, r) in enumerate(out):
         assert rel(got, ref) <= 1e-6, (i, ref, got)
+
+
+def test_adaptive_run_replayed_by_oracle():
+    """run.py's adaptive driver (A-34) on the GPU, then the oracle replays the accepted strain
+    sequence (cut-back sub-steps included): same macroscopic stress up to the peak."""
+    from paper_2103_04770_b200.run import run_config
+    cfg = synth.config0(16, ell_over_L=2.0 / 16)
+    cfg.dE = 4e-3                 # 10x the nominal step: the driver has to cut back near the peak
+    tol = (TOL.tol_stag, TOL.tol_newton, TOL.tol_cg, TOL.tol_helm)
+    res = run_config(cfg, n_incr=4, tol=tol, adaptive=True, max_cg=TOL.max_cg, max_helm=TOL.max_helm)
+    assert not res["failed"]
+    assert res["curve"][-1][0] == pytest.approx(4 * cfg.dE)
+    cell = make_cell(cfg)
+    st = State.zero(cell)
+    s = np.array([c[1] for c in res["curve"]])
+    peak = int(np.argmax(s))
+    for i, (E, sig) in enumerate(res["curve"][1:], start=1):
+        Et = np.zeros(6)
+        Et[cfg.load_comp] = E
+        st, rep = solve_increment(cell, st, Et, np.zeros(6), TOL)
+        assert rep.converged, (i, E)
+        if i <= peak:
+            assert abs(rep.macro_stress[cfg.load_comp] - sig) <= 1e-6 * abs(rep.macro_stress[cfg.load_comp]), (i, E)
