@@ -63,7 +63,7 @@ def adaptive_schedule(solve, E_end, dE0, dE_max=None, dE_min=1e-5, grow=1.5, gro
 
 
 def run_config(cfg, n_incr=None, tol=(1e-4, 1e-6, 1e-8, 1e-6), max_halvings=6, max_cg=5000, max_helm=5000,
-               adaptive=False, de_min=1e-5):
+               adaptive=False, de_min=1e-5, log=False):
     """Load the cell along cfg.load_comp to n_incr * cfg.dE: fixed increments with deterministic
     halving (A-21), or the adaptive schedule (A-34); returns a result dict."""
     import torch
@@ -88,6 +88,9 @@ def run_config(cfg, n_incr=None, tol=(1e-4, 1e-6, 1e-8, 1e-6), max_halvings=6, m
         if st == 0:
             counts["substeps"] += 1
             curve.append((E_try, float(rep["macro_stress"][cfg.load_comp])))
+            if log:   # one line per accepted increment: a run cut short still leaves its curve
+                print(json.dumps({"E": E_try, "S": curve[-1][1], "t": time.perf_counter() - t0}), file=sys.stderr,
+                      flush=True)
             return True
         if st != _fgd.ENOCONV:
             raise RuntimeError(f"solve_increment failed with status {st}")
@@ -154,6 +157,9 @@ def main(argv=None):
     p.add_argument("--max-cg", type=int, default=5000)
     p.add_argument("--halvings", type=int, default=6)
     p.add_argument("--adaptive", action="store_true", help="adaptive increments (A-34) instead of fixed + halving")
+    p.add_argument("--log", action="store_true", help="one JSON line per accepted increment on stderr")
+    p.add_argument("--ell", type=float, default=None,
+                   help="gtn2d: matrix ell_M / L (ell_I = min(ell_M, 0.001 L); 1e-4 gives the local variant)")
     a = p.parse_args(argv)
     if a.config == "0":
         cfg = synth.config0(a.n or 32)
@@ -162,13 +168,15 @@ def main(argv=None):
     elif a.config == "3":
         cfg = synth.config3(n=a.n or 128)
     elif a.config == "gtn2d":
-        cfg = synth.config_gtn2d(a.n or 64)
+        ell = a.ell if a.ell else 0.05
+        cfg = synth.config_gtn2d(a.n or 64, ell_over_L=ell, ell_i_over_L=min(ell, 0.001))
     else:
         cfg = synth.config_gtn3d(a.n or 32)
     if a.de:
         cfg.dE = a.de
     tol = (1e-8, 1e-10, 1e-11, 1e-11) if a.tight else (1e-4, 1e-6, 1e-8, 1e-6)
-    print(json.dumps(run_config(cfg, a.incr, tol, a.halvings, a.max_cg, a.max_cg, adaptive=a.adaptive)), flush=True)
+    print(json.dumps(run_config(cfg, a.incr, tol, a.halvings, a.max_cg, a.max_cg, adaptive=a.adaptive, log=a.log)),
+          flush=True)
 
 
 if __name__ == "__main__":

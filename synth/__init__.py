@@ -237,7 +237,7 @@ MATRIX_GTN_3D = Material(model=3, E=70.0e3, nu=0.33, sigma_y=200.0, q1=1.5, q2=1
                          f_n=0.04, eps_n=0.1, s_n=0.05, n_hard=0.1, fstar_max=0.6)
 
 
-def config_gtn2d(n: int = 32, ell_over_L: float = 0.05) -> CellConfig:
+def config_gtn2d(n: int = 32, ell_over_L: float = 0.05, ell_i_over_L: float = 0.001) -> CellConfig:
     """Non-local GTN in 2D (paper Sec. 4.1): the centred disc r = 0.2 L of config 0,
     GTN matrix (E = 300 GPa, nu = 0.3, sigma_Y = 1 GPa, q1 = 1.5, q2 = 1, q3 = 2.25, f_C = 0.15,
     f_F = 0.25, f_N = 0.04, eps_N = 0.3, s_N = 0.1, Aravas N = 0.1, f* <= 0.6), elastic inclusion
@@ -247,7 +247,7 @@ def config_gtn2d(n: int = 32, ell_over_L: float = 0.05) -> CellConfig:
     L = 1.0
     ph = disc_phases(n, 0.2 * L, L)
     ellM = ell_over_L * L
-    row = [ellM, 0.001 * L]
+    row = [ellM, ell_i_over_L * L]     # the local variant of P:843 is ell_M = ell_I = 1e-4 L
     return CellConfig(name=f"gtn2d_{n}", n=(n, n, 1), L=(L, L, L / n), phases=ph,
                       materials=[MATRIX_GTN_2D, INCLUSION_EL_2D], ell=np.array([row, row]), source_phase=[0, 0],
                       stress_mask=(0, 1, 0, 0, 0, 1), load_comp=0, dE=2.5e-3, n_incr=200)
