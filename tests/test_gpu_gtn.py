@@ -160,3 +160,56 @@ def test_gtn_needs_two_fields():
     ctx.set_control(cfg.stress_mask)
     with pytest.raises(FgdError):
         ctx.constitutive(dev(np.zeros((6,) + cfg.phases.shape)), None)
+
+
+def test_gtn_full_size_sampled():
+    """The 256^3 GTN update in the bench's launch configuration (bench.gtn_measurement's state
+    recipe): 400 sampled voxels recomputed one by one by the oracle's point update."""
+    from oracle import gtn as GT
+    n = 256
+    cfg_m = synth.MATRIX_GTN_3D
+    ph = synth.config1_phases(n, 0)
+    ctx = Context((n, n, n), (1.0, 1.0, 1.0))
+    ctx.set_phases(dev(ph), 2)
+    ctx.set_material(0, Material.of(cfg_m))
+    ctx.set_material(1, Material.of(synth.INCLUSION_EL))
+    ctx.set_nonlocal(np.array([[0.05, 0.001], [0.05, 0.001]]), [0, 0])
+    ctx.set_control(synth.CONFIG1_MASK)
+    g = torch.Generator(device="cuda")
+    g.manual_seed(77)
+    f64 = torch.float64
+    ey = cfg_m.sigma_y / cfg_m.E
+    eps = torch.randn((6, n, n, n), generator=g, dtype=f64, device="cuda") * (2.5 * ey)
+    epsp = torch.randn((6, n, n, n), generator=g, dtype=f64, device="cuda") * (0.5 * ey)
+    e0 = torch.randn((n, n, n), generator=g, dtype=f64, device="cuda").abs() * (2 * ey)
+    hist = torch.rand((n, n, n), generator=g, dtype=f64, device="cuda") * 0.3
+    ab_n = torch.randn((2, n, n, n), generator=g, dtype=f64, device="cuda").abs() * (2 * ey)
+    ab = ab_n + torch.randn((2, n, n, n), generator=g, dtype=f64, device="cuda").abs() * (0.5 * ey)
+    ctx.set_field(_fgd.FIELD_EPS_P, epsp)
+    ctx.set_field(_fgd.FIELD_EQPS, e0)
+    ctx.set_field(_fgd.FIELD_HIST, hist)
+    for j in range(2):
+        ctx.set_field(_fgd.FIELD_NONLOCAL + j, ab_n[j].contiguous())
+        ctx.set_field(_fgd.FIELD_NONLOCAL_ITERATE + j, ab[j].contiguous())
+    sig = torch.empty_like(eps)
+    ctx.constitutive(eps, sig)
+    Cg = torch.empty((21, n * n * n), dtype=f64, device="cuda")
+    ctx.get_field(_fgd.FIELD_TANGENT, Cg)
+    rng = np.random.default_rng(5)
+    vox = rng.choice(n ** 3, size=400, replace=False)
+    flat = lambda t, c: t.reshape(c, -1)[:, vox].cpu().numpy()   # noqa: E731
+    E6, P6, S6, C21 = flat(eps, 6), flat(epsp, 6), flat(sig, 6), Cg[:, vox].cpu().numpy()
+    E0, H, A, An = flat(e0, 1)[0], flat(hist, 1)[0], flat(ab, 2), flat(ab_n, 2)
+    phv = ph.reshape(-1)[vox]
+    iu = np.triu_indices(6)
+    nplastic = 0
+    for i in range(vox.size):
+        if phv[i] != 0:
+            continue                                   # elastic inclusion: covered by the J2 tests
+        f = GT.porosity(H[i], A[0, i], An[0, i], A[1, i], An[1, i], cfg_m)
+        r = GT.gtn_point(E6[:, i], P6[:, i], E0[i], f, cfg_m)
+        nplastic += r["plastic"]
+        assert np.abs(S6[:, i] - r["sigma"]).max() <= 1e-11 * np.abs(r["sigma"]).max(), i
+        assert np.abs(C21[:, i] - r["C_sym"][iu]).max() <= 1e-9 * np.abs(r["C_sym"]).max(), i
+    assert nplastic > 200
+    ctx.close()
