@@ -140,11 +140,15 @@ fgd_status fgd_solve_helmholtz(fgd_ctx* ctx, int field, const double* src, doubl
 fgd_status fgd_solve_tangent_cg(fgd_ctx* ctx, const double* b, double* de, double tol, int maxit,
                                 int* iters, double* relres);
 
-/* Per-voxel constitutive update (A-14..A-18) at strain eps (6 comps;
- * NULL = the internal iterate) with the committed state and damage frozen from the current
- * non-local fields (A-16).  Produces sigma, the packed consistent tangent and the
- * Helmholtz sources alpha_j internally; sigma_out (may be NULL) receives sigma; macro[6]
- * (may be NULL) receives <sigma>. */
+/* Per-voxel constitutive update (A-14..A-18; GTN P:89-166,
+ * P:1100-1129, A-30..A-33) at strain eps (6 comps; NULL = the internal iterate) with the
+ * committed state and damage / porosity frozen from the current non-local fields
+ * (FGD_FIELD_NONLOCAL_ITERATE, A-16).  Produces sigma, the consistent tangent (GTN:
+ * its symmetric part) and the Helmholtz sources alpha_j internally; sigma_out (may be NULL)
+ * receives sigma; macro[6] (may be NULL) receives <sigma>.  Returns FGD_ENOCONV (outputs
+ * written, the failing points hold their last return-mapping iterate) if a GTN return mapping
+ * did not converge in 50 Newton steps; FGD_ESTATE if a GTN phase lacks its two consecutive
+ * non-local fields. */
 fgd_status fgd_constitutive(fgd_ctx* ctx, const double* eps, double* sigma_out, double* macro);
 
 /* Newton residual b = -G*(sigma - Sigma_bar) of the last fgd_constitutive,
@@ -152,8 +156,10 @@ fgd_status fgd_constitutive(fgd_ctx* ctx, const double* eps, double* sigma_out, 
 fgd_status fgd_mech_residual(fgd_ctx* ctx, const double* S_target, double* b_out, double* rms);
 
 /* One increment of Algorithm 1: mixed-control Newton + CG mechanics and J
- * Helmholtz PCG solves iterated until ERR < tol_stag (A-01, A-02).  Commits on FGD_OK;
- * on FGD_ENOCONV the committed state is unchanged (rollback) and the caller cuts back. */
+ * Helmholtz PCG solves iterated until ERR < tol_stag (A-01, A-02).  Commits on FGD_OK
+ * (eps^p, eps_p from the last mechanical solve, histories from the accepted non-local fields,
+ * A-16, A-30); on FGD_ENOCONV (Newton, staggered or GTN return-mapping failure) the committed
+ * state is unchanged (rollback) and the caller cuts back (A-21, A-34). */
 typedef struct {
   double E_target[6], S_target[6];
   double tol_stag, tol_newton, tol_cg, tol_helm;
