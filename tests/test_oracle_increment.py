@@ -188,3 +188,22 @@ def test_homogeneous_gtn_cell_equals_material_point():
         assert np.allclose(st.hist, ref[i][1], rtol=1e-9, atol=1e-15)
     assert st.hist.max() > 0.01          # porosity grew (nucleation + dilatant growth)
     assert np.all(st.epsp[:3].sum(axis=0) > 0)
+
+
+def test_homogeneous_gtn_plane_strain_equals_material_point():
+    """Plane strain (A-19, A-20: eps33 = eps13 = eps23 = 0, Sigma22 = Sigma12 = 0) GTN cell."""
+    mat = Material(model=3, E=300e3, nu=0.3, sigma_y=1000.0, eps_n=0.02, s_n=0.01, f_n=0.04)
+    g = Grid((4, 4, 1))
+    mask = (0, 1, 0, 0, 0, 1)
+    cell = Cell(g, np.zeros(g.shape, np.uint8), [mat], np.array([[0.1], [0.1]]), [0, 0], mask)
+    st = State.zero(cell)
+    Es = [5e-3 * i for i in range(1, 7)]
+    ref = gtn_point_driver(mat, mask, 0, Es)
+    for i, E in enumerate(Es):
+        Et = np.zeros(6); Et[0] = E
+        st, rep = solve_increment(cell, st, Et, np.zeros(6), TOL)
+        assert rep.converged
+        assert np.allclose(rep.macro_stress, ref[i][0], rtol=1e-9, atol=1e-7)
+        assert np.allclose(st.hist, ref[i][1], rtol=1e-9, atol=1e-15)
+        assert abs(rep.macro_stress[2]) > 0          # sigma33 carried (A-19)
+    assert st.hist.max() > 0.01
