@@ -153,3 +153,35 @@ def test_adaptive_run_replayed_by_oracle():
         assert rep.converged, (i, E)
         if i <= peak:
             assert abs(rep.macro_stress[cfg.load_comp] - sig) <= 1e-6 * abs(rep.macro_stress[cfg.load_comp]), (i, E)
+
+
+@pytest.mark.parametrize("n", [4, 16, 32, (32, 16)])
+def test_mech_cg_compact_tangent_2d(n):
+    """CG on the compact tangent written by fgd_constitutive on small 2D cells (the single-CTA
+    k_cg_small path at <= 1024 voxels) against the oracle CG with the oracle's tangent."""
+    from oracle.mech import cg
+    n1, n2 = (n, n) if isinstance(n, int) else n
+    cfg = synth.config0(32)
+    cfg.n = (n1, n2, 1)
+    cfg.L = (1.0, 1.0, 1.0 / n1)
+    cfg.phases = synth.disc_phases(n1, 0.2, 1.0) if n1 == n2 else (np.arange(n1 * n2) % 5 == 0).astype(np.uint8).reshape(1, n2, n1)
+    cell = make_cell(cfg)
+    ctx = ctx_from_cfg(cfg)
+    g = cell.grid
+    rng = np.random.default_rng(3)
+    eps = rng.normal(scale=4e-3, size=(6,) + g.shape)
+    eps[2] = eps[3] = eps[4] = 0.0
+    st = State.zero(cell)
+    ctx.constitutive(dev(eps), None)
+    D = frozen_damage(cell, st, st.abar)
+    _, C_ref, _, _, _ = evaluate(cell, eps, st, D)
+    mask = cfg.stress_mask
+    b = apply_projection(g, rng.normal(size=(6,) + g.shape), mask)
+    out = torch.empty((6,) + g.shape, dtype=torch.float64, device="cuda")
+    it7, _ = ctx.solve_tangent_cg(dev(b), out, tol=0.0, maxit=7)
+    ref7, _, _ = cg(g, C_ref, b, mask, tol=0.0, maxit=7)
+    assert it7 == 7 and rel(out.cpu().numpy(), ref7) <= 1e-10
+    it, _ = ctx.solve_tangent_cg(dev(b), out, tol=1e-12, maxit=5000)
+    ref, it_ref, _ = cg(g, C_ref, b, mask, tol=1e-12, maxit=5000)
+    assert abs(it - it_ref) <= 1
+    assert rel(out.cpu().numpy(), ref) <= 1e-9
