@@ -95,7 +95,7 @@ __device__ double gtn_aravas_x(double e, const Material& m, double mu) {
   const double iN = 1.0 / m.n_hard;
   double x = 1.0;
   for (int it = 0; it < 100; ++it) {
-    const double xp = pow(x, iN - 1.0);
+    const double xp = exp((iN - 1.0) * log(x));
     const double dx = (xp * x - x - c) / (iN * xp - 1.0);
     x -= dx;
     if (fabs(dx) <= 1e-15 * x) break;
@@ -117,7 +117,7 @@ __device__ void gtn_eval(const Material& m, const GtnCtx& g, const double u[3], 
   const double ex = exp(xi), iex = 1.0 / ex;   // cosh and sinh from one exponential
   const double ch = 0.5 * (ex + iex), sh = 0.5 * (ex - iex);
   const double iN = 1.0 / m.n_hard;
-  const double xp = pow(x, iN - 1.0);
+  const double xp = exp((iN - 1.0) * log(x));   // x^(1/N - 1), x >= 1 (cheaper than the IEEE pow)
   const double e0 = m.sigma_y * (xp * x - x) / (3.0 * g.mu);
   R[0] = a * Q + b * c * sh;
   R[1] = Q * Q + 2.0 * g.fs * m.q1 * ch - 1.0 - m.q3 * g.fs * g.fs;
