@@ -213,3 +213,30 @@ def test_gtn_full_size_sampled():
         assert np.abs(C21[:, i] - r["C_sym"][iu]).max() <= 1e-9 * np.abs(r["C_sym"]).max(), i
     assert nplastic > 200
     ctx.close()
+
+
+def test_gtn_hydrostatic_degenerate_branch():
+    """Pure hydrostatic strain on a porous GTN cell: q_tr = 0 (n = 0, theta = 1 branch) and
+    purely dilatant flow, against the oracle."""
+    cfg = synth.config_gtn2d(16)
+    cfg.phases = np.zeros_like(cfg.phases)           # all GTN matrix
+    cell = make_cell(cfg)
+    ctx = ctx_from_cfg(cfg)
+    g = cell.grid
+    st = State.zero(cell)
+    st.hist = np.full(g.nvox, 0.05)
+    ctx.set_field(_fgd.FIELD_HIST, dev(st.hist))
+    eps = np.zeros((6,) + g.shape)
+    eps[:3] = np.linspace(0.002, 0.02, g.nvox).reshape(g.shape)   # from elastic to deep plastic
+    sig = torch.empty((6,) + g.shape, dtype=torch.float64, device="cuda")
+    ctx.constitutive(dev(eps), sig)
+    s_ref, C_ref, a_ref, epsp_ref, _ = evaluate(cell, eps, st, frozen_damage(cell, st, st.abar))
+    assert rel(sig.cpu().numpy(), s_ref) < 1e-11
+    assert np.abs(s_ref[3:]).max() == 0.0 and np.allclose(s_ref[0], s_ref[1]) and np.allclose(s_ref[1], s_ref[2])
+    Cg = torch.empty((21, g.nvox), dtype=torch.float64, device="cuda")
+    ctx.get_field(_fgd.FIELD_TANGENT, Cg)
+    assert rel(Cg.cpu().numpy(), pack21(C_ref.reshape(6, 6, -1))) < 1e-10
+    tr = torch.empty(g.shape, dtype=torch.float64, device="cuda")
+    ctx.get_field(_fgd.FIELD_SOURCE + 1, tr)                     # tr eps^p source
+    assert rel(tr.cpu().numpy(), a_ref[1]) < 1e-11
+    assert (a_ref[1] > 0).sum() > g.nvox // 2                    # most points flowed (dilatancy)
