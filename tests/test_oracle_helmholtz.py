@@ -82,3 +82,15 @@ def test_mean_ell2_golden():
     ph = np.zeros((2, 4, 4), np.uint8)
     ph[:, :, :2] = 1
     assert abs(np.mean(ell2_field(ph, gv["ell"])) - gv["mean_ell2"]) < 1e-15
+
+
+def test_local_limit_zero_length():
+    """ell = 0 (the local limit): L = I, the non-local field equals its source and the
+    preconditioned CG stops after one iteration."""
+    g = Grid((8, 8, 4))
+    rng = np.random.default_rng(9)
+    a = rng.normal(size=g.shape)
+    e2 = ell2_field(np.zeros(g.shape, np.uint8), [0.0])
+    abar, it, res = solve_helmholtz(g, a, e2, tol=1e-14, maxit=50)
+    assert it == 1
+    assert np.max(np.abs(abar - a)) < 1e-14 * np.max(np.abs(a))

@@ -207,3 +207,24 @@ def test_homogeneous_gtn_plane_strain_equals_material_point():
         assert np.allclose(st.hist, ref[i][1], rtol=1e-9, atol=1e-15)
         assert abs(rep.macro_stress[2]) > 0          # sigma33 carried (A-19)
     assert st.hist.max() > 0.01
+
+
+def test_voigt_reuss_bounds_and_exact_strain_averages():
+    """Elastic two-phase disc cell, all components strain-controlled with a random macroscopic
+    strain E: <eps> = E exactly and E:C_Reuss:E <= <sigma>:E <= E:C_Voigt:E."""
+    cfg = config0(8)
+    g = Grid(cfg.n, cfg.L)
+    m0 = Material(model=0, E=70e3, nu=0.3)
+    cell = Cell(g, cfg.phases, [m0, INCLUSION_EL], cfg.ell, cfg.source_phase, (0,) * 6)
+    rng = np.random.default_rng(2)
+    E = rng.normal(scale=1e-3, size=6)
+    st, rep = solve_increment(cell, State.zero(cell), E, np.zeros(6), TOL)
+    assert rep.converged
+    assert np.max(np.abs(st.eps.reshape(6, -1).mean(1) - E)) < 1e-15
+    f1 = float(np.mean(cfg.phases == 1))
+    C0, C1 = M.elastic_stiffness(m0.E, m0.nu), M.elastic_stiffness(INCLUSION_EL.E, INCLUSION_EL.nu)
+    CV = (1 - f1) * C0 + f1 * C1
+    CR = np.linalg.inv((1 - f1) * np.linalg.inv(C0) + f1 * np.linalg.inv(C1))
+    w = float(rep.macro_stress @ E)
+    assert E @ CR @ E <= w <= E @ CV @ E
+    assert E @ CR @ E < 0.999 * w and w < 0.999 * E @ CV @ E     # strictly inside for this contrast
