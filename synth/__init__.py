@@ -3,7 +3,8 @@
 This module holds NO arithmetic of the paper's method (no transforms, projections,
 Helmholtz operators, constitutive updates or solvers).  It only draws inputs:
 phase maps (disc, RSA spheres, Bernoulli), random SPD tangents, Gaussian fields,
-and the five BASELINE.json configurations as plain parameter records.
+the five BASELINE.json configurations and the non-local GTN cells of the paper's
+Sec. 4.1 / 4.2 (config_gtn2d, config_gtn3d) as plain parameter records.
 
 Units: stresses/moduli in MPa, lengths in cell units (L = 1) unless a config says
 otherwise.  Array layout: numpy C order [z][y][x] (x fastest) for scalars and
