@@ -17,7 +17,8 @@ a dot product.  The paper writes s for the Mises stress; it is q here (s is the 
   A_N        = f_N / (s_N sqrt(2 pi)) exp(-((ebar0 - eps_N)/s_N)^2 / 2)
   porosity   f_{n+1} = f_n + A_N(ebar0_{n+1}) d ebar0 + (1 - f_{n+1}) d trbar          (P:455-458,
              App. A), with the non-local fields frozen at the staggered iterate
-             (P:600-601), so it is explicit:  f = (f_n + A_N d ebar0 + d trbar) / (1 + d trbar)
+             (P:600-601), so it is explicit:  f = (f_n + A_N d ebar0 + d trbar) / (1 + d trbar),
+             kept irreversible, f_{n+1} = max(f_n, f) (A-30, as D in A-16)
   hardening  sigma_0/sigma_Y = (sigma_0/sigma_Y + 3 mu eps0p/sigma_Y)^N  (Aravas, P:826-829);
              with x = sigma_0/sigma_Y this is eps0p(x) = sigma_Y (x^(1/N) - x) / (3 mu)
   sources    alpha_0 = eps0p, alpha_1 = tr eps^p
@@ -129,11 +130,12 @@ def aravas_x(e0: float, m: GTNParams, mu: float) -> float:
 
 
 def porosity(f_n: float, ebar0: float, ebar0_n: float, trbar: float, trbar_n: float, m: GTNParams) -> float:
-    """f_{n+1} from the frozen non-local increments (App. A), clamped to [0, 1]."""
+    """f_{n+1} from the frozen non-local increments (App. A), irreversible
+    (A-30: f_{n+1} >= f_n, as damage in A-16) and at most 1."""
     d0 = ebar0 - ebar0_n
     dt = trbar - trbar_n
     f = (f_n + nucleation_rate(ebar0, m) * d0 + dt) / (1.0 + dt)
-    return min(max(f, 0.0), 1.0)
+    return min(max(f, f_n), 1.0)
 
 
 def _yield(P, Q, fs, m):

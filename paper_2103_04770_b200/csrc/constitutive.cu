@@ -56,7 +56,7 @@ __device__ __forceinline__ void elastic_C(double K, double mu, double f, PointOu
 // Non-local GTN (model 3): Sec. 2.1.1, Sec. 2.2.2, App. A P:1100-1129.
 // Mandel vectors; q = Mises stress (the paper's s), p = -tr(sigma)/3, sigma_0 = sigma_y x.
 // Frozen porosity (App. A P:1119 with the non-local fields of the staggered iterate, A-30):
-//   f = (f_n + A_N(ebar0) (ebar0 - ebar0_n) + (trbar - trbar_n)) / (1 + trbar - trbar_n) in [0, 1]
+//   f = max(f_n, (f_n + A_N(ebar0) (ebar0 - ebar0_n) + (trbar - trbar_n)) / (1 + trbar - trbar_n)), <= 1
 // Return mapping in u = (a, b, x): d eps^p = (a/3) 1 + b n, n = 1.5 s_tr/q_tr, p = p_tr + K a,
 // q = q_tr - 3 mu b, residuals (scaled)
 //   R1 = a Q + b c sinh(xi)                         (normality with dlam eliminated)
@@ -84,7 +84,7 @@ __device__ __forceinline__ double gtn_porosity(double fn, double e0, double e0n,
   const double AN = m.f_n / (m.s_n * 2.50662827463100050242) * exp(-0.5 * z * z);   // sqrt(2 pi)
   const double dt = t - tn;
   double f = (fn + AN * (e0 - e0n) + dt) / (1.0 + dt);
-  f = f < 0.0 ? 0.0 : f;
+  f = f > fn ? f : fn;   // irreversible (A-30): no net void closure
   return f > 1.0 ? 1.0 : f;
 }
 

@@ -192,3 +192,11 @@ def test_porosity_update_against_growth_and_nucleation_odes():
     def Phi(z):
         return 0.5 * (1 + math.erf(z / math.sqrt(2)))
     assert f == pytest.approx(M.f_n * (Phi((E - M.eps_n) / M.s_n) - Phi(-M.eps_n / M.s_n)), rel=1e-4)
+
+
+def test_porosity_is_irreversible():
+    # A-30 (as D in A-16): void closure (d trbar < 0) never lowers the committed porosity
+    m = G.GTNParams()
+    assert G.porosity(0.05, 0.01, 0.01, -0.01, 0.0, m) == 0.05
+    assert G.porosity(0.05, 0.01, 0.01, 0.01, 0.0, m) > 0.05
+    assert G.porosity(0.999, m.eps_n, m.eps_n - 1.0, 0.0, 0.0, m) == 1.0   # 0.999 + A_N(peak) * 1 > 1
