@@ -1018,6 +1018,9 @@ __global__ void __launch_bounds__(512, 2) k_yreg512(YArgs a) {
       }
       __syncthreads();
     } else {
+      // the staging loop below writes EVERY line buffer, and the previous tile's inverse FFT
+      // synchronises only the warps of its own plane (named barrier): wait for all planes first
+      __syncthreads();
       for (int idx = threadIdx.x; idx < 2 * N * TZ; idx += blockDim.x) {
         const int z2 = idx % TZ, ky = (idx / TZ) & (N - 1), k2l = idx / (TZ * N);
         const int kxo = kx0 + k2l;

@@ -370,3 +370,36 @@ def test_factorised_z_projection(n, monkeypatch):
         x = gaussian_field(6, g.shape, 1e-3, 32)
         yt = ctx.apply_projected_tangent(dev(x)).cpu().numpy()
         assert rel(yt, apply_projected_tangent(g, unpack21(Cp).reshape((6, 6) + g.shape), x, mask)) <= TOL_APPLY
+
+
+@pytest.mark.parametrize("n", [256, 512])
+def test_full_size_run_to_run_bitwise(n):
+    """Every kernel on the path reduces in a fixed order, so repeated applies on the same input
+    must agree BIT FOR BIT.  A shared-memory race (e.g. a line buffer restaged while another
+    plane's warps still exchange through it) shows up here as run-to-run differences long
+    before a sampled-frequency parity check happens to hit a corrupted line: at 512^3 the
+    y-inverse pass once restaged its line buffers after a per-plane named barrier only and
+    corrupted ~2000 z-lines per apply."""
+    import synth
+    ctx = Context((n, n, n), (float(n),) * 3)
+    ctx.set_control(synth.CONFIG1_MASK)
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(3)
+    ctx.set_tangent(synth.random_spd_tangent_torch(n ** 3, 7, device="cuda"))
+    x = torch.randn((6, n, n, n), generator=gen, dtype=torch.float64, device="cuda") * 1e-3
+    y0 = ctx.apply_projected_tangent(x)
+    for _ in range(4):
+        assert torch.equal(ctx.apply_projected_tangent(x), y0)
+    p0 = ctx.apply_projection(x)
+    for _ in range(3):
+        assert torch.equal(ctx.apply_projection(x), p0)
+    del y0, p0
+    ph = (torch.rand((n, n, n), generator=gen, device="cuda", dtype=torch.float64) < 0.2).to(torch.uint8)
+    ctx.set_phases(ph, 2)
+    ctx.set_nonlocal(np.array([[2.0, 4.0]]), [0])
+    a = x[0].contiguous()
+    z0 = ctx.apply_helmholtz_precond(0, a)
+    h0 = ctx.apply_helmholtz(0, a)
+    for _ in range(4):
+        assert torch.equal(ctx.apply_helmholtz_precond(0, a), z0)
+        assert torch.equal(ctx.apply_helmholtz(0, a), h0)
