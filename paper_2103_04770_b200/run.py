@@ -4,6 +4,7 @@ Alg. 1 per increment, fixed strain increments with deterministic halving on non-
 (`synth.config_gtn2d`, `synth.config_gtn3d`) from `synth`.
 
     python -m paper_2103_04770_b200.run --config 3 [--n 128] [--incr 60] [--tight]
+    python -m paper_2103_04770_b200.run --config 4 [--n 512] --incr 4 --log   (first increments of the 512^3 cell)
     python -m paper_2103_04770_b200.run --config gtn2d [--n 64] [--de 2.5e-3] [--incr 200]
 
 prints one JSON line: the macroscopic stress-strain curve (load component), the peak, the strain
@@ -149,7 +150,7 @@ def main(argv=None):
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     import synth
     p = argparse.ArgumentParser()
-    p.add_argument("--config", default="0", choices=["0", "2", "3", "gtn2d", "gtn3d"])
+    p.add_argument("--config", default="0", choices=["0", "2", "3", "4", "gtn2d", "gtn3d"])
     p.add_argument("--de", type=float, default=None, help="override the fixed strain increment")
     p.add_argument("--n", type=int, default=None)
     p.add_argument("--incr", type=int, default=None)
@@ -167,6 +168,8 @@ def main(argv=None):
         cfg = synth.config2(a.n or 256)
     elif a.config == "3":
         cfg = synth.config3(n=a.n or 128)
+    elif a.config == "4":
+        cfg = synth.config4(n=a.n or 512)
     elif a.config == "gtn2d":
         ell = a.ell if a.ell else 0.05
         cfg = synth.config_gtn2d(a.n or 64, ell_over_L=ell, ell_i_over_L=min(ell, 0.001))

@@ -230,6 +230,14 @@ def config3(n: int = 128, n_spheres: int = 30, phi: float = 0.20, seed: int = 3)
                       extra={"centres": centres, "radius": r})
 
 
+def config4(n: int = 512, n_spheres: int = 400, phi: float = 0.25, seed: int = 4) -> CellConfig:
+    """BJ config 4: the 512^3 RSA cell, 400 spheres at 25 % volume fraction, same phases,
+    materials, two-ell regularisation (ell_m = 5h, ell_p = 3h), mask and loading as config 3."""
+    c = config3(n=n, n_spheres=n_spheres, phi=phi, seed=seed)
+    c.name = f"config4_{n}"
+    return c
+
+
 # GTN matrices of the paper (model 3): Sec. 4.1 (2D, P:825-832) and Sec. 4.2 (3D, P:984-986)
 MATRIX_GTN_2D = Material(model=3, E=300.0e3, nu=0.3, sigma_y=1000.0, q1=1.5, q2=1.0, q3=2.25, f_c=0.15, f_f=0.25,
                          f_n=0.04, eps_n=0.3, s_n=0.1, n_hard=0.1, fstar_max=0.6)
