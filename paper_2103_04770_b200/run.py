@@ -119,6 +119,9 @@ def run_config(cfg, n_incr=None, tol=(1e-4, 1e-6, 1e-8, 1e-6), max_halvings=6, m
                 E_done = E_try
                 counts["substeps"] += 1
                 curve.append((E_try, float(rep["macro_stress"][cfg.load_comp])))
+                if log:
+                    print(json.dumps({"E": E_try, "S": curve[-1][1], "t": time.perf_counter() - t0,
+                                      "cg": counts["cg"], "helm": counts["helm"]}), file=sys.stderr, flush=True)
             elif st == _fgd.ENOCONV and halvings < max_halvings:
                 step *= 0.5
                 halvings += 1
