@@ -195,7 +195,7 @@ def peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-TRAFFIC_KERNEL = {"xfwd6": "k_xtan<{n}, 2, 1, 2>", "xinv6": "k_xipipe<{n}, 1>", "z6": "k_zreg256<6, 0>",
+TRAFFIC_KERNEL = {"xfwd6cg": "k_xtan<{n}, 2, 1, 2>", "xinv6": "k_xipipe<{n}, 1>", "z6": "k_zreg256<6, 0>",
                   "yfwd6": "k_yreg256<0>", "yinv6": "k_yreg256<1>", "stencil": "k_stencil<1, 2>"}
 
 
@@ -213,15 +213,22 @@ def measured_traffic(cls, n):
 
 def class_bytes(n, kcg, khelm, world=1):
     """Algorithmic (compulsory) bytes per STEP and per rank for each kernel class of the fused
-    5-pass design.  Mechanical CG with the solution update deferred into the next forward pass:
-    K2 = read r, p, x (144) + compact tangent (72) + write p, x (96) + spectrum (~48) B/voxel,
-    K3/K4/K3 ~96 B each, K5 = spectrum (~48) + read/write r (96); 1-comp analogues; stencil 33 B;
-    constitutive ~300 B.  S = spectral bytes of one component (16 B x Hx*Ny*Nz)."""
+    5-pass design.  S = spectral bytes of one component (16 B x Hx*Ny*Nz).
+    x forward, 6 comps:
+      xfwd6   = residual pass (read sigma 48 B/voxel + write 6S) + the FIRST CG tangent launch,
+                which reads r = b (48) and the compact tangent (72) and writes p, x (96) + 6S --
+                it reads neither p_old nor x (216 B/voxel + 6S);
+      xfwd6cg = every later CG tangent launch (the steady launch): read r, p_old, x (144) +
+                compact tangent (72), write p, x (96) + 6S = 312 B/voxel + 6S (~360 B/voxel).
+    y/z passes: read + write of the 6-comp spectrum (2 x 6S) per apply.  x inverse: 6S + r
+    read/write (96) per CG iteration, 6S + write b (48) for the residual.  1-comp analogues for
+    the PCG; stencil 33 B/voxel; constitutive ~300 B/voxel."""
     V = n ** 3 // world
     S = 16 * (n // 2 + 1) * n * n // world
     b = {}
     TB = 72                                                                       # compact J2 tangent (9 doubles)
-    b["xfwd6"] = (48 * V + 6 * S) + kcg * (48 * 5 * V + TB * V + 6 * S)         # residual + CG (r, p, x, C -> p, x, spec)
+    b["xfwd6"] = (48 * V + 6 * S) + (1 if kcg > 0 else 0) * ((48 + TB + 96) * V + 6 * S)
+    b["xfwd6cg"] = max(0, kcg - 1) * ((144 + TB + 96) * V + 6 * S)
     b["yfwd6"] = b["yinv6"] = b["z6"] = (1 + kcg) * 2 * 6 * S
     b["xinv6"] = (6 * S + 48 * V) + kcg * (6 * S + 96 * V)                      # residual store + CG r update
     b["xfwd1"] = (8 * V + S) + khelm * (32 * V + 16 * V + S)                      # precond init + PCG x/r update
@@ -484,7 +491,8 @@ def run_ours(a):
     traffic, traffic_src = measured_traffic(dom, n)
     roof = {"bound": "hbm", "kernel": dom, "achieved": d["GBs"], "peak": peak, "unit": "GB/s", "frac": d["frac"],
             "traffic": traffic, "traffic_source": traffic_src, "peak_source": peak_src,
-            "algorithmic_bytes_per_launch": cb[dom] / d["launches_per_step"]}
+            "algorithmic_bytes_per_launch": cb[dom] / d["launches_per_step"],
+            "traffic_vs_algorithmic": (traffic / (cb[dom] / d["launches_per_step"])) if traffic else None}
     # whole-step efficiency against the fused-design byte model
     step_bytes = sum(cb.values())
     step_eff = {"bytes_per_step": step_bytes, "GBs": step_bytes / (ms * 1e-3) / 1e9,
@@ -533,14 +541,23 @@ def run_ours(a):
                 "alltoall_GBs_per_gpu": a2a_bytes / (cms * 1e-3) / 1e9 if cms else None,
                 "nvlink_GBs_per_direction": 900.0,
                 "note": "comm = NCCL all-to-all transposes + stencil z-halos + Krylov allreduces (event-timed)"}
-    # per-solver rates inside the step (kernel-class times, this rank)
-    t_mech = sum(per_class[k]["ms_per_step"] for k in ("xfwd6", "yfwd6", "z6", "yinv6", "xinv6") if k in per_class)
+    # per-solver rates inside the step (kernel-class times, this rank): one mechanical apply = the
+    # five 6-comp passes (the residual projection costs the same passes as a CG iteration), one PCG
+    # iteration = the stencil + the five 1-comp passes
+    t_mech = sum(per_class[k]["ms_per_step"] for k in ("xfwd6", "xfwd6cg", "yfwd6", "z6", "yinv6", "xinv6")
+                 if k in per_class)
     t_helm = sum(per_class[k]["ms_per_step"] for k in ("xfwd1", "yfwd1", "z1", "yinv1", "xinv1", "stencil")
                  if k in per_class)
-    rates = {"mech_cg_iter_per_s": 1e3 / ms * a.kcg,
-             "mech_apply_ms": t_mech / (a.kcg + 1) if t_mech else None,
-             "helm_pcg_iter_ms": t_helm / (a.khelm + 1) if t_helm else None,
-             "helm_pcg_voxel_iter_per_s": V * (a.khelm + 1) / (t_helm * 1e-3) if t_helm else None}
+    mech_apply_ms = t_mech / (a.kcg + 1) if t_mech else None
+    helm_iter_ms = t_helm / (a.khelm + 1) if t_helm else None
+    rates = {"mech_cg_iter_per_s": 1e3 / mech_apply_ms if mech_apply_ms else None,
+             "mech_apply_ms": mech_apply_ms,
+             "mech_cg_voxel_iter_per_s": V / (mech_apply_ms * 1e-3) if mech_apply_ms else None,
+             "helm_pcg_iter_per_s": 1e3 / helm_iter_ms if helm_iter_ms else None,
+             "helm_pcg_iter_ms": helm_iter_ms,
+             "helm_pcg_voxel_iter_per_s": V / (helm_iter_ms * 1e-3) if helm_iter_ms else None,
+             "note": "Krylov iteration rates from the event-timed kernel classes of one rank (the step's "
+                     "constitutive update and reductions excluded); value/ms_per_step is the whole step"}
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
                 "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True,

@@ -198,8 +198,9 @@ fgd_status fgd_macro_stress(fgd_ctx* ctx, double out[6]);
  * 6 y-fwd (1), 7 z (1), 8 y-inv (1), 9 x-inv (1), 10 Helmholtz stencil, 11 constitutive,
  * 12 other (dots, axpy, commit, error norms), 13 communication (slab all-to-all transposes,
  * stencil z-halos and Krylov allreduces when nranks > 1; the block copies of the single-GPU slab
- * emulation). */
-#define FGD_NUM_KCLASS 14
+ * emulation), 14 x-fwd (6) of the mechanical CG iterations after the first (the steady tangent
+ * launch; class 0 then holds the residual pass and the first CG iteration). */
+#define FGD_NUM_KCLASS 15
 fgd_status fgd_set_timing(fgd_ctx* ctx, int enable);
 fgd_status fgd_kernel_times(fgd_ctx* ctx, double* ms, unsigned long long* count, int n);
 

@@ -86,7 +86,7 @@ _SIGS = {
     "fgd_kernel_times": ([_P, _P, _P, _I], _I),
 }
 KCLASS = ("xfwd6", "yfwd6", "z6", "yinv6", "xinv6", "xfwd1", "yfwd1", "z1", "yinv1", "xinv1", "stencil",
-          "constitutive", "other", "comm")
+          "constitutive", "other", "comm", "xfwd6cg")
 EXPORTED = tuple(_SIGS)
 for _name, (_args, _res) in _SIGS.items():
     _f = getattr(lib, _name)

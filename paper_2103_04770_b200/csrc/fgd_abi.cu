@@ -965,47 +965,81 @@ fgd_status fgd_solve_increment(fgd_ctx* c, const fgd_increment* inc, fgd_report*
   double err = INFINITY;
   bool converged = false;
   double macro[6] = {0, 0, 0, 0, 0, 0};
+  std::string why = "increment did not converge";
+  // every exit fills rep with the work done so far (failed attempts included)
+  auto fill_rep = [&]() {
+    if (!rep) return;
+    for (int i = 0; i < 6; ++i) rep->macro_stress[i] = macro[i];
+    rep->err = err;
+    rep->stag_it = k + (converged ? 1 : 0);
+    rep->newton_it = newton_total;
+    rep->cg_it = cg_total;
+    rep->helm_it = helm_total;
+  };
+  // a hard (non-convergence-unrelated) error: report and return it
+  auto hard = [&](fgd_status s) {
+    fill_rep();
+    return s;
+  };
+#define TRY_INC(x)                  \
+  do {                              \
+    fgd_status s_ = (x);            \
+    if (s_ != FGD_OK) return hard(s_); \
+  } while (0)
   for (k = 0; k < inc->max_stag; ++k) {
     FGD_CUDA(c, cudaMemcpyAsync(c->w_eps_prev, c->w_eps, 6 * n * 8, cudaMemcpyDeviceToDevice, c->stream));
     bool newton_ok = false;
     for (int r = 0; r <= inc->max_newton; ++r) {
       const fgd_status cs = fgd_constitutive(c, nullptr, nullptr, macro);
-      if (cs == FGD_ENOCONV) break;   // a GTN return mapping failed: roll back, the caller cuts back
-      if (cs != FGD_OK) return cs;
+      if (cs == FGD_ENOCONV) {   // a GTN return mapping failed: roll back, the caller cuts back
+        why = "GTN return mapping failed in increment";
+        break;
+      }
+      if (cs != FGD_OK) return hard(cs);
       double rms;
-      TRY(fgd_mech_residual(c, S, nullptr, &rms));
+      TRY_INC(fgd_mech_residual(c, S, nullptr, &rms));
       const double nm = std::sqrt(macro[0] * macro[0] + macro[1] * macro[1] + macro[2] * macro[2] + macro[3] * macro[3] +
                                   macro[4] * macro[4] + macro[5] * macro[5]);
       if (rms < inc->tol_newton * std::max(nm, 1e-6 * sref)) {
         newton_ok = true;
         break;
       }
-      if (r == inc->max_newton) break;
+      if (r == inc->max_newton) {
+        why = "Newton did not converge in increment";
+        break;
+      }
       int it = 0;
       fgd_status s = cg_mech(c, c->w_b, c->w_de, inc->tol_cg, inc->max_cg, &it, nullptr);
       cg_total += it;
-      if (s != FGD_OK && s != FGD_ENOCONV) return s;
+      if (s != FGD_OK && s != FGD_ENOCONV) return hard(s);
       ++newton_total;
-      TRY(launch_axpy(c, 6 * n, c->w_eps, c->w_de, 1.0));
+      TRY_INC(launch_axpy(c, 6 * n, c->w_eps, c->w_de, 1.0));
     }
     if (!newton_ok) break;
     // Helmholtz solves with the converged sources (A-28)
-    for (int j = 0; j < J; ++j) {
+    bool helm_ok = true;
+    for (int j = 0; j < J && helm_ok; ++j) {
       int it = 0;
       fgd_status s = pcg_helmholtz(c, j, c->w_alpha + (size_t)j * n, nullptr, inc->tol_helm, inc->max_helm, &it,
                                    nullptr);
       helm_total += it;
-      if (s != FGD_OK) return s == FGD_ENOCONV ? set_err(c, FGD_ENOCONV, "Helmholtz PCG failed in increment") : s;
+      if (s == FGD_ENOCONV) {
+        why = "Helmholtz PCG did not converge in increment";
+        helm_ok = false;
+        break;
+      }
+      if (s != FGD_OK) return hard(s);
       // the new non-local field is in hb[0]; w_D holds abar^(k+1) until ERR is known
       FGD_CUDA(c, cudaMemcpyAsync(c->w_D + (size_t)j * n, c->hb[0], n * 8, cudaMemcpyDeviceToDevice, c->stream));
     }
+    if (!helm_ok) break;
     // ERR (A-02)
     FGD_CUDA(c, cudaMemsetAsync(&c->sc->maxbits, 0, 8, c->stream));
-    TRY(err_reduce(c, c->w_eps, c->w_eps_prev, c->w_D, c->w_abar));
+    TRY_INC(err_reduce(c, c->w_eps, c->w_eps_prev, c->w_D, c->w_abar));
     double red[14];
     unsigned long long mb;
-    TRY(sync_read(c, &c->sc->red[16], 8 * 14, red));
-    TRY(sync_read(c, &c->sc->maxbits, 8, &mb));
+    TRY_INC(sync_read(c, &c->sc->red[16], 8 * 14, red));
+    TRY_INC(sync_read(c, &c->sc->maxbits, 8, &mb));
     double mx;
     std::memcpy(&mx, &mb, 8);
     double den = 0.0;
@@ -1022,20 +1056,14 @@ fgd_status fgd_solve_increment(fgd_ctx* c, const fgd_increment* inc, fgd_report*
     }
     if (J > 0) FGD_CUDA(c, cudaMemcpyAsync(c->w_abar, c->w_D, (size_t)J * n * 8, cudaMemcpyDeviceToDevice, c->stream));
   }
-  if (rep) {
-    for (int i = 0; i < 6; ++i) rep->macro_stress[i] = macro[i];
-    rep->err = err;
-    rep->stag_it = k + (converged ? 1 : 0);
-    rep->newton_it = newton_total;
-    rep->cg_it = cg_total;
-    rep->helm_it = helm_total;
-  }
+#undef TRY_INC
+  fill_rep();
   if (!converged) {
     // rollback: committed state untouched; reset the iterate
     FGD_CUDA(c, cudaMemcpyAsync(c->w_eps, c->st_eps, 6 * n * 8, cudaMemcpyDeviceToDevice, c->stream));
     if (J > 0) FGD_CUDA(c, cudaMemcpyAsync(c->w_abar, c->st_abar, (size_t)J * n * 8, cudaMemcpyDeviceToDevice, c->stream));
     FGD_CUDA(c, cudaStreamSynchronize(c->stream));
-    return set_err(c, FGD_ENOCONV, "increment did not converge");
+    return set_err(c, FGD_ENOCONV, why);
   }
   // 3. commit (A-16, A-30): eps^p, eps_p recomputed at the converged strain with the fields the last
   // mechanics was frozen at; history from the accepted abar^(k+1)

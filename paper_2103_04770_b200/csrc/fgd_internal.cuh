@@ -69,6 +69,10 @@ struct DevScalars {
   unsigned long long maxbits;
 };
 
+// Every hot kernel tests guard_done() BEFORE pdl_wait(): correct only while PDL is off (with PDL a
+// dependent grid could read a stale done = 0 and run while later kernels of its iteration skip).
+// Move the test after pdl_wait() before enabling kUsePdl.
+static_assert(!kUsePdl, "guard_done() is read before pdl_wait(); see the note above");
 __device__ __forceinline__ bool guard_done(const DevScalars* g) {
   return g != nullptr && *(volatile const int*)&g->done != 0;
 }
@@ -213,7 +217,7 @@ fgd_status set_err(fgd_ctx* c, fgd_status s, const std::string& m);
 
 // scoped event timer around one kernel launch (no-op unless ctx->timing)
 enum KClass : int { KC_XFWD6 = 0, KC_YFWD6, KC_Z6, KC_YINV6, KC_XINV6, KC_XFWD1, KC_YFWD1, KC_Z1, KC_YINV1, KC_XINV1,
-                    KC_STENCIL, KC_CONST, KC_OTHER, KC_COMM };
+                    KC_STENCIL, KC_CONST, KC_OTHER, KC_COMM, KC_XFWD6_CG };
 struct KTimer {
   fgd_ctx* c;
   int cls, e0 = -1;

@@ -503,7 +503,7 @@ static fgd_status launch_xtan(fgd_ctx* c, int mode, double* r, double* p, double
   XTArgs a{c->guard ? c->sc : nullptr, Ny, c->nz_l, c->HxA, CW, S, R, first, c->nvox, r, p, x, Cp, c->specA, c->sc, c->partials, red_op, red_slot,
            c->tabs.tw[ilog2(Nx / 2)], c->tabs.tw[ilog2(Nx)]};
   const int ntiles = (Ny / R) * c->nz_l;
-  KTimer kt(c, helm ? KC_XFWD1 : KC_XFWD6);
+  KTimer kt(c, helm ? KC_XFWD1 : (mode == XF_TANGENT_CG && !first) ? KC_XFWD6_CG : KC_XFWD6);
   int grid = 1;
 #define XTL(NN)                                                                                       \
   {                                                                                                   \
@@ -571,7 +571,7 @@ fgd_status launch_xfwd_io(fgd_ctx* c, int ncomp, int mode, const double* in0, co
   }
   const double2* tw = c->tabs.tw[ilog2(Nx / 2)];
   const double2* twN = c->tabs.tw[ilog2(Nx)];
-  KTimer kt(c, ncomp == 6 ? KC_XFWD6 : KC_XFWD1);
+  KTimer kt(c, ncomp == 6 ? ((mode == XF_TANGENT_CG && !first) ? KC_XFWD6_CG : KC_XFWD6) : KC_XFWD1);
 #define XF(NN)                                                                                   \
   if (ncomp == 6 && mode == XF_PLAIN) FGD_LAUNCH(c, (k_xfwd<NN, 6, XF_PLAIN>), grid, thr, smem, a, tw, twN);            \
   else if (ncomp == 6 && mode == XF_TANGENT) FGD_LAUNCH(c, (k_xfwd<NN, 6, XF_TANGENT>), grid, thr, smem, a, tw, twN);   \

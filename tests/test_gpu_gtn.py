@@ -119,7 +119,26 @@ def run_both(cfg, n_incr):
     return out, ctx, st
 
 
-def _check_committed(ctx, st):
+def _check_committed(ctx, st, cfg=None):
+    if cfg is not None:
+        # App. A: the GTN stress is the elastic law at the returned plastic strain,
+        # sigma = C^e (eps - eps^p), also at the dilatant (f* > 0) returns; on the GPU the stress of
+        # the last mechanical solve and the committed eps, eps^p belong to the same converged state
+        sh = (6,) + tuple(cfg.phases.shape)
+        sig, eps, epsp = (torch.empty(sh, dtype=torch.float64, device="cuda") for _ in range(3))
+        ctx.get_field(_fgd.FIELD_STRESS, sig)
+        ctx.get_field(_fgd.FIELD_STRAIN, eps)
+        ctx.get_field(_fgd.FIELD_EPS_P, epsp)
+        sig, eps, epsp = (t.cpu().numpy().reshape(6, -1) for t in (sig, eps, epsp))
+        ph = cfg.phases.reshape(-1)
+        one = np.r_[1.0, 1, 1, 0, 0, 0]
+        for q, m in enumerate(cfg.materials):
+            K, mu = m.E / (3.0 * (1.0 - 2.0 * m.nu)), m.E / (2.0 * (1.0 + m.nu))
+            Ce = K * np.outer(one, one) + 2.0 * mu * (np.eye(6) - np.outer(one, one) / 3.0)
+            sel = ph == q
+            s_el = Ce @ (eps[:, sel] - epsp[:, sel])
+            assert np.abs(sig[:, sel] - s_el).max() <= 1e-10 * np.abs(s_el).max(), q
+        assert np.abs(epsp[:3, ph == 0].sum(0)).max() > 0.0     # dilatant returns present
     h = torch.empty(st.hist.shape, dtype=torch.float64, device="cuda")
     ctx.get_field(_fgd.FIELD_HIST, h)
     assert np.max(np.abs(h.cpu().numpy() - st.hist)) < 1e-7
@@ -137,7 +156,7 @@ def test_gtn_increment_parity_2d():
         if i <= peak:
             assert rel(got, ref) <= 1e-6, (i, ref, got)
     assert st.hist.max() > 1e-3                    # porosity grew
-    _check_committed(ctx, st)
+    _check_committed(ctx, st, cfg)
 
 
 def test_gtn_increment_parity_3d():
@@ -147,7 +166,7 @@ def test_gtn_increment_parity_3d():
     for i, (ref, got) in enumerate(out):
         assert rel(got, ref) <= 1e-6, (i, ref, got)
     assert st.hist.max() > 1e-4
-    _check_committed(ctx, st)
+    _check_committed(ctx, st, cfg)
 
 
 def test_gtn_needs_two_fields():

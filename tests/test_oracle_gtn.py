@@ -137,6 +137,29 @@ def test_yield_consistency_normality_and_work_identity():
     assert nplastic >= 20
 
 
+def test_elastic_law_at_plastic_returns():
+    """sigma = C^e : (eps - eps^p) at every plastic return with f* > 0 (App. A: the
+    stress is the elastic law at the returned plastic strain).  Unlike the yield, normality and
+    work pins, this fixes the coefficient of the volumetric return (p = p_tr + K a): a slip such as
+    3K a or K a / 3 leaves sigma off the elastic law.  C^e from the textbook isotropic moduli."""
+    E, nu = M.E, M.nu
+    Kt, mut = E / (3.0 * (1.0 - 2.0 * nu)), E / (2.0 * (1.0 + nu))
+    one = np.r_[1.0, 1, 1, 0, 0, 0]
+    Ce = Kt * np.outer(one, one) + 2.0 * mut * (np.eye(6) - np.outer(one, one) / 3.0)
+    nchk = 0
+    for eps, epsp_n, e0n, f in _random_states(21, 60):
+        r = G.gtn_point(eps, epsp_n, e0n, f, M)
+        if not r["plastic"] or G.effective_porosity(f, M) == 0.0:
+            continue
+        assert r["converged"]
+        s_el = Ce @ (eps - r["epsp"])
+        assert np.linalg.norm(r["sigma"] - s_el) <= 1e-12 * np.linalg.norm(s_el)
+        # and the return is genuinely dilatant (the volumetric term is exercised)
+        assert abs((r["epsp"] - epsp_n)[:3].sum()) > 0.0
+        nchk += 1
+    assert nchk >= 20
+
+
 def test_consistent_tangent_central_differences():
     for eps, epsp_n, e0n, f in list(_random_states(9, 14)):
         r = G.gtn_point(eps, epsp_n, e0n, f, M)
