@@ -3,7 +3,9 @@
 "FP64 FFT-Galerkin Krylov voxel*iter/s at 256^3/512^3; % of HBM roofline").
 
 One STEP = one staggered Krylov sweep over the whole hot path on
-the BASELINE config-1 recipe at the metric size (default 256^3; --n 512 for 512^3):
+the BASELINE config-1 recipe at the metric size (default 512^3, the cell of the multi-GPU
+target, so that the N = 1 line and the scaling lines measure the same cell; --size 256 for 256^3;
+on one GPU the other size is measured too and reported under "by_size"):
   a1      constitutive update at the strain field (J2-Lemaitre matrix / elastic inclusion,
           damage frozen from the non-local field) -> sigma, consistent tangent, source alpha
   a3-a5   Newton residual b = -G*(sigma - Sigma_bar)  (5-pass FFT with the projection)
@@ -13,6 +15,8 @@ the BASELINE config-1 recipe at the metric size (default 256^3; --n 512 for 512^
 value = N_vox * KCG / (step time)  [voxel*iter/s of the mechanical Krylov solver], all ranks.
 Inputs are generated on the device (seeded) and stay resident; every field (134 MB/comp at
 256^3) and the tangent (2.8 GB) exceed the 126 MB L2, so no explicit flush is needed.
+--gpus N without a torchrun environment re-executes itself under torch.distributed.run (N ranks,
+one per GPU, 127.0.0.1); the cell is slab-decomposed over the ranks (strong scaling).
 
 --impl reference: the CPU oracle (oracle/, NumPy/SciPy FP64) on a bounded 64^3 sample of the
 same recipe, same metric and unit.
@@ -43,7 +47,8 @@ def args_():
     p.add_argument("--steps", type=int, default=10)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--size", dest="n", type=int, default=256, help="cell edge (voxels)")
+    p.add_argument("--size", dest="n", type=int, default=512, help="cell edge (voxels)")
+    p.add_argument("--no-by-size", action="store_true", help="skip the second metric size (256^3 / 512^3)")
     p.add_argument("--kcg", type=int, default=10)
     p.add_argument("--khelm", type=int, default=10)
     p.add_argument("--no-e2e", action="store_true")
@@ -391,25 +396,15 @@ def gtn_measurement(n, dev, peak, reps=5):
                     "voxel); FP64-ALU bound on plastic voxels, see profiles/ for the ncu pipe utilisation"}
 
 
-def run_ours(a):
+def measure(a, n, rank, world, local, nid, e2e_on, extras):
+    """One size: K timed steps (headline), K instrumented steps (kernel classes), optional e2e and,
+    with extras (one GPU, n <= 256), the cuFFT comparison arm on the same tangent."""
     import numpy as np
     import torch
 
-    rank, world, local = dist_env()
-    torch.cuda.set_device(local)
     import synth
-    from paper_2103_04770_b200 import Context, Material, nccl_id
+    from paper_2103_04770_b200 import Context, Material
 
-    nid = None
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        t = torch.zeros(128, dtype=torch.uint8, device="cuda")
-        if rank == 0:
-            t.copy_(torch.frombuffer(bytearray(nccl_id()), dtype=torch.uint8))
-        dist.broadcast(t, 0)
-        nid = bytes(t.cpu().numpy().tobytes())
-    n = a.n
     V = n ** 3
     dev = torch.device("cuda", local)
     ctx = Context((n, n, n), (float(n),) * 3, device=local, rank=rank, nranks=world, nccl_id=nid)
@@ -455,6 +450,8 @@ def run_ours(a):
     ms = ev0.elapsed_time(ev1) / a.steps
     # per-kernel-class durations: the same K steps again with a CUDA event pair around every
     # launch (fgd_set_timing) -- the roofline numbers come from this instrumented pass
+    if world > 1:
+        torch.distributed.barrier()
     ctx.set_timing(True)
     torch.cuda.synchronize()
     ev0.record(stream)
@@ -489,10 +486,11 @@ def run_ours(a):
     dom = max((k for k in per_class if k in cb), key=lambda k: per_class[k]["ms_per_step"])
     d = per_class[dom]
     traffic, traffic_src = measured_traffic(dom, n)
+    alg = cb[dom] / d["launches_per_step"]
     roof = {"bound": "hbm", "kernel": dom, "achieved": d["GBs"], "peak": peak, "unit": "GB/s", "frac": d["frac"],
             "traffic": traffic, "traffic_source": traffic_src, "peak_source": peak_src,
-            "algorithmic_bytes_per_launch": cb[dom] / d["launches_per_step"],
-            "traffic_vs_algorithmic": (traffic / (cb[dom] / d["launches_per_step"])) if traffic else None}
+            "algorithmic_bytes_per_launch": alg,
+            "traffic_vs_algorithmic": (traffic / alg) if traffic else None}
     # whole-step efficiency against the fused-design byte model
     step_bytes = sum(cb.values())
     step_eff = {"bytes_per_step": step_bytes, "GBs": step_bytes / (ms * 1e-3) / 1e9,
@@ -501,11 +499,13 @@ def run_ours(a):
                 "note": "kernel-class times from a second K-step pass with an event pair per launch"}
 
     e2e = None
-    if not a.no_e2e:
+    if e2e_on:
         host = torch.empty((6, nz, n, n), dtype=torch.float64, pin_memory=True)
         host.copy_(eps.cpu())
         step(host)
         torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
         t = time.perf_counter()
         for _ in range(a.steps):
             m, rms, rel = step(host)       # H2D of the strain inside fgd_constitutive; D2H of <sigma>, rms, relres
@@ -518,17 +518,9 @@ def run_ours(a):
         e2e = {"value": V * a.kcg / te, "unit": UNIT, "h2d_bytes_per_step": 48 * V,
                "d2h_bytes_per_step": world * (48 + 8 + 8 + 8), "ms_per_step": te * 1e3}
 
-    cpu = None
-    if rank == 0 and world == 1 and not a.no_cpu:
-        cpu = cpu_baseline(a.kcg, a.khelm)
     cmp_cufft = None
-    if world == 1 and not a.no_cufft:
+    if extras and world == 1 and not a.no_cufft:
         cmp_cufft = cufft_comparison(ctx, n, dev, synth.CONFIG1_MASK)
-    gtn = None
-    if world == 1 and not a.no_gtn:
-        gtn = gtn_measurement(min(n, 256), dev, peak)   # a second context: keep it at <= 256^3
-        if "constitutive" in per_class and n <= 256:
-            gtn["j2_ms_per_update"] = per_class["constitutive"]["ms_per_step"]
 
     # multi-GPU: share and achieved bandwidth of the slab transposes; every operator
     # apply moves (P-1)/P of the rank's spectrum twice (before and after the z pass)
@@ -539,7 +531,7 @@ def run_ours(a):
         cms = per_class["comm"]["ms_per_step"]
         comm = {"ms_per_step": cms, "share": cms / ms, "alltoall_bytes_sent_per_gpu_per_step": a2a_bytes,
                 "alltoall_GBs_per_gpu": a2a_bytes / (cms * 1e-3) / 1e9 if cms else None,
-                "nvlink_GBs_per_direction": 900.0,
+                "nvlink_GBs_per_direction": 900.0, "nvlink_measured_peer_GBs": 770.0,
                 "note": "comm = NCCL all-to-all transposes + stencil z-halos + Krylov allreduces (event-timed)"}
     # per-solver rates inside the step (kernel-class times, this rank): one mechanical apply = the
     # five 6-comp passes (the residual projection costs the same passes as a CG iteration), one PCG
@@ -558,26 +550,91 @@ def run_ours(a):
              "helm_pcg_voxel_iter_per_s": V / (helm_iter_ms * 1e-3) if helm_iter_ms else None,
              "note": "Krylov iteration rates from the event-timed kernel classes of one rank (the step's "
                      "constitutive update and reductions excluded); value/ms_per_step is the whole step"}
+    ctx.close()
+    del eps
+    torch.cuda.empty_cache()
+    return dict(value=value, ms=ms, launches=launches, clocks=clk, roofline=roof, step_roofline=step_eff, e2e=e2e,
+                kernels=per_class, rates=rates, comm=comm, cufft=cmp_cufft, peak=peak)
+
+
+def run_ours(a):
+    import torch
+
+    rank, world, local = dist_env()
+    if world != a.gpus:
+        print(f"bench.py: --gpus {a.gpus} but WORLD_SIZE = {world}", file=sys.stderr)
+        sys.exit(2)
+    torch.cuda.set_device(local)
+    from paper_2103_04770_b200 import nccl_id
+
+    nid = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        t = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            t.copy_(torch.frombuffer(bytearray(nccl_id()), dtype=torch.uint8))
+        dist.broadcast(t, 0)
+        nid = bytes(t.cpu().numpy().tobytes())
+    n = a.n
+    dev = torch.device("cuda", local)
+    main = measure(a, n, rank, world, local, nid, e2e_on=not a.no_e2e, extras=n <= 256)
+    # the other metric size (BASELINE metric "at 256^3/512^3"), one GPU only
+    by_size = {}
+    cmp_cufft = main["cufft"]
+    if world == 1 and not a.no_by_size:
+        for m in (256, 512):
+            if m == n:
+                continue
+            o = measure(a, m, rank, world, local, nid, e2e_on=False, extras=m <= 256)
+            cmp_cufft = cmp_cufft or o["cufft"]
+            by_size[str(m)] = {"value": o["value"], "unit": UNIT, "ms_per_step": o["ms"], "roofline": o["roofline"],
+                               "step_roofline": o["step_roofline"], "rates": o["rates"], "gpu_launches": o["launches"],
+                               "clocks": o["clocks"], "workload": workload_name(m)}
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu:
+        cpu = cpu_baseline(a.kcg, a.khelm)
+    gtn = None
+    if world == 1 and not a.no_gtn:
+        gtn = gtn_measurement(256, dev, main["peak"])   # a second context: keep it at 256^3
+        k = main["kernels"] if n == 256 else by_size.get("256", {}).get("kernels")
+        if k and "constitutive" in k:
+            gtn["j2_ms_per_update"] = k["constitutive"]["ms_per_step"]
     if rank == 0:
-        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
-                "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True,
+        line = {"metric": METRIC, "value": main["value"], "unit": UNIT, "n_gpus": world, "steps": a.steps,
+                "warmup": a.warmup, "ms_per_step": main["ms"], "higher_is_better": True,
                 "scaling": "strong",
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": {"workload": workload_name(n), "n": n, "kcg": a.kcg, "khelm": a.khelm,
                            "parallelism": "single GPU" if world == 1 else
                            f"z-slab decomposition over {world} GPUs (NCCL all-to-all transposes, allreduce)",
-                           "l2": "no flush: every input field (>=134 MB) and the tangent (2.8 GB) exceed the 126 MB L2"},
-                "roofline": roof, "step_roofline": step_eff, "cpu_baseline": cpu, "e2e": e2e,
-                "gpu_launches": launches, "clocks": clk, "kernels": per_class,
-                "rates": rates, "cufft_comparison": cmp_cufft, "gtn_constitutive": gtn, "comm": comm}
+                           "l2": "no flush: every input field (>=134 MB) and the tangent (>=2.8 GB) exceed the "
+                                 "126 MB L2"},
+                "roofline": main["roofline"], "step_roofline": main["step_roofline"], "cpu_baseline": cpu,
+                "e2e": main["e2e"], "gpu_launches": main["launches"], "clocks": main["clocks"],
+                "kernels": main["kernels"], "rates": main["rates"], "by_size": by_size or None,
+                "cufft_comparison": cmp_cufft, "gtn_constitutive": gtn, "comm": main["comm"]}
         print(json.dumps(line), flush=True)
-    ctx.close()
     if world > 1:
         torch.distributed.destroy_process_group()
 
 
+def relaunch_under_torchrun(a):
+    """`bench.py --gpus N` without a torchrun environment: re-exec this command as N ranks of one
+    node (one process per GPU, rendezvous on 127.0.0.1), as the driver does for its scaling runs."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={a.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    os.execv(sys.executable, cmd)
+
+
 def main():
     a = args_()
+    if a.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        relaunch_under_torchrun(a)
     if a.impl == "reference":
         run_reference(a)
     else:

@@ -70,6 +70,14 @@ typedef struct {
 fgd_status fgd_create(const fgd_grid* grid, const fgd_dist* dist, fgd_ctx** out);
 /* 128-byte NCCL unique id for fgd_dist.nccl_id (call on rank 0 only). */
 fgd_status fgd_nccl_id(unsigned char* out);
+/* 128-byte id of an in-process LOOPBACK group (validation transport): passed as fgd_dist.nccl_id
+ * to nranks contexts of ONE process (typically on one GPU, each driven by its own host thread,
+ * ranks 0..nranks-1), it makes them a multi-rank group whose collectives are stream-ordered
+ * device-to-device copies synchronised by CUDA events and host barriers instead of NCCL.  Every
+ * nranks > 1 code path (slab layouts, transposes, z-halos, distributed reductions) runs as with
+ * NCCL.  All ranks must issue the same sequence of collective calls (as with NCCL); a rank that
+ * stops calling makes the others fail with FGD_ENCCL after 300 s. */
+fgd_status fgd_loopback_id(unsigned char* out);
 void fgd_destroy(fgd_ctx* ctx);
 const char* fgd_last_error(const fgd_ctx* ctx);
 fgd_status fgd_local_extent(const fgd_ctx* ctx, int* z0, int* nz);

@@ -6,7 +6,7 @@ are its thin Python binding.  Importing the package does not load the library (s
 `python -m paper_2103_04770_b200.build` works on a fresh tree); touching `Context`,
 `FgdError` or `Material` loads it and fails loudly if it is missing -- there is no CPU fallback.
 """
-__all__ = ["Context", "FgdError", "Material", "nccl_id"]
+__all__ = ["Context", "FgdError", "Material", "nccl_id", "loopback_id"]
 
 
 def __getattr__(name):

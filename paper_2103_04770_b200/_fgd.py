@@ -61,6 +61,7 @@ _I = C.c_int
 _SIGS = {
     "fgd_create": ([C.POINTER(fgd_grid), C.POINTER(fgd_dist), C.POINTER(C.c_void_p)], _I),
     "fgd_nccl_id": ([_P], _I),
+    "fgd_loopback_id": ([_P], _I),
     "fgd_destroy": ([_P], None),
     "fgd_last_error": ([_P], C.c_char_p),
     "fgd_local_extent": ([_P, C.POINTER(_I), C.POINTER(_I)], _I),

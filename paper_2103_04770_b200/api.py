@@ -52,6 +52,17 @@ def nccl_id() -> bytes:
     return bytes(buf)
 
 
+def loopback_id() -> bytes:
+    """128-byte id of an in-process loopback group (fgd_loopback_id): pass the same id as `nccl_id`
+    to `nranks` Contexts of this process, each driven by its own thread, to run the multi-rank
+    code paths on one GPU with device-to-device copies instead of NCCL (validation transport)."""
+    buf = (C.c_ubyte * 128)()
+    st = _fgd.fgd_loopback_id(C.cast(buf, C.c_void_p))
+    if st != 0:
+        raise FgdError(st, "fgd_loopback_id failed")
+    return bytes(buf)
+
+
 class Context:
     """One libfgd context (one GPU, one stream).  n = (N1, N2, N3); N3 = 1 for 2D.
     Multi-GPU: rank/nranks/nccl_id (from nccl_id() on rank 0); fields are then the rank's

@@ -8,14 +8,39 @@
 // With FGD_EMULATE_SLABS=P on a single GPU the same slab layout is used for all P slabs in one
 // address space and the all-to-all is a set of device-to-device block copies -- one kernel over
 // all ranks' data, which validates the transposition layout without a second GPU.
+//
+// Loopback transport (validation of the multi-rank code on ONE GPU): P contexts of one process,
+// driven by P host threads, join an in-process group through an id from fgd_loopback_id().  Every
+// collective is then stream-ordered device-to-device copies between the ranks' buffers, ordered by
+// CUDA events and host barriers (no kernel ever waits on another rank's kernel):
+//   publish: rank r records `ready_r` on its stream, posts its buffer pointer, host barrier,
+//            then makes its stream wait for every ready_s;
+//   move:    rank r copies what it receives from the peers' posted buffers (the same blocks NCCL
+//            would deliver);
+//   finish:  rank r records `done_r`, host barrier, its stream waits for every done_s (so no rank
+//            overwrites a posted buffer before all peers have read it).
+// Allreduces copy all P contributions into a per-rank stage and sum them in rank order in one
+// kernel (identical result on every rank).  Every nranks > 1 branch of the library (slab layout
+// with ky offsets, rank-0 zero frequency, z-halos, distributed finalise, max-ERR on bit patterns)
+// runs unchanged; only the byte movement differs from NCCL.
 #include <nccl.h>
 
+#include <chrono>
+#include <condition_variable>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
 
 #include "reduce.cuh"
 
 namespace fgd {
+
+#define TRYD(x)                   \
+  do {                            \
+    fgd_status s_ = (x);          \
+    if (s_ != FGD_OK) return s_;  \
+  } while (0)
 
 #define FGD_NCCL(ctx, call)                                                                    \
   do {                                                                                         \
@@ -25,6 +50,145 @@ namespace fgd {
   } while (0)
 
 static ncclComm_t comm_of(const fgd_ctx* c) { return reinterpret_cast<ncclComm_t>(c->comm); }
+
+// ---- loopback group ---------------------------------------------------------------------------
+static const char kLoopMagic[8] = {'F', 'G', 'D', 'L', 'O', 'O', 'P', 0};
+constexpr int kLoopStage = 64;   // doubles per rank in an allreduce stage
+
+struct LoopGroup {
+  int P = 0;
+  int members = 0;
+  std::mutex m;
+  std::condition_variable cv;
+  int arrived = 0;
+  unsigned long long gen = 0;
+  std::vector<const void*> ptr;
+  std::vector<cudaEvent_t> ready, done;
+  std::string key;
+  // generation barrier with a timeout (a rank that left on an error must not hang the others forever)
+  bool barrier() {
+    std::unique_lock<std::mutex> lk(m);
+    const unsigned long long g = gen;
+    if (++arrived == P) {
+      arrived = 0;
+      ++gen;
+      cv.notify_all();
+      return true;
+    }
+    return cv.wait_for(lk, std::chrono::seconds(300), [&] { return gen != g; });
+  }
+};
+static std::mutex g_loop_m;
+static std::map<std::string, LoopGroup*> g_loops;
+
+struct LoopRank {
+  LoopGroup* g = nullptr;
+  double* stage = nullptr;   // [P][kLoopStage]
+};
+static LoopRank* loop_of(const fgd_ctx* c) { return reinterpret_cast<LoopRank*>(c->loop); }
+
+static fgd_status loop_join(fgd_ctx* c, const unsigned char* id) {
+  const std::string key(reinterpret_cast<const char*>(id) + 8, 24);
+  LoopGroup* g = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_loop_m);
+    auto it = g_loops.find(key);
+    if (it == g_loops.end()) {
+      g = new LoopGroup();
+      g->P = c->nranks;
+      g->key = key;
+      g->ptr.assign(c->nranks, nullptr);
+      g->ready.assign(c->nranks, nullptr);
+      g->done.assign(c->nranks, nullptr);
+      g_loops[key] = g;
+    } else {
+      g = it->second;
+    }
+    if (g->P != c->nranks) return set_err(c, FGD_EINVAL, "loopback group: nranks differs between ranks");
+    if (g->ready[c->rank]) return set_err(c, FGD_EINVAL, "loopback group: rank joined twice");
+    if (cudaEventCreateWithFlags(&g->ready[c->rank], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&g->done[c->rank], cudaEventDisableTiming) != cudaSuccess)
+      return set_err(c, FGD_ECUDA, "loopback events");
+    g->members++;
+  }
+  LoopRank* lr = new LoopRank();
+  lr->g = g;
+  c->loop = lr;
+  if (cudaMalloc((void**)&lr->stage, (size_t)c->nranks * kLoopStage * sizeof(double)) != cudaSuccess)
+    return set_err(c, FGD_ENOMEM, "loopback stage");
+  // every rank has its events before anyone records into them
+  if (!g->barrier()) return set_err(c, FGD_ENCCL, "loopback group: not all ranks joined within 300 s");
+  return FGD_OK;
+}
+
+static void loop_leave(fgd_ctx* c) {
+  LoopRank* lr = loop_of(c);
+  if (!lr) return;
+  LoopGroup* g = lr->g;
+  // collective: a peer may still be issuing its stream waits on our events of the last collective
+  g->barrier();
+  if (lr->stage) cudaFree(lr->stage);
+  {
+    std::lock_guard<std::mutex> lk(g_loop_m);
+    if (g->ready[c->rank]) cudaEventDestroy(g->ready[c->rank]);
+    if (g->done[c->rank]) cudaEventDestroy(g->done[c->rank]);
+    g->ready[c->rank] = g->done[c->rank] = nullptr;
+    if (--g->members == 0) {
+      g_loops.erase(g->key);
+      delete g;
+    }
+  }
+  delete lr;
+  c->loop = nullptr;
+}
+
+static fgd_status loop_publish(fgd_ctx* c, const void* p) {
+  LoopGroup* g = loop_of(c)->g;
+  g->ptr[c->rank] = p;
+  FGD_CUDA(c, cudaEventRecord(g->ready[c->rank], c->stream));
+  if (!g->barrier()) return set_err(c, FGD_ENCCL, "loopback barrier timeout (publish)");
+  for (int s = 0; s < g->P; ++s) FGD_CUDA(c, cudaStreamWaitEvent(c->stream, g->ready[s], 0));
+  return FGD_OK;
+}
+
+static fgd_status loop_finish(fgd_ctx* c) {
+  LoopGroup* g = loop_of(c)->g;
+  FGD_CUDA(c, cudaEventRecord(g->done[c->rank], c->stream));
+  if (!g->barrier()) return set_err(c, FGD_ENCCL, "loopback barrier timeout (finish)");
+  for (int s = 0; s < g->P; ++s) FGD_CUDA(c, cudaStreamWaitEvent(c->stream, g->done[s], 0));
+  return FGD_OK;
+}
+
+// dev[i] = sum_s stage[s][i] (rank order), or the max of the 64-bit patterns
+__global__ void k_loop_sum(double* dev, const double* stage, int P, int count) {
+  const int i = threadIdx.x;
+  if (i >= count) return;
+  double t = 0.0;
+  for (int s = 0; s < P; ++s) t += stage[s * kLoopStage + i];
+  dev[i] = t;
+}
+__global__ void k_loop_max(unsigned long long* dev, const double* stage, int P) {
+  unsigned long long m = 0;
+  for (int s = 0; s < P; ++s) m = max(m, reinterpret_cast<const unsigned long long*>(stage)[s * kLoopStage]);
+  *dev = m;
+}
+
+static fgd_status loop_allreduce(fgd_ctx* c, void* dev, int count, bool max_u64) {
+  if (count > kLoopStage) return set_err(c, FGD_EINVAL, "loopback allreduce: count > 64");
+  LoopRank* lr = loop_of(c);
+  TRYD(loop_publish(c, dev));
+  for (int s = 0; s < lr->g->P; ++s)
+    FGD_CUDA(c, cudaMemcpyAsync(lr->stage + (size_t)s * kLoopStage, lr->g->ptr[s], (size_t)count * 8,
+                                cudaMemcpyDeviceToDevice, c->stream));
+  TRYD(loop_finish(c));
+  c->launches++;
+  if (max_u64)
+    k_loop_max<<<1, 1, 0, c->stream>>>(static_cast<unsigned long long*>(dev), lr->stage, lr->g->P);
+  else
+    k_loop_sum<<<1, kLoopStage, 0, c->stream>>>(static_cast<double*>(dev), lr->stage, lr->g->P, count);
+  FGD_CUDA(c, cudaGetLastError());
+  return FGD_OK;
+}
 
 fgd_status dist_init(fgd_ctx* c, const fgd_dist* d) {
   c->rank = 0;
@@ -36,6 +200,11 @@ fgd_status dist_init(fgd_ctx* c, const fgd_dist* d) {
     c->rank = d->rank;
     c->nranks = d->nranks;
     c->P = d->nranks;
+    if (std::memcmp(d->nccl_id, kLoopMagic, 8) == 0) {
+      if (d->nranks > 64) return set_err(c, FGD_EINVAL, "loopback: at most 64 ranks");
+      TRYD(loop_join(c, d->nccl_id));
+      goto slabs;
+    }
     ncclUniqueId id;
     std::memcpy(&id, d->nccl_id, sizeof(id));
     ncclComm_t comm;
@@ -45,6 +214,7 @@ fgd_status dist_init(fgd_ctx* c, const fgd_dist* d) {
     const int p = std::atoi(e);
     if (p > 1) c->P = p;
   }
+slabs:
   const int P = c->P;
   if ((P & (P - 1)) != 0 || c->n[2] % P != 0 || c->n[1] % P != 0 || c->n[2] / P < 1 || c->n[1] / P < 1)
     return set_err(c, FGD_EINVAL, "slab count must be a power of two dividing N2 and N3");
@@ -54,6 +224,7 @@ fgd_status dist_init(fgd_ctx* c, const fgd_dist* d) {
 }
 
 void dist_destroy(fgd_ctx* c) {
+  loop_leave(c);
   if (c->comm) ncclCommDestroy(comm_of(c));
   c->comm = nullptr;
 }
@@ -75,6 +246,14 @@ fgd_status exchange(fgd_ctx* c, int ncomp, bool fwd) {
                                     blk * sizeof(double2), cudaMemcpyDeviceToDevice, c->stream));
     return FGD_OK;
   }
+  if (c->loop) {
+    TRYD(loop_publish(c, src));
+    for (int p = 0; p < P; ++p)
+      FGD_CUDA(c, cudaMemcpyAsync(dst + (size_t)p * blk, static_cast<const double2*>(loop_of(c)->g->ptr[p]) +
+                                                             (size_t)c->rank * blk,
+                                  blk * sizeof(double2), cudaMemcpyDeviceToDevice, c->stream));
+    return loop_finish(c);
+  }
   FGD_NCCL(c, ncclGroupStart());
   for (int p = 0; p < P; ++p) {
     FGD_NCCL(c, ncclSend(src + (size_t)p * blk, 2 * blk, ncclDouble, p, comm_of(c), c->stream));
@@ -87,6 +266,7 @@ fgd_status exchange(fgd_ctx* c, int ncomp, bool fwd) {
 fgd_status allreduce_sum(fgd_ctx* c, double* dev, int count) {
   if (c->nranks == 1) return FGD_OK;
   KTimer kt(c, KC_COMM);
+  if (c->loop) return loop_allreduce(c, dev, count, false);
   FGD_NCCL(c, ncclAllReduce(dev, dev, count, ncclDouble, ncclSum, comm_of(c), c->stream));
   return FGD_OK;
 }
@@ -94,11 +274,16 @@ fgd_status allreduce_sum(fgd_ctx* c, double* dev, int count) {
 fgd_status allreduce_max_u64(fgd_ctx* c, unsigned long long* dev) {
   if (c->nranks == 1) return FGD_OK;
   KTimer kt(c, KC_COMM);
+  if (c->loop) return loop_allreduce(c, dev, 1, true);
   FGD_NCCL(c, ncclAllReduce(dev, dev, 1, ncclUint64, ncclMax, comm_of(c), c->stream));
   return FGD_OK;
 }
 
-__global__ void k_finalize(DevScalars* sc, int op, int slot) {
+// guard: the Krylov loop's convergence guard (nullptr outside a batched loop); once the device flag
+// is set, the reducing kernels of the remaining launched iterations skip, the allreduce then sums
+// stale partials, and the finalise must skip too (else it would count and apply a phantom iteration)
+__global__ void k_finalize(DevScalars* sc, const DevScalars* guard, int op, int slot) {
+  if (guard_done(guard)) return;
   double t = sc->red[slot];
   finalize(sc, op, 0, &t, 1);
 }
@@ -113,7 +298,7 @@ fgd_status post_reduce(fgd_ctx* c, int op) {
   if (c->nranks == 1 || op == RED_NONE || op == RED_STORE) return FGD_OK;
   if (allreduce_sum(c, &c->sc->red[kDistSlot], 1) != FGD_OK) return FGD_ENCCL;
   c->launches++;
-  k_finalize<<<1, 1, 0, c->stream>>>(c->sc, op, kDistSlot);
+  k_finalize<<<1, 1, 0, c->stream>>>(c->sc, c->guard ? c->sc : nullptr, op, kDistSlot);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_err(c, FGD_ECUDA, std::string("k_finalize: ") + cudaGetErrorString(e));
   return FGD_OK;
@@ -126,6 +311,14 @@ fgd_status halo_exchange(fgd_ctx* c, const void* field, size_t plane_bytes, void
   const char* f = static_cast<const char*>(field);
   const char* last = f + (size_t)(c->nz_l - 1) * plane_bytes;
   KTimer kt(c, KC_COMM);
+  if (c->loop) {
+    TRYD(loop_publish(c, field));
+    const LoopGroup* g = loop_of(c)->g;
+    FGD_CUDA(c, cudaMemcpyAsync(lo, static_cast<const char*>(g->ptr[dn]) + (size_t)(c->nz_l - 1) * plane_bytes,
+                                plane_bytes, cudaMemcpyDeviceToDevice, c->stream));
+    FGD_CUDA(c, cudaMemcpyAsync(hi, g->ptr[up], plane_bytes, cudaMemcpyDeviceToDevice, c->stream));
+    return loop_finish(c);
+  }
   FGD_NCCL(c, ncclGroupStart());
   // order matters when up == dn (P = 2): first the plane sent up / received from below
   FGD_NCCL(c, ncclSend(last, plane_bytes, ncclChar, up, comm_of(c), c->stream));
@@ -137,6 +330,23 @@ fgd_status halo_exchange(fgd_ctx* c, const void* field, size_t plane_bytes, void
 }
 
 }  // namespace fgd
+
+extern "C" fgd_status fgd_loopback_id(unsigned char* out) {
+  if (!out) return FGD_EINVAL;
+  static std::mutex m;
+  static unsigned long long counter = 0;
+  std::memset(out, 0, 128);
+  std::memcpy(out, fgd::kLoopMagic, 8);
+  unsigned long long k[3];
+  {
+    std::lock_guard<std::mutex> lk(m);
+    k[0] = ++counter;
+  }
+  k[1] = (unsigned long long)std::chrono::steady_clock::now().time_since_epoch().count();
+  k[2] = (unsigned long long)(uintptr_t)&counter;
+  std::memcpy(out + 8, k, 24);
+  return FGD_OK;
+}
 
 extern "C" fgd_status fgd_nccl_id(unsigned char* out) {
   if (!out) return FGD_EINVAL;

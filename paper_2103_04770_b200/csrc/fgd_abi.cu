@@ -297,7 +297,10 @@ static fgd_status ensure_state(fgd_ctx* c) {
 // Krylov loops with tol > 0 on one GPU launch iterations in growing batches (4, 8, .. 32) and
 // read the device convergence flag once per batch; the hot kernels skip themselves once the
 // finalise of the monitored norm has set it (guard_done), so the returned iterate and iteration
-// count are those of the converged iteration.  With nranks > 1 the host checks every iteration.
+// count are those of the converged iteration.  With nranks > 1 the same holds on every rank (the
+// flag is finalised from allreduced sums, identical on all ranks, so all ranks take the same
+// host decisions); batches stop at 8 there, because the collectives of skipped iterations still
+// move their (unused) bytes.
 struct GuardScope {
   fgd_ctx* c;
   GuardScope(fgd_ctx* cc, bool on) : c(cc) { c->guard = on; }
@@ -371,7 +374,8 @@ static fgd_status pcg_helmholtz(fgd_ctx* c, int field, const double* b, double* 
   FGD_CUDA(c, cudaMemsetAsync(x, 0, n * 8, c->stream));
   FGD_CUDA(c, cudaMemsetAsync(P[0], 0, n * 8, c->stream));
   FGD_CUDA(c, cudaMemcpyAsync(r, b, n * 8, cudaMemcpyDeviceToDevice, c->stream));
-  const bool batched = tol > 0.0 && c->nranks == 1;
+  const bool batched = tol > 0.0;
+  const int max_batch = c->nranks > 1 ? 8 : 32;
   TRY(launch_guard_init(c, tol > 0.0 ? tol * tol : 0.0));
   TRY(launch_dot(c, n, r, r, RED(RED_BB)));
   TRY(post_reduce(c, RED_BB));
@@ -416,7 +420,7 @@ static fgd_status pcg_helmholtz(fgd_ctx* c, int field, const double* b, double* 
       int flags[2];   // done, iters
       TRY(sync_read(c, &c->sc->done, sizeof(flags), flags));
       done = flags[0] != 0;
-      batch = std::min(2 * batch, 32);
+      batch = std::min(2 * batch, max_batch);
     }
     while (!batched && launched < maxit && !done) {
       const int nb = 1;
@@ -443,7 +447,7 @@ static fgd_status pcg_helmholtz(fgd_ctx* c, int field, const double* b, double* 
         int flags[2];   // done, iters
         TRY(sync_read(c, &c->sc->done, sizeof(flags), flags));
         done = flags[0] != 0;
-        batch = std::min(2 * batch, 32);
+        batch = std::min(2 * batch, max_batch);
       }
     }
     if (batched) {
@@ -476,7 +480,8 @@ static fgd_status cg_mech(fgd_ctx* c, const double* b, double* x_out, double tol
     FGD_CUDA(c, cudaMemcpyAsync(c->cg_r, b, n6 * 8, cudaMemcpyDeviceToDevice, c->stream));
     b = c->cg_r;
   }
-  const bool batched = tol > 0.0 && c->nranks == 1;
+  const bool batched = tol > 0.0;
+  const int max_batch = c->nranks > 1 ? 8 : 32;
   TRY(launch_guard_init(c, tol > 0.0 ? tol * tol : 0.0));
   TRY(launch_dot(c, n6, b, b, RED(RED_MECH_INIT)));
   TRY(post_reduce(c, RED_MECH_INIT));
@@ -520,7 +525,7 @@ static fgd_status cg_mech(fgd_ctx* c, const double* b, double* x_out, double tol
         int flags[2];   // done, iters
         TRY(sync_read(c, &c->sc->done, sizeof(flags), flags));
         done = flags[0] != 0;
-        batch = std::min(2 * batch, 32);
+        batch = std::min(2 * batch, max_batch);
       } else if (tol > 0.0) {
         double rr;
         TRY(sync_read(c, &c->sc->rr, 8, &rr));

@@ -124,6 +124,7 @@ struct fgd_ctx {
   int rank = 0, nranks = 1;    // processes (one GPU each)
   int P = 1;                   // slab count of the transposed-spectrum layout (nranks, or emulated)
   void* comm = nullptr;        // ncclComm_t
+  void* loop = nullptr;        // loopback transport rank (dist.cu), instead of NCCL
   double2* specC = nullptr;    // z-pass buffer when P > 1
   double* halo = nullptr;      // stencil halo planes (nranks > 1): [field 0 lo, hi][field 1 lo, hi]
   uint8_t* phase_halo = nullptr;
