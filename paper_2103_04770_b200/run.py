@@ -36,13 +36,14 @@ def _context(cfg):
     return ctx
 
 
-def adaptive_schedule(solve, E_end, dE0, dE_max=None, dE_min=1e-5, grow=1.5, grow_after=2):
+def adaptive_schedule(solve, E_end, dE0, dE_max=None, dE_min=1e-5, grow=1.5, grow_after=2, stop=None):
     """Adaptive incrementation (the paper's "variable strain increment",
     P:990, rule A-34 of DESIGN.md): try dE = min(step, E_end - E); on failure halve the step and
     retry from the last converged state; after `grow_after` consecutive first-try successes
     multiply the step by `grow` (at most dE_max = dE0 by default).  Stops with failure when the
     step falls below dE_min.  `solve(E) -> bool` runs one increment to macroscopic strain E (and
-    commits it on success).  Returns (accepted strains, number of cutbacks, reached E_end)."""
+    commits it on success); `stop() -> bool` (optional) ends the run early after an accepted
+    increment.  Returns (accepted strains, number of cutbacks, reached E_end or stopped)."""
     dE_max = dE0 if dE_max is None else dE_max
     E, step, streak, cuts, accepted = 0.0, dE0, 0, 0, []
     while E < E_end - 1e-15:
@@ -50,6 +51,8 @@ def adaptive_schedule(solve, E_end, dE0, dE_max=None, dE_min=1e-5, grow=1.5, gro
         if solve(E + dE):
             E += dE
             accepted.append(E)
+            if stop is not None and stop():
+                return accepted, cuts, True
             streak += 1
             if streak >= grow_after:
                 step = min(step * grow, dE_max)
@@ -64,7 +67,7 @@ def adaptive_schedule(solve, E_end, dE0, dE_max=None, dE_min=1e-5, grow=1.5, gro
 
 
 def run_config(cfg, n_incr=None, tol=(1e-4, 1e-6, 1e-8, 1e-6), max_halvings=6, max_cg=5000, max_helm=5000,
-               adaptive=False, de_min=1e-5, log=False):
+               adaptive=False, de_min=1e-5, log=False, grow=1.5, stop_frac=None, max_stag=100):
     """Load the cell along cfg.load_comp to n_incr * cfg.dE: fixed increments with deterministic
     halving (A-21), or the adaptive schedule (A-34); returns a result dict."""
     import torch
@@ -83,9 +86,12 @@ def run_config(cfg, n_incr=None, tol=(1e-4, 1e-6, 1e-8, 1e-6), max_halvings=6, m
         Et = np.zeros(6)
         Et[cfg.load_comp] = E_try
         st, rep = ctx.solve_increment(Et, np.zeros(6), tol_stag, tol_newton, tol_cg, tol_helm,
-                                      max_cg=max_cg, max_helm=max_helm)
+                                      max_stag=max_stag, max_cg=max_cg, max_helm=max_helm)
         for k in ("stag", "newton", "cg", "helm"):
             counts[k] += rep[k]
+        if log and st != 0:
+            print(json.dumps({"E_try": E_try, "failed": True, "stag": rep["stag"], "newton": rep["newton"],
+                              "cg": rep["cg"], "helm": rep["helm"], "err": rep["err"]}), file=sys.stderr, flush=True)
         if st == 0:
             counts["substeps"] += 1
             curve.append((E_try, float(rep["macro_stress"][cfg.load_comp])))
@@ -97,8 +103,14 @@ def run_config(cfg, n_incr=None, tol=(1e-4, 1e-6, 1e-8, 1e-6), max_halvings=6, m
             raise RuntimeError(f"solve_increment failed with status {st}")
         return False
 
+    def stop():
+        if stop_frac is None:
+            return False
+        sv = [c[1] for c in curve]
+        return max(sv) > 0 and sv[-1] < stop_frac * max(sv)
+
     if adaptive:
-        acc, cuts, ok = adaptive_schedule(solve, n_incr * cfg.dE, cfg.dE, dE_min=de_min)
+        acc, cuts, ok = adaptive_schedule(solve, n_incr * cfg.dE, cfg.dE, dE_min=de_min, grow=grow, stop=stop)
         counts.update(increments=len(acc), cutbacks=cuts, failed=int(not ok))
         n_incr = 0
     for i in range(1, n_incr + 1):
@@ -162,6 +174,10 @@ def main(argv=None):
     p.add_argument("--halvings", type=int, default=6)
     p.add_argument("--adaptive", action="store_true", help="adaptive increments (A-34) instead of fixed + halving")
     p.add_argument("--log", action="store_true", help="one JSON line per accepted increment on stderr")
+    p.add_argument("--grow", type=float, default=1.5, help="adaptive: step growth after two first-try successes")
+    p.add_argument("--stop-frac", type=float, default=None,
+                   help="adaptive: stop once the load stress falls below this fraction of the peak")
+    p.add_argument("--max-stag", type=int, default=100)
     p.add_argument("--ell", type=float, default=None,
                    help="gtn2d: matrix ell_M / L (ell_I = min(ell_M, 0.001 L); 1e-4 gives the local variant)")
     a = p.parse_args(argv)
@@ -181,8 +197,8 @@ def main(argv=None):
     if a.de:
         cfg.dE = a.de
     tol = (1e-8, 1e-10, 1e-11, 1e-11) if a.tight else (1e-4, 1e-6, 1e-8, 1e-6)
-    print(json.dumps(run_config(cfg, a.incr, tol, a.halvings, a.max_cg, a.max_cg, adaptive=a.adaptive, log=a.log)),
-          flush=True)
+    print(json.dumps(run_config(cfg, a.incr, tol, a.halvings, a.max_cg, a.max_cg, adaptive=a.adaptive, log=a.log,
+                                grow=a.grow, stop_frac=a.stop_frac, max_stag=a.max_stag)), flush=True)
 
 
 if __name__ == "__main__":

@@ -1,0 +1,89 @@
+"""Config-level parity (BASELINE.json north_star): the GPU's increment solver replays the oracle's
+load path of a BASELINE configuration -- the same accepted strain targets, the same parity
+tolerances -- and must reproduce
+
+  * <sigma> (all 6 Mandel components) on every pre-peak increment within 1e-6 (relative),
+  * the peak of the load-component stress within 1e-4,
+  * the strain at 50 % post-peak drop (A-26, linear interpolation) within 1e-4.
+
+The oracle curves are golden files written by tests/golden/make_oracle_curves.py (oracle/ only):
+config 0 at 32^2 (BJ config 0, also config 2's 32^2 objectivity run), config 2's 64^2 objectivity
+run (ell = L/16 = 4h), and the reduced config 3 (32^3, 30 RSA spheres, ell_m = 5h, ell_p = 3h).
+Each GPU curve is also written to gpurun_out/ for the record.
+"""
+import json
+import os
+import sys
+import time
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs CUDA", allow_module_level=True)
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.join(HERE, "golden"))
+import make_oracle_curves as moc  # noqa: E402
+from paper_2103_04770_b200 import Context, Material  # noqa: E402
+
+ROOT = os.path.dirname(HERE)
+CASES = [c for c in ("config0_32", "config2_64", "config3_32")
+         if os.path.exists(os.path.join(HERE, "golden", f"curve_{c}.json"))]
+
+
+def rel(a, b):
+    return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(np.asarray(b)), 1e-300))
+
+
+def ctx_from_cfg(cfg):
+    ctx = Context(cfg.n, cfg.L)
+    ctx.set_phases(torch.from_numpy(np.ascontiguousarray(cfg.phases)).cuda(), len(cfg.materials))
+    for q, m in enumerate(cfg.materials):
+        ctx.set_material(q, Material.of(m))
+    ctx.set_nonlocal(np.asarray(cfg.ell), cfg.source_phase)
+    ctx.set_control(cfg.stress_mask)
+    return ctx
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_config_curve_parity(case):
+    gold = json.load(open(os.path.join(HERE, "golden", f"curve_{case}.json")))
+    cfg = moc.cases()[case][0]()
+    tol = gold["tolerances"]
+    ctx = ctx_from_cfg(cfg)
+    lc = gold["load_comp"]
+    got = []
+    t0 = time.perf_counter()
+    for rec in gold["increments"]:
+        Et = np.zeros(6)
+        Et[lc] = rec["E"]
+        st, rep = ctx.solve_increment(Et, np.zeros(6), tol["tol_stag"], tol["tol_newton"], tol["tol_cg"],
+                                      tol["tol_helm"], tol["max_stag"], tol["max_newton"], tol["max_cg"],
+                                      tol["max_helm"])
+        assert st == 0, (case, rec["E"], rep)
+        got.append(dict(E=rec["E"], stress=rep["macro_stress"].tolist(), stag=rep["stag"], newton=rep["newton"],
+                        cg=rep["cg"], helm=rep["helm"]))
+    wall = time.perf_counter() - t0
+    ctx.close()
+    E = np.array([0.0] + [g["E"] for g in got])
+    Sg = np.array([0.0] + [g["stress"][lc] for g in got])
+    So = np.array([0.0] + [r["stress"][lc] for r in gold["increments"]])
+    ip = int(np.argmax(So))
+    res = dict(case=case, wall_s=wall, peak_stress=float(Sg.max()), strain_at_peak=float(E[int(np.argmax(Sg))]),
+               strain_at_failure=moc.failure_strain(E, Sg), oracle_peak=gold["peak_stress"],
+               oracle_failure=gold["strain_at_failure"], oracle_wall_s=gold["wall_s"], increments=got)
+    os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+    with open(os.path.join(ROOT, "gpurun_out", f"curve_gpu_{case}.json"), "w") as f:
+        json.dump(res, f, indent=1)
+    # every pre-peak increment (up to and including the oracle's peak)
+    for i in range(ip):
+        assert rel(got[i]["stress"], gold["increments"][i]["stress"]) <= 1e-6, (case, i)
+    assert int(np.argmax(Sg)) == ip
+    assert abs(Sg.max() - gold["peak_stress"]) <= 1e-4 * gold["peak_stress"]
+    if gold["strain_at_failure"] is not None:
+        f = res["strain_at_failure"]
+        assert f is not None and abs(f - gold["strain_at_failure"]) <= 1e-4 * gold["strain_at_failure"]
