@@ -141,6 +141,12 @@ fgd_status fgd_apply_helmholtz_precond(fgd_ctx* ctx, int field, const double* r,
 fgd_status fgd_solve_helmholtz(fgd_ctx* ctx, int field, const double* src, double* abar, double tol,
                                int maxit, int* iters, double* relres);
 
+/* Algorithm 2 from an initial guess x0 (NULL = 0; the warm start of S:262): the same stopping rule
+ * ||L abar - src|| < tol ||src|| (relative to the source, not to the initial residual); a guess
+ * that already meets it is returned after 0 iterations.  src, x0, abar: 1-component fields. */
+fgd_status fgd_solve_helmholtz_from(fgd_ctx* ctx, int field, const double* src, const double* x0, double* abar,
+                                    double tol, int maxit, int* iters, double* relres);
+
 /* Mechanical linear solve of one Newton step: unpreconditioned CG for
  * G*(C : de) = b with de_0 = 0; b must lie in range(G*) (e.g. a Newton residual).  Same
  * stopping rule and NULL conventions as fgd_solve_helmholtz (b == NULL: the residual of the
@@ -172,6 +178,9 @@ typedef struct {
   double E_target[6], S_target[6];
   double tol_stag, tol_newton, tol_cg, tol_helm;
   int max_stag, max_newton, max_cg, max_helm;
+  int warm_start;  /* 1: every Helmholtz PCG of the staggered loop starts from the current iterate
+                      abar_j^(k) instead of 0 (fgd_solve_helmholtz_from); 0: Algorithm 2 as
+                      printed (abar^(0) = 0) */
 } fgd_increment;
 typedef struct {
   double macro_stress[6], macro_strain[6], err;

@@ -13,7 +13,8 @@ Step by step (readings A-01, A-02, A-07, A-16, A-20-A-22, A-28)
        stop if rms(b) < tol_N * max(|<sigma>|, 1e-6 sigma_ref); else CG (mech.cg) and eps += de
     c. alpha_j from the converged point update (A-28): eps_p (J2), eps_eq (brittle), 0 outside
        the source phase
-    d. abar_j^(k+1) = Algorithm 2 (helmholtz.solve_helmholtz) for every field j
+    d. abar_j^(k+1) = Algorithm 2 (helmholtz.solve_helmholtz) for every field j, from
+       abar^(0) = 0 as printed, or from abar_j^(k) with Tolerances.warm_start
     e. ERR = max( max_{x,ij}|eps^(k+1) - eps^(k)| / |<eps^(k+1)>|,
                   ||abar_j^(k+1) - abar_j^(k)|| / ||abar_j^(k+1)|| )  (P:615, A-02; tensor
        components, Frobenius norm of the mean; denominators < 1e-12 -> absolute term)
@@ -54,6 +55,7 @@ class Tolerances:
     max_newton: int = 50
     max_cg: int = 5000
     max_helm: int = 5000
+    warm_start: bool = False    # Helmholtz PCG from abar^(k) instead of 0; Alg. 2 as printed: False
 
 
 @dataclass
@@ -246,7 +248,7 @@ def solve_increment(cell: Cell, state: State, E_target, S_target, tol: Tolerance
         abar_new = np.empty_like(abar)
         for j in range(cell.J):
             abar_new[j], it, _ = solve_helmholtz(g, alpha[j], ell2[j], tol.tol_helm, tol.max_helm,
-                                                 backend=backend)
+                                                 x0=abar[j] if tol.warm_start else None, backend=backend)
             helm_total += it
         emean = eps.reshape(6, n).mean(axis=1)
         den = np.linalg.norm(emean)

@@ -47,7 +47,7 @@ class fgd_increment(C.Structure):
     _fields_ = [("E_target", C.c_double * 6), ("S_target", C.c_double * 6),
                 ("tol_stag", C.c_double), ("tol_newton", C.c_double), ("tol_cg", C.c_double),
                 ("tol_helm", C.c_double), ("max_stag", C.c_int), ("max_newton", C.c_int),
-                ("max_cg", C.c_int), ("max_helm", C.c_int)]
+                ("max_cg", C.c_int), ("max_helm", C.c_int), ("warm_start", C.c_int)]
 
 
 class fgd_report(C.Structure):
@@ -76,6 +76,7 @@ _SIGS = {
     "fgd_apply_helmholtz": ([_P, _I, _P, _P], _I),
     "fgd_apply_helmholtz_precond": ([_P, _I, _P, _P], _I),
     "fgd_solve_helmholtz": ([_P, _I, _P, _P, _D, _I, C.POINTER(_I), C.POINTER(_D)], _I),
+    "fgd_solve_helmholtz_from": ([_P, _I, _P, _P, _P, _D, _I, C.POINTER(_I), C.POINTER(_D)], _I),
     "fgd_solve_tangent_cg": ([_P, _P, _P, _D, _I, C.POINTER(_I), C.POINTER(_D)], _I),
     "fgd_constitutive": ([_P, _P, _P, _P], _I),
     "fgd_mech_residual": ([_P, _P, _P, C.POINTER(_D)], _I),

@@ -174,6 +174,15 @@ class Context:
             self._chk(st)
         return it.value, rel.value
 
+    def solve_helmholtz_from(self, field: int, src, x0, abar, tol=1e-10, maxit=1000, check=True):
+        """Algorithm 2 from the initial guess x0 (None = 0), fgd_solve_helmholtz_from."""
+        it, rel = C.c_int(0), C.c_double(0.0)
+        st = _fgd.fgd_solve_helmholtz_from(self.h, int(field), ptr(src), ptr(x0), ptr(abar), float(tol), int(maxit),
+                                           C.byref(it), C.byref(rel))
+        if check:
+            self._chk(st)
+        return it.value, rel.value
+
     def solve_tangent_cg(self, b=None, de=None, tol=1e-10, maxit=1000, check=True):
         it, rel = C.c_int(0), C.c_double(0.0)
         st = _fgd.fgd_solve_tangent_cg(self.h, ptr(b), ptr(de), float(tol), int(maxit), C.byref(it), C.byref(rel))
@@ -196,10 +205,11 @@ class Context:
         return rms.value
 
     def solve_increment(self, E_target, S_target=None, tol_stag=1e-8, tol_newton=1e-10, tol_cg=1e-11,
-                        tol_helm=1e-11, max_stag=100, max_newton=50, max_cg=5000, max_helm=5000):
+                        tol_helm=1e-11, max_stag=100, max_newton=50, max_cg=5000, max_helm=5000, warm_start=False):
         S_target = np.zeros(6) if S_target is None else S_target
         inc = _fgd.fgd_increment((C.c_double * 6)(*map(float, E_target)), (C.c_double * 6)(*map(float, S_target)),
-                                 tol_stag, tol_newton, tol_cg, tol_helm, max_stag, max_newton, max_cg, max_helm)
+                                 tol_stag, tol_newton, tol_cg, tol_helm, max_stag, max_newton, max_cg, max_helm,
+                                 1 if warm_start else 0)
         rep = _fgd.fgd_report()
         st = _fgd.fgd_solve_increment(self.h, C.byref(inc), C.byref(rep))
         if st not in (0, _fgd.ENOCONV):

@@ -361,8 +361,10 @@ static fgd_status replay_graph(fgd_ctx* c, const KGraph& g) {
   return FGD_OK;
 }
 
+// x0 (may be null = 0): initial guess (warm start).  The stopping test stays relative to
+// ||b|| (Algorithm 2); an initial residual already below it returns x0 after 0 iterations.
 static fgd_status pcg_helmholtz(fgd_ctx* c, int field, const double* b, double* x_out, double tol, int maxit,
-                                int* iters, double* relres) {
+                                int* iters, double* relres, const double* x0 = nullptr) {
   TRY(ensure_helm(c));
   TRY(ensure_spectral(c));
   const size_t n = c->nvox;
@@ -371,19 +373,36 @@ static fgd_status pcg_helmholtz(fgd_ctx* c, int field, const double* b, double* 
   double* z = c->hb[2];
   double* P[2] = {c->hb[3], c->hb[4]};
   double* q = c->hb[5];
-  FGD_CUDA(c, cudaMemsetAsync(x, 0, n * 8, c->stream));
   FGD_CUDA(c, cudaMemsetAsync(P[0], 0, n * 8, c->stream));
-  FGD_CUDA(c, cudaMemcpyAsync(r, b, n * 8, cudaMemcpyDeviceToDevice, c->stream));
+  if (x0) {
+    // x = x0, r = b - L x0 (the stencil writes L x0 into q)
+    if (x0 != x) FGD_CUDA(c, cudaMemcpyAsync(x, x0, n * 8, cudaMemcpyDeviceToDevice, c->stream));
+    TRY(launch_stencil(c, field, 0, x, nullptr, nullptr, nullptr, q, RED_NONE));
+    FGD_CUDA(c, cudaMemcpyAsync(r, b, n * 8, cudaMemcpyDeviceToDevice, c->stream));
+    TRY(launch_axpy(c, n, r, q, -1.0));
+  } else {
+    FGD_CUDA(c, cudaMemsetAsync(x, 0, n * 8, c->stream));
+    FGD_CUDA(c, cudaMemcpyAsync(r, b, n * 8, cudaMemcpyDeviceToDevice, c->stream));
+  }
   const bool batched = tol > 0.0;
   const int max_batch = c->nranks > 1 ? 8 : 32;
   TRY(launch_guard_init(c, tol > 0.0 ? tol * tol : 0.0));
-  TRY(launch_dot(c, n, r, r, RED(RED_BB)));
+  TRY(launch_dot(c, n, b, b, RED(RED_BB)));
   TRY(post_reduce(c, RED_BB));
   double bb = 0.0;
   TRY(sync_read(c, &c->sc->bb, 8, &bb));
   int it = 0;
   double rel = 0.0;
-  if (bb > 0.0) {
+  bool start = bb > 0.0;
+  if (start && x0) {
+    TRY(launch_dot(c, n, r, r, RED_S(RED_STORE, 9)));
+    TRY(allreduce_sum(c, &c->sc->red[9], 1));
+    double rr0 = 0.0;
+    TRY(sync_read(c, &c->sc->red[9], 8, &rr0));
+    rel = std::sqrt(rr0 / bb);
+    if (tol > 0.0 && rel < tol) start = false;   // the guess already solves the system
+  }
+  if (start) {
     TRY(op_precond(c, field, r, z, RED_HELM_INIT));
     int cur = 0;
     rel = 1.0;
@@ -842,6 +861,23 @@ fgd_status fgd_solve_helmholtz(fgd_ctx* c, int field, const double* src, double*
   return s != FGD_OK ? s : f;
 }
 
+fgd_status fgd_solve_helmholtz_from(fgd_ctx* c, int field, const double* src, const double* x0, double* abar,
+                                    double tol, int maxit, int* iters, double* relres) {
+  if (!c) return FGD_EINVAL;
+  TRY(check_field(c, field));
+  if (maxit < 0) return set_err(c, FGD_EINVAL, "maxit < 0");
+  if (!src || !abar) return set_err(c, FGD_EINVAL, "null argument");
+  Stage st(c);
+  const double *ds = nullptr, *dx0 = nullptr;
+  TRY(st.in(src, c->nvox, &ds));
+  if (x0) TRY(st.in(x0, c->nvox, &dx0));
+  double* dout = nullptr;
+  TRY(st.out(abar, c->nvox, &dout));
+  fgd_status s = pcg_helmholtz(c, field, ds, dout, tol, maxit, iters, relres, dx0);
+  fgd_status f = st.finish();
+  return s != FGD_OK ? s : f;
+}
+
 fgd_status fgd_solve_tangent_cg(fgd_ctx* c, const double* b, double* de, double tol, int maxit, int* iters,
                                 double* relres) {
   if (!c) return FGD_EINVAL;
@@ -1026,7 +1062,7 @@ fgd_status fgd_solve_increment(fgd_ctx* c, const fgd_increment* inc, fgd_report*
     for (int j = 0; j < J && helm_ok; ++j) {
       int it = 0;
       fgd_status s = pcg_helmholtz(c, j, c->w_alpha + (size_t)j * n, nullptr, inc->tol_helm, inc->max_helm, &it,
-                                   nullptr);
+                                   nullptr, inc->warm_start ? c->w_abar + (size_t)j * n : nullptr);
       helm_total += it;
       if (s == FGD_ENOCONV) {
         why = "Helmholtz PCG did not converge in increment";

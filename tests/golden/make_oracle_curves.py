@@ -52,6 +52,9 @@ def cases():
         "config0_32": (lambda: synth.config0(32), None),
         # config 2's objectivity runs: ell = L/16 in physical units (A-13)
         "config2_64": (lambda: synth.config2(64), None),
+        # BJ config 2 itself (256^2, ell = L/16 = 16h): the oracle run that classifies the GPU's
+        # post-peak stall at this size (hours of CPU; not used by the GPU test unless present)
+        "config2_256": (lambda: synth.config2(256), None),
         # reduced config 3: 32^3 RSA cell (30 spheres, 20 %), ell_m = 5h, ell_p = 3h, E_zz ramp
         "config3_32": (lambda: synth.config3(n=32), None),
         # small cells for quick checks of the generator itself

@@ -185,3 +185,60 @@ def test_mech_cg_compact_tangent_2d(n):
     ref, it_ref, _ = cg(g, C_ref, b, mask, tol=1e-12, maxit=5000)
     assert abs(it - it_ref) <= 1
     assert rel(out.cpu().numpy(), ref) <= 1e-9
+
+
+def test_helmholtz_warm_start_iterates():
+    """fgd_solve_helmholtz_from (S:262 warm start): PCG iterates from a guess x0 after k fixed
+    iterations against the oracle's Algorithm 2 from the same x0, and the 0-iteration exit when the
+    guess already meets the tolerance."""
+    from oracle.helmholtz import ell2_field, solve_helmholtz
+    from oracle.spectral import Grid
+    for n in [(16, 8, 8), (256, 8, 8), (8, 256, 256)]:
+        g = Grid(n, (1.0, 1.0, 1.0))
+        rng = np.random.default_rng(7)
+        ph = (rng.random(g.shape) < 0.3).astype(np.uint8)
+        ell = [0.05, 0.01]
+        ctx = Context(n, (1.0, 1.0, 1.0))
+        ctx.set_phases(dev(ph), 2)
+        ctx.set_nonlocal(np.array([ell]), [0])
+        e2 = ell2_field(ph, ell)
+        src = np.abs(rng.normal(size=g.shape))
+        x0 = rng.normal(size=g.shape)
+        out = torch.empty(g.shape, dtype=torch.float64, device="cuda")
+        for k in (1, 4):
+            it, _ = ctx.solve_helmholtz_from(0, dev(src), dev(x0), out, tol=0.0, maxit=k)
+            ref, _, _ = solve_helmholtz(g, src, e2, tol=0.0, maxit=k, x0=x0)
+            assert it == k and rel(out.cpu().numpy(), ref) <= 1e-10, (n, k)
+        ref, it_ref, _ = solve_helmholtz(g, src, e2, tol=1e-11, maxit=2000)
+        it, _ = ctx.solve_helmholtz_from(0, dev(src), dev(ref), out, tol=1e-9, maxit=2000)
+        assert it == 0 and rel(out.cpu().numpy(), ref) <= 1e-14
+        ctx.close()
+
+
+def test_increment_parity_warm_start():
+    """Staggered increments with warm-started Helmholtz solves on both sides (Tolerances.warm_start,
+    fgd_increment.warm_start): same <sigma> (1e-6) and fewer PCG iterations than cold starts."""
+    cfg = small_config3(16)
+    cfg.dE = 1.5e-3
+    tol = dataclasses.replace(TOL, warm_start=True)
+    cell = make_cell(cfg)
+    ctx = ctx_from_cfg(cfg)
+    ctx_cold = ctx_from_cfg(cfg)
+    st = State.zero(cell)
+    helm_warm = helm_cold = 0
+    for i in range(1, 4):
+        Et = np.zeros(6)
+        Et[cfg.load_comp] = i * cfg.dE
+        st, rep = solve_increment(cell, st, Et, np.zeros(6), tol)
+        assert rep.converged
+        s, r = ctx.solve_increment(Et, np.zeros(6), tol.tol_stag, tol.tol_newton, tol.tol_cg, tol.tol_helm,
+                                   tol.max_stag, tol.max_newton, tol.max_cg, tol.max_helm, warm_start=True)
+        assert s == 0, r
+        assert rel(r["macro_stress"], rep.macro_stress) <= 1e-6, i
+        assert abs(r["helm"] - rep.helm_it) <= 2 * r["stag"] * cell.J, (r["helm"], rep.helm_it)
+        helm_warm += r["helm"]
+        s, rc = ctx_cold.solve_increment(Et, np.zeros(6), tol.tol_stag, tol.tol_newton, tol.tol_cg, tol.tol_helm,
+                                         tol.max_stag, tol.max_newton, tol.max_cg, tol.max_helm, warm_start=False)
+        assert s == 0
+        helm_cold += rc["helm"]
+    assert helm_warm < helm_cold

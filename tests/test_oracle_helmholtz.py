@@ -77,6 +77,25 @@ def test_pcg_equals_dense_direct_solve(shape):
     assert abs(got.mean() - alpha.mean()) < 1e-12          # mean preservation
 
 
+def test_warm_start_pcg():
+    """Warm start (S:262): from the dense direct solution the PCG stops before its first iteration;
+    from a perturbed guess it converges to the same dense solution, with fewer iterations than from 0
+    when the guess is close (the stopping test stays relative to ||alpha||)."""
+    shape = (6, 6, 6)
+    g = Grid((shape[2], shape[1], shape[0]))
+    ell2 = ell2_field(two_phase(shape, 0.4, 5), [0.25, 0.005])
+    alpha = rng.random(shape)
+    L = dense_helmholtz(shape, g.h, ell2.reshape(-1))
+    ref = np.linalg.solve(L, alpha.reshape(-1)).reshape(shape)
+    got, it, _ = solve_helmholtz(g, alpha, ell2, tol=1e-10, x0=ref)
+    assert it == 0 and np.linalg.norm(got - ref) < 1e-13 * np.linalg.norm(ref)
+    _, it_cold, _ = solve_helmholtz(g, alpha, ell2, tol=1e-12)
+    guess = ref + 1e-6 * rng.random(shape)
+    got, it_warm, _ = solve_helmholtz(g, alpha, ell2, tol=1e-12, x0=guess)
+    assert np.linalg.norm(got - ref) < 1e-10 * np.linalg.norm(ref)
+    assert it_warm < it_cold
+
+
 def test_mean_ell2_golden():
     gv = GOLD["mean_ell2_two_phase"]
     ph = np.zeros((2, 4, 4), np.uint8)
