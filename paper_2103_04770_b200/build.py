@@ -28,6 +28,7 @@ def _nccl_dir():
 
 
 LIB = os.path.join(HERE, "libfgd.so")
+LIB_JITTER = os.path.join(HERE, "libfgd_jitter.so")   # race-hunting build (-DFGD_JITTER, tests only)
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -40,21 +41,23 @@ def deps():
     return sources() + sorted(glob.glob(os.path.join(CSRC, "*.cuh"))) + [os.path.join(INCLUDE, "fgd.h")]
 
 
-def up_to_date() -> bool:
-    if not os.path.exists(LIB):
+def up_to_date(lib=LIB) -> bool:
+    if not os.path.exists(lib):
         return False
-    t = os.path.getmtime(LIB)
+    t = os.path.getmtime(lib)
     return all(os.path.getmtime(d) <= t for d in deps())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
-        return LIB
-    objs = []
-    for src in sources():
-        obj = os.path.join(CSRC, os.path.basename(src)[:-3] + ".o")
+def build(force: bool = False, verbose: bool = False, jitter: bool = False) -> str:
+    lib = LIB_JITTER if jitter else LIB
+    if not force and up_to_date(lib):
+        return lib
+    def compile_one(src):
+        obj = os.path.join(CSRC, os.path.basename(src)[:-3] + ("_jit.o" if jitter else ".o"))
         cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", INCLUDE,
                "-I", os.path.join(_nccl_dir(), "include"), "--expt-relaxed-constexpr", "-c", src, "-o", obj]
+        if jitter:
+            cmd.insert(1, "-DFGD_JITTER")
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
         r = subprocess.run(cmd, capture_output=True, text=True)
@@ -62,17 +65,21 @@ def build(force: bool = False, verbose: bool = False) -> str:
             raise RuntimeError(f"nvcc failed for {src}:\n{r.stdout}\n{r.stderr}")
         if verbose:
             sys.stderr.write(r.stderr)
-        objs.append(obj)
+        return obj
+
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
+        objs = list(ex.map(compile_one, sources()))
     nlib = os.path.join(_nccl_dir(), "lib")
-    cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", LIB, *objs, "-L", nlib, "-l:libnccl.so.2",
+    cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", lib, *objs, "-L", nlib, "-l:libnccl.so.2",
            "-Xlinker", "-rpath", "-Xlinker", nlib]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
     for o in objs:
         os.remove(o)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="--verbose" in sys.argv))
+    print(build(force="--force" in sys.argv, verbose="--verbose" in sys.argv, jitter="--jitter" in sys.argv))

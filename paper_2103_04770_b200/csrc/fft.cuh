@@ -179,6 +179,7 @@ __device__ __forceinline__ void line_sync(int bar) {
   } else {
     asm volatile("bar.sync %0, %1;" ::"r"(bar), "n"(TPL) : "memory");
   }
+  FGD_JIT();
 }
 
 template <int N, int P, int NS, bool INV, bool W, int PASS>

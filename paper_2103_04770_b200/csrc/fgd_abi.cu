@@ -967,6 +967,12 @@ static fgd_status err_reduce(fgd_ctx* c, const double* eps, const double* eps_pr
   return allreduce_max_u64(c, &c->sc->maxbits);
 }
 
+// FGD_TRACE=1: one stderr line per Newton iteration and per staggered iteration (diagnostics)
+static bool trace_on() {
+  static const bool on = std::getenv("FGD_TRACE") != nullptr;
+  return on;
+}
+
 static double sigma_ref(const fgd_ctx* c) {
   double s = 0.0, e = 0.0;
   for (int q = 0; q < c->nphases; ++q) {
@@ -1050,8 +1056,12 @@ fgd_status fgd_solve_increment(fgd_ctx* c, const fgd_increment* inc, fgd_report*
         break;
       }
       int it = 0;
-      fgd_status s = cg_mech(c, c->w_b, c->w_de, inc->tol_cg, inc->max_cg, &it, nullptr);
+      double cg_rel = 0.0;
+      fgd_status s = cg_mech(c, c->w_b, c->w_de, inc->tol_cg, inc->max_cg, &it, &cg_rel);
       cg_total += it;
+      if (trace_on() && c->rank == 0)
+        fprintf(stderr, "fgd trace: stag %d newton %d rms/|S| %.3e cg %d relres %.2e\n", k, r,
+                rms / std::max(nm, 1e-6 * sref), it, cg_rel);
       if (s != FGD_OK && s != FGD_ENOCONV) return hard(s);
       ++newton_total;
       TRY_INC(launch_axpy(c, 6 * n, c->w_eps, c->w_de, 1.0));
@@ -1091,6 +1101,7 @@ fgd_status fgd_solve_increment(fgd_ctx* c, const fgd_increment* inc, fgd_report*
       const double dn = std::sqrt(red[7 + 2 * j]), nm = std::sqrt(red[6 + 2 * j]);
       err = std::max(err, dn > 1e-12 ? nm / dn : nm);
     }
+    if (trace_on() && c->rank == 0) fprintf(stderr, "fgd trace: stag %d ERR %.3e\n", k, err);
     if (err < inc->tol_stag) {   // w_abar = abar^(k) (frozen in the mechanics), w_D = abar^(k+1)
       converged = true;
       break;

@@ -4,13 +4,51 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <string>
 #include <vector>
+
+// Race hunting without compute-sanitizer (closed on this pool): a build with -DFGD_JITTER
+// (build.py --jitter -> libfgd_jitter.so) makes every warp leaving a CTA barrier (__syncthreads,
+// named barriers, warp syncs of the FFT exchanges) sleep a pseudo-random 0-4 us with probability
+// 1/4.  Accesses that are not ordered by a barrier then interleave very differently from the
+// production build, so tests/test_gpu_race.py compares both builds bit for bit.
+#ifdef FGD_JITTER
+__device__ __forceinline__ void fgd_jitter() {
+  unsigned t = (unsigned)clock64() ^ ((threadIdx.x >> 5) * 2654435761u) ^ (blockIdx.x * 40503u);
+  t ^= t >> 13;
+  t *= 0x5bd1e995u;
+  t ^= t >> 15;
+  if ((t & 3u) == 0u) __nanosleep(t & 4095u);
+}
+__device__ __forceinline__ void fgd_syncthreads_jitter() {
+  __syncthreads();
+  fgd_jitter();
+}
+#define __syncthreads() fgd_syncthreads_jitter()
+#define FGD_JIT() fgd_jitter()
+#else
+#define FGD_JIT() \
+  do {            \
+  } while (0)
+#endif
 
 #include "../../include/fgd.h"
 #include "fft.cuh"
 
 namespace fgd {
+
+// Persistent grids are sized SMs x occupancy, so the per-CTA partial sums of a reduction (and
+// therefore the last bits of the Krylov scalars) depend on the kernel's register / shared-memory
+// footprint.  FGD_GRID_CAP=n caps every persistent grid at n CTAs (validation only: two builds
+// with different footprints then reduce in the same order, tests/test_gpu_race.py).
+inline int grid_cap(int g) {
+  static const int cap = [] {
+    const char* e = std::getenv("FGD_GRID_CAP");
+    return e ? std::atoi(e) : 0;
+  }();
+  return cap > 0 && g > cap ? cap : g;
+}
 
 constexpr int kMaxPhases = 16;
 constexpr int kMaxFields = 4;

@@ -514,7 +514,7 @@ static fgd_status launch_xtan(fgd_ctx* c, int mode, double* r, double* p, double
     if (e != cudaSuccess) return set_err(c, FGD_ECUDA, std::string("k_xtan smem attr: ") + cudaGetErrorString(e)); \
     int occ = 0;                                                                                      \
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, thr, smem) != cudaSuccess || occ < 1) occ = 1; \
-    grid = std::max(1, std::min(ntiles, sm_count() * occ));                                           \
+    grid = grid_cap(std::max(1, std::min(ntiles, sm_count() * occ)));                                 \
     if (red_op != RED_NONE) {                                                                         \
       fgd_status s_ = ensure_partials(c, (size_t)grid);                                               \
       if (s_ != FGD_OK) return s_;                                                                    \

@@ -842,7 +842,10 @@ template <bool INV>
 __device__ __forceinline__ void fft512_reg(double2 (&v)[8], int t, double2* ls, const double2* tw1,
                                            const double2* tw2, int bar, int nbar) {
   // the exchanges only involve the warps that carry this line: named barrier `bar` over `nbar` threads
-  auto sync = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(nbar) : "memory"); };
+  auto sync = [&]() {
+    asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(nbar) : "memory");
+    FGD_JIT();
+  };
   dft8<INV>(v);
 #pragma unroll
   for (int ka = 1; ka < 8; ++ka) {
@@ -1510,7 +1513,7 @@ static fgd_status launch_persistent(fgd_ctx* c, K kernel, int threads, size_t sm
   int occ = 0;
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, threads, smem);
   if (e != cudaSuccess || occ < 1) occ = 1;
-  *grid_out = std::max(1, std::min(ntiles, num_sms() * occ));
+  *grid_out = grid_cap(std::max(1, std::min(ntiles, num_sms() * occ)));
   return FGD_OK;
 }
 
