@@ -181,6 +181,9 @@ typedef struct {
   int warm_start;  /* 1: every Helmholtz PCG of the staggered loop starts from the current iterate
                       abar_j^(k) instead of 0 (fgd_solve_helmholtz_from); 0: Algorithm 2 as
                       printed (abar^(0) = 0) */
+  int line_search; /* 1: Newton with residual backtracking (reading R-LS of DESIGN.md: a step that
+                      does not lower the RMS of -G*(sigma - Sigma) is halved, at most 5 times);
+                      0: plain Newton-Raphson */
 } fgd_increment;
 typedef struct {
   double macro_stress[6], macro_strain[6], err;

@@ -10,7 +10,9 @@ Step by step (readings A-01, A-02, A-07, A-16, A-20-A-22, A-28)
     a. damage frozen from abar^(k): D = max(D_n, D(abar_m)) (J2 phases), kappa = max(kappa_n,
        abar_p), d = d(kappa) (brittle phases) (A-16, A-18)
     b. Newton r: sigma, C = point update(eps); b = -G*(sigma - Sigma_bar) (P:680-683);
-       stop if rms(b) < tol_N * max(|<sigma>|, 1e-6 sigma_ref); else CG (mech.cg) and eps += de
+       stop if rms(b) < tol_N * max(|<sigma>|, 1e-6 sigma_ref); else CG (mech.cg) and eps += de;
+       with Tolerances.line_search (reading R-LS) a step that does not lower rms(b) is halved
+       (eps -= lam de, lam = 1/2, 1/4, ..., at most max_backtrack times) before the next CG
     c. alpha_j from the converged point update (A-28): eps_p (J2), eps_eq (brittle), 0 outside
        the source phase
     d. abar_j^(k+1) = Algorithm 2 (helmholtz.solve_helmholtz) for every field j, from
@@ -56,6 +58,8 @@ class Tolerances:
     max_cg: int = 5000
     max_helm: int = 5000
     warm_start: bool = False    # Helmholtz PCG from abar^(k) instead of 0; Alg. 2 as printed: False
+    line_search: bool = True    # Newton with residual backtracking (reading R-LS of DESIGN.md); False: plain N-R
+    max_backtrack: int = 5
 
 
 @dataclass
@@ -224,6 +228,7 @@ def solve_increment(cell: Cell, state: State, E_target, S_target, tol: Tolerance
         D = frozen_damage(cell, state, abar)
         eps_prev = eps.copy()
         newton_ok = False
+        rms_prev, lam, nback, de = np.inf, 1.0, 0, None
         for r in range(tol.max_newton + 1):
             try:
                 sigma, C, alpha, epsp, ep = evaluate(cell, eps, state, D)
@@ -236,8 +241,16 @@ def solve_increment(cell: Cell, state: State, E_target, S_target, tol: Tolerance
             if rms < tol.tol_newton * max(np.linalg.norm(smean), 1e-6 * sref):
                 newton_ok = True
                 break
+            # R-LS: a Newton step that does not lower the residual RMS is halved (at most
+            # max_backtrack times), re-evaluating sigma and the residual at eps_r + lam de
+            if tol.line_search and de is not None and rms >= rms_prev and nback < tol.max_backtrack:
+                lam *= 0.5
+                nback += 1
+                eps = eps - lam * de
+                continue
             if r == tol.max_newton:
                 break
+            rms_prev, lam, nback = rms, 1.0, 0
             de, it, _ = cg(g, C, b, mask, tol.tol_cg, tol.max_cg, backend)
             cg_total += it
             newton_total += 1

@@ -47,7 +47,8 @@ class fgd_increment(C.Structure):
     _fields_ = [("E_target", C.c_double * 6), ("S_target", C.c_double * 6),
                 ("tol_stag", C.c_double), ("tol_newton", C.c_double), ("tol_cg", C.c_double),
                 ("tol_helm", C.c_double), ("max_stag", C.c_int), ("max_newton", C.c_int),
-                ("max_cg", C.c_int), ("max_helm", C.c_int), ("warm_start", C.c_int)]
+                ("max_cg", C.c_int), ("max_helm", C.c_int), ("warm_start", C.c_int),
+                ("line_search", C.c_int)]
 
 
 class fgd_report(C.Structure):

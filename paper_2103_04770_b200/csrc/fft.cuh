@@ -159,6 +159,52 @@ template <bool INV> __device__ __forceinline__ void dft16(double2* v) {
 template <> __device__ __forceinline__ void dft<16, false>(double2* v) { dft16<false>(v); }
 template <> __device__ __forceinline__ void dft<16, true>(double2* v) { dft16<true>(v); }
 
+// cos(pi e / 16) for any integer e (compile-time constant after unrolling)
+__host__ __device__ constexpr double cos_pi16(int e) {
+  constexpr double C[9] = {1.0,
+                           0.98078528040323044912618223613424,
+                           0.92387953251128675612818318939679,
+                           0.83146961230254523707878837761791,
+                           0.70710678118654752440084436210485,
+                           0.55557023301960222474283081394853,
+                           0.38268343236508977172845998403040,
+                           0.19509032201612826784828486847702,
+                           0.0};
+  e &= 31;
+  return e <= 8 ? C[e] : (e <= 16 ? -C[16 - e] : (e <= 24 ? -C[e - 16] : C[32 - e]));
+}
+// a * W32^e, W32 = e^{-2 pi i / 32} (forward) / e^{+2 pi i / 32} (inverse)
+template <bool INV> __device__ __forceinline__ double2 w32(double2 a, int e) {
+  if ((e & 31) == 8) return mul_mi<INV>(a);
+  const double c = cos_pi16(e), s = cos_pi16(8 - e);   // sin(pi e / 16) = cos(pi (8 - e) / 16)
+  return cmul(a, make_double2(c, INV ? s : -s));
+}
+// radix-32 as 4 x 8: n = n2 + 8 n1 (n1 < 4, n2 < 8), k = k1 + 4 k2 (k1 < 4, k2 < 8):
+// DFT4 over n1, twiddle W32^{n2 k1}, DFT8 over n2, reorder to natural order (free after unrolling)
+// First stage (DFT4 over n1 and the W32 twiddles, in place): afterwards dft8(v + 8 k1) leaves
+// X[k1 + 4 k2] at v[8 k1 + k2] -- callers that consume the outputs group by group (storing each
+// group at once, to keep the register footprint down) call the two stages themselves.
+template <bool INV> __device__ __forceinline__ void dft32_stage1(double2* v) {
+#pragma unroll
+  for (int n2 = 0; n2 < 8; ++n2) dft4<INV>(v[n2], v[8 + n2], v[16 + n2], v[24 + n2]);   // v[n2 + 8 k1] = Y[n2][k1]
+#pragma unroll
+  for (int k1 = 1; k1 < 4; ++k1)
+#pragma unroll
+    for (int n2 = 1; n2 < 8; ++n2) v[n2 + 8 * k1] = w32<INV>(v[n2 + 8 * k1], n2 * k1);
+}
+template <bool INV> __device__ __forceinline__ void dft32(double2* v) {
+  dft32_stage1<INV>(v);
+#pragma unroll
+  for (int k1 = 0; k1 < 4; ++k1) dft8<INV>(v + 8 * k1);                                  // v[8 k1 + k2] = X[k1 + 4 k2]
+  double2 t[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) t[i] = v[i];
+#pragma unroll
+  for (int k1 = 0; k1 < 4; ++k1)
+#pragma unroll
+    for (int k2 = 0; k2 < 8; ++k2) v[k1 + 4 * k2] = t[8 * k1 + k2];
+}
+
 // Twiddle load from the shared-memory table through a volatile asm.  Keeps the compiler
 // from hoisting every twiddle of every pass out of a persistent tile loop into registers.
 __device__ __forceinline__ double2 ld_tw(const double2* p) {

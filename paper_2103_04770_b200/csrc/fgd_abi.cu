@@ -967,6 +967,8 @@ static fgd_status err_reduce(fgd_ctx* c, const double* eps, const double* eps_pr
   return allreduce_max_u64(c, &c->sc->maxbits);
 }
 
+constexpr int kMaxBacktrack = 5;   // R-LS: at most 5 halvings of a Newton step
+
 // FGD_TRACE=1: one stderr line per Newton iteration and per staggered iteration (diagnostics)
 static bool trace_on() {
   static const bool on = std::getenv("FGD_TRACE") != nullptr;
@@ -1036,6 +1038,9 @@ fgd_status fgd_solve_increment(fgd_ctx* c, const fgd_increment* inc, fgd_report*
   for (k = 0; k < inc->max_stag; ++k) {
     FGD_CUDA(c, cudaMemcpyAsync(c->w_eps_prev, c->w_eps, 6 * n * 8, cudaMemcpyDeviceToDevice, c->stream));
     bool newton_ok = false;
+    double rms_prev = INFINITY, lam = 1.0;
+    int nback = 0;
+    bool have_step = false;
     for (int r = 0; r <= inc->max_newton; ++r) {
       const fgd_status cs = fgd_constitutive(c, nullptr, nullptr, macro);
       if (cs == FGD_ENOCONV) {   // a GTN return mapping failed: roll back, the caller cuts back
@@ -1051,10 +1056,23 @@ fgd_status fgd_solve_increment(fgd_ctx* c, const fgd_increment* inc, fgd_report*
         newton_ok = true;
         break;
       }
+      // R-LS: a Newton step that does not lower the residual RMS is halved (at most 5 times),
+      // re-evaluating sigma and the residual at eps_r + lam de (no new linear solve)
+      if (inc->line_search && have_step && rms >= rms_prev && nback < kMaxBacktrack) {
+        lam *= 0.5;
+        ++nback;
+        if (trace_on() && c->rank == 0) fprintf(stderr, "fgd trace: stag %d newton %d backtrack lam %.4g\n", k, r, lam);
+        TRY_INC(launch_axpy(c, 6 * n, c->w_eps, c->w_de, -lam));
+        continue;
+      }
       if (r == inc->max_newton) {
         why = "Newton did not converge in increment";
         break;
       }
+      rms_prev = rms;
+      lam = 1.0;
+      nback = 0;
+      have_step = true;
       int it = 0;
       double cg_rel = 0.0;
       fgd_status s = cg_mech(c, c->w_b, c->w_de, inc->tol_cg, inc->max_cg, &it, &cg_rel);

@@ -963,6 +963,181 @@ __global__ void __launch_bounds__(NC * 64, NC == 6 ? 2 : 8) k_zreg512(ZPArgs a) 
   }
 }
 
+// Z pass, Nz = 512, wide plan: 16 threads per line, 32 points per thread and ONE shared-memory
+// exchange per transform (512 = 32 x 16), instead of the 8 x 8 x 8 plan of k_zreg512 (64 threads
+// per line, two exchanges per transform).  Thread t loads x[t + 16 m] (m < 32, 256 B per
+// half-warp instruction), runs a register DFT32 over m, multiplies by W512^{t k2}, and one
+// transpose through the line buffer (32 rows k2 x 16 columns t, pitch 17: row and column
+// accesses conflict free) gives it rows k2 = t and t + 16, whose DFT16 over t yields
+// X[k2 + 32 k1].  The inverse runs the mirror image and ends in the coalesced store layout.
+// Shared accesses per element: 2 per transform + 4 for the six-component projection (was 4 + 4).
+// Line buffer of 512 slots, no padding: exchange element (row r, column n) at r * 16 + (n ^ (r & 15))
+// (XOR swizzle: row accesses and column accesses are both conflict free), staged frequency kz at kz;
+// twiddle W512^{t k2} at (k2 - 1) * 16 + (t ^ (k2 & 15)).  55.75 KB per six-component CTA, so four
+// CTAs fit on an SM.
+constexpr int kZ5Line = 512;
+__device__ __forceinline__ int z5x(int r, int n) { return r * 16 + (n ^ (r & 15)); }
+__device__ __forceinline__ int z5slot(int kz) { return kz; }
+
+// SLAB = false (one slab, P = 1): the z offsets are compile-time immediates from one base pointer
+// (otherwise 32 64-bit addresses stay live across the tile and the kernel spills).
+template <int NC, int MODE, bool SLAB>
+__global__ void __launch_bounds__(NC == 6 ? 96 : 128, NC == 6 ? 4 : 2) k_zreg512w(ZPArgs a) {
+  if (guard_done(a.guard)) return;   // converged Krylov loop: skip
+  extern __shared__ double2 sm[];
+  constexpr int N = 512;
+  const int TL = a.TL;
+  const int nl = NC * TL;                       // blockDim.x == 16 * nl
+  double2* tw = sm + (size_t)nl * kZ5Line;      // W512^{t k2} at (k2 - 1) * 16 + (t ^ (k2 & 15)), k2 in [1, 32)
+  pdl_trigger();
+  for (int i = threadIdx.x; i < 31 * 16; i += blockDim.x) {
+    const int k2 = 1 + (i >> 4), tt = i & 15;
+    tw[(k2 - 1) * 16 + (tt ^ (k2 & 15))] = __ldg(&a.twz[tt * k2]);
+  }
+  __syncthreads();
+  pdl_wait();
+  const int line = threadIdx.x >> 4, t = threadIdx.x & 15;
+  const int c = line >> a.lgTL, ll = line & (TL - 1);
+  double2* ls = sm + (size_t)line * kZ5Line;
+  const int nyt = a.Nyl / TL;
+  const int ntiles = a.Hx * nyt;
+  const int BS = NC * a.Hx * a.SL.nys * a.SL.nzs, zm = a.SL.nzs - 1, lgz = a.SL.lg_nzs;
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int kx = tile / nyt, ky0 = (tile % nyt) * TL;
+    const int kyl = ky0 + ll;
+    double2* Bl = a.B + r_index(a.SL, NC, a.Hx, c, kx, kyl, 0) + (SLAB ? 0 : t);
+    auto zoff = [&](int z) -> size_t { return SLAB ? (size_t)((z >> lgz) * BS + (z & zm)) : (size_t)(z - t); };
+    double2 v[32];
+#pragma unroll
+    for (int m = 0; m < 32; ++m) v[m] = __ldcg(Bl + zoff(t + 16 * m));
+    // ---- forward: DFT32 over m, twiddle, transpose, DFT16 over t ----
+    // (each group of 8 outputs of the DFT32 is twiddled and stored at once: register footprint)
+    dft32_stage1<false>(v);
+    __syncwarp();
+#pragma unroll
+    for (int k1 = 0; k1 < 4; ++k1) {
+      dft8<false>(v + 8 * k1);                               // v[8 k1 + j] = Y[t][k2 = k1 + 4 j]
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int k2 = k1 + 4 * j;
+        double2 y = v[8 * k1 + j];
+        if (k2 > 0) y = cmul(y, ld_tw(tw + (k2 - 1) * 16 + (t ^ (k2 & 15))));
+        ls[z5x(k2, t)] = y;
+      }
+    }
+    __syncwarp();
+    const int ky = kyl + a.ky_off;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {                            // rows k2 = t, t + 16
+      double2 u[16];
+#pragma unroll
+      for (int n = 0; n < 16; ++n) u[n] = ls[z5x(t + 16 * h, n)];
+      dft16<false>(u);                                       // u[k1] = X[t + 16 h + 32 k1]
+#pragma unroll
+      for (int k1 = 0; k1 < 16; ++k1) v[16 * h + k1] = u[k1];
+    }
+    // ---- spectral multiply ----
+    __syncwarp();
+#pragma unroll
+    for (int k1 = 0; k1 < 16; ++k1) {
+      ls[z5slot(t + 32 * k1)] = v[k1];
+      ls[z5slot(t + 16 + 32 * k1)] = v[16 + k1];
+    }
+    if (MODE == Z_PRECOND) {
+      // own slots only (no cross-thread traffic); |k|^2 from the per-axis factors as in k_zreg256
+      double fx[2], fy[2];
+      zaxis(a, 0, kx, a.Nx, nullptr, fx);
+      zaxis(a, 1, ky, a.Ny, nullptr, fy);
+#pragma unroll 1
+      for (int j = 0; j < 32; ++j) {
+        const int kz = t + 16 * (j & 1) + 32 * (j >> 1);
+        double fz[2];
+        if (a.scheme == 1) {
+          const double cs = __ldg(&a.twz[kz]).x;
+          fz[0] = (2.0 - 2.0 * cs) * a.qh2[2];
+          fz[1] = 2.0 + 2.0 * cs;
+        } else {
+          zaxis(a, 2, kz, N, nullptr, fz);
+        }
+        const double k2 = a.scheme == 1 ? (fx[0] * fy[1] * fz[1] + fx[1] * fy[0] * fz[1] + fx[1] * fy[1] * fz[0])
+                                        : fx[0] + fy[0] + fz[0];
+        ls[z5slot(kz)] = cscale(ls[z5slot(kz)], a.scale / (1.0 + a.mean_ell2 * k2));
+      }
+    } else {
+      __syncthreads();
+      // Willot symbol with the (kx, ky) factors hoisted (TL = 1: one ky per tile)
+      double2 P0 = make_double2(0.0, 0.0), P1 = P0, P2 = P0;
+      const bool hoist = a.scheme == 1 && TL == 1;
+      if (hoist) {
+        const double2 wx = __ldg(&a.twx[kx]), wy = __ldg(&a.twy[ky0 + a.ky_off]);
+        const double2 ex = make_double2(wx.x, -wx.y), ey = make_double2(wy.x, -wy.y);
+        const double2 dx = make_double2(ex.x - 1.0, ex.y), dy = make_double2(ey.x - 1.0, ey.y);
+        const double2 cx = make_double2(ex.x + 1.0, ex.y), cy = make_double2(ey.x + 1.0, ey.y);
+        P0 = cscale(cmul(dx, cy), a.qh[0]);
+        P1 = cscale(cmul(cx, dy), a.qh[1]);
+        P2 = cscale(cmul(cx, cy), a.qh[2]);
+      }
+      for (int idx = threadIdx.x; idx < TL * N; idx += blockDim.x) {
+        const int kz = idx & (N - 1), l2 = idx >> 9;
+        const int kyg = ky0 + l2 + a.ky_off;
+        double2 k[3];
+        if (hoist) {
+          const double2 wz = __ldg(&a.twz[kz]);
+          const double2 cz = make_double2(wz.x + 1.0, -wz.y), dz = make_double2(wz.x - 1.0, -wz.y);
+          k[0] = cmul(P0, cz);
+          k[1] = cmul(P1, cz);
+          k[2] = cmul(P2, dz);
+        } else {
+          zsymbol(a, N, kx, kyg, kz, k, a.twz);
+        }
+        double2* pv[6];
+#pragma unroll
+        for (int cc = 0; cc < 6; ++cc) pv[cc] = &sm[(size_t)(cc * TL + l2) * kZ5Line + z5slot(kz)];
+        project6(a, pv, k, kx == 0 && kyg == 0 && kz == 0);
+      }
+      __syncthreads();
+    }
+    // ---- inverse: DFT16 over k1, conjugate twiddle, transpose, DFT32 over k2 ----
+    // rows k2 = t + 16 h: read the 16 frequencies k1 from the staging slots, inverse DFT16, twiddle
+    // and put them back in the exchange layout (row k2, column n) -- the staging slots of the line
+    // are all read before any exchange slot is written (the two layouts overlap)
+    double2 u[2][16];
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int k1 = 0; k1 < 16; ++k1) u[h][k1] = ls[z5slot(t + 16 * h + 32 * k1)];
+    __syncwarp();
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      dft16<true>(u[h]);                                     // u[h][n] = Z[k2 = t + 16 h][n]
+      const int k2 = t + 16 * h;
+#pragma unroll
+      for (int n = 0; n < 16; ++n) {
+        double2 y = u[h][n];
+        if (n > 0) {
+          double2 w = ld_tw(tw + (k2 > 0 ? k2 - 1 : 0) * 16 + (n ^ (k2 & 15)));
+          if (k2 == 0) w = make_double2(1.0, 0.0);
+          w.y = -w.y;
+          y = cmul(y, w);
+        }
+        ls[z5x(k2, n)] = y;
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int k2 = 0; k2 < 32; ++k2) v[k2] = ls[z5x(k2, t)];
+    dft32_stage1<true>(v);
+#pragma unroll
+    for (int k1 = 0; k1 < 4; ++k1) {
+      dft8<true>(v + 8 * k1);                                // v[8 k1 + j] = z[t + 16 (k1 + 4 j)]
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        Bl[zoff(t + 16 * (k1 + 4 * j))] = v[8 * k1 + j];
+      }
+    }
+  }
+}
+
 // Y pass, Ny = 512: tile (c, kx pair, TZ planes), 2 TZ lines of 64 threads.  Warp w carries 16
 // threads of each kx of the pair for plane zz = w / 4 (t = 16 (w % 4) + lane % 16), so that the
 // A-side loads / stores are 512 B per warp instruction.  Line l = kl TZ + zz at pitch k512Line + 1.
@@ -1650,6 +1825,29 @@ fgd_status pipe_z(fgd_ctx* c, int ncomp, int mode, double scale, const double* d
   a.twy = c->tabs.tw[ilog2(Ny)];
   a.twz = c->tabs.tw[ilog2(Nz)];
   KTimer kt(c, ncomp == 6 ? KC_Z6 : KC_Z1);
+  static const int z512w = [] {
+    const char* e = std::getenv("FGD_Z512");
+    return e ? std::atoi(e) : 1;   // 1: wide 32 x 16 plan (k_zreg512w), 0: 8 x 8 x 8 plan (k_zreg512)
+  }();
+  // measured at 512^3 (per sweep): 6 components 49.6 -> 46.2 ms with the wide plan; the 1-component
+  // preconditioner pass 8.1 -> 10.8 ms (16-thread lines, 8 lines per CTA: too little parallelism per
+  // SM), so it keeps the 8 x 8 x 8 plan unless FGD_Z512=2
+  if (Nz == 512 && z512w && ((ncomp == 6 && mode == Z_PROJECT) || (ncomp == 1 && mode == Z_PRECOND && z512w == 2))) {
+    const int TLr = std::min(ncomp == 6 ? 1 : 8, Nyl);
+    a.TL = TLr;
+    a.lgTL = ilog2(TLr);
+    const int thr_r = 16 * ncomp * TLr;
+    const size_t smem_r = ((size_t)ncomp * TLr * kZ5Line + 31 * 16) * sizeof(double2);
+    const int nt_r = c->Hx * (Nyl / TLr);
+    if (c->P > 1) {
+      if (ncomp == 6) FGD_PLAUNCH(c, (k_zreg512w<6, Z_PROJECT, true>), thr_r, smem_r, nt_r, a);
+      else FGD_PLAUNCH(c, (k_zreg512w<1, Z_PRECOND, true>), thr_r, smem_r, nt_r, a);
+    } else {
+      if (ncomp == 6) FGD_PLAUNCH(c, (k_zreg512w<6, Z_PROJECT, false>), thr_r, smem_r, nt_r, a);
+      else FGD_PLAUNCH(c, (k_zreg512w<1, Z_PRECOND, false>), thr_r, smem_r, nt_r, a);
+    }
+    return FGD_OK;
+  }
   if (Nz == 512 && ((ncomp == 6 && mode == Z_PROJECT) || (ncomp == 1 && mode == Z_PRECOND))) {
     const int thr_r = 64 * ncomp;
     const size_t smem_r = ((size_t)ncomp * k512Line + 448 + 56 + 512) * sizeof(double2);

@@ -123,7 +123,8 @@ def run_case(name, stop_frac=0.3, de_min_halvings=8, log=None, n_incr=None):
                 tolerances=dict(tol_stag=PARITY_TOL.tol_stag, tol_newton=PARITY_TOL.tol_newton,
                                 tol_cg=PARITY_TOL.tol_cg, tol_helm=PARITY_TOL.tol_helm,
                                 max_stag=PARITY_TOL.max_stag, max_newton=PARITY_TOL.max_newton,
-                                max_cg=PARITY_TOL.max_cg, max_helm=PARITY_TOL.max_helm),
+                                max_cg=PARITY_TOL.max_cg, max_helm=PARITY_TOL.max_helm,
+                                warm_start=PARITY_TOL.warm_start, line_search=PARITY_TOL.line_search),
                 schedule="halve on failure, x2 after 2 first-try successes, <= dE", cutbacks=cut,
                 stalled=stalled, peak_stress=float(Sv[ip]), strain_at_peak=float(Ev[ip]),
                 peak_index=ip - 1, strain_at_failure=failure_strain(Ev, Sv),

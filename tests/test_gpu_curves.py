@@ -63,7 +63,8 @@ def test_config_curve_parity(case):
         Et[lc] = rec["E"]
         st, rep = ctx.solve_increment(Et, np.zeros(6), tol["tol_stag"], tol["tol_newton"], tol["tol_cg"],
                                       tol["tol_helm"], tol["max_stag"], tol["max_newton"], tol["max_cg"],
-                                      tol["max_helm"])
+                                      tol["max_helm"], warm_start=tol.get("warm_start", False),
+                                      line_search=tol.get("line_search", False))
         assert st == 0, (case, rec["E"], rep)
         got.append(dict(E=rec["E"], stress=rep["macro_stress"].tolist(), stag=rep["stag"], newton=rep["newton"],
                         cg=rep["cg"], helm=rep["helm"]))

@@ -228,3 +228,23 @@ def test_voigt_reuss_bounds_and_exact_strain_averages():
     w = float(rep.macro_stress @ E)
     assert E @ CR @ E <= w <= E @ CV @ E
     assert E @ CR @ E < 0.999 * w and w < 0.999 * E @ CV @ E     # strictly inside for this contrast
+
+
+def test_line_search_keeps_the_converged_increment():
+    """R-LS (backtracking on the Newton residual) is a globalisation only: on a plastic disc cell
+    where plain Newton converges, both reach the same increment solution (and with a large load
+    step the backtracking variant converges with no more Newton iterations than plain Newton)."""
+    import dataclasses
+    import synth
+    from oracle.increment import State, Tolerances, make_cell, solve_increment
+    cfg = synth.config0(8, ell_over_L=0.25)
+    cell = make_cell(cfg)
+    st = State.zero(cell)
+    E = np.zeros(6)
+    E[0] = 4e-3                                   # one large step well into plasticity
+    tol = Tolerances(tol_stag=1e-9, tol_newton=1e-11, tol_cg=1e-12, tol_helm=1e-12)
+    s1, r1 = solve_increment(cell, st, E, np.zeros(6), dataclasses.replace(tol, line_search=True))
+    s0, r0 = solve_increment(cell, st, E, np.zeros(6), dataclasses.replace(tol, line_search=False))
+    assert r1.converged and r0.converged
+    assert np.max(np.abs(s1.eps - s0.eps)) <= 1e-10 * np.max(np.abs(s0.eps))
+    assert np.allclose(r1.macro_stress, r0.macro_stress, rtol=1e-9, atol=1e-9)
