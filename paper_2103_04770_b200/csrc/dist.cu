@@ -31,6 +31,7 @@
 #include <cstring>
 #include <map>
 #include <mutex>
+#include <vector>
 
 #include "reduce.cuh"
 
@@ -142,22 +143,24 @@ static void loop_leave(fgd_ctx* c) {
   c->loop = nullptr;
 }
 
-static fgd_status loop_publish(fgd_ctx* c, const void* p) {
+static fgd_status loop_publish(fgd_ctx* c, const void* p, cudaStream_t st) {
   LoopGroup* g = loop_of(c)->g;
   g->ptr[c->rank] = p;
-  FGD_CUDA(c, cudaEventRecord(g->ready[c->rank], c->stream));
+  FGD_CUDA(c, cudaEventRecord(g->ready[c->rank], st));
   if (!g->barrier()) return set_err(c, FGD_ENCCL, "loopback barrier timeout (publish)");
-  for (int s = 0; s < g->P; ++s) FGD_CUDA(c, cudaStreamWaitEvent(c->stream, g->ready[s], 0));
+  for (int s = 0; s < g->P; ++s) FGD_CUDA(c, cudaStreamWaitEvent(st, g->ready[s], 0));
   return FGD_OK;
 }
+static fgd_status loop_publish(fgd_ctx* c, const void* p) { return loop_publish(c, p, c->stream); }
 
-static fgd_status loop_finish(fgd_ctx* c) {
+static fgd_status loop_finish(fgd_ctx* c, cudaStream_t st) {
   LoopGroup* g = loop_of(c)->g;
-  FGD_CUDA(c, cudaEventRecord(g->done[c->rank], c->stream));
+  FGD_CUDA(c, cudaEventRecord(g->done[c->rank], st));
   if (!g->barrier()) return set_err(c, FGD_ENCCL, "loopback barrier timeout (finish)");
-  for (int s = 0; s < g->P; ++s) FGD_CUDA(c, cudaStreamWaitEvent(c->stream, g->done[s], 0));
+  for (int s = 0; s < g->P; ++s) FGD_CUDA(c, cudaStreamWaitEvent(st, g->done[s], 0));
   return FGD_OK;
 }
+static fgd_status loop_finish(fgd_ctx* c) { return loop_finish(c, c->stream); }
 
 // dev[i] = sum_s stage[s][i] (rank order), or the max of the 64-bit patterns
 __global__ void k_loop_sum(double* dev, const double* stage, int P, int count) {
@@ -224,6 +227,11 @@ slabs:
 }
 
 void dist_destroy(fgd_ctx* c) {
+  if (c->comm_stream) cudaStreamSynchronize(c->comm_stream);
+  for (cudaEvent_t e : c->ov_ev) cudaEventDestroy(e);
+  c->ov_ev.clear();
+  if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
+  c->comm_stream = nullptr;
   loop_leave(c);
   if (c->comm) ncclCommDestroy(comm_of(c));
   c->comm = nullptr;
@@ -260,6 +268,111 @@ fgd_status exchange(fgd_ctx* c, int ncomp, bool fwd) {
     FGD_NCCL(c, ncclRecv(dst + (size_t)p * blk, 2 * blk, ncclDouble, p, comm_of(c), c->stream));
   }
   FGD_NCCL(c, ncclGroupEnd());
+  return FGD_OK;
+}
+
+// One kx chunk [kxa, kxb) of the transpose, on stream st: for every peer p and component cc the
+// contiguous run of (kxb - kxa) * nys * nzs complex values at kx = kxa of block p (nranks > 1 only).
+static fgd_status exchange_chunk(fgd_ctx* c, int ncomp, bool fwd, int kxa, int kxb, cudaStream_t st) {
+  const int P = c->P;
+  kxb = std::min(kxb, c->Hx);
+  if (kxb <= kxa) return FGD_OK;
+  const size_t nn = (size_t)(c->n[1] / P) * (c->n[2] / P);
+  const size_t blk = (size_t)ncomp * c->Hx * nn;
+  const size_t cnt = (size_t)(kxb - kxa) * nn;
+  double2* src = fwd ? c->specB : c->specC;
+  double2* dst = fwd ? c->specC : c->specB;
+  if (c->loop) {
+    TRYD(loop_publish(c, src, st));
+    for (int p = 0; p < P; ++p) {
+      const double2* peer = static_cast<const double2*>(loop_of(c)->g->ptr[p]) + (size_t)c->rank * blk;
+      for (int cc = 0; cc < ncomp; ++cc) {
+        const size_t off = ((size_t)cc * c->Hx + kxa) * nn;
+        FGD_CUDA(c, cudaMemcpyAsync(dst + (size_t)p * blk + off, peer + off, cnt * sizeof(double2),
+                                    cudaMemcpyDeviceToDevice, st));
+      }
+    }
+    return loop_finish(c, st);
+  }
+  FGD_NCCL(c, ncclGroupStart());
+  for (int p = 0; p < P; ++p)
+    for (int cc = 0; cc < ncomp; ++cc) {
+      const size_t off = (size_t)p * blk + ((size_t)cc * c->Hx + kxa) * nn;
+      FGD_NCCL(c, ncclSend(src + off, 2 * cnt, ncclDouble, p, comm_of(c), st));
+      FGD_NCCL(c, ncclRecv(dst + off, 2 * cnt, ncclDouble, p, comm_of(c), st));
+    }
+  FGD_NCCL(c, ncclGroupEnd());
+  return FGD_OK;
+}
+
+// Number of kx chunks of the overlapped round trip (nranks > 1): FGD_OVERLAP (default 4; 1 = the
+// monolithic transpose), at most HxA / 4.
+static int overlap_chunks(const fgd_ctx* c) {
+  const char* e = std::getenv("FGD_OVERLAP");   // read per call (the tests switch it)
+  const int k = e ? std::atoi(e) : 4;
+  return std::max(1, std::min(k, c->HxA / 4));
+}
+
+// y-forward, transpose, z pass (projection or preconditioner), transpose back, y-inverse of the
+// spectra in specA/specB: the y/z half of every operator apply.  With nranks > 1 the kx range is
+// cut into K chunks (multiples of 4 columns) and pipelined over two streams:
+//   compute: y(0) .. y(K-1) | z(0) .. z(K-1) | yinv(0) .. yinv(K-1)
+//   comm:          a2a(0) .. a2a(K-1) | a2a'(0) .. a2a'(K-1)
+// chunk i's transpose runs while the compute stream works on chunk i+1, each compute step waiting
+// only for its own chunk's transpose (events).  The persistent kernels of the overlapped phase
+// leave kCommSMs SMs free for the communication kernels.
+constexpr int kCommSMs = 8;
+fgd_status yz_round_trip(fgd_ctx* c, int ncomp, int zmode, double scale, const double* shift, double mean_ell2) {
+  const int K = c->nranks > 1 ? overlap_chunks(c) : 1;
+  if (K <= 1) {
+    TRYD(pipe_y(c, ncomp, false));
+    TRYD(exchange(c, ncomp, true));
+    TRYD(pipe_z(c, ncomp, zmode, scale, shift, mean_ell2));
+    TRYD(exchange(c, ncomp, false));
+    return pipe_y(c, ncomp, true);
+  }
+  if (!c->comm_stream) {
+    FGD_CUDA(c, cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking));
+  }
+  while ((int)c->ov_ev.size() < 4 * K) {
+    cudaEvent_t e;
+    FGD_CUDA(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    c->ov_ev.push_back(e);
+  }
+  cudaEvent_t* ey = c->ov_ev.data();
+  cudaEvent_t *ea = ey + K, *ez = ey + 2 * K, *eb = ey + 3 * K;
+  std::vector<int> kb(K + 1);
+  const int n4 = c->HxA / 4;
+  for (int i = 0; i <= K; ++i) kb[i] = 4 * (int)((long long)i * n4 / K);
+  struct Reserve {
+    fgd_ctx* c;
+    explicit Reserve(fgd_ctx* cc) : c(cc) { c->sm_reserve = kCommSMs; }
+    ~Reserve() { c->sm_reserve = 0; }
+  } reserve(c);
+  cudaStream_t cs = c->comm_stream;
+  for (int i = 0; i < K; ++i) {
+    TRYD(pipe_y(c, ncomp, false, kb[i], kb[i + 1]));
+    FGD_CUDA(c, cudaEventRecord(ey[i], c->stream));
+  }
+  for (int i = 0; i < K; ++i) {
+    FGD_CUDA(c, cudaStreamWaitEvent(cs, ey[i], 0));
+    TRYD(exchange_chunk(c, ncomp, true, kb[i], kb[i + 1], cs));
+    FGD_CUDA(c, cudaEventRecord(ea[i], cs));
+  }
+  for (int i = 0; i < K; ++i) {
+    FGD_CUDA(c, cudaStreamWaitEvent(c->stream, ea[i], 0));
+    TRYD(pipe_z(c, ncomp, zmode, scale, shift, mean_ell2, kb[i], kb[i + 1]));
+    FGD_CUDA(c, cudaEventRecord(ez[i], c->stream));
+  }
+  for (int i = 0; i < K; ++i) {
+    FGD_CUDA(c, cudaStreamWaitEvent(cs, ez[i], 0));
+    TRYD(exchange_chunk(c, ncomp, false, kb[i], kb[i + 1], cs));
+    FGD_CUDA(c, cudaEventRecord(eb[i], cs));
+  }
+  for (int i = 0; i < K; ++i) {
+    FGD_CUDA(c, cudaStreamWaitEvent(c->stream, eb[i], 0));
+    TRYD(pipe_y(c, ncomp, true, kb[i], kb[i + 1]));
+  }
   return FGD_OK;
 }
 

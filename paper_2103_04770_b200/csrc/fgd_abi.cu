@@ -216,11 +216,7 @@ static double inv_nvox(const fgd_ctx* c) { return 1.0 / (double)c->nvox_g; }
 static fgd_status op_projected_tangent(fgd_ctx* c, const double* x, double* y) {
   TRY(ensure_spectral(c));
   TRY(launch_xfwd(c, 6, XF_TANGENT, x, nullptr, nullptr, c->compact ? c->Cc : c->C, RED_NONE, 0));
-  TRY(launch_yfwd(c, 6));
-  TRY(exchange(c, 6, true));
-  TRY(launch_z(c, 6, Z_PROJECT, inv_nvox(c), nullptr, 0.0));
-  TRY(exchange(c, 6, false));
-  TRY(launch_yinv(c, 6));
+  TRY(yz_round_trip(c, 6, Z_PROJECT, inv_nvox(c), nullptr, 0.0));
   return launch_xinv(c, 6, XI_STORE, y, nullptr, nullptr, nullptr, RED_NONE, 0);
 }
 
@@ -232,11 +228,7 @@ static fgd_status op_projection(fgd_ctx* c, const double* tau, const double* S, 
   if (S)
     for (int i = 0; i < 6; ++i) shift[i] = S[i] * (double)c->nvox_g;
   TRY(launch_xfwd(c, 6, XF_PLAIN, tau, nullptr, nullptr, nullptr, RED_NONE, 0));
-  TRY(launch_yfwd(c, 6));
-  TRY(exchange(c, 6, true));
-  TRY(launch_z(c, 6, Z_PROJECT, scale * inv_nvox(c), shift, 0.0));
-  TRY(exchange(c, 6, false));
-  TRY(launch_yinv(c, 6));
+  TRY(yz_round_trip(c, 6, Z_PROJECT, scale * inv_nvox(c), shift, 0.0));
   if (red_op == RED_NONE) return launch_xinv(c, 6, XI_STORE, y, nullptr, nullptr, nullptr, RED_NONE, 0);
   TRY(launch_xinv(c, 6, XI_STORE_RR, y, nullptr, nullptr, nullptr, red_op_for(c, red_op), red_slot_for(c, red_op, red_slot)));
   if (red_op == RED_STORE) return allreduce_sum(c, &c->sc->red[red_slot], 1);
@@ -516,12 +508,8 @@ static fgd_status cg_mech(fgd_ctx* c, const double* b, double* x_out, double tol
     auto iteration = [&](bool first) -> fgd_status {
       TRY(launch_xfwd_io(c, 6, XF_TANGENT_CG, first ? b : c->cg_r, nullptr, c->cg_p, c->cg_x,
                          c->compact ? c->Cc : c->C, RED(RED_MECH_PQ), first ? 1 : 0));
-      TRY(launch_yfwd(c, 6));
-      TRY(exchange(c, 6, true));
-      TRY(launch_z(c, 6, Z_PROJECT, inv_nvox(c), nullptr, 0.0));
-      TRY(exchange(c, 6, false));
+      TRY(yz_round_trip(c, 6, Z_PROJECT, inv_nvox(c), nullptr, 0.0));
       TRY(post_reduce(c, RED_MECH_PQ));
-      TRY(launch_yinv(c, 6));
       TRY(launch_xinv(c, 6, XI_MECH_CG, nullptr, nullptr, c->cg_r, first ? b : c->cg_r, RED(RED_MECH_RR)));
       TRY(post_reduce(c, RED_MECH_RR));
       return FGD_OK;

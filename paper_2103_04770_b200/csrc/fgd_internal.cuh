@@ -163,6 +163,9 @@ struct fgd_ctx {
   int P = 1;                   // slab count of the transposed-spectrum layout (nranks, or emulated)
   void* comm = nullptr;        // ncclComm_t
   void* loop = nullptr;        // loopback transport rank (dist.cu), instead of NCCL
+  cudaStream_t comm_stream = nullptr;   // transposes of the overlapped y/z round trip (nranks > 1)
+  std::vector<cudaEvent_t> ov_ev;       // chunk events of the overlapped round trip
+  int sm_reserve = 0;          // SMs the persistent kernels leave free (overlapped communication)
   double2* specC = nullptr;    // z-pass buffer when P > 1
   double* halo = nullptr;      // stencil halo planes (nranks > 1): [field 0 lo, hi][field 1 lo, hi]
   uint8_t* phase_halo = nullptr;
@@ -276,8 +279,9 @@ fgd_status launch_xinv(fgd_ctx* c, int ncomp, int mode, double* out0, double* io
                        const double* in1, int red_op, int red_slot);
 fgd_status ensure_spectral(fgd_ctx* c);
 // pipes.cu (persistent cp.async pipelines)
-fgd_status pipe_y(fgd_ctx* c, int ncomp, bool inv);
-fgd_status pipe_z(fgd_ctx* c, int ncomp, int mode, double scale, const double* dc_shift, double mean_ell2);
+fgd_status pipe_y(fgd_ctx* c, int ncomp, bool inv, int kxa = 0, int kxb = -1);
+fgd_status pipe_z(fgd_ctx* c, int ncomp, int mode, double scale, const double* dc_shift, double mean_ell2, int kxa = 0,
+                  int kxb = -1);
 fgd_status pipe_xinv(fgd_ctx* c, int ncomp, int mode, double* out0, double* io1, double* io2, const double* in1,
                      int red_op, int red_slot);
 fgd_status pipe_xfwd_plain(fgd_ctx* c, int ncomp, const double* in0);
@@ -288,6 +292,7 @@ fgd_status ensure_partials(fgd_ctx* c, size_t nblocks);
 fgd_status dist_init(fgd_ctx* c, const fgd_dist* d);
 void dist_destroy(fgd_ctx* c);
 fgd_status exchange(fgd_ctx* c, int ncomp, bool fwd);
+fgd_status yz_round_trip(fgd_ctx* c, int ncomp, int zmode, double scale, const double* shift, double mean_ell2);
 fgd_status allreduce_sum(fgd_ctx* c, double* dev, int count);
 fgd_status allreduce_max_u64(fgd_ctx* c, unsigned long long* dev);
 int red_op_for(const fgd_ctx* c, int op);

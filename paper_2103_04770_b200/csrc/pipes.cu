@@ -95,15 +95,16 @@ struct YArgs {
   int Nz, Hx, HxA, TZ, TK, ncomp, lgTZ, lgTK;
   const double2* tw;
   SlabL L;
+  int kb0, nkbc;   // kx blocks [kb0, kb0 + nkbc) of TK (or kKB) columns handled by this launch (kx chunk)
 };
 
 struct YTile {
   int c, kx0, z0;
 };
 __device__ __forceinline__ YTile y_tile(const YArgs& a, int t) {
-  const int nzt = a.Nz / a.TZ, nkb = a.HxA / a.TK;
+  const int nzt = a.Nz / a.TZ, nkb = a.nkbc;
   const int zt = t % nzt, r = t / nzt;
-  return YTile{r / nkb, (r % nkb) * a.TK, zt * a.TZ};
+  return YTile{r / nkb, (a.kb0 + r % nkb) * a.TK, zt * a.TZ};
 }
 
 template <int N, bool INV>
@@ -137,7 +138,7 @@ __global__ void __launch_bounds__(256, 2) k_ypipe(YArgs a) {
   pdl_trigger();
   double2* tws = sm + 2 * NL * LP;
   build_pass_tables<N, true>(tws, a.tw);
-  const int ntiles = a.ncomp * (a.HxA / a.TK) * (a.Nz / a.TZ);
+  const int ntiles = a.ncomp * a.nkbc * (a.Nz / a.TZ);
   int t = blockIdx.x;
   pdl_wait();
   if (t < ntiles) y_issue<N, INV>(a, t, sm);
@@ -181,6 +182,7 @@ struct ZPArgs {
   int ky_off;          // global index of the first local ky (distributed y-slab)
   int Nyl;             // local ky rows
   int Nx, Ny, Hx, TL, scheme, lgTL;
+  int kx0, nkx;        // kx in [kx0, kx0 + nkx) handled by this launch (kx chunk); Hx stays the layout extent
   double h[3], L[3];
   double qh[3];        // 0.25 / h_j      (host-side reciprocals: no FP64 division in the passes)
   double qh2[3];       // 1 / (16 h_j^2)
@@ -291,7 +293,7 @@ __device__ __forceinline__ void z_issue(const ZPArgs& a, int t, double2* buf) {
   constexpr int LP = cline(N);
   const int TL = a.TL;
   const int nyt = a.Nyl / TL;
-  const int kx = t / nyt, ky0 = (t % nyt) * TL;
+  const int kx = a.kx0 + t / nyt, ky0 = (t % nyt) * TL;
   for (int idx = threadIdx.x; idx < NC * TL * N; idx += blockDim.x) {
     const int kz = idx % N, rest = idx / N;
     const int ll = rest & (TL - 1), c = rest >> a.lgTL;
@@ -311,7 +313,7 @@ __global__ void __launch_bounds__(192, 3) k_zpipe(ZPArgs a) {
   load_table(tws, a.twz, N);
   build_pass_tables<N>(tpz, a.twz);
   const int nyt = a.Nyl / TL;
-  const int ntiles = a.Hx * nyt;
+  const int ntiles = a.nkx * nyt;
   int t = blockIdx.x;
   pdl_wait();
   if (t < ntiles) z_issue<N, NC>(a, t, sm);
@@ -323,7 +325,7 @@ __global__ void __launch_bounds__(192, 3) k_zpipe(ZPArgs a) {
     cp_async_wait<1>();
     __syncthreads();
     double2* buf = sm + (i & 1) * NC * TL * LP;
-    const int kx = t / nyt, ky0 = (t % nyt) * TL;
+    const int kx = a.kx0 + t / nyt, ky0 = (t % nyt) * TL;
     fft_lines<N, false>(buf, NC * TL, LP, tpz);
     __syncthreads();
     for (int idx = threadIdx.x; idx < TL * N; idx += blockDim.x) {
@@ -392,9 +394,9 @@ __global__ void __launch_bounds__(NC == 6 ? 96 : 128) __maxnreg__(NC == 6 ? 128 
   const int c = line >> a.lgTL, ll = line & (TL - 1);
   double2* ls = sm + (size_t)line * kZLine;
   const int nyt = a.Nyl / TL;
-  const int ntiles = a.Hx * nyt;
+  const int ntiles = a.nkx * nyt;
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int kx = tile / nyt, ky0 = (tile % nyt) * TL;
+    const int kx = a.kx0 + tile / nyt, ky0 = (tile % nyt) * TL;
     const int kyl = ky0 + ll;
     // z -> offset from the line start: z-slab block (z >> lg_nzs) of stride BS, then z within it
     double2* Bl = a.B + r_index(a.SL, NC, a.Hx, c, kx, kyl, 0);
@@ -534,11 +536,11 @@ __global__ void __launch_bounds__(96, 5) k_zfac256(ZPArgs a) {
   pdl_wait();
   const int line = threadIdx.x >> 4, t = threadIdx.x & 15;   // line = Mandel component in phases A, B, G
   double2* ls = sm + (size_t)line * kZLine;
-  const int ntiles = a.Hx * a.Nyl;
+  const int ntiles = a.nkx * a.Nyl;
   const int BS = 6 * a.Hx * a.SL.nys * a.SL.nzs, zm = a.SL.nzs - 1, lgz = a.SL.lg_nzs;
   auto slot = [](int z) { return z + (z >> 4); };
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int kx = tile / a.Nyl, kyl = tile % a.Nyl;
+    const int kx = a.kx0 + tile / a.Nyl, kyl = tile % a.Nyl;
     const int ky = kyl + a.ky_off;
     double2* Bl = a.B + r_index(a.SL, 6, a.Hx, line, kx, kyl, 0);
     // per-line symbol factors
@@ -713,8 +715,8 @@ __host__ __device__ constexpr int ypitch(int base, int TZ) { return base + (TZ >
 __device__ __forceinline__ void y256_issue_inv(const YArgs& a, int tile, double2* buf) {
   constexpr int N = 256;
   const int TZ = a.TZ;
-  const int nzt = a.Nz / TZ, nkb = a.HxA / kKB;
-  const int zt = tile % nzt, r = tile / nzt, kb = r % nkb, c = r / nkb;
+  const int nzt = a.Nz / TZ, nkb = a.nkbc;
+  const int zt = tile % nzt, r = tile / nzt, kb = a.kb0 + r % nkb, c = r / nkb;
   const int z0 = zt * TZ, kx0 = kb * kKB;
   for (int idx = threadIdx.x; idx < 2 * N * TZ; idx += blockDim.x) {
     const int z2 = idx % TZ, ky = (idx / TZ) & (N - 1), k2l = idx / (TZ * N);
@@ -740,7 +742,7 @@ __global__ void __launch_bounds__(256, 2) k_yreg256(YArgs a) {
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int kl = lane >> 4, t = lane & 15, zz = w;
   const int l = kl * TZ + zz;
-  const int nzt = a.Nz / TZ, nkb = a.HxA / kKB;
+  const int nzt = a.Nz / TZ, nkb = a.nkbc;
   const int ntiles = a.ncomp * nkb * nzt;
   int tile = blockIdx.x;
   if (INV) {
@@ -752,7 +754,7 @@ __global__ void __launch_bounds__(256, 2) k_yreg256(YArgs a) {
   // fwd: the A-side loads of the next tile are issued into v as soon as v is dead (before the
   // B-side stores of the current tile), so they are in flight while the stores drain
   auto arow_of = [&](int tl) {
-    const int zt = tl % nzt, r = tl / nzt, kb = r % nkb, c = r / nkb;
+    const int zt = tl % nzt, r = tl / nzt, kb = a.kb0 + r % nkb, c = r / nkb;
     return a.A + aidx(a.HxA, N, a.Nz, c, zt * TZ + zz, 0, kb * kKB) + kl;
   };
   if (!INV && tile < ntiles) {
@@ -761,7 +763,7 @@ __global__ void __launch_bounds__(256, 2) k_yreg256(YArgs a) {
     for (int j = 0; j < 16; ++j) v[j] = __ldcs(A0 + kKB * (t + 16 * j));
   }
   for (int i = 0; tile < ntiles; ++i, tile += gridDim.x) {
-    const int zt = tile % nzt, r = tile / nzt, kb = r % nkb, c = r / nkb;
+    const int zt = tile % nzt, r = tile / nzt, kb = a.kb0 + r % nkb, c = r / nkb;
     const int z0 = zt * TZ, kx0 = kb * kKB, kx = kx0 + kl;
     double2* Arow = a.A + aidx(a.HxA, N, a.Nz, c, z0 + zz, 0, kx0) + kl;   // element y at Arow[kKB * y]
     if (!INV) {
@@ -898,10 +900,10 @@ __global__ void __launch_bounds__(NC * 64, NC == 6 ? 2 : 8) k_zreg512(ZPArgs a) 
   pdl_wait();
   const int c = threadIdx.x >> 6, t = threadIdx.x & 63;
   double2* ls = sm + (size_t)c * k512Line;
-  const int ntiles = a.Hx * a.Nyl;
+  const int ntiles = a.nkx * a.Nyl;
   const int BS = NC * a.Hx * a.SL.nys * a.SL.nzs, zm = a.SL.nzs - 1, lgz = a.SL.lg_nzs;
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int kx = tile / a.Nyl, kyl = tile % a.Nyl;
+    const int kx = a.kx0 + tile / a.Nyl, kyl = tile % a.Nyl;
     double2* Bl = a.B + r_index(a.SL, NC, a.Hx, c, kx, kyl, 0);
     double2 v[8];
 #pragma unroll
@@ -1000,10 +1002,10 @@ __global__ void __launch_bounds__(NC == 6 ? 96 : 128, NC == 6 ? 4 : 2) k_zreg512
   const int c = line >> a.lgTL, ll = line & (TL - 1);
   double2* ls = sm + (size_t)line * kZ5Line;
   const int nyt = a.Nyl / TL;
-  const int ntiles = a.Hx * nyt;
+  const int ntiles = a.nkx * nyt;
   const int BS = NC * a.Hx * a.SL.nys * a.SL.nzs, zm = a.SL.nzs - 1, lgz = a.SL.lg_nzs;
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int kx = tile / nyt, ky0 = (tile % nyt) * TL;
+    const int kx = a.kx0 + tile / nyt, ky0 = (tile % nyt) * TL;
     const int kyl = ky0 + ll;
     double2* Bl = a.B + r_index(a.SL, NC, a.Hx, c, kx, kyl, 0) + (SLAB ? 0 : t);
     auto zoff = [&](int z) -> size_t { return SLAB ? (size_t)((z >> lgz) * BS + (z & zm)) : (size_t)(z - t); };
@@ -1159,12 +1161,12 @@ __global__ void __launch_bounds__(512, 2) k_yreg512(YArgs a) {
   const int kl = lane >> 4, t = 16 * (w & 3) + (lane & 15), zz = w >> 2;
   const int l = kl * TZ + zz;
   double2* ls = sm + (size_t)l * LPY;
-  const int nzt = a.Nz / TZ, nkb = a.HxA / kKB;
+  const int nzt = a.Nz / TZ, nkb = a.nkbc;
   const int ntiles = a.ncomp * nkb * nzt;
   __syncthreads();
   double2 v[8];
   auto arow_of = [&](int tl) {
-    const int zt = tl % nzt, r = tl / nzt, kb = r % nkb, c = r / nkb;
+    const int zt = tl % nzt, r = tl / nzt, kb = a.kb0 + r % nkb, c = r / nkb;
     return a.A + aidx(a.HxA, N, a.Nz, c, zt * TZ + zz, 0, kb * kKB) + kl;
   };
   if (!INV && (int)blockIdx.x < ntiles) {
@@ -1173,7 +1175,7 @@ __global__ void __launch_bounds__(512, 2) k_yreg512(YArgs a) {
     for (int j = 0; j < 8; ++j) v[j] = __ldcs(A0 + kKB * (t + 64 * j));
   }
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int zt = tile % nzt, r = tile / nzt, kb = r % nkb, c = r / nkb;
+    const int zt = tile % nzt, r = tile / nzt, kb = a.kb0 + r % nkb, c = r / nkb;
     const int z0 = zt * TZ, kx0 = kb * kKB, kx = kx0 + kl;
     double2* Arow = a.A + aidx(a.HxA, N, a.Nz, c, z0 + zz, 0, kx0) + kl;   // element y at Arow[kKB * y]
     if (!INV) {
@@ -1219,6 +1221,71 @@ __global__ void __launch_bounds__(512, 2) k_yreg512(YArgs a) {
       }
     }
   }
+}
+
+// Y pass inverse, Ny = 512, double-buffered: the NEXT tile's B-side input (TZ runs of 16 B per ky,
+// z fastest) is staged by cp.async into the second set of line buffers while the current tile is
+// transformed (k_yreg512<true> waits for its own staging before every tile: long-scoreboard bound).
+// TZ = 2 (256 threads, two buffers of 4 lines, three CTAs per SM); the current buffer doubles as the
+// exchange buffer once its column has been read into registers.
+__global__ void __launch_bounds__(256, 3) k_yreg512i(YArgs a) {
+  if (guard_done(a.guard)) return;   // converged Krylov loop: skip
+  extern __shared__ double2 sm[];
+  constexpr int N = 512;
+  const int TZ = a.TZ;                             // blockDim.x == 128 * TZ
+  const int LPY = ypitch(k512Line, TZ);
+  const int NLB = 2 * TZ;                          // lines per buffer
+  double2* tw1 = sm + (size_t)2 * NLB * LPY;
+  double2* tw2 = tw1 + 448;
+  pdl_trigger();
+  fft512_tables(tw1, tw2, a.tw);
+  pdl_wait();
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int kl = lane >> 4, t = 16 * (w & 3) + (lane & 15), zz = w >> 2;
+  const int l = kl * TZ + zz;
+  const int nzt = a.Nz / TZ, nkb = a.nkbc;
+  const int ntiles = a.ncomp * nkb * nzt;
+  auto issue = [&](int tile, double2* buf) {
+    const int zt = tile % nzt, r = tile / nzt, kb = a.kb0 + r % nkb, c = r / nkb;
+    const int z0 = zt * TZ, kx0 = kb * kKB;
+    for (int idx = threadIdx.x; idx < 2 * N * TZ; idx += blockDim.x) {
+      const int z2 = idx % TZ, ky = (idx / TZ) & (N - 1), k2l = idx / (TZ * N);
+      const int kxo = kx0 + k2l;
+      if (kxo < a.Hx)
+        cp_async16(&buf[(size_t)(k2l * TZ + z2) * LPY + (ky >> 6) * 65 + (ky & 63)],
+                   &a.B[s_index(a.L, a.ncomp, a.Hx, c, kxo, ky, z0 + z2)]);
+    }
+  };
+  int i = 0;
+  if ((int)blockIdx.x < ntiles) issue(blockIdx.x, sm);
+  cp_async_commit();
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++i) {
+    double2* cur = sm + (size_t)(i & 1) * NLB * LPY;
+    double2* nxt = sm + (size_t)((i + 1) & 1) * NLB * LPY;
+    // every thread is done with `nxt` (the previous tile's exchanges) before it is refilled
+    __syncthreads();
+    const int tn = tile + gridDim.x;
+    if (tn < ntiles) issue(tn, nxt);
+    cp_async_commit();
+    cp_async_wait<1>();                            // this tile's staging has landed
+    __syncthreads();
+    const int zt = tile % nzt, r = tile / nzt, kb = a.kb0 + r % nkb, c = r / nkb;
+    const int z0 = zt * TZ, kx = kb * kKB + kl;
+    double2* ls = cur + (size_t)l * LPY;
+    double2 v[8];
+#pragma unroll
+    for (int kc = 0; kc < 8; ++kc) v[kc] = ls[kc * 65 + t];
+    __syncthreads();
+    // CTA-wide barrier 0 inside the FFT (both planes run in step): a constant barrier id keeps the
+    // kernel at one hardware barrier (runtime ids reserve all 16 and cap the CTAs per SM)
+    fft512_reg<true>(v, t, ls, tw1, tw2, 0, 128 * TZ);     // v[m] = y-line value at y = t + 64 m
+    if (kx < a.Hx) {
+      double2* Arow = a.A + aidx(a.HxA, N, a.Nz, c, z0 + zz, 0, kb * kKB) + kl;
+#pragma unroll
+      for (int m = 0; m < 8; ++m) Arow[kKB * (t + 64 * m)] = v[m];
+    }
+  }
+  cp_async_wait<0>();
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -1688,7 +1755,7 @@ static fgd_status launch_persistent(fgd_ctx* c, K kernel, int threads, size_t sm
   int occ = 0;
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, threads, smem);
   if (e != cudaSuccess || occ < 1) occ = 1;
-  *grid_out = grid_cap(std::max(1, std::min(ntiles, num_sms() * occ)));
+  *grid_out = grid_cap(std::max(1, std::min(ntiles, (num_sms() - c->sm_reserve) * occ)));
   return FGD_OK;
 }
 
@@ -1726,16 +1793,31 @@ static SlabL slab_layout(const fgd_ctx* c) {
   return L;
 }
 
-fgd_status pipe_y(fgd_ctx* c, int ncomp, bool inv) {
+fgd_status pipe_y(fgd_ctx* c, int ncomp, bool inv, int kxa, int kxb) {
   const int Ny = c->n[1], Nz = c->nz_l;
+  if (kxb < 0) kxb = c->HxA;   // kx chunk [kxa, kxb): multiples of 4 (kx blocks of kKB or TK <= 4)
   if (Ny == 512 && !std::getenv("FGD_NO_YREG")) {
     const int TZ = std::min(4, std::min(Nz, c->n[2] / c->P));
     const int thr = 128 * TZ;
     const size_t smem = ((size_t)2 * TZ * kY512Line + 448 + 56) * sizeof(double2);
-    const int ntiles = ncomp * (c->HxA / kKB) * (Nz / TZ);
+    const int ntiles = ncomp * ((kxb - kxa) / kKB) * (Nz / TZ);
     YArgs a{c->guard ? c->sc : nullptr, c->specA, c->specB, Nz, c->Hx, c->HxA, TZ, kKB, ncomp, ilog2(TZ), ilog2(kKB), c->tabs.tw[ilog2(Ny)],
-            slab_layout(c)};
+            slab_layout(c), kxa / kKB, (kxb - kxa) / kKB};
     KTimer kt(c, inv ? (ncomp == 6 ? KC_YINV6 : KC_YINV1) : (ncomp == 6 ? KC_YFWD6 : KC_YFWD1));
+    static const int y512i = [] {
+      const char* e = std::getenv("FGD_Y512I");
+      return e ? std::atoi(e) : 1;   // 1: double-buffered inverse (k_yreg512i, TZ = 2)
+    }();
+    if (inv && y512i && std::min(Nz, c->n[2] / c->P) >= 2) {
+      const int TZi = 2;
+      YArgs ai = a;
+      ai.TZ = TZi;
+      ai.lgTZ = 1;
+      const size_t smem_i = ((size_t)4 * TZi * ypitch(k512Line, TZi) + 448 + 56) * sizeof(double2);
+      const int nt_i = ncomp * ((kxb - kxa) / kKB) * (Nz / TZi);
+      FGD_PLAUNCH(c, k_yreg512i, 128 * TZi, smem_i, nt_i, ai);
+      return FGD_OK;
+    }
     if (inv) FGD_PLAUNCH(c, k_yreg512<true>, thr, smem, ntiles, a);
     else FGD_PLAUNCH(c, k_yreg512<false>, thr, smem, ntiles, a);
     return FGD_OK;
@@ -1750,9 +1832,9 @@ fgd_status pipe_y(fgd_ctx* c, int ncomp, bool inv) {
     const int TZ = std::min(inv ? 4 : tzf, std::min(Nz, c->n[2] / c->P));
     const int thr = 32 * TZ;
     const size_t smem = ((inv ? 2 : 1) * (size_t)2 * TZ * kYLine + 240) * sizeof(double2);
-    const int ntiles = ncomp * (c->HxA / kKB) * (Nz / TZ);
+    const int ntiles = ncomp * ((kxb - kxa) / kKB) * (Nz / TZ);
     YArgs a{c->guard ? c->sc : nullptr, c->specA, c->specB, Nz, c->Hx, c->HxA, TZ, kKB, ncomp, ilog2(TZ), ilog2(kKB), c->tabs.tw[ilog2(Ny)],
-            slab_layout(c)};
+            slab_layout(c), kxa / kKB, (kxb - kxa) / kKB};
     KTimer kt(c, inv ? (ncomp == 6 ? KC_YINV6 : KC_YINV1) : (ncomp == 6 ? KC_YFWD6 : KC_YFWD1));
     if (inv) FGD_PLAUNCH(c, k_yreg256<true>, thr, smem, ntiles, a);
     else FGD_PLAUNCH(c, k_yreg256<false>, thr, smem, ntiles, a);
@@ -1774,9 +1856,9 @@ fgd_status pipe_y(fgd_ctx* c, int ncomp, bool inv) {
   TK = std::min(NL / TZ, 4);
   const int thr = std::min(256, r32(TZ * TK * TPL));
   const size_t smem = (2 * (size_t)TZ * TK * cline(Ny) + Ny) * sizeof(double2);
-  const int ntiles = ncomp * (c->HxA / TK) * (Nz / TZ);
+  const int ntiles = ncomp * ((kxb - kxa) / TK) * (Nz / TZ);
   YArgs a{c->guard ? c->sc : nullptr, c->specA, c->specB, Nz, c->Hx, c->HxA, TZ, TK, ncomp, ilog2(TZ), ilog2(TK), c->tabs.tw[ilog2(Ny)],
-          slab_layout(c)};
+          slab_layout(c), kxa / TK, (kxb - kxa) / TK};
   KTimer kt(c, inv ? (ncomp == 6 ? KC_YINV6 : KC_YINV1) : (ncomp == 6 ? KC_YFWD6 : KC_YFWD1));
 #define YPP(NN)                                                                  \
   if (inv) FGD_PLAUNCH(c, (k_ypipe<NN, true>), thr, smem, ntiles, a);            \
@@ -1786,7 +1868,11 @@ fgd_status pipe_y(fgd_ctx* c, int ncomp, bool inv) {
   return FGD_OK;
 }
 
-fgd_status pipe_z(fgd_ctx* c, int ncomp, int mode, double scale, const double* dc_shift, double mean_ell2) {
+fgd_status pipe_z(fgd_ctx* c, int ncomp, int mode, double scale, const double* dc_shift, double mean_ell2, int kxa,
+                  int kxb) {
+  kxb = kxb < 0 ? c->Hx : std::min(kxb, c->Hx);
+  const int nkx = kxb - kxa;
+  if (nkx <= 0) return FGD_OK;
   const int Ny = c->n[1], Nz = c->n[2];
   const int Nyl = c->nranks > 1 ? Ny / c->P : Ny;
   const int TPL = fft_TPL(Nz);
@@ -1795,7 +1881,7 @@ fgd_status pipe_z(fgd_ctx* c, int ncomp, int mode, double scale, const double* d
   TL = std::min(TL, Nyl);
   const int thr = std::min(192, std::max(r32(ncomp * TL * TPL), r32(std::min(TL * Nz, 192))));
   const size_t smem = (2 * (size_t)ncomp * TL * cline(Nz) + 2 * Nz) * sizeof(double2);
-  const int ntiles = c->Hx * (Nyl / TL);
+  const int ntiles = nkx * (Nyl / TL);
   ZPArgs a{};
   a.guard = c->guard ? c->sc : nullptr;
   a.B = c->P > 1 ? c->specC : c->specB;
@@ -1805,6 +1891,8 @@ fgd_status pipe_z(fgd_ctx* c, int ncomp, int mode, double scale, const double* d
   a.Nx = c->n[0];
   a.Ny = Ny;
   a.Hx = c->Hx;
+  a.kx0 = kxa;
+  a.nkx = nkx;
   a.TL = TL;
   a.lgTL = ilog2(TL);
   a.scheme = c->scheme;
@@ -1838,7 +1926,7 @@ fgd_status pipe_z(fgd_ctx* c, int ncomp, int mode, double scale, const double* d
     a.lgTL = ilog2(TLr);
     const int thr_r = 16 * ncomp * TLr;
     const size_t smem_r = ((size_t)ncomp * TLr * kZ5Line + 31 * 16) * sizeof(double2);
-    const int nt_r = c->Hx * (Nyl / TLr);
+    const int nt_r = nkx * (Nyl / TLr);
     if (c->P > 1) {
       if (ncomp == 6) FGD_PLAUNCH(c, (k_zreg512w<6, Z_PROJECT, true>), thr_r, smem_r, nt_r, a);
       else FGD_PLAUNCH(c, (k_zreg512w<1, Z_PRECOND, true>), thr_r, smem_r, nt_r, a);
@@ -1851,7 +1939,7 @@ fgd_status pipe_z(fgd_ctx* c, int ncomp, int mode, double scale, const double* d
   if (Nz == 512 && ((ncomp == 6 && mode == Z_PROJECT) || (ncomp == 1 && mode == Z_PRECOND))) {
     const int thr_r = 64 * ncomp;
     const size_t smem_r = ((size_t)ncomp * k512Line + 448 + 56 + 512) * sizeof(double2);
-    const int nt_r = c->Hx * Nyl;
+    const int nt_r = nkx * Nyl;
     if (ncomp == 6) FGD_PLAUNCH(c, (k_zreg512<6, Z_PROJECT>), thr_r, smem_r, nt_r, a);
     else FGD_PLAUNCH(c, (k_zreg512<1, Z_PRECOND>), thr_r, smem_r, nt_r, a);
     return FGD_OK;
@@ -1862,7 +1950,7 @@ fgd_status pipe_z(fgd_ctx* c, int ncomp, int mode, double scale, const double* d
     a.lgTL = ilog2(TLr);
     const int thr_r = 16 * ncomp * TLr;
     const size_t smem_r = ((size_t)ncomp * TLr * kZLine + 240 + 256) * sizeof(double2);
-    const int nt_r = c->Hx * (Nyl / TLr);
+    const int nt_r = nkx * (Nyl / TLr);
     // factorised form (3 transformed components each way) is opt-in: measured 7.66 vs 4.72 ms per
     // 256^3 sweep -- its serial phases leave half of the CTA idle and spill; the FP64 saving does
     // not pay for that at this occupancy
@@ -1988,12 +2076,7 @@ fgd_status launch_precond_yz(fgd_ctx* c, double scale, double mean_ell2) {
     if (e != cudaSuccess) return set_err(c, FGD_ECUDA, std::string("k_yzy256: ") + cudaGetErrorString(e));
     return FGD_OK;
   }
-  fgd_status s = launch_yfwd(c, 1);
-  if (s == FGD_OK) s = exchange(c, 1, true);
-  if (s == FGD_OK) s = launch_z(c, 1, Z_PRECOND, scale, nullptr, mean_ell2);
-  if (s == FGD_OK) s = exchange(c, 1, false);
-  if (s == FGD_OK) s = launch_yinv(c, 1);
-  return s;
+  return yz_round_trip(c, 1, Z_PRECOND, scale, nullptr, mean_ell2);
 }
 
 }  // namespace fgd

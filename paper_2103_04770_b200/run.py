@@ -67,7 +67,8 @@ def adaptive_schedule(solve, E_end, dE0, dE_max=None, dE_min=1e-5, grow=1.5, gro
 
 
 def run_config(cfg, n_incr=None, tol=(1e-4, 1e-6, 1e-8, 1e-6), max_halvings=6, max_cg=5000, max_helm=5000,
-               adaptive=False, de_min=1e-5, log=False, grow=1.5, stop_frac=None, max_stag=100, warm=False):
+               adaptive=False, de_min=1e-5, log=False, grow=1.5, stop_frac=None, max_stag=100, warm=False,
+               max_newton=50):
     """Load the cell along cfg.load_comp to n_incr * cfg.dE: fixed increments with deterministic
     halving (A-21), or the adaptive schedule (A-34); returns a result dict."""
     import torch
@@ -86,7 +87,8 @@ def run_config(cfg, n_incr=None, tol=(1e-4, 1e-6, 1e-8, 1e-6), max_halvings=6, m
         Et = np.zeros(6)
         Et[cfg.load_comp] = E_try
         st, rep = ctx.solve_increment(Et, np.zeros(6), tol_stag, tol_newton, tol_cg, tol_helm,
-                                      max_stag=max_stag, max_cg=max_cg, max_helm=max_helm, warm_start=warm)
+                                      max_stag=max_stag, max_newton=max_newton, max_cg=max_cg, max_helm=max_helm,
+                                      warm_start=warm)
         for k in ("stag", "newton", "cg", "helm"):
             counts[k] += rep[k]
         if log and st != 0:
@@ -122,7 +124,8 @@ def run_config(cfg, n_incr=None, tol=(1e-4, 1e-6, 1e-8, 1e-6), max_halvings=6, m
             Et = np.zeros(6)
             Et[cfg.load_comp] = E_try
             st, rep = ctx.solve_increment(Et, np.zeros(6), tol_stag, tol_newton, tol_cg, tol_helm,
-                                          max_stag=max_stag, max_cg=max_cg, max_helm=max_helm, warm_start=warm)
+                                          max_stag=max_stag, max_newton=max_newton, max_cg=max_cg, max_helm=max_helm,
+                                      warm_start=warm)
             counts["stag"] += rep["stag"]
             counts["newton"] += rep["newton"]
             counts["cg"] += rep["cg"]
@@ -179,6 +182,7 @@ def main(argv=None):
                    help="adaptive: stop once the load stress falls below this fraction of the peak")
     p.add_argument("--max-stag", type=int, default=100)
     p.add_argument("--warm", action="store_true", help="warm-started Helmholtz PCG (S:262)")
+    p.add_argument("--max-newton", type=int, default=50)
     p.add_argument("--ell", type=float, default=None,
                    help="gtn2d: matrix ell_M / L (ell_I = min(ell_M, 0.001 L); 1e-4 gives the local variant)")
     a = p.parse_args(argv)
@@ -199,7 +203,8 @@ def main(argv=None):
         cfg.dE = a.de
     tol = (1e-8, 1e-10, 1e-11, 1e-11) if a.tight else (1e-4, 1e-6, 1e-8, 1e-6)
     print(json.dumps(run_config(cfg, a.incr, tol, a.halvings, a.max_cg, a.max_cg, adaptive=a.adaptive, log=a.log,
-                                grow=a.grow, stop_frac=a.stop_frac, max_stag=a.max_stag, warm=a.warm)), flush=True)
+                                grow=a.grow, stop_frac=a.stop_frac, max_stag=a.max_stag, warm=a.warm,
+                                max_newton=a.max_newton)), flush=True)
 
 
 if __name__ == "__main__":

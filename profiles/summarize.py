@@ -69,7 +69,9 @@ def full(path):
              "|---|---|---|---|---|---|---|---|---|"]
     seen = set()
     traffic = {}
-    for x in recs:
+    # the LAST capture of each kernel name: the steady launch (e.g. a CG tangent pass after the first,
+    # which skips p_old and x)
+    for x in reversed(recs):
         if x["kernel"] in seen:
             continue
         seen.add(x["kernel"])
@@ -85,8 +87,8 @@ if __name__ == "__main__":
     lt, s = launches(lpath)
     open(os.path.join(HERE, f"{tag}_launches.md"), "w").write(
         f"# {tag}: ncu launch list (cold-cache, serialised; compare shares)\n\n"
-        f"`ncu --metrics gpu__time_duration.sum --clock-control none` over the launches of "
-        f"`bench.py --steps 2 --warmup 3 --no-cpu --no-e2e --no-cufft` (256^3) after set-up; total {s:.2f} ms.\n\n{lt}\n")
+        f"`ncu --metrics gpu__time_duration.sum --clock-control none` over the launches of the bench command "
+        f"(see profiles/{tag}_profile.sh when present); total {s:.2f} ms.\n\n{lt}\n")
     # several reports (comma-separated) are concatenated in order
     ft, traffic = "", {}
     for k, fp in enumerate(fpath.split(",")):
@@ -94,7 +96,7 @@ if __name__ == "__main__":
         ft = t_k if k == 0 else ft + "\n" + "\n".join(t_k.splitlines()[2:])
         traffic.update({key: val for key, val in tr_k.items() if key not in traffic})
     open(os.path.join(HERE, f"{tag}_ncu_full.md"), "w").write(
-        f"# {tag}: `ncu --set full` capture of the hot kernels (256^3 sweep)\n\n{ft}\n")
+        f"# {tag}: `ncu --set full` capture of the hot kernels (last capture of each kernel name)\n\n{ft}\n")
     json.dump(traffic, open(os.path.join(HERE, f"{tag}_traffic.json"), "w"), indent=1)
     print(lt)
     print(ft)

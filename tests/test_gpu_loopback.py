@@ -85,10 +85,14 @@ GRIDS = [(2, (16, 8, 8)), (4, (16, 8, 8)), (2, (32, 16, 16)), (4, (8, 32, 32)), 
          (2, (16, 256, 256)), (4, (8, 512, 512))]
 
 
+@pytest.mark.parametrize("overlap", ["1", "4", "3"])
 @pytest.mark.parametrize("P,n", GRIDS)
-def test_loopback_operators(P, n):
+def test_loopback_operators(P, n, overlap, monkeypatch):
     """Projection (with a stress-controlled macroscopic shift on rank 0's zero frequency), projected
-    tangent, Helmholtz apply (z-halos) and preconditioner on P ranks vs the oracle on the cell."""
+    tangent, Helmholtz apply (z-halos) and preconditioner on P ranks vs the oracle on the cell, with
+    the monolithic transposes (FGD_OVERLAP=1) and the kx-chunked round trip overlapped on a second
+    stream (4 and 3 chunks)."""
+    monkeypatch.setenv("FGD_OVERLAP", overlap)
     L = (1.0, 0.9, 1.1)
     g = Grid(n, L)
     tau = gaussian_field(6, g.shape, 1.0, 2)
