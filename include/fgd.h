@@ -45,7 +45,9 @@ typedef struct fgd_ctx fgd_ctx;
 
 /* Grid.  scheme: 0 = continuous frequencies k = i xi (A-06),
  * 1 = Willot rotated finite-difference scheme (A-04; default).
- * The Helmholtz operator and solver are implemented for scheme 1 only (FGD_EINVAL otherwise). */
+ * The Helmholtz operator is applied as the exact 27-point real-space stencil of the Willot symbol
+ * (scheme 1) or in its Fourier form L^ = 1 + sum_j conj(k_j) F(l^2 F^-1(k_j .)) (A-09;
+ * scheme 0: two 3-component FFT round trips per apply). */
 typedef struct {
   int dims;       /* 2 or 3 */
   int n[3];       /* N1, N2, N3 (N3 = 1 for dims = 2) */

@@ -645,6 +645,7 @@ void fgd_destroy(fgd_ctx* c) {
     if (b) cudaFree(b);
   for (int i = 0; i < 6; ++i)
     if (c->hb[i]) cudaFree(c->hb[i]);
+  if (c->hg) cudaFree(c->hg);
   if (c->pinned) cudaFreeHost(c->pinned);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
@@ -795,7 +796,6 @@ fgd_status fgd_apply_projection(fgd_ctx* c, const double* tau, const double* S, 
 static fgd_status check_field(fgd_ctx* c, int field) {
   TRY(check_ready(c, true, true, false));
   if (field < 0 || field >= c->nfields) return set_err(c, FGD_EINVAL, "field out of range");
-  if (c->scheme != 1) return set_err(c, FGD_EINVAL, "the Helmholtz operator is implemented for the Willot scheme only");
   return FGD_OK;
 }
 

@@ -211,6 +211,7 @@ struct fgd_ctx {
   double* cg_r = nullptr;
   double* cg_p = nullptr;
   double* hb[6] = {};          // helmholtz work vectors: x r z p0 p1 q
+  double* hg = nullptr;        // 3 * nvox: gradient field of the Fourier-form Helmholtz operator
   fgd::DevScalars* sc = nullptr;
   double* partials = nullptr;  // per-CTA partial sums
   size_t partials_cap = 0;
@@ -303,6 +304,11 @@ fgd_status halo_exchange(fgd_ctx* c, const void* field, size_t plane_bytes, void
 // helmholtz.cu
 fgd_status launch_stencil(fgd_ctx* c, int field, int mode, const double* a, const double* zin,
                           const double* pold, double* pout, double* q, int red_op);
+// Fourier form of the Helmholtz operator (continuous scheme, any scheme): y = a + F^-1 sum_j
+// conj(k_j) F(l^2 F^-1(k_j F a)); with zin/pold: a = zin + beta pold is formed first and written to
+// pout, and p.y is reduced with red_op (the PCG step, like launch_stencil's ST_PCG)
+fgd_status helm_fourier(fgd_ctx* c, int field, const double* a, const double* zin, const double* pold, double* pout,
+                        double* y, int red_op);
 double mean_ell2(const fgd_ctx* c, int field);
 
 // constitutive.cu
@@ -329,7 +335,12 @@ enum XFwdMode : int {
   XF_HELM_UPDATE = 3,  // x(out0) += alpha p(in0); r(io) -= alpha q(in1); tau = r ; reduce r.r
   XF_PLAIN_RED = 4,    // tau_c = in0[c]; reduce sum_c tau_c (means)
 };
-enum ZMode : int { Z_PROJECT = 0, Z_PRECOND = 1 };
+enum ZMode : int {
+  Z_PROJECT = 0,   // 6 comps: Galerkin projection G^*(xi)
+  Z_PRECOND = 1,   // 1 comp: scale / (1 + <l^2> |k|^2)
+  Z_GRAD = 2,      // 3 comps (three copies of a^): comp j *= scale k_j          (Fourier-form Helmholtz)
+  Z_DIV = 3,       // 3 comps: comp 0 = scale sum_j conj(k_j) g^_j, comps 1, 2 = 0
+};
 enum XInvMode : int {
   XI_STORE = 0,        // out0 = q
   XI_MECH_CG = 1,      // r(io2) = r_old(in1) - alpha q ; reduce r.r  (x is updated one step late, in

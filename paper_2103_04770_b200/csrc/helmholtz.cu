@@ -16,6 +16,17 @@
 
 namespace fgd {
 
+#define TRYH(x)                   \
+  do {                            \
+    fgd_status s_ = (x);          \
+    if (s_ != FGD_OK) return s_;  \
+  } while (0)
+#define FGD_CHECK_K(c, name)                                                                       \
+  do {                                                                                             \
+    cudaError_t e_ = cudaGetLastError();                                                           \
+    if (e_ != cudaSuccess) return set_err(c, FGD_ECUDA, std::string(name) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
 struct SArgs {
   const DevScalars* guard;
   int Nx, Ny, Nz, TX, TY, TZ;   // Nz: local planes
@@ -239,6 +250,75 @@ __global__ void __launch_bounds__(256, RY == 4 ? 2 : 3) k_stencil(SArgs s, const
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// Fourier form of the Helmholtz operator (the paper's L^ of P:716-718 / A-09 for ANY derivative
+// symbol; required by the continuous scheme k_j = i xi_j, which is not a stencil):
+//   y = a + F^-1 [ sum_j conj(k_j) F( l^2(x) F^-1( k_j F a ) ) ]
+// as two 3-component FFT round trips of the library's passes: forward transform of three copies of
+// a, z pass Z_GRAD (comp j *= k_j / N), inverse -> g_j = D_j a; g_j *= l^2(phase); forward, z pass
+// Z_DIV (comp 0 = sum_j conj(k_j) g^_j / N), inverse of comp 0; y = a + that.  The PCG variant first
+// forms p = z + beta p_old (written to pout) and reduces p.y.
+// ---------------------------------------------------------------------------------------------
+__global__ void k_hf_prep(const DevScalars* guard, size_t n, const double* a, const double* zin, const double* pold,
+                          const DevScalars* sc, double* pout, double* g) {
+  if (guard_done(guard)) return;
+  const double beta = zin ? sc->beta : 0.0;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const double v = zin ? fma(beta, pold[i], zin[i]) : a[i];
+    if (pout) pout[i] = v;
+    g[i] = v;
+    g[n + i] = v;
+    g[2 * n + i] = v;
+  }
+}
+__global__ void k_hf_ell2(const DevScalars* guard, size_t n, double* g, const uint8_t* phase, SArgs s) {
+  if (guard_done(guard)) return;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const double l2 = s.lut[phase[i]];
+    g[i] *= l2;
+    g[n + i] *= l2;
+    g[2 * n + i] *= l2;
+  }
+}
+__global__ void k_hf_add(const DevScalars* guard, size_t n, const double* a, const double* t, double* y) {
+  if (guard_done(guard)) return;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    y[i] = a[i] + t[i];
+}
+
+fgd_status helm_fourier(fgd_ctx* c, int field, const double* a, const double* zin, const double* pold, double* pout,
+                        double* y, int red_op) {
+  const size_t n = c->nvox;
+  if (!c->hg && cudaMalloc((void**)&c->hg, 3 * n * sizeof(double) + 16) != cudaSuccess)
+    return set_err(c, FGD_ENOMEM, "Fourier-form Helmholtz gradient field");
+  TRYH(ensure_spectral(c));
+  const DevScalars* guard = c->guard ? c->sc : nullptr;
+  const int nb = (int)std::min<size_t>((n + 255) / 256, 148 * 8);
+  // p (or a) into the three gradient slots; the value of a itself stays in pout (PCG) or a
+  const double* av = zin ? pout : a;
+  c->launches++;
+  k_hf_prep<<<nb, 256, 0, c->stream>>>(guard, n, a, zin, pold, c->sc, zin ? pout : nullptr, c->hg);
+  FGD_CHECK_K(c, "k_hf_prep");
+  const double inv = 1.0 / (double)c->nvox_g;
+  TRYH(pipe_xfwd_plain(c, 3, c->hg));
+  TRYH(yz_round_trip(c, 3, Z_GRAD, inv, nullptr, 0.0));
+  TRYH(pipe_xinv(c, 3, XI_STORE, c->hg, nullptr, nullptr, nullptr, RED_NONE, 0));
+  SArgs s{};
+  for (int p = 0; p < kMaxPhases; ++p) s.lut[p] = (p < c->nphases) ? c->ell[field][p] * c->ell[field][p] : 0.0;
+  c->launches++;
+  k_hf_ell2<<<nb, 256, 0, c->stream>>>(guard, n, c->hg, c->phase, s);
+  FGD_CHECK_K(c, "k_hf_ell2");
+  TRYH(pipe_xfwd_plain(c, 3, c->hg));
+  TRYH(yz_round_trip(c, 3, Z_DIV, inv, nullptr, 0.0));
+  TRYH(pipe_xinv(c, 1, XI_STORE, c->hg, nullptr, nullptr, nullptr, RED_NONE, 0));   // div term -> hg[0..n)
+  c->launches++;
+  k_hf_add<<<nb, 256, 0, c->stream>>>(guard, n, av, c->hg, y);
+  FGD_CHECK_K(c, "k_hf_add");
+  // p.y with the caller's reduction (the caller runs post_reduce, as after launch_stencil)
+  if (red_op != RED_NONE) TRYH(launch_dot(c, n, av, y, red_op_for(c, red_op), red_slot_for(c, red_op, 0)));
+  return FGD_OK;
+}
+
 double mean_ell2(const fgd_ctx* c, int field) {
   double s = 0.0;
   for (int q = 0; q < c->nphases; ++q) s += (double)c->phase_count[q] * c->ell[field][q] * c->ell[field][q];
@@ -247,6 +327,11 @@ double mean_ell2(const fgd_ctx* c, int field) {
 
 fgd_status launch_stencil(fgd_ctx* c, int field, int mode, const double* a, const double* zin, const double* pold,
                           double* pout, double* q, int red_op) {
+  // the 27-point stencil is the Willot symbol's exact real-space form (R-HELM); any other scheme
+  // (continuous k = i xi, A-06) takes the Fourier form of the operator
+  if (c->scheme != 1)
+    return mode == ST_APPLY ? helm_fourier(c, field, a, nullptr, nullptr, nullptr, q, red_op)
+                            : helm_fourier(c, field, nullptr, zin, pold, pout, q, red_op);
   SArgs s{};
   s.guard = c->guard ? c->sc : nullptr;
   s.Nx = c->n[0];

@@ -339,6 +339,19 @@ __global__ void __launch_bounds__(192, 3) k_zpipe(ZPArgs a) {
         const double k2 = k[0].x * k[0].x + k[0].y * k[0].y + k[1].x * k[1].x + k[1].y * k[1].y + k[2].x * k[2].x +
                           k[2].y * k[2].y;
         *v = cscale(*v, a.scale / (1.0 + a.mean_ell2 * k2));
+      } else if (MODE == Z_GRAD) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          double2* v = &buf[(c * TL + ll) * LP + SWZ(c * TL + ll, kz)];
+          *v = cscale(cmul(k[c], *v), a.scale);
+        }
+      } else if (MODE == Z_DIV) {
+        double2 t = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) t = cadd(t, cmul(conjg(k[c]), buf[(c * TL + ll) * LP + SWZ(c * TL + ll, kz)]));
+        buf[ll * LP + SWZ(ll, kz)] = cscale(t, a.scale);
+        buf[(TL + ll) * LP + SWZ(TL + ll, kz)] = make_double2(0.0, 0.0);
+        buf[(2 * TL + ll) * LP + SWZ(2 * TL + ll, kz)] = make_double2(0.0, 0.0);
       } else {
         double2* v[6];
 #pragma unroll
@@ -1963,6 +1976,8 @@ fgd_status pipe_z(fgd_ctx* c, int ncomp, int mode, double scale, const double* d
 #define ZPP(NN)                                                                                         \
   if (ncomp == 6 && mode == Z_PROJECT) FGD_PLAUNCH(c, (k_zpipe<NN, 6, Z_PROJECT>), thr, smem, ntiles, a);      \
   else if (ncomp == 1 && mode == Z_PRECOND) FGD_PLAUNCH(c, (k_zpipe<NN, 1, Z_PRECOND>), thr, smem, ntiles, a); \
+  else if (ncomp == 3 && mode == Z_GRAD) FGD_PLAUNCH(c, (k_zpipe<NN, 3, Z_GRAD>), thr, smem, ntiles, a);       \
+  else if (ncomp == 3 && mode == Z_DIV) FGD_PLAUNCH(c, (k_zpipe<NN, 3, Z_DIV>), thr, smem, ntiles, a);         \
   else return set_err(c, FGD_EINVAL, "z mode");
   switch (Nz) {
     case 1: ZPP(1); break;

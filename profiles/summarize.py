@@ -40,7 +40,11 @@ def launches(path):
 
 
 def full(path):
-    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    # an .ncu-rep, or its `--page raw --csv` export (512^3 captures are exported on the GPU box)
+    if path.endswith(".csv"):
+        out = open(path).read()
+    else:
+        out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     r = list(csv.reader(out.splitlines()))
     h, units = r[0], r[1]
     scale = {"ns": 1e-6, "us": 1e-3, "usecond": 1e-3, "msecond": 1.0, "ms": 1.0, "nsecond": 1e-6, "s": 1e3,
@@ -71,11 +75,14 @@ def full(path):
     traffic = {}
     # the LAST capture of each kernel name: the steady launch (e.g. a CG tangent pass after the first,
     # which skips p_old and x)
+    # keyed by (name, traffic class): the 6- and 1-component launches of one kernel are separate rows
     for x in reversed(recs):
-        if x["kernel"] in seen:
+        key = (x["kernel"], round(x["dram_GB"] / max(x["dram_GB"], 1e-9) * 0 + x["dram_GB"], 0))
+        if key in seen:
             continue
-        seen.add(x["kernel"])
-        traffic[x["kernel"]] = x["dram_GB"] * 1e9
+        seen.add(key)
+        if x["kernel"] not in traffic or x["dram_GB"] * 1e9 > traffic[x["kernel"]]:
+            traffic[x["kernel"]] = x["dram_GB"] * 1e9
         lines.append(f"| `{x['kernel']}` | {x['ms']:.3f} | {x['dram_GB']:.3f} | {x['dram_pct']:.1f} | "
                      f"{x['l1tex_pct']:.1f} | {x['fp64_pct']:.1f} | {x['warps_pct']:.1f} | {x['regs']} | "
                      f"{x['grid']} x {x['block']} |")

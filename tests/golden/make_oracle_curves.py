@@ -22,6 +22,7 @@ run's wall time.  A run stops at the end of the ramp, when the load stress has f
 (the record says so: "stalled").
 
     python tests/golden/make_oracle_curves.py config0_32      # -> tests/golden/curve_config0_32.json
+    python tests/golden/make_oracle_curves.py config2_256 --E-max 0.0056   # the pre-peak part only
     python tests/golden/make_oracle_curves.py --list
 """
 from __future__ import annotations
@@ -72,7 +73,7 @@ def failure_strain(E, S):
     return None
 
 
-def run_case(name, stop_frac=0.3, de_min_halvings=8, log=None, n_incr=None):
+def run_case(name, stop_frac=0.3, de_min_halvings=8, log=None, n_incr=None, E_max=None):
     build, nin = cases()[name]
     cfg = build()
     n_incr = n_incr or nin or cfg.n_incr
@@ -105,6 +106,8 @@ def run_case(name, stop_frac=0.3, de_min_halvings=8, log=None, n_incr=None):
                 streak = 0
             S = np.array([r["stress"][cfg.load_comp] for r in recs])
             if S.max() > 0 and S[-1] < stop_frac * S.max():
+                break
+            if E_max is not None and E >= E_max - 1e-15:
                 break
         else:
             cut += 1
@@ -139,6 +142,7 @@ def main():
     p.add_argument("--out", default=None)
     p.add_argument("--incr", type=int, default=None)
     p.add_argument("--stop-frac", type=float, default=0.3)
+    p.add_argument("--E-max", type=float, default=None, help="stop after the increment reaching this strain")
     a = p.parse_args()
     if a.list or not a.case:
         print("\n".join(cases()))
@@ -148,7 +152,8 @@ def main():
     def log(r):
         print(json.dumps(r), file=sys.stderr, flush=True)
 
-    res = run_case(a.case, stop_frac=a.stop_frac, log=log, n_incr=a.incr)
+    res = run_case(a.case, stop_frac=a.stop_frac, log=log, n_incr=a.incr, E_max=a.E_max)
+    res["E_max"] = a.E_max
     with open(out, "w") as f:
         json.dump(res, f, indent=1)
     print(json.dumps({k: v for k, v in res.items() if k != "increments"}))
