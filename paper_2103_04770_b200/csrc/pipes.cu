@@ -853,6 +853,8 @@ __global__ void __launch_bounds__(256, 2) k_yreg256(YArgs a) {
 // Calls __syncthreads(): every thread of the CTA must call it.
 constexpr int k512Line = 8 * 65;
 
+constexpr bool kFft512TwProducts = true;
+
 template <bool INV>
 __device__ __forceinline__ void fft512_reg(double2 (&v)[8], int t, double2* ls, const double2* tw1,
                                            const double2* tw2, int bar, int nbar) {
@@ -862,11 +864,33 @@ __device__ __forceinline__ void fft512_reg(double2 (&v)[8], int t, double2* ls, 
     FGD_JIT();
   };
   dft8<INV>(v);
+  // twiddles W^{1,2,4} from the table, W^{3,5,6,7} as products (3 shared loads instead of 7 per
+  // stage: the 512 y/z passes are shared-memory bound; products round to ~2 ulp)
+  auto twiddle7 = [&](const double2* tab, int stride) {
+    double2 w1 = ld_tw(tab), w2 = ld_tw(tab + stride), w4 = ld_tw(tab + 3 * stride);
+    if (INV) {
+      w1.y = -w1.y;
+      w2.y = -w2.y;
+      w4.y = -w4.y;
+    }
+    const double2 w3 = cmul(w1, w2);
+    v[1] = cmul(v[1], w1);
+    v[2] = cmul(v[2], w2);
+    v[3] = cmul(v[3], w3);
+    v[4] = cmul(v[4], w4);
+    v[5] = cmul(v[5], cmul(w4, w1));
+    v[6] = cmul(v[6], cmul(w4, w2));
+    v[7] = cmul(v[7], cmul(w4, w3));
+  };
+  if (kFft512TwProducts) {
+    twiddle7(tw1 + t, 64);
+  } else {
 #pragma unroll
-  for (int ka = 1; ka < 8; ++ka) {
-    double2 w = ld_tw(tw1 + (ka - 1) * 64 + t);
-    if (INV) w.y = -w.y;
-    v[ka] = cmul(v[ka], w);
+    for (int ka = 1; ka < 8; ++ka) {
+      double2 w = ld_tw(tw1 + (ka - 1) * 64 + t);
+      if (INV) w.y = -w.y;
+      v[ka] = cmul(v[ka], w);
+    }
   }
 #pragma unroll
   for (int ka = 0; ka < 8; ++ka) ls[ka * 65 + t] = v[ka];
@@ -876,11 +900,15 @@ __device__ __forceinline__ void fft512_reg(double2 (&v)[8], int t, double2* ls, 
   for (int t2 = 0; t2 < 8; ++t2) v[t2] = ls[ka * 65 + hi + 8 * t2];
   sync();
   dft8<INV>(v);
+  if (kFft512TwProducts) {
+    twiddle7(tw2 + hi, 8);
+  } else {
 #pragma unroll
-  for (int kb = 1; kb < 8; ++kb) {
-    double2 w = ld_tw(tw2 + (kb - 1) * 8 + hi);
-    if (INV) w.y = -w.y;
-    v[kb] = cmul(v[kb], w);
+    for (int kb = 1; kb < 8; ++kb) {
+      double2 w = ld_tw(tw2 + (kb - 1) * 8 + hi);
+      if (INV) w.y = -w.y;
+      v[kb] = cmul(v[kb], w);
+    }
   }
 #pragma unroll
   for (int kb = 0; kb < 8; ++kb) ls[kb * 65 + ka + 8 * hi] = v[kb];
@@ -1157,6 +1185,88 @@ __global__ void __launch_bounds__(NC == 6 ? 96 : 128, NC == 6 ? 4 : 2) k_zreg512
 // threads of each kx of the pair for plane zz = w / 4 (t = 16 (w % 4) + lane % 16), so that the
 // A-side loads / stores are 512 B per warp instruction.  Line l = kl TZ + zz at pitch k512Line + 1.
 constexpr int kY512Line = k512Line + 2;   // max pitch (see ypitch)
+
+// Y pass forward, Ny = 512, wide plan (the 32 x 16 decomposition of k_zreg512w): tile (c, kx pair,
+// TZ = 4 planes), 8 lines of 16 threads (warp w = plane, half-warp = kx of the pair, so that an A-row
+// load of one m is 512 contiguous bytes per warp instruction).  One exchange per transform (swizzled
+// rows), the spectrum staged at slot ky of the line (pitch 513: the z-fastest B-side stores read
+// TZ lines at one ky conflict free), the next tile's A rows loaded into the registers while the
+// B-side stores of this tile run.  Shared accesses per element ~5 (8x8x8 plan: ~8).
+constexpr int kY5Pitch = 513;
+__global__ void __launch_bounds__(128, 3) k_yreg512w(YArgs a) {
+  if (guard_done(a.guard)) return;   // converged Krylov loop: skip
+  extern __shared__ double2 sm[];
+  constexpr int N = 512, TZ = 4;
+  double2* tw = sm + (size_t)2 * TZ * kY5Pitch;   // W512^{t k2} at (k2 - 1) * 16 + (t ^ (k2 & 15))
+  pdl_trigger();
+  for (int i = threadIdx.x; i < 31 * 16; i += blockDim.x) {
+    const int k2 = 1 + (i >> 4), tt = i & 15;
+    tw[(k2 - 1) * 16 + (tt ^ (k2 & 15))] = __ldg(&a.tw[tt * k2]);
+  }
+  __syncthreads();
+  pdl_wait();
+  const int zz = threadIdx.x >> 5, lane = threadIdx.x & 31, kl = lane >> 4, t = lane & 15;
+  double2* ls = sm + (size_t)(kl * TZ + zz) * kY5Pitch;
+  const int nzt = a.Nz / TZ, nkb = a.nkbc;
+  const int ntiles = a.ncomp * nkb * nzt;
+  auto arow_of = [&](int tl) {
+    const int zt = tl % nzt, r = tl / nzt, kb = a.kb0 + r % nkb, c = r / nkb;
+    return a.A + aidx(a.HxA, N, a.Nz, c, zt * TZ + zz, 0, kb * kKB) + kl + kKB * t;
+  };
+  double2 v[32];
+  if ((int)blockIdx.x < ntiles) {
+    const double2* A0 = arow_of(blockIdx.x);
+#pragma unroll
+    for (int m = 0; m < 32; ++m) v[m] = __ldcs(A0 + kKB * 16 * m);
+  }
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int zt = tile % nzt, r = tile / nzt, kb = a.kb0 + r % nkb, c = r / nkb;
+    const int z0 = zt * TZ, kx0 = kb * kKB;
+    // ---- DFT32 over m, twiddle, transpose (row k2, column t), DFT16 over t ----
+    dft32_stage1<false>(v);
+    __syncwarp();
+#pragma unroll
+    for (int k1 = 0; k1 < 4; ++k1) {
+      dft8<false>(v + 8 * k1);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int k2 = k1 + 4 * j;
+        double2 y = v[8 * k1 + j];
+        if (k2 > 0) y = cmul(y, ld_tw(tw + (k2 - 1) * 16 + (t ^ (k2 & 15))));
+        ls[z5x(k2, t)] = y;
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      double2 u[16];
+#pragma unroll
+      for (int n = 0; n < 16; ++n) u[n] = ls[z5x(t + 16 * h, n)];
+      dft16<false>(u);                                     // u[k1] = X[ky = t + 16 h + 32 k1]
+#pragma unroll
+      for (int k1 = 0; k1 < 16; ++k1) v[16 * h + k1] = u[k1];
+    }
+    __syncwarp();
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int k1 = 0; k1 < 16; ++k1) ls[t + 16 * h + 32 * k1] = v[16 * h + k1];
+    __syncthreads();
+    const int tn = tile + gridDim.x;                       // next tile's A rows in flight during the stores
+    if (tn < ntiles) {
+      const double2* An = arow_of(tn);
+#pragma unroll
+      for (int m = 0; m < 32; ++m) v[m] = __ldcs(An + kKB * 16 * m);
+    }
+    for (int idx = threadIdx.x; idx < 2 * N * TZ; idx += blockDim.x) {
+      const int z2 = idx % TZ, ky = (idx / TZ) & (N - 1), k2l = idx / (TZ * N);
+      const int kxo = kx0 + k2l;
+      if (kxo < a.Hx) a.B[s_index(a.L, a.ncomp, a.Hx, c, kxo, ky, z0 + z2)] = sm[(size_t)(k2l * TZ + z2) * kY5Pitch + ky];
+    }
+    __syncthreads();
+  }
+}
+
 
 template <bool INV>
 __global__ void __launch_bounds__(512, 2) k_yreg512(YArgs a) {
@@ -1829,6 +1939,19 @@ fgd_status pipe_y(fgd_ctx* c, int ncomp, bool inv, int kxa, int kxb) {
       const size_t smem_i = ((size_t)4 * TZi * ypitch(k512Line, TZi) + 448 + 56) * sizeof(double2);
       const int nt_i = ncomp * ((kxb - kxa) / kKB) * (Nz / TZi);
       FGD_PLAUNCH(c, k_yreg512i, 128 * TZi, smem_i, nt_i, ai);
+      return FGD_OK;
+    }
+    static const int y512w = [] {
+      const char* e = std::getenv("FGD_Y512W");
+      return e ? std::atoi(e) : 1;   // 1: wide 32 x 16 forward (k_yreg512w, TZ = 4)
+    }();
+    if (!inv && y512w && std::min(Nz, c->n[2] / c->P) >= 4) {
+      YArgs aw = a;
+      aw.TZ = 4;
+      aw.lgTZ = 2;
+      const size_t smem_w = ((size_t)8 * kY5Pitch + 31 * 16) * sizeof(double2);
+      const int nt_w = ncomp * ((kxb - kxa) / kKB) * (Nz / 4);
+      FGD_PLAUNCH(c, k_yreg512w, 128, smem_w, nt_w, aw);
       return FGD_OK;
     }
     if (inv) FGD_PLAUNCH(c, k_yreg512<true>, thr, smem, ntiles, a);

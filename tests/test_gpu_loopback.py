@@ -219,3 +219,89 @@ def test_loopback_increments(P):
     assert st.ep.max() > 0.0
     assert np.abs(gather([r[1] for r in res]).reshape(-1) - st.ep).max() <= 1e-8
     assert rel(gather([r[2] for r in res]), st.abar[1]) <= 1e-6
+
+
+@pytest.mark.parametrize("P,n", [(2, (16, 8, 8)), (4, (8, 32, 32)), (2, (16, 256, 256))])
+def test_loopback_continuous_helmholtz(P, n):
+    """The Fourier-form Helmholtz operator (continuous scheme: two 3-component FFT round trips with
+    the slab transposes) and its PCG on P ranks vs the oracle's Fourier form."""
+    L = (1.0, 0.9, 1.1)
+    g = Grid(n, L, "continuous")
+    ph = bernoulli_phases(g.shape, 0.3, 41)
+    ell = np.array([[0.08, 0.02]])
+    a = gaussian_field(1, g.shape, 1.0, 42)[0]
+
+    def body(r, ctx, z0, nz):
+        ctx.set_phases(slab(ph, z0, nz), 2)
+        ctx.set_nonlocal(ell, [0])
+        yh = ctx.apply_helmholtz(0, slab(a, z0, nz)).cpu().numpy()
+        o1 = torch.empty((nz,) + g.shape[1:], dtype=torch.float64, device="cuda")
+        ctx.solve_helmholtz(0, slab(np.abs(a), z0, nz), o1, tol=0.0, maxit=4)
+        return yh, o1.cpu().numpy()
+
+    lid = loopback_id()
+    out = [None] * P
+    errs = []
+
+    def worker(r):
+        try:
+            torch.cuda.set_device(0)
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                ctx = Context(n, L, scheme=0, rank=r, nranks=P, nccl_id=lid, stream=s.cuda_stream)
+                try:
+                    out[r] = body(r, ctx, ctx.z0, ctx.nz)
+                    s.synchronize()
+                finally:
+                    ctx.close()
+        except BaseException as e:   # noqa: BLE001
+            errs.append(e)
+
+    th = [threading.Thread(target=worker, args=(r,)) for r in range(P)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=900)
+    if errs:
+        raise errs[0]
+    e2 = ell2_field(ph, ell[0])
+    assert rel(gather([o[0] for o in out]), apply_helmholtz(g, a, e2)) <= 1e-10
+    ref, _, _ = solve_helmholtz(g, np.abs(a), e2, tol=0.0, maxit=4)
+    assert rel(gather([o[1] for o in out]), ref) <= 1e-10
+
+
+def test_loopback_increments_warm_start():
+    """Two staggered increments on 2 ranks with warm-started Helmholtz PCG on both sides (R-WARM)."""
+    cfg = synth.config3(n=16, n_spheres=4, phi=0.2, seed=3)
+    cfg.dE = 2.0e-3
+    tol = Tolerances(tol_stag=1e-9, tol_newton=1e-10, tol_cg=1e-11, tol_helm=1e-11, warm_start=True)
+    cell = make_cell(cfg)
+    st = State.zero(cell)
+    refs = []
+    for i in (1, 2):
+        Et = np.zeros(6)
+        Et[cfg.load_comp] = i * cfg.dE
+        st, rep = solve_increment(cell, st, Et, np.zeros(6), tol)
+        assert rep.converged
+        refs.append(rep.macro_stress.copy())
+
+    def body(r, ctx, z0, nz):
+        ctx.set_phases(slab(cfg.phases, z0, nz), len(cfg.materials))
+        for q, m in enumerate(cfg.materials):
+            ctx.set_material(q, Material.of(m))
+        ctx.set_nonlocal(np.asarray(cfg.ell), cfg.source_phase)
+        ctx.set_control(cfg.stress_mask)
+        got = []
+        for i in (1, 2):
+            Et = np.zeros(6)
+            Et[cfg.load_comp] = i * cfg.dE
+            s, rp = ctx.solve_increment(Et, np.zeros(6), tol.tol_stag, tol.tol_newton, tol.tol_cg, tol.tol_helm,
+                                        tol.max_stag, tol.max_newton, tol.max_cg, tol.max_helm, warm_start=True)
+            assert s == 0, rp
+            got.append(rp["macro_stress"])
+        return got
+
+    res = run_ranks(2, cfg.n, cfg.L, body)
+    for i in range(2):
+        for r in range(2):
+            assert rel(res[r][i], refs[i]) <= 1e-6, (i, r)

@@ -170,10 +170,11 @@ def test_errors_and_edge_cases():
 
 @pytest.mark.parametrize("n", [128, 256])
 def test_full_size_operators_256(n):
-    """The bench workload size (config-1 recipe at 256^3) in the launch configuration bench.py
-    times.  Projected tangent: at sampled frequencies xi the oracle evaluates, one by one,
-    F(y)(xi) = G^*(xi) F(C:x)(xi) (explicit separable DFT sums of the inputs and of the GPU
-    output); Helmholtz apply and preconditioner: every voxel against the oracle."""
+    """The config-1 sizes (128^3, and 256^3 of the bench's by_size line) in the launch configuration
+    bench.py times.  Projected tangent: at sampled frequencies xi the oracle evaluates, one by one,
+    F(y)(xi) = G^*(xi) F(C:x)(xi) (explicit separable DFT sums of the inputs and of the GPU output),
+    and then every voxel against the oracle's full apply; Helmholtz apply and preconditioner: every
+    voxel against the oracle."""
     import synth
     from oracle.projection import project_spectrum
     from oracle.spectral import cis
@@ -215,7 +216,15 @@ def test_full_size_operators_256(n):
                                    dc_index=(0,))[:, 1]
         scale = max(np.linalg.norm(ft), 1e-300)
         assert np.linalg.norm(fy - ref) <= 1e-10 * scale, (kx, ky, kz)
-    del tau, Cd
+    del tau
+    # and every voxel: the oracle's projected tangent on the whole field (the unpacked 6x6
+    # tangent is 4.8 GB of host memory at 256^3)
+    Cn = unpack21(Cd.cpu().numpy()).reshape((6, 6) + g.shape)
+    del Cd
+    ref_full = apply_projected_tangent(g, Cn, x.cpu().numpy(), mask)
+    del Cn
+    assert rel(y.cpu().numpy(), ref_full) <= TOL_APPLY
+    del ref_full
     ph = synth.config1_phases(n, 0)
     ctx.set_phases(dev(ph), 2)
     ctx.set_nonlocal(synth.CONFIG1_ELL, [0])

@@ -34,3 +34,23 @@ def test_gives_up_below_min_step():
     assert not ok and acc[-1] < 0.002
     # every failure halves: reaching 1e-5 from 1e-3 takes at most log2(100) + 1 cuts per stall
     assert cuts <= 8 * 2
+
+
+def test_doubling_schedule_and_early_stop():
+    """grow = 2 (the golden curves' rule: halve on failure, x2 after two first-try successes, never
+    beyond dE) keeps every accepted target a dyadic multiple of dE, and stop() ends the run after
+    the accepted increment that triggers it."""
+    last = [0.0]
+
+    def solve(E):
+        ok = E - last[0] <= 2.5e-4 + 1e-15 or E <= 0.002 + 1e-15
+        if ok:
+            last[0] = E
+        return ok
+
+    acc, cuts, ok = adaptive_schedule(solve, 0.004, 1e-3, grow=2.0, stop=lambda: last[0] >= 0.003 - 1e-15)
+    assert ok and cuts >= 2
+    assert acc[-1] == pytest.approx(0.003, abs=1e-15)          # stopped, not run to 0.004
+    for E in acc:
+        q = E / 2.5e-4
+        assert abs(q - round(q)) < 1e-9                           # dyadic targets
