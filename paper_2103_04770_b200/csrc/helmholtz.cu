@@ -13,6 +13,7 @@
 #include <cstdlib>
 
 #include "reduce.cuh"
+#include "tma.cuh"
 
 namespace fgd {
 
@@ -90,41 +91,137 @@ constexpr int kRing = 5;
 // phase ids of a plane: rows y0-1 .. y0+TY-1, 4-byte words covering x0-4 .. x0+TX+3 (aligned, so
 // that the periodic wrap never splits a word); byte of x at (x - x0 + 4)
 constexpr int kPhW = SBX + 8;
+// BULK staging (TMA engine, 1-D bulk copies): plane rows at pitch SBX + 4 holding x0-2 .. x0+TX+1
+// (16 B aligned runs), phase rows at pitch kPhWB holding x0-16 .. x0+TX-1
+constexpr int kPhWB = SBX + 16;
 template <int RY>
-constexpr size_t stencil_smem(int na) {
-  return (size_t)kRing * na * (SBX + 2) * (SBY * RY + 2) * sizeof(double) + (size_t)kRing * (SBY * RY + 1) * kPhW;
+constexpr size_t stencil_smem(int na, bool bulk = false) {
+  return bulk ? (size_t)kRing * na * (SBX + 4) * (SBY * RY + 2) * sizeof(double) + (size_t)kRing * (SBY * RY + 1) * kPhWB
+              : (size_t)kRing * na * (SBX + 2) * (SBY * RY + 2) * sizeof(double) + (size_t)kRing * (SBY * RY + 1) * kPhW;
 }
 __device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(gmem) : "memory");
 }
 
-template <int MODE, int RY>
+// FACT = true (default): the vertex fluxes and their D^T scatter in factored form.  D_j = Delta_j A_k A_l
+// (forward difference along j, 2-point sums along the other two axes; all of them commute), so per
+// level the 2 x 2 x 2 cube of a vertex is reduced through the z pair sums / differences
+// S = a(z+1) + a(z), Dd = a(z+1) - a(z) of each column, their y pair sums and x pair sums, which the
+// neighbouring vertices of the thread share:  D_x ~ sy(c+1) - sy(c), D_y ~ sx(r+1) - sx(r),
+// D_z ~ dy(c) + dy(c+1).  The scatter D_j^T is factored the same way: per vertex row
+// P = f_x(x-1) - f_x(x), Q = f_y(x-1) + f_y(x), R = f_z(x-1) + f_z(x); voxel row k takes
+// E = (P + Q)(k) + (P - Q)(k+1) and Fz = R(k) + R(k+1), i.e. E - Fz on this level and E + Fz on the
+// next.  Same operator, ~64 instead of ~113 FP64 operations per voxel (RY = 2); the
+// additions are associated differently, so results agree with FACT = false to rounding only.
+//
+// BULK = true (opt-in, FGD_ST_BULK=1; needs N1 % 16 == 0): each plane of the ring arrives by 1-D bulk copies (the TMA
+// engine; one per row and array, split in two or three only where the row wraps periodically),
+// issued by warp 0 and completed on the slot's mbarrier -- no per-element copy instructions or index
+// arithmetic in the other warps.  Measured and rejected at 512^3: 2.73 vs 1.73 ms per PCG stencil --
+// ~100 row copies of 16-288 B per plane keep the bulk-copy engine busy far longer than the same bytes
+// as per-thread 8 B cp.async.
+template <int MODE, int RY, bool FACT, bool BULK>
 __global__ void __launch_bounds__(256, RY == 4 ? 2 : 3) k_stencil(SArgs s, const double* __restrict__ ain, const double* __restrict__ pold,
                                                      double* __restrict__ pout, double* __restrict__ q,
                                                      const uint8_t* __restrict__ phase, DevScalars* sc, double* partials,
                                                      int red_op, int red_slot) {
   if (guard_done(s.guard)) return;   // converged Krylov loop: skip
   constexpr int NA = MODE == ST_PCG ? 2 : 1;
-  constexpr int PX = SBX + 2, PY = SBY * RY + 2, PL = PX * PY, PHL = (SBY * RY + 1) * kPhW;
+  constexpr int PHW = BULK ? kPhWB : kPhW;
+  constexpr int PX = BULK ? SBX + 4 : SBX + 2, PY = SBY * RY + 2, PL = PX * PY, PHL = (SBY * RY + 1) * PHW;
+  constexpr int XO = BULK ? 1 : 0, PO = BULK ? 15 : 3;   // ring column of x - 1, phase byte of x - 1
   extern __shared__ double ring[];                 // [kRing][NA][PL], then phase ids [kRing][PHL]
   uint8_t* phs = reinterpret_cast<uint8_t*>(ring + (size_t)kRing * NA * PL);
+  __shared__ uint64_t fullb[kRing];
   __shared__ double lut[kMaxPhases];
+  __shared__ double2 lutw[kMaxPhases][2];          // FACT: (l^2 w_x, l^2 w_y), (l^2 w_z, 0) per phase
   const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * SBX + tx, nthr = SBX * blockDim.y;
   const int TX = s.TX, TY = s.TY, TZ = s.TZ;      // TY = blockDim.y * RY
   const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY, z0 = blockIdx.z * TZ;
   const int Nx = s.Nx, Ny = s.Ny, Nz = s.Nz;
   pdl_trigger();
-  if (tid < kMaxPhases) lut[tid] = s.lut[tid];
+  const bool iso = FACT && s.ih[0] == s.ih[1] && s.ih[1] == s.ih[2];
+  if (tid < kMaxPhases) {
+    lut[tid] = iso ? s.lut[tid] * (s.ih[0] * s.ih[0]) : s.lut[tid];   // FACT + iso: l^2 w
+    const double l2 = s.lut[tid];
+    lutw[tid][0] = make_double2(l2 * (s.ih[0] * s.ih[0]), l2 * (s.ih[1] * s.ih[1]));
+    lutw[tid][1] = make_double2(l2 * (s.ih[2] * s.ih[2]), 0.0);
+  }
+  if (BULK && tid == 0) {
+    for (int i = 0; i < kRing; ++i) mbar_init(&fullb[i], 1);
+    fence_mbar_init();
+  }
+  if (BULK) __syncthreads();
   pdl_wait();
   const double beta = (MODE == ST_PCG) ? sc->beta : 0.0;
   const bool act = tx < TX;
   const int gx = x0 + tx, gyb = y0 + ty * RY;
   // D^T D carries 1/(4h_j) twice
   const double w0 = s.ih[0] * s.ih[0], w1 = s.ih[1] * s.ih[1], w2 = s.ih[2] * s.ih[2];
-  const int PW = TX + 2, PN = (TY + 2) * PW;
+  const int PW = TX + 2, WYb = blockDim.y;
+  const bool cp0 = tx < PW, cp1 = tx + 32 < PW;
+  const int cx0 = wrapi(x0 - 1 + tx, Nx), cx1 = cp1 ? wrapi(x0 + 31 + tx, Nx) : 0;
+  const int nw = (TX + 8) / 4, cw = tx < nw ? wrapi(x0 - 4 + 4 * tx, Nx) : 0;
+  // bytes of one ring slot (BULK): the split copies of a wrapping row add up to the same total
+  const unsigned slot_bytes = (unsigned)((TY + 2) * (TX + 4) * 8 * NA + (TY + 1) * (16 + TX));
+  const bool wl = x0 == 0, wr = x0 + TX == Nx;
+  // one plane row (global row start g) -> ring row d: x0-2 .. x0+TX+1
+  auto copy_row = [&](double* d, const double* g, uint64_t* bar) {
+    if (!wl && !wr) {
+      bulk_g2s(d, g + x0 - 2, (unsigned)(TX + 4) * 8, bar);
+    } else {
+      bulk_g2s(d, g + (wl ? Nx - 2 : x0 - 2), 16, bar);
+      bulk_g2s(d + 2, g + x0, (unsigned)TX * 8, bar);
+      bulk_g2s(d + TX + 2, g + (wr ? 0 : x0 + TX), 16, bar);
+    }
+  };
+  auto issue_bulk = [&](int pi) {
+    if (pi > TZ + 1 || ty != 0) return;
+    const int zl = z0 - 1 + pi;
+    const double* pa;
+    const double* pp;
+    if (s.dist && zl < 0) {
+      pa = s.a_lo;
+      pp = s.p_lo;
+    } else if (s.dist && zl >= Nz) {
+      pa = s.a_hi;
+      pp = s.p_hi;
+    } else {
+      const size_t base = (size_t)wrapi(zl, Nz) * Ny * Nx;
+      pa = ain + base;
+      pp = pold + base;
+    }
+    const uint8_t* pb = (s.dist && zl < 0) ? s.ph_lo : phase + (size_t)wrapi(zl, Nz) * Ny * Nx;
+    const int slot = pi % kRing;
+    double* d = ring + (size_t)slot * NA * PL;
+    uint8_t* dph = phs + (size_t)slot * PHL;
+    uint64_t* bar = &fullb[slot];
+    if (tx == 0) {
+      fence_proxy_async();                        // the slot's earlier generic reads before the async writes
+      mbar_arrive_expect_tx(bar, slot_bytes);
+    }
+    __syncwarp();
+    for (int row = tx; row < TY + 2; row += 32) {
+      const size_t r = (size_t)wrapi(y0 - 1 + row, Ny) * Nx;
+      copy_row(d + row * PX, pa + r, bar);
+      if (MODE == ST_PCG) copy_row(d + PL + row * PX, pp + r, bar);
+      if (row < TY + 1) {                         // phase bytes x0-16 .. x0+TX-1
+        if (!wl) {
+          bulk_g2s(dph + row * PHW, pb + r + x0 - 16, (unsigned)(16 + TX), bar);
+        } else {
+          bulk_g2s(dph + row * PHW, pb + r + Nx - 16, 16, bar);
+          bulk_g2s(dph + row * PHW + 16, pb + r, (unsigned)TX, bar);
+        }
+      }
+    }
+  };
   // plane index pi = 0 .. TZ + 1 <-> level z0 - 1 + pi; one commit group per plane (possibly empty)
   auto issue = [&](int pi) {
+    if (BULK) {
+      issue_bulk(pi);
+      return;
+    }
     if (pi <= TZ + 1) {
       const int zl = z0 - 1 + pi;
       const double* pa;
@@ -140,21 +237,27 @@ __global__ void __launch_bounds__(256, RY == 4 ? 2 : 3) k_stencil(SArgs s, const
         pa = ain + base;
         pp = pold + base;
       }
+      // thread (tx, ty) copies columns px = tx and px = tx + 32 (the two right halo columns when
+      // TX = 32) of the rows py = ty, ty + WY, ...; the column offsets are fixed per thread (no
+      // per-element index arithmetic: it dominated the instruction mix)
       double* d = ring + (size_t)(pi % kRing) * NA * PL;
-      for (int e = tid; e < PN; e += nthr) {
-        const int py = e / PW, px = e - py * PW;
-        const size_t r = (size_t)wrapi(y0 - 1 + py, Ny) * Nx + wrapi(x0 - 1 + px, Nx);
-        cp_async8(d + py * PX + px, pa + r);
-        if (MODE == ST_PCG) cp_async8(d + PL + py * PX + px, pp + r);
+      for (int py = ty; py < TY + 2; py += WYb) {
+        const size_t r = (size_t)wrapi(y0 - 1 + py, Ny) * Nx;
+        double* drow = d + py * PX;
+        if (cp0) {
+          cp_async8(drow + tx, pa + r + cx0);
+          if (MODE == ST_PCG) cp_async8(drow + PL + tx, pp + r + cx0);
+        }
+        if (cp1) {
+          cp_async8(drow + tx + 32, pa + r + cx1);
+          if (MODE == ST_PCG) cp_async8(drow + PL + tx + 32, pp + r + cx1);
+        }
       }
       const uint8_t* pb = (s.dist && zl < 0) ? s.ph_lo : phase + (size_t)wrapi(zl, Nz) * Ny * Nx;
       uint8_t* dph = phs + (size_t)(pi % kRing) * PHL;
-      const int nw = (TX + 8) / 4;                 // words per row (TX is a multiple of 4)
-      for (int e = tid; e < (TY + 1) * nw; e += nthr) {
-        const int row = e / nw, wd = e - row * nw;
-        const size_t r = (size_t)wrapi(y0 - 1 + row, Ny) * Nx + wrapi(x0 - 4 + 4 * wd, Nx);
-        cp_async4(dph + row * kPhW + 4 * wd, pb + r);
-      }
+      if (tx < nw)                                  // words per row: (TX + 8) / 4 <= 10
+        for (int row = ty; row < TY + 1; row += WYb)
+          cp_async4(dph + row * kPhW + 4 * tx, pb + (size_t)wrapi(y0 - 1 + row, Ny) * Nx + cw);
     }
     cp_async_commit_s();
   };
@@ -165,19 +268,19 @@ __global__ void __launch_bounds__(256, RY == 4 ? 2 : 3) k_stencil(SArgs s, const
     for (int r = 0; r < RY + 2; ++r)
 #pragma unroll
       for (int dx = 0; dx < 3; ++dx) {
-        const int o = (ty * RY + r) * PX + tx + dx;
+        const int o = (ty * RY + r) * PX + tx + dx + XO;
         A[r][dx] = MODE == ST_PCG ? fma(beta, pa[PL + o], pa[o]) : pa[o];
       }
   };
   // fluxes of the vertices of level zl (between Alo = level zl and Ahi = level zl + 1):
   // cur[k] += contribution to voxel (x, gyb + k, zl), nxt[k] += contribution to voxel (.., zl + 1)
   auto vertices = [&](int pi, double* cur, double* nxt) {
-    const uint8_t* ph = phs + (size_t)(pi % kRing) * PHL + ty * RY * kPhW + tx + 3;
+    const uint8_t* ph = phs + (size_t)(pi % kRing) * PHL + ty * RY * PHW + tx + PO;
 #pragma unroll
     for (int vr = 0; vr <= RY; ++vr) {            // vertex row yv = gyb - 1 + vr: A rows vr, vr + 1
 #pragma unroll
       for (int cx = 0; cx < 2; ++cx) {            // xv = x - 1 + cx: A columns cx, cx + 1
-        const double l2 = lut[ph[vr * kPhW + cx]];
+        const double l2 = lut[ph[vr * PHW + cx]];
         const double a000 = Alo[vr][cx], a100 = Alo[vr][cx + 1], a010 = Alo[vr + 1][cx], a110 = Alo[vr + 1][cx + 1];
         const double a001 = Ahi[vr][cx], a101 = Ahi[vr][cx + 1], a011 = Ahi[vr + 1][cx], a111 = Ahi[vr + 1][cx + 1];
         const double f0 = l2 * w0 * ((a100 - a000) + (a110 - a010) + (a101 - a001) + (a111 - a011));
@@ -195,12 +298,74 @@ __global__ void __launch_bounds__(256, RY == 4 ? 2 : 3) k_stencil(SArgs s, const
       }
     }
   };
+  // factored form of vertices() (see the note above the kernel)
+  auto vertices_f = [&](int pi, double* cur, double* nxt) {
+    const uint8_t* ph = phs + (size_t)(pi % kRing) * PHL + ty * RY * PHW + tx + PO;
+    double Sp[3], Dp[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      Sp[c] = Ahi[0][c] + Alo[0][c];
+      Dp[c] = Ahi[0][c] - Alo[0][c];
+    }
+    double sxp0 = Sp[0] + Sp[1], sxp1 = Sp[1] + Sp[2];
+    double Up = 0.0, Rp = 0.0;
+#pragma unroll
+    for (int vr = 0; vr <= RY; ++vr) {            // vertex row yv = gyb - 1 + vr: A rows vr, vr + 1
+      double Sn[3], Dn[3];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        Sn[c] = Ahi[vr + 1][c] + Alo[vr + 1][c];
+        Dn[c] = Ahi[vr + 1][c] - Alo[vr + 1][c];
+      }
+      const double sxn0 = Sn[0] + Sn[1], sxn1 = Sn[1] + Sn[2];
+      const double sy0 = Sp[0] + Sn[0], sy1 = Sp[1] + Sn[1], sy2 = Sp[2] + Sn[2];
+      const double dy0 = Dp[0] + Dn[0], dy1 = Dp[1] + Dn[1], dy2 = Dp[2] + Dn[2];
+      double2 wa0, wb0, wa1, wb1;
+      if (iso) {                                  // h_x = h_y = h_z: one l^2 w per vertex
+        const double l0 = lut[ph[vr * PHW]], l1 = lut[ph[vr * PHW + 1]];
+        wa0 = make_double2(l0, l0);
+        wb0 = make_double2(l0, 0.0);
+        wa1 = make_double2(l1, l1);
+        wb1 = make_double2(l1, 0.0);
+      } else {
+        wa0 = lutw[ph[vr * PHW]][0];
+        wb0 = lutw[ph[vr * PHW]][1];
+        wa1 = lutw[ph[vr * PHW + 1]][0];
+        wb1 = lutw[ph[vr * PHW + 1]][1];
+      }
+      // vertex xv = x - 1 (columns 0, 1) and xv = x (columns 1, 2)
+      const double fx0 = wa0.x * (sy1 - sy0), fx1 = wa1.x * (sy2 - sy1);
+      const double fy0 = wa0.y * (sxn0 - sxp0), fy1 = wa1.y * (sxn1 - sxp1);
+      const double fz0 = wb0.x * (dy0 + dy1), fz1 = wb1.x * (dy1 + dy2);
+      const double P = fx0 - fx1, Q = fy0 + fy1, R = fz0 + fz1;
+      const double U = P + Q, V = P - Q;
+      if (vr >= 1) {                              // voxel row vr - 1: vertex rows vr - 1 (U) and vr (V)
+        const double E = Up + V, Fz = Rp + R;
+        cur[vr - 1] += E - Fz;
+        nxt[vr - 1] += E + Fz;
+      }
+      Up = U;
+      Rp = R;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        Sp[c] = Sn[c];
+        Dp[c] = Dn[c];
+      }
+      sxp0 = sxn0;
+      sxp1 = sxn1;
+    }
+  };
   double cur[RY], nxt[RY];
   double red = 0.0;
 #pragma unroll
   for (int k = 0; k < RY; ++k) nxt[k] = 0.0;
   for (int pi = 0; pi < kRing; ++pi) issue(pi);
-  cp_async_wait_s<kRing - 2>();       // planes 0 and 1 (levels z0 - 1, z0) have landed
+  if (BULK) {
+    mbar_wait(&fullb[0], 0);
+    mbar_wait(&fullb[1], 0);
+  } else {
+    cp_async_wait_s<kRing - 2>();     // planes 0 and 1 (levels z0 - 1, z0) have landed
+  }
   __syncthreads();
   if (act) {
     readcol(0, Alo);
@@ -208,12 +373,13 @@ __global__ void __launch_bounds__(256, RY == 4 ? 2 : 3) k_stencil(SArgs s, const
     double scratch[RY];
 #pragma unroll
     for (int k = 0; k < RY; ++k) scratch[k] = 0.0;
-    vertices(0, scratch, nxt);
+    if (FACT) vertices_f(0, scratch, nxt); else vertices(0, scratch, nxt);
   }
   __syncthreads();                    // planes 0 and 1 have been read by every thread
   for (int zz = 0; zz < TZ; ++zz) {
     const int z = z0 + zz;
-    cp_async_wait_s<kRing - 3>();     // plane zz + 2 (level z + 1) has landed
+    if (BULK) mbar_wait(&fullb[(zz + 2) % kRing], ((zz + 2) / kRing) & 1);
+    else cp_async_wait_s<kRing - 3>();   // plane zz + 2 (level z + 1) has landed
     __syncthreads();
     // the slot of plane zz was last read at iteration zz - 1 (its phase ids, by vertices(zz)) or in
     // the prologue: every thread has passed the barrier above since, so it can be refilled now
@@ -229,7 +395,7 @@ __global__ void __launch_bounds__(256, RY == 4 ? 2 : 3) k_stencil(SArgs s, const
         cur[k] = nxt[k];
         nxt[k] = 0.0;
       }
-      vertices(zz + 1, cur, nxt);                // vertex level z = plane zz + 1
+      if (FACT) vertices_f(zz + 1, cur, nxt); else vertices(zz + 1, cur, nxt);   // vertex level z = plane zz + 1
 #pragma unroll
       for (int k = 0; k < RY; ++k) {
         const double ac = Alo[k + 1][1];
@@ -243,7 +409,7 @@ __global__ void __launch_bounds__(256, RY == 4 ? 2 : 3) k_stencil(SArgs s, const
       }
     }
   }
-  cp_async_wait_s<0>();
+  if (!BULK) cp_async_wait_s<0>();
   if (MODE == ST_PCG) {
     double rr[1] = {red};
     reduce_finalize<1>(rr, partials, sc, red_op, red_slot);
@@ -340,7 +506,7 @@ fgd_status launch_stencil(fgd_ctx* c, int field, int mode, const double* a, cons
   // rows per thread: 4 when the tile can be 32 rows high, else 2 / 1
   static const int ry_env = [] {
     const char* e = std::getenv("FGD_ST_RY");
-    return e ? std::atoi(e) : 2;   // measured at 256^3: RY 2 / 32 levels 2.32 ms, RY 4 / 16 levels 2.43 ms
+    return e ? std::atoi(e) : 4;   // factored form: RY 4 (2 CTAs/SM, 128 registers, no spill)
   }();
   const int RY = (s.Ny >= 4 * SBY && ry_env >= 4) ? 4 : (s.Ny >= 2 * SBY && ry_env >= 2 ? 2 : 1);
   const int WY = std::min(SBY, s.Ny / RY);
@@ -382,22 +548,42 @@ fgd_status launch_stencil(fgd_ctx* c, int field, int mode, const double* a, cons
   KTimer kt(c, KC_STENCIL);
   const int rop = red_op_for(c, red_op), rslot = red_slot_for(c, red_op, 0);
   cudaError_t e = cudaSuccess;
-#define STL(RYV)                                                                                                  \
+  static const bool fact = [] {
+    const char* e = std::getenv("FGD_ST_FACT");
+    return e ? std::atoi(e) != 0 : true;
+  }();
+  // bulk-copy staging: rows of 16 B multiples at 16 B aligned addresses (N1 % 16 == 0, aligned fields)
+  static const bool bulk_env = [] {
+    const char* e = std::getenv("FGD_ST_BULK");   // opt-in: measured slower (2.73 vs 1.73 ms at 512^3)
+    return e ? std::atoi(e) != 0 : false;
+  }();
+  auto al16 = [](const void* p) { return ((uintptr_t)p & 15) == 0; };
+  const bool bulk = bulk_env && s.Nx % 16 == 0 && al16(a) && al16(zin) && al16(pold) && al16(c->phase) &&
+                    (!s.dist || (al16(s.a_lo) && al16(s.a_hi) && al16(s.p_lo) && al16(s.p_hi) && al16(s.ph_lo)));
+#define STL(RYV, FV, BV)                                                                                          \
   {                                                                                                               \
-    const size_t smem = stencil_smem<RYV>(mode == ST_PCG ? 2 : 1);                                               \
+    const size_t smem = stencil_smem<RYV>(mode == ST_PCG ? 2 : 1, BV);                                           \
     if (mode == ST_APPLY) {                                                                                       \
-      e = cudaFuncSetAttribute(k_stencil<ST_APPLY, RYV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+      auto kf = k_stencil<ST_APPLY, RYV, FV, BV>;                                                                 \
+      e = cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);                      \
       if (e == cudaSuccess)                                                                                       \
-        e = launch_pdl(k_stencil<ST_APPLY, RYV>, grid, block, smem, c->stream, s, a, (const double*)nullptr,     \
-                       (double*)nullptr, q, (const uint8_t*)c->phase, c->sc, c->partials, rop, rslot);           \
-    } else {                                                                                                      \
-      e = cudaFuncSetAttribute(k_stencil<ST_PCG, RYV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);   \
-      if (e == cudaSuccess)                                                                                       \
-        e = launch_pdl(k_stencil<ST_PCG, RYV>, grid, block, smem, c->stream, s, zin, pold, pout, q,              \
+        e = launch_pdl(kf, grid, block, smem, c->stream, s, a, (const double*)nullptr, (double*)nullptr, q,      \
                        (const uint8_t*)c->phase, c->sc, c->partials, rop, rslot);                                \
+    } else {                                                                                                      \
+      auto kf = k_stencil<ST_PCG, RYV, FV, BV>;                                                                   \
+      e = cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);                      \
+      if (e == cudaSuccess)                                                                                       \
+        e = launch_pdl(kf, grid, block, smem, c->stream, s, zin, pold, pout, q, (const uint8_t*)c->phase, c->sc, \
+                       c->partials, rop, rslot);                                                                  \
     }                                                                                                             \
   }
-  if (RY == 4) STL(4) else if (RY == 2) STL(2) else STL(1)
+  if (bulk) {
+    if (RY == 4) STL(4, true, true) else if (RY == 2) STL(2, true, true) else STL(1, true, true)
+  } else if (fact) {
+    if (RY == 4) STL(4, true, false) else if (RY == 2) STL(2, true, false) else STL(1, true, false)
+  } else {
+    if (RY == 4) STL(4, false, false) else if (RY == 2) STL(2, false, false) else STL(1, false, false)
+  }
 #undef STL
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return set_err(c, FGD_ECUDA, std::string("k_stencil: ") + cudaGetErrorString(e));
