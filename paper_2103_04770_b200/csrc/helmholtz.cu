@@ -94,14 +94,55 @@ constexpr int kPhW = SBX + 8;
 // BULK staging (TMA engine, 1-D bulk copies): plane rows at pitch SBX + 4 holding x0-2 .. x0+TX+1
 // (16 B aligned runs), phase rows at pitch kPhWB holding x0-16 .. x0+TX-1
 constexpr int kPhWB = SBX + 16;
+// plane staging: per-thread cp.async (SG_CP), 1-D bulk copies per row (SG_BULK), or one tensor-map
+// TMA box per array and plane (SG_TENSOR; ring slots padded to 128 B multiples, the TMA destination
+// alignment)
+enum StencilStage : int { SG_CP = 0, SG_BULK = 1, SG_TENSOR = 2 };
+constexpr int pad16(int n) { return (n + 15) / 16 * 16; }
 template <int RY>
-constexpr size_t stencil_smem(int na, bool bulk = false) {
-  return bulk ? (size_t)kRing * na * (SBX + 4) * (SBY * RY + 2) * sizeof(double) + (size_t)kRing * (SBY * RY + 1) * kPhWB
-              : (size_t)kRing * na * (SBX + 2) * (SBY * RY + 2) * sizeof(double) + (size_t)kRing * (SBY * RY + 1) * kPhW;
+constexpr int stencil_pl(int stg) {
+  return stg == SG_TENSOR ? pad16((SBX + 4) * (SBY * RY + 2)) : (stg == SG_BULK ? (SBX + 4) : (SBX + 2)) * (SBY * RY + 2);
+}
+template <int RY>
+constexpr int stencil_phl(int stg) {
+  return stg == SG_TENSOR ? pad16((SBY * RY + 1) * kPhWB / 8) * 8 : (SBY * RY + 1) * (stg == SG_BULK ? kPhWB : kPhW);
+}
+template <int RY>
+constexpr size_t stencil_smem(int na, int stg = SG_CP) {
+  return (size_t)kRing * na * stencil_pl<RY>(stg) * sizeof(double) + (size_t)kRing * stencil_phl<RY>(stg) +
+         (stg == SG_TENSOR ? 128 : 0);
 }
 __device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+
+// SG_TENSOR, CTAs on the cell boundary: one plane (a, p_old if NA = 2, phase ids) into a ring slot of
+// the wide layout by per-thread cp.async with the periodic wrap.  Out of line, so that its index
+// registers are not live through the z march of the interior CTAs (which spilled otherwise).
+template <int NA>
+__device__ __noinline__ void stage_plane_wrap(int TX, int TY, int Nx, int Ny, const double* pa, const double* pp,
+                                              const uint8_t* pb, double* d, uint8_t* dph, int PL) {
+  constexpr int PX = SBX + 4;
+  const int tx = threadIdx.x, ty = threadIdx.y, WYb = blockDim.y;
+  const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
+  const bool cp1 = tx + 32 < TX + 2;
+  const int cx0 = wrapi(x0 - 1 + tx, Nx), cx1 = wrapi(x0 + 31 + tx, Nx);
+  for (int py = ty; py < TY + 2; py += WYb) {
+    const size_t r = (size_t)wrapi(y0 - 1 + py, Ny) * Nx;
+    double* drow = d + py * PX + 1;
+    cp_async8(drow + tx, pa + r + cx0);
+    if (NA == 2) cp_async8(drow + PL + tx, pp + r + cx0);
+    if (cp1) {
+      cp_async8(drow + tx + 32, pa + r + cx1);
+      if (NA == 2) cp_async8(drow + PL + tx + 32, pp + r + cx1);
+    }
+  }
+  if (tx < (TX + 8) / 4) {
+    const int cw = wrapi(x0 - 4 + 4 * tx, Nx);
+    for (int row = ty; row < TY + 1; row += WYb)
+      cp_async4(dph + row * kPhWB + 12 + 4 * tx, pb + (size_t)wrapi(y0 - 1 + row, Ny) * Nx + cw);
+  }
 }
 
 // FACT = true (default): the vertex fluxes and their D^T scatter in factored form.  D_j = Delta_j A_k A_l
@@ -121,17 +162,21 @@ __device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
 // arithmetic in the other warps.  Measured and rejected at 512^3: 2.73 vs 1.73 ms per PCG stencil --
 // ~100 row copies of 16-288 B per plane keep the bulk-copy engine busy far longer than the same bytes
 // as per-thread 8 B cp.async.
-template <int MODE, int RY, bool FACT, bool BULK>
+template <int MODE, int RY, bool FACT, int STG>
 __global__ void __launch_bounds__(256, RY == 4 ? 2 : 3) k_stencil(SArgs s, const double* __restrict__ ain, const double* __restrict__ pold,
                                                      double* __restrict__ pout, double* __restrict__ q,
                                                      const uint8_t* __restrict__ phase, DevScalars* sc, double* partials,
-                                                     int red_op, int red_slot) {
+                                                     int red_op, int red_slot, const __grid_constant__ StencilMaps tm) {
   if (guard_done(s.guard)) return;   // converged Krylov loop: skip
   constexpr int NA = MODE == ST_PCG ? 2 : 1;
-  constexpr int PHW = BULK ? kPhWB : kPhW;
-  constexpr int PX = BULK ? SBX + 4 : SBX + 2, PY = SBY * RY + 2, PL = PX * PY, PHL = (SBY * RY + 1) * PHW;
-  constexpr int XO = BULK ? 1 : 0, PO = BULK ? 15 : 3;   // ring column of x - 1, phase byte of x - 1
-  extern __shared__ double ring[];                 // [kRing][NA][PL], then phase ids [kRing][PHL]
+  constexpr bool BULK = STG == SG_BULK;
+  constexpr bool WIDE = STG != SG_CP;              // ring rows hold x0-2 .. x0+TX+1, phase rows x0-16 .. x0+TX-1
+  constexpr int PHW = WIDE ? kPhWB : kPhW;
+  constexpr int PX = WIDE ? SBX + 4 : SBX + 2, PL = stencil_pl<RY>(STG), PHL = stencil_phl<RY>(STG);
+  constexpr int XO = WIDE ? 1 : 0, PO = WIDE ? 15 : 3;   // ring column of x - 1, phase byte of x - 1
+  extern __shared__ __align__(128) double ring_raw[];
+  // [kRing][NA][PL], then phase ids [kRing][PHL]; SG_TENSOR: 128 B aligned slots
+  double* ring = STG == SG_TENSOR ? reinterpret_cast<double*>(((uintptr_t)ring_raw + 127) & ~(uintptr_t)127) : ring_raw;
   uint8_t* phs = reinterpret_cast<uint8_t*>(ring + (size_t)kRing * NA * PL);
   __shared__ uint64_t fullb[kRing];
   __shared__ double lut[kMaxPhases];
@@ -148,11 +193,11 @@ __global__ void __launch_bounds__(256, RY == 4 ? 2 : 3) k_stencil(SArgs s, const
     lutw[tid][0] = make_double2(l2 * (s.ih[0] * s.ih[0]), l2 * (s.ih[1] * s.ih[1]));
     lutw[tid][1] = make_double2(l2 * (s.ih[2] * s.ih[2]), 0.0);
   }
-  if (BULK && tid == 0) {
+  if ((BULK || STG == SG_TENSOR) && tid == 0) {
     for (int i = 0; i < kRing; ++i) mbar_init(&fullb[i], 1);
     fence_mbar_init();
   }
-  if (BULK) __syncthreads();
+  if (BULK || STG == SG_TENSOR) __syncthreads();
   pdl_wait();
   const double beta = (MODE == ST_PCG) ? sc->beta : 0.0;
   const bool act = tx < TX;
@@ -217,9 +262,28 @@ __global__ void __launch_bounds__(256, RY == 4 ? 2 : 3) k_stencil(SArgs s, const
     }
   };
   // plane index pi = 0 .. TZ + 1 <-> level z0 - 1 + pi; one commit group per plane (possibly empty)
+  // SG_TENSOR: CTAs whose haloed tile lies inside the periodic cell take each plane as one TMA box
+  // per array (a, p_old, phase ids) on the slot's mbarrier, issued by one thread -- no per-element
+  // copy instructions or index arithmetic; CTAs on the cell boundary (the box would need the
+  // periodic wrap) stage the same ring layout with the per-thread cp.async copies below.
+  const bool tmi = STG == SG_TENSOR && x0 >= 16 && x0 + TX + 2 <= Nx && y0 >= 1 && y0 + TY + 1 <= Ny;
+  auto issue_tensor = [&](int pi) {
+    if (pi > TZ + 1 || tid != 0) return;
+    const int zw = wrapi(z0 - 1 + pi, Nz), slot = pi % kRing;
+    uint64_t* bar = &fullb[slot];
+    fence_proxy_async();                          // the slot's earlier generic reads before the async writes
+    mbar_arrive_expect_tx(bar, (unsigned)((TY + 2) * (TX + 4) * 8 * NA + (TY + 1) * (16 + TX)));
+    tma_load_3d(ring + (size_t)slot * NA * PL, &tm.a, x0 - 2, y0 - 1, zw, bar);
+    if (MODE == ST_PCG) tma_load_3d(ring + (size_t)slot * NA * PL + PL, &tm.p, x0 - 2, y0 - 1, zw, bar);
+    tma_load_3d(phs + (size_t)slot * PHL, &tm.ph, x0 - 16, y0 - 1, zw, bar);
+  };
   auto issue = [&](int pi) {
     if (BULK) {
       issue_bulk(pi);
+      return;
+    }
+    if (tmi) {
+      issue_tensor(pi);
       return;
     }
     if (pi <= TZ + 1) {
@@ -237,6 +301,12 @@ __global__ void __launch_bounds__(256, RY == 4 ? 2 : 3) k_stencil(SArgs s, const
         pa = ain + base;
         pp = pold + base;
       }
+      if (STG == SG_TENSOR) {                       // boundary CTA of the tensor variant (single slab)
+        stage_plane_wrap<NA>(TX, TY, Nx, Ny, pa, pp, phase + (size_t)wrapi(zl, Nz) * Ny * Nx, ring + (size_t)(pi % kRing) * NA * PL,
+                             phs + (size_t)(pi % kRing) * PHL, PL);
+        cp_async_commit_s();
+        return;
+      }
       // thread (tx, ty) copies columns px = tx and px = tx + 32 (the two right halo columns when
       // TX = 32) of the rows py = ty, ty + WY, ...; the column offsets are fixed per thread (no
       // per-element index arithmetic: it dominated the instruction mix)
@@ -245,19 +315,19 @@ __global__ void __launch_bounds__(256, RY == 4 ? 2 : 3) k_stencil(SArgs s, const
         const size_t r = (size_t)wrapi(y0 - 1 + py, Ny) * Nx;
         double* drow = d + py * PX;
         if (cp0) {
-          cp_async8(drow + tx, pa + r + cx0);
-          if (MODE == ST_PCG) cp_async8(drow + PL + tx, pp + r + cx0);
+          cp_async8(drow + tx + XO, pa + r + cx0);
+          if (MODE == ST_PCG) cp_async8(drow + PL + tx + XO, pp + r + cx0);
         }
         if (cp1) {
-          cp_async8(drow + tx + 32, pa + r + cx1);
-          if (MODE == ST_PCG) cp_async8(drow + PL + tx + 32, pp + r + cx1);
+          cp_async8(drow + tx + 32 + XO, pa + r + cx1);
+          if (MODE == ST_PCG) cp_async8(drow + PL + tx + 32 + XO, pp + r + cx1);
         }
       }
       const uint8_t* pb = (s.dist && zl < 0) ? s.ph_lo : phase + (size_t)wrapi(zl, Nz) * Ny * Nx;
       uint8_t* dph = phs + (size_t)(pi % kRing) * PHL;
       if (tx < nw)                                  // words per row: (TX + 8) / 4 <= 10
         for (int row = ty; row < TY + 1; row += WYb)
-          cp_async4(dph + row * kPhW + 4 * tx, pb + (size_t)wrapi(y0 - 1 + row, Ny) * Nx + cw);
+          cp_async4(dph + row * PHW + (WIDE ? 12 : 0) + 4 * tx, pb + (size_t)wrapi(y0 - 1 + row, Ny) * Nx + cw);
     }
     cp_async_commit_s();
   };
@@ -360,7 +430,7 @@ __global__ void __launch_bounds__(256, RY == 4 ? 2 : 3) k_stencil(SArgs s, const
 #pragma unroll
   for (int k = 0; k < RY; ++k) nxt[k] = 0.0;
   for (int pi = 0; pi < kRing; ++pi) issue(pi);
-  if (BULK) {
+  if (BULK || tmi) {
     mbar_wait(&fullb[0], 0);
     mbar_wait(&fullb[1], 0);
   } else {
@@ -378,7 +448,7 @@ __global__ void __launch_bounds__(256, RY == 4 ? 2 : 3) k_stencil(SArgs s, const
   __syncthreads();                    // planes 0 and 1 have been read by every thread
   for (int zz = 0; zz < TZ; ++zz) {
     const int z = z0 + zz;
-    if (BULK) mbar_wait(&fullb[(zz + 2) % kRing], ((zz + 2) / kRing) & 1);
+    if (BULK || tmi) mbar_wait(&fullb[(zz + 2) % kRing], ((zz + 2) / kRing) & 1);
     else cp_async_wait_s<kRing - 3>();   // plane zz + 2 (level z + 1) has landed
     __syncthreads();
     // the slot of plane zz was last read at iteration zz - 1 (its phase ids, by vertices(zz)) or in
@@ -552,37 +622,54 @@ fgd_status launch_stencil(fgd_ctx* c, int field, int mode, const double* a, cons
     const char* e = std::getenv("FGD_ST_FACT");
     return e ? std::atoi(e) != 0 : true;
   }();
-  // bulk-copy staging: rows of 16 B multiples at 16 B aligned addresses (N1 % 16 == 0, aligned fields)
-  static const bool bulk_env = [] {
-    const char* e = std::getenv("FGD_ST_BULK");   // opt-in: measured slower (2.73 vs 1.73 ms at 512^3)
-    return e ? std::atoi(e) != 0 : false;
+  // plane staging (FGD_ST_STAGE): 2 = tensor-map TMA boxes (default where it applies), 1 = 1-D bulk
+  // copies per row (measured slower: 2.73 vs 1.73 ms at 512^3), 0 = per-thread cp.async
+  const int stage_env = [] {                      // read per call (the tests switch it)
+    const char* e = std::getenv("FGD_ST_STAGE");
+    if (!e && std::getenv("FGD_ST_BULK")) return (int)SG_BULK;
+    return e ? std::atoi(e) : (int)SG_TENSOR;
   }();
   auto al16 = [](const void* p) { return ((uintptr_t)p & 15) == 0; };
-  const bool bulk = bulk_env && s.Nx % 16 == 0 && al16(a) && al16(zin) && al16(pold) && al16(c->phase) &&
-                    (!s.dist || (al16(s.a_lo) && al16(s.a_hi) && al16(s.p_lo) && al16(s.p_hi) && al16(s.ph_lo)));
-#define STL(RYV, FV, BV)                                                                                          \
+  const double* src_a = (mode == ST_APPLY) ? a : zin;
+  const bool aligned = s.Nx % 16 == 0 && al16(src_a) && (mode == ST_APPLY || al16(pold)) && al16(c->phase);
+  int stage = SG_CP;
+  if (stage_env == SG_BULK && fact && aligned &&
+      (!s.dist || (al16(s.a_lo) && al16(s.a_hi) && al16(s.p_lo) && al16(s.p_hi) && al16(s.ph_lo))))
+    stage = SG_BULK;
+  // tensor maps: full 32 x (8 RY) tiles of a single-slab cell with at least one interior tile
+  StencilMaps tm{};
+  if (stage_env == SG_TENSOR && fact && aligned && !s.dist && s.TX == SBX && WY == SBY && s.Nx >= 3 * SBX &&
+      s.Ny >= 3 * s.TY) {
+    const bool ok = tma_encode_3d(&tm.a, src_a, 8, s.Nx, s.Ny, s.Nz, s.TX + 4, s.TY + 2) &&
+                    tma_encode_3d(&tm.p, mode == ST_PCG ? pold : src_a, 8, s.Nx, s.Ny, s.Nz, s.TX + 4, s.TY + 2) &&
+                    tma_encode_3d(&tm.ph, c->phase, 1, s.Nx, s.Ny, s.Nz, s.TX + 16, s.TY + 1);
+    if (ok) stage = SG_TENSOR;
+  }
+#define STL(RYV, FV, SV)                                                                                          \
   {                                                                                                               \
-    const size_t smem = stencil_smem<RYV>(mode == ST_PCG ? 2 : 1, BV);                                           \
+    const size_t smem = stencil_smem<RYV>(mode == ST_PCG ? 2 : 1, SV);                                           \
     if (mode == ST_APPLY) {                                                                                       \
-      auto kf = k_stencil<ST_APPLY, RYV, FV, BV>;                                                                 \
+      auto kf = k_stencil<ST_APPLY, RYV, FV, SV>;                                                                 \
       e = cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);                      \
       if (e == cudaSuccess)                                                                                       \
         e = launch_pdl(kf, grid, block, smem, c->stream, s, a, (const double*)nullptr, (double*)nullptr, q,      \
-                       (const uint8_t*)c->phase, c->sc, c->partials, rop, rslot);                                \
+                       (const uint8_t*)c->phase, c->sc, c->partials, rop, rslot, tm);                            \
     } else {                                                                                                      \
-      auto kf = k_stencil<ST_PCG, RYV, FV, BV>;                                                                   \
+      auto kf = k_stencil<ST_PCG, RYV, FV, SV>;                                                                   \
       e = cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);                      \
       if (e == cudaSuccess)                                                                                       \
         e = launch_pdl(kf, grid, block, smem, c->stream, s, zin, pold, pout, q, (const uint8_t*)c->phase, c->sc, \
-                       c->partials, rop, rslot);                                                                  \
+                       c->partials, rop, rslot, tm);                                                              \
     }                                                                                                             \
   }
-  if (bulk) {
-    if (RY == 4) STL(4, true, true) else if (RY == 2) STL(2, true, true) else STL(1, true, true)
+  if (stage == SG_TENSOR) {
+    if (RY == 4) STL(4, true, SG_TENSOR) else if (RY == 2) STL(2, true, SG_TENSOR) else STL(1, true, SG_TENSOR)
+  } else if (stage == SG_BULK) {
+    if (RY == 4) STL(4, true, SG_BULK) else if (RY == 2) STL(2, true, SG_BULK) else STL(1, true, SG_BULK)
   } else if (fact) {
-    if (RY == 4) STL(4, true, false) else if (RY == 2) STL(2, true, false) else STL(1, true, false)
+    if (RY == 4) STL(4, true, SG_CP) else if (RY == 2) STL(2, true, SG_CP) else STL(1, true, SG_CP)
   } else {
-    if (RY == 4) STL(4, false, false) else if (RY == 2) STL(2, false, false) else STL(1, false, false)
+    if (RY == 4) STL(4, false, SG_CP) else if (RY == 2) STL(2, false, SG_CP) else STL(1, false, SG_CP)
   }
 #undef STL
   if (e == cudaSuccess) e = cudaGetLastError();

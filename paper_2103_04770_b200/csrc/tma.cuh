@@ -3,6 +3,7 @@
 // sides); the issuing thread arms the stage's mbarrier with the byte count of the whole stage and
 // the copies complete_tx on it, so consumers wait on one phase bit per stage.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -30,6 +31,18 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
                : "memory");
 }
 
+// Tensor-map TMA (tiled mode): one instruction moves a whole box {b0, b1, 1} of a rank-3 tensor
+// [n2][n1][n0] into shared memory (dense, row pitch b0 elements, 128 B aligned destination) and
+// completes its bytes on the mbarrier; coordinates are element indices of the box origin (out-of-range
+// parts of a box are zero-filled, never used here).
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+
 __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, unsigned parity) {
   unsigned ok;
   asm volatile(
@@ -45,5 +58,37 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
   while (!mbar_try_wait(bar, parity)) {
   }
 }
+
+// Host side: cuTensorMapEncodeTiled through the runtime's driver entry point (no link-time
+// dependency on libcuda, so the library still loads on a machine without a driver).
+// Rank-3 tensor [n2][n1][n0] of `esize`-byte elements (esize 8: FLOAT64, 1: UINT8), box {b0, b1, 1}.
+inline bool tma_encode_3d(CUtensorMap* map, const void* base, int esize, int n0, int n1, int n2, int b0, int b1) {
+  typedef CUresult (*Enc)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
+                          const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                          CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static Enc enc = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult qr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &qr) != cudaSuccess ||
+        qr != cudaDriverEntryPointSuccess) {
+      (void)cudaGetLastError();
+      fn = nullptr;
+    }
+    return reinterpret_cast<Enc>(fn);
+  }();
+  if (!enc) return false;
+  const cuuint64_t dims[3] = {(cuuint64_t)n0, (cuuint64_t)n1, (cuuint64_t)n2};
+  const cuuint64_t strides[2] = {(cuuint64_t)n0 * esize, (cuuint64_t)n0 * n1 * esize};
+  const cuuint32_t box[3] = {(cuuint32_t)b0, (cuuint32_t)b1, 1};
+  const cuuint32_t es[3] = {1, 1, 1};
+  return enc(map, esize == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(base),
+             dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// the three maps of one stencil launch (a / z, p_old, phase ids)
+struct StencilMaps {
+  CUtensorMap a, p, ph;
+};
 
 }  // namespace fgd

@@ -68,7 +68,7 @@ def adaptive_schedule(solve, E_end, dE0, dE_max=None, dE_min=1e-5, grow=1.5, gro
 
 def run_config(cfg, n_incr=None, tol=(1e-4, 1e-6, 1e-8, 1e-6), max_halvings=6, max_cg=5000, max_helm=5000,
                adaptive=False, de_min=1e-5, log=False, grow=1.5, stop_frac=None, max_stag=100, warm=False,
-               max_newton=50):
+               max_newton=50, profile=None):
     """Load the cell along cfg.load_comp to n_incr * cfg.dE: fixed increments with deterministic
     halving (A-21), or the adaptive schedule (A-34); returns a result dict."""
     import torch
@@ -148,6 +148,7 @@ def run_config(cfg, n_incr=None, tol=(1e-4, 1e-6, 1e-8, 1e-6), max_halvings=6, m
         counts["increments"] += 1
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
+    prof = _profiles(ctx, cfg) if profile else None
     ctx.close()
     e = np.array([c[0] for c in curve])
     s = np.array([c[1] for c in curve])
@@ -161,7 +162,27 @@ def run_config(cfg, n_incr=None, tol=(1e-4, 1e-6, 1e-8, 1e-6), max_halvings=6, m
     return dict(config=cfg.name, n=list(cfg.n), load_comp=cfg.load_comp, dE=cfg.dE, wall_s=wall,
                 peak_stress=float(s[ip]), strain_at_peak=float(e[ip]), strain_at_failure=fail,
                 curve=[[float(a), float(b)] for a, b in curve], tolerances=list(tol), max_cg=max_cg,
-                max_halvings=max_halvings, adaptive=adaptive, max_stag=max_stag, warm_start=warm, **counts)
+                max_halvings=max_halvings, adaptive=adaptive, max_stag=max_stag, warm_start=warm,
+                ell=np.asarray(cfg.ell).tolist(), **({"profile": prof} if prof else {}), **counts)
+
+
+def _profiles(ctx, cfg):
+    """Committed fields along the row through the cell centre, from the centre to the cell edge
+    (the paper's direction r, Fig. impactelli: profiles across the matrix/inclusion
+    interface): non-local field 0 (the regularised eps0p / eps_p) and the history variable (GTN:
+    porosity f; J2: damage).  Read-back only -- the fields are the library's."""
+    import torch
+
+    from . import _fgd
+    n1, n2, n3 = cfg.n
+    out = torch.empty((n3, n2, n1), dtype=torch.float64, device="cuda")
+    row = {}
+    for name, fid in (("nonlocal0", _fgd.FIELD_NONLOCAL + 0), ("hist", _fgd.FIELD_HIST), ("eqps", _fgd.FIELD_EQPS)):
+        ctx.get_field(fid, out)
+        row[name] = out[n3 // 2, n2 // 2, n1 // 2:].cpu().numpy().tolist()
+    row["x_over_L"] = [((i + 0.5) / n1 - 0.5) for i in range(n1 // 2, n1)]
+    row["phase"] = np.asarray(cfg.phases).reshape(n3, n2, n1)[n3 // 2, n2 // 2, n1 // 2:].astype(int).tolist()
+    return row
 
 
 def main(argv=None):
@@ -185,6 +206,10 @@ def main(argv=None):
     p.add_argument("--max-newton", type=int, default=50)
     p.add_argument("--ell", type=float, default=None,
                    help="gtn2d: matrix ell_M / L (ell_I = min(ell_M, 0.001 L); 1e-4 gives the local variant)")
+    p.add_argument("--ell-i", type=float, default=None,
+                   help="gtn2d: inclusion ell_I / L (interface-contrast study P:941-952; default min(ell_M, 0.001 L))")
+    p.add_argument("--profile", action="store_true",
+                   help="add the committed non-local / history fields along the centre row to the result")
     a = p.parse_args(argv)
     if a.config == "0":
         cfg = synth.config0(a.n or 32)
@@ -196,7 +221,7 @@ def main(argv=None):
         cfg = synth.config4(n=a.n or 512)
     elif a.config == "gtn2d":
         ell = a.ell if a.ell else 0.05
-        cfg = synth.config_gtn2d(a.n or 64, ell_over_L=ell, ell_i_over_L=min(ell, 0.001))
+        cfg = synth.config_gtn2d(a.n or 64, ell_over_L=ell, ell_i_over_L=a.ell_i if a.ell_i else min(ell, 0.001))
     else:
         cfg = synth.config_gtn3d(a.n or 32)
     if a.de:
@@ -204,7 +229,7 @@ def main(argv=None):
     tol = (1e-8, 1e-10, 1e-11, 1e-11) if a.tight else (1e-4, 1e-6, 1e-8, 1e-6)
     print(json.dumps(run_config(cfg, a.incr, tol, a.halvings, a.max_cg, a.max_cg, adaptive=a.adaptive, log=a.log,
                                 grow=a.grow, stop_frac=a.stop_frac, max_stag=a.max_stag, warm=a.warm,
-                                max_newton=a.max_newton)), flush=True)
+                                max_newton=a.max_newton, profile=a.profile)), flush=True)
 
 
 if __name__ == "__main__":

@@ -88,6 +88,31 @@ def test_helmholtz_apply_and_precond(n):
     assert rel(z, apply_precond(g, a, e2)) <= TOL_APPLY
 
 
+@pytest.mark.parametrize("n", [(128, 128, 4), (128, 256, 2), (256, 128, 1), (128, 128, 64)])
+def test_helmholtz_stencil_tensor_staging(n, monkeypatch):
+    """Plane staging of the 27-point stencil by tensor-map TMA boxes (interior CTAs) mixed with the
+    per-thread periodic-wrap copies (boundary CTAs), P:704-726 / R-HELM: grids with both kinds of CTA,
+    a z extent that is not a multiple of the ring depth and the 2D case.  Against the oracle's Fourier
+    form (apply, and PCG iterates), and bit for bit against the cp.async staging (same arithmetic)."""
+    ctx, g, ph = helm_ctx(n)
+    e2 = ell2_field(ph, [0.06, 0.12])
+    a = gaussian_field(1, g.shape, 1e-3, 4)[0]
+    src = np.random.default_rng(5).random(g.shape)
+    out = {}
+    for stage in ("2", "0"):
+        monkeypatch.setenv("FGD_ST_STAGE", stage)
+        y = ctx.apply_helmholtz(0, dev(a))
+        x3 = torch.empty(g.shape, dtype=torch.float64, device="cuda")
+        it3, _ = ctx.solve_helmholtz(0, dev(src), x3, tol=0.0, maxit=3)
+        assert it3 == 3
+        out[stage] = (y, x3)
+    assert rel(out["2"][0].cpu().numpy(), apply_helmholtz(g, a, e2)) <= TOL_APPLY
+    ref3, _, _ = solve_helmholtz(g, src, e2, tol=0.0, maxit=3)
+    assert rel(out["2"][1].cpu().numpy(), ref3) <= 1e-10
+    assert torch.equal(out["2"][0], out["0"][0])
+    assert torch.equal(out["2"][1], out["0"][1])
+
+
 @pytest.mark.parametrize("n", [(16, 16, 16), (32, 32, 1), (64, 32, 8)])
 def test_helmholtz_pcg(n):
     ctx, g, ph = helm_ctx(n, (0.08, 0.08 / 50))
