@@ -176,11 +176,10 @@ __global__ void __launch_bounds__(256, RY == 4 ? 2 : 3) k_stencil(SArgs s, const
   constexpr int XO = WIDE ? 1 : 0, PO = WIDE ? 15 : 3;   // ring column of x - 1, phase byte of x - 1
   extern __shared__ __align__(128) double ring_raw[];
   // [kRing][NA][PL], then phase ids [kRing][PHL]; SG_TENSOR: 128 B aligned slots
-  double* ring = STG == SG_TENSOR ? reinterpret_cast<double*>(((uintptr_t)ring_raw + 127) & ~(uintptr_t)127) : ring_raw;
+  double* ring = ring_raw + (STG == SG_TENSOR ? ((128u - (smem_u32(ring_raw) & 127u)) & 127u) / 8u : 0u);
   uint8_t* phs = reinterpret_cast<uint8_t*>(ring + (size_t)kRing * NA * PL);
   __shared__ uint64_t fullb[kRing];
   __shared__ double lut[kMaxPhases];
-  __shared__ double2 lutw[kMaxPhases][2];          // FACT: (l^2 w_x, l^2 w_y), (l^2 w_z, 0) per phase
   const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * SBX + tx, nthr = SBX * blockDim.y;
   const int TX = s.TX, TY = s.TY, TZ = s.TZ;      // TY = blockDim.y * RY
   const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY, z0 = blockIdx.z * TZ;
@@ -189,9 +188,6 @@ __global__ void __launch_bounds__(256, RY == 4 ? 2 : 3) k_stencil(SArgs s, const
   const bool iso = FACT && s.ih[0] == s.ih[1] && s.ih[1] == s.ih[2];
   if (tid < kMaxPhases) {
     lut[tid] = iso ? s.lut[tid] * (s.ih[0] * s.ih[0]) : s.lut[tid];   // FACT + iso: l^2 w
-    const double l2 = s.lut[tid];
-    lutw[tid][0] = make_double2(l2 * (s.ih[0] * s.ih[0]), l2 * (s.ih[1] * s.ih[1]));
-    lutw[tid][1] = make_double2(l2 * (s.ih[2] * s.ih[2]), 0.0);
   }
   if ((BULK || STG == SG_TENSOR) && tid == 0) {
     for (int i = 0; i < kRing; ++i) mbar_init(&fullb[i], 1);
@@ -390,24 +386,19 @@ __global__ void __launch_bounds__(256, RY == 4 ? 2 : 3) k_stencil(SArgs s, const
       const double sxn0 = Sn[0] + Sn[1], sxn1 = Sn[1] + Sn[2];
       const double sy0 = Sp[0] + Sn[0], sy1 = Sp[1] + Sn[1], sy2 = Sp[2] + Sn[2];
       const double dy0 = Dp[0] + Dn[0], dy1 = Dp[1] + Dn[1], dy2 = Dp[2] + Dn[2];
-      double2 wa0, wb0, wa1, wb1;
-      if (iso) {                                  // h_x = h_y = h_z: one l^2 w per vertex
-        const double l0 = lut[ph[vr * PHW]], l1 = lut[ph[vr * PHW + 1]];
-        wa0 = make_double2(l0, l0);
-        wb0 = make_double2(l0, 0.0);
-        wa1 = make_double2(l1, l1);
-        wb1 = make_double2(l1, 0.0);
-      } else {
-        wa0 = lutw[ph[vr * PHW]][0];
-        wb0 = lutw[ph[vr * PHW]][1];
-        wa1 = lutw[ph[vr * PHW + 1]][0];
-        wb1 = lutw[ph[vr * PHW + 1]][1];
-      }
+      // one l^2 per vertex (times the common w = 1/(4h)^2 when h_x = h_y = h_z, else the three
+      // weights scale the row sums P, Q, R below)
+      const double l0 = lut[ph[vr * PHW]], l1 = lut[ph[vr * PHW + 1]];
       // vertex xv = x - 1 (columns 0, 1) and xv = x (columns 1, 2)
-      const double fx0 = wa0.x * (sy1 - sy0), fx1 = wa1.x * (sy2 - sy1);
-      const double fy0 = wa0.y * (sxn0 - sxp0), fy1 = wa1.y * (sxn1 - sxp1);
-      const double fz0 = wb0.x * (dy0 + dy1), fz1 = wb1.x * (dy1 + dy2);
-      const double P = fx0 - fx1, Q = fy0 + fy1, R = fz0 + fz1;
+      const double fx0 = l0 * (sy1 - sy0), fx1 = l1 * (sy2 - sy1);
+      const double fy0 = l0 * (sxn0 - sxp0), fy1 = l1 * (sxn1 - sxp1);
+      const double fz0 = l0 * (dy0 + dy1), fz1 = l1 * (dy1 + dy2);
+      double P = fx0 - fx1, Q = fy0 + fy1, R = fz0 + fz1;
+      if (!iso) {
+        P *= w0;
+        Q *= w1;
+        R *= w2;
+      }
       const double U = P + Q, V = P - Q;
       if (vr >= 1) {                              // voxel row vr - 1: vertex rows vr - 1 (U) and vr (V)
         const double E = Up + V, Fz = Rp + R;
