@@ -1207,10 +1207,10 @@ __global__ void __launch_bounds__(128, 3) k_yreg512w(YArgs a) {
   pdl_wait();
   const int zz = threadIdx.x >> 5, lane = threadIdx.x & 31, kl = lane >> 4, t = lane & 15;
   double2* ls = sm + (size_t)(kl * TZ + zz) * kY5Pitch;
-  const int nzt = a.Nz / TZ, nkb = a.nkbc;
+  const int nzt = a.Nz / TZ, nkb = a.nkbc, lg_nzt = 31 - __clz(nzt);   // Nz is a power of two
   const int ntiles = a.ncomp * nkb * nzt;
   auto arow_of = [&](int tl) {
-    const int zt = tl % nzt, r = tl / nzt, kb = a.kb0 + r % nkb, c = r / nkb;
+    const int zt = tl & (nzt - 1), r = tl >> lg_nzt, kb = a.kb0 + r % nkb, c = r / nkb;
     return a.A + aidx(a.HxA, N, a.Nz, c, zt * TZ + zz, 0, kb * kKB) + kl + kKB * t;
   };
   double2 v[32];
@@ -1220,7 +1220,7 @@ __global__ void __launch_bounds__(128, 3) k_yreg512w(YArgs a) {
     for (int m = 0; m < 32; ++m) v[m] = __ldcs(A0 + kKB * 16 * m);
   }
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int zt = tile % nzt, r = tile / nzt, kb = a.kb0 + r % nkb, c = r / nkb;
+    const int zt = tile & (nzt - 1), r = tile >> lg_nzt, kb = a.kb0 + r % nkb, c = r / nkb;
     const int z0 = zt * TZ, kx0 = kb * kKB;
     // ---- DFT32 over m, twiddle, transpose (row k2, column t), DFT16 over t ----
     dft32_stage1<false>(v);
@@ -1258,10 +1258,24 @@ __global__ void __launch_bounds__(128, 3) k_yreg512w(YArgs a) {
 #pragma unroll
       for (int m = 0; m < 32; ++m) v[m] = __ldcs(An + kKB * 16 * m);
     }
-    for (int idx = threadIdx.x; idx < 2 * N * TZ; idx += blockDim.x) {
-      const int z2 = idx % TZ, ky = (idx / TZ) & (N - 1), k2l = idx / (TZ * N);
-      const int kxo = kx0 + k2l;
-      if (kxo < a.Hx) a.B[s_index(a.L, a.ncomp, a.Hx, c, kxo, ky, z0 + z2)] = sm[(size_t)(k2l * TZ + z2) * kY5Pitch + ky];
+    // B-side stores: element idx = tid + 128 it is (z2, ky, k2l) = (tid % 4, tid / 4 + 32 (it % 16), it / 16);
+    // the slab terms that do not depend on ky are formed once per tile (no per-element s_index)
+    {
+      const int z = z0 + (threadIdx.x & 3), kyb = threadIdx.x >> 2;
+      const int zl = z & (a.L.nzs - 1), zb = z >> a.L.lg_nzs;
+      const size_t row0 = ((size_t)(zb * a.L.P) * a.ncomp + c) * a.Hx + kx0, ybstep = (size_t)a.ncomp * a.Hx;
+      const double2* sp = sm + (size_t)(threadIdx.x & 3) * kY5Pitch + kyb;
+#pragma unroll
+      for (int k2l = 0; k2l < 2; ++k2l) {
+        if (kx0 + k2l < a.Hx) {
+#pragma unroll 4
+          for (int j = 0; j < 16; ++j) {
+            const int ky = kyb + 32 * j;
+            const size_t rr = (row0 + k2l + (size_t)(ky >> a.L.lg_nys) * ybstep) * a.L.nys + (ky & (a.L.nys - 1));
+            a.B[(rr << a.L.lg_nzs) + zl] = sp[(size_t)k2l * TZ * kY5Pitch + 32 * j];
+          }
+        }
+      }
     }
     __syncthreads();
   }
@@ -1368,15 +1382,25 @@ __global__ void __launch_bounds__(256, 3) k_yreg512i(YArgs a) {
   const int l = kl * TZ + zz;
   const int nzt = a.Nz / TZ, nkb = a.nkbc;
   const int ntiles = a.ncomp * nkb * nzt;
+  // B-side staging: element idx = tid + 128 TZ it (it < 8) is (z2, ky, k2l) = (tid % TZ, tid / TZ + 128 (it % 4),
+  // it / 4): z2 and ky mod 128 are fixed per thread, so the thread's four ky addresses are formed once
+  // per tile and the second kx of the pair is one slab row further (the per-element index arithmetic
+  // with its runtime divisions made up half of this kernel's instructions)
+  const int lg_nzt = 31 - __clz(nzt);              // Nz and TZ are powers of two
+  const int z2t = threadIdx.x & (TZ - 1), ky0 = threadIdx.x >> a.lgTZ;
+  const int soff = z2t * LPY + (ky0 >> 6) * 65 + (ky0 & 63);
+  const size_t kxstep = (size_t)a.L.nys << a.L.lg_nzs;
   auto issue = [&](int tile, double2* buf) {
-    const int zt = tile % nzt, r = tile / nzt, kb = a.kb0 + r % nkb, c = r / nkb;
-    const int z0 = zt * TZ, kx0 = kb * kKB;
-    for (int idx = threadIdx.x; idx < 2 * N * TZ; idx += blockDim.x) {
-      const int z2 = idx % TZ, ky = (idx / TZ) & (N - 1), k2l = idx / (TZ * N);
-      const int kxo = kx0 + k2l;
-      if (kxo < a.Hx)
-        cp_async16(&buf[(size_t)(k2l * TZ + z2) * LPY + (ky >> 6) * 65 + (ky & 63)],
-                   &a.B[s_index(a.L, a.ncomp, a.Hx, c, kxo, ky, z0 + z2)]);
+    const int zt = tile & (nzt - 1), r = tile >> lg_nzt, kb = a.kb0 + r % nkb, c = r / nkb;
+    const int z = zt * TZ + z2t, kx0 = kb * kKB;
+    const bool two = kx0 + 1 < a.Hx;
+    double2* sb = buf + soff;
+    if (kx0 >= a.Hx) return;                       // padding block of layout A (HxA = Hx rounded up to 4)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const double2* g = a.B + s_index(a.L, a.ncomp, a.Hx, c, kx0, ky0 + 128 * j, z);
+      cp_async16(sb + 130 * j, g);
+      if (two) cp_async16(sb + 130 * j + TZ * LPY, g + kxstep);
     }
   };
   int i = 0;
@@ -1392,7 +1416,7 @@ __global__ void __launch_bounds__(256, 3) k_yreg512i(YArgs a) {
     cp_async_commit();
     cp_async_wait<1>();                            // this tile's staging has landed
     __syncthreads();
-    const int zt = tile % nzt, r = tile / nzt, kb = a.kb0 + r % nkb, c = r / nkb;
+    const int zt = tile & (nzt - 1), r = tile >> lg_nzt, kb = a.kb0 + r % nkb, c = r / nkb;
     const int z0 = zt * TZ, kx = kb * kKB + kl;
     double2* ls = cur + (size_t)l * LPY;
     double2 v[8];
