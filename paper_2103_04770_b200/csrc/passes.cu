@@ -308,12 +308,15 @@ __global__ void __launch_bounds__(256) k_xtan(XTArgs a) {
   if (MODE == XF_TANGENT_CG || MODE == XF_HELM_UPDATE) alpha = a.sc->alpha;
   double red = 0.0;
   double* fbd = reinterpret_cast<double*>(fb);
+  // chunk coordinates (tile t, row rr, part h), stage and mbarrier phase advance incrementally: a thread
+  // consumes one voxel per chunk when CW = blockDim.x, so per-chunk divisions are per-voxel work
+  int t = blockIdx.x, rr = 0, h = 0, sq = 0;
+  unsigned ph = 0;
   for (int q = 0; q < nq; ++q) {
     // refill the stage consumed at q - 1 (released by the barriers at the end of that iteration)
     if (threadIdx.x < 32 && q + S - 1 < nq) issue(q + S - 1);
-    mbar_wait(&bars[q % S], (q / S) & 1);
-    const int t = blockIdx.x + (q / (R * nch)) * gridDim.x, rr = (q / nch) % R, h = q % nch;
-    const double* st = stg + (size_t)(q % S) * NOP * CW;
+    mbar_wait(&bars[sq], ph);
+    const double* st = stg + (size_t)sq * NOP * CW;
     for (int v = threadIdx.x; v < CW; v += blockDim.x) {
       const int xg = h * CW + v;
       const size_t g = ((size_t)t * R + rr) * N + xg;
@@ -383,13 +386,49 @@ __global__ void __launch_bounds__(256) k_xtan(XTArgs a) {
       __syncthreads();
       const int z = t / (a.Ny / R), y0 = (t % (a.Ny / R)) * R;
       constexpr int NB = (Hx + kKB - 1) / kKB;   // kx blocks holding data
-      for (int idx = threadIdx.x; idx < NC * NB * R * kKB; idx += blockDim.x) {
-        // order (kx % kKB, row, kx / kKB, c): runs of R * kKB contiguous elements
-        const int kl = idx % kKB, r2 = (idx / kKB) % R, kb = (idx / (kKB * R)) % NB, c = idx / (kKB * R * NB);
-        const int kx = kb * kKB + kl, l = c * R + r2;
-        if (kx < Hx) a.spec[aidx(a.HxA, a.Ny, a.Nz, c, z, y0 + r2, kx)] = fb[l * LP + SWZ(l, kx)];
+      if constexpr (R == kXR && kKB == 2 && kXR == 2) {
+        // order (kx % 2, row, kx / 2, c): runs of 4 contiguous elements (64 B) of layout A.  Thread tid
+        // owns (kl, r2) = (tid & 1, (tid >> 1) & 1) and the kx blocks tid / 4 + j blockDim / 4: the
+        // address is one base per tile plus constant steps (no per-element index arithmetic)
+        constexpr int THR = N >= 512 ? 256 : 128, KS = THR / 4, NJ = (NB + KS - 1) / KS;   // blockDim.x == THR
+        const int kl = threadIdx.x & 1, r2 = (threadIdx.x >> 1) & 1, kb0 = threadIdx.x >> 2;
+        const size_t cstep = (size_t)a.Nz * (a.HxA / kKB) * a.Ny * kKB, kstep = (size_t)KS * a.Ny * kKB;
+        double2* g0 = a.spec + (((size_t)z * (a.HxA / kKB) + kb0) * a.Ny + y0 + r2) * kKB + kl;
+        // all loads of a thread first, then its stores (only the last kx block column can fall past Hx)
+        const bool last = (kb0 + (NJ - 1) * KS) * kKB + kl < Hx;
+        double2 val[NC][NJ];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+          const int l = c * R + r2;
+#pragma unroll
+          for (int j = 0; j < NJ; ++j)
+            if (j < NJ - 1 || last) val[c][j] = fb[l * LP + SWZ(l, (kb0 + j * KS) * kKB + kl)];
+        }
+#pragma unroll
+        for (int c = 0; c < NC; ++c)
+#pragma unroll
+          for (int j = 0; j < NJ; ++j)
+            if (j < NJ - 1 || last) g0[c * cstep + j * kstep] = val[c][j];
+      } else {
+        for (int idx = threadIdx.x; idx < NC * NB * R * kKB; idx += blockDim.x) {
+          // order (kx % kKB, row, kx / kKB, c): runs of R * kKB contiguous elements
+          const int kl = idx % kKB, r2 = (idx / kKB) % R, kb = (idx / (kKB * R)) % NB, c = idx / (kKB * R * NB);
+          const int kx = kb * kKB + kl, l = c * R + r2;
+          if (kx < Hx) a.spec[aidx(a.HxA, a.Ny, a.Nz, c, z, y0 + r2, kx)] = fb[l * LP + SWZ(l, kx)];
+        }
       }
       __syncthreads();
+    }
+    if (++h == nch) {
+      h = 0;
+      if (++rr == R) {
+        rr = 0;
+        t += gridDim.x;
+      }
+    }
+    if (++sq == S) {
+      sq = 0;
+      ph ^= 1u;
     }
   }
   if (MODE == XF_TANGENT_CG || MODE == XF_HELM_UPDATE) {
