@@ -201,10 +201,12 @@ def peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-TRAFFIC_KERNEL = {"xfwd6cg": "k_xtan<{n}, 2, 1, 2>", "xinv6": "k_xipipe<{n}, 1>", "stencil": "k_stencil<1, 2>",
-                  "z6": {256: "k_zreg256<6, 0>", 512: "k_zreg512w<6, 0, 0>"},
-                  "yfwd6": {256: "k_yreg256<0>", 512: "k_yreg512<0>"},
-                  "yinv6": {256: "k_yreg256<1>", 512: "k_yreg512i"}}
+# kernel of each class in the ncu summaries (first candidate present in the newest summary wins)
+TRAFFIC_KERNEL = {"xfwd6cg": ["k_xtan_pp<{n}, 2, 1>", "k_xtan<{n}, 2, 1, 2>"], "xinv6": ["k_xipipe<{n}, 1>"],
+                  "stencil": ["k_stencil<1, 4, 1, 2>", "k_stencil<1, 2>"],
+                  "z6": ["k_zreg512w<6, 0, 0>", "k_zreg256<6, 0>"],
+                  "yfwd6": ["k_yreg512w", "k_yreg512<0>", "k_yreg256<0>"],
+                  "yinv6": ["k_yreg512i", "k_yreg256<1>"]}
 
 
 def measured_traffic(cls, n):
@@ -215,9 +217,11 @@ def measured_traffic(cls, n):
     if not files or cls not in TRAFFIC_KERNEL:
         return None, None
     d = json.load(open(files[-1]))
-    k = TRAFFIC_KERNEL[cls]
-    k = k.get(n, "") if isinstance(k, dict) else k.format(n=n)
-    return d.get(k), os.path.basename(files[-1]) + ":" + k
+    for k in TRAFFIC_KERNEL[cls]:
+        k = k.format(n=n)
+        if (str(n) in k or cls == "stencil") and k in d:
+            return d[k], os.path.basename(files[-1]) + ":" + k
+    return None, None
 
 
 def class_bytes(n, kcg, khelm, world=1):

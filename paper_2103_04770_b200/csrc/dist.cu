@@ -27,6 +27,7 @@
 
 #include <chrono>
 #include <condition_variable>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -232,6 +233,10 @@ void dist_destroy(fgd_ctx* c) {
   c->ov_ev.clear();
   if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
   c->comm_stream = nullptr;
+  for (void* q : c->peer_ipc) cudaIpcCloseMemHandle(q);
+  c->peer_ipc.clear();
+  if (c->bar_buf) cudaFree(c->bar_buf);
+  c->bar_buf = nullptr;
   loop_leave(c);
   if (c->comm) ncclCommDestroy(comm_of(c));
   c->comm = nullptr;
@@ -305,6 +310,71 @@ static fgd_status exchange_chunk(fgd_ctx* c, int ncomp, bool fwd, int kxa, int k
   return FGD_OK;
 }
 
+// ---- peer-store transposes -------------------------------------------------
+// FGD_PEER=1 (opt-in; nranks in [2, kMaxPeers], one NVLink domain): the y-forward pass stores its output
+// straight into the z-pass buffers R of the destination ranks and the y-inverse pass loads from them
+// (YArgs::peer), so the two transposes of a round trip disappear into the passes; what remains are two
+// stream-ordered rank barriers (after the y-forward stores, after the z pass).  The peers' buffers are
+// mapped once: loopback ranks share the address space; NCCL ranks allgather cudaIpcMemHandles of their
+// specC allocations and open them (same node, P2P capable -- the 8 x B200 NVSwitch box).  Measured
+// alternative to the ncclSend/ncclRecv transposes; unmeasured here (one GPU per call).
+bool peer_mode(fgd_ctx* c) {
+  const char* e = std::getenv("FGD_PEER");   // read per call (the tests switch it)
+  return e && std::atoi(e) != 0 && c->nranks > 1 && c->nranks <= kMaxPeers;
+}
+
+static fgd_status peer_setup(fgd_ctx* c) {
+  if (c->peer_ready) return FGD_OK;
+  const int P = c->nranks;
+  if (!c->bar_buf) {
+    FGD_CUDA(c, cudaMalloc((void**)&c->bar_buf, 64));
+    FGD_CUDA(c, cudaMemsetAsync(c->bar_buf, 0, 64, c->stream));
+  }
+  if (c->loop) {
+    TRYD(loop_publish(c, c->specC));
+    for (int s = 0; s < P; ++s) c->peerC[s] = static_cast<double2*>(const_cast<void*>(loop_of(c)->g->ptr[s]));
+    TRYD(loop_finish(c));
+  } else {
+    cudaIpcMemHandle_t mine;
+    FGD_CUDA(c, cudaIpcGetMemHandle(&mine, c->specC));
+    unsigned char* dh = nullptr;
+    FGD_CUDA(c, cudaMalloc((void**)&dh, (size_t)(P + 1) * sizeof(mine)));
+    FGD_CUDA(c, cudaMemcpyAsync(dh + (size_t)P * sizeof(mine), &mine, sizeof(mine), cudaMemcpyHostToDevice, c->stream));
+    FGD_NCCL(c, ncclAllGather(dh + (size_t)P * sizeof(mine), dh, sizeof(mine), ncclChar, comm_of(c), c->stream));
+    std::vector<cudaIpcMemHandle_t> all(P);
+    FGD_CUDA(c, cudaMemcpyAsync(all.data(), dh, (size_t)P * sizeof(mine), cudaMemcpyDeviceToHost, c->stream));
+    FGD_CUDA(c, cudaStreamSynchronize(c->stream));
+    cudaFree(dh);
+    for (int s = 0; s < P; ++s) {
+      if (s == c->rank) {
+        c->peerC[s] = c->specC;
+        continue;
+      }
+      void* q = nullptr;
+      cudaError_t e = cudaIpcOpenMemHandle(&q, all[s], cudaIpcMemLazyEnablePeerAccess);
+      if (e != cudaSuccess) {
+        (void)cudaGetLastError();
+        return set_err(c, FGD_ECUDA, std::string("peer-store transposes: cudaIpcOpenMemHandle: ") + cudaGetErrorString(e));
+      }
+      c->peer_ipc.push_back(q);
+      c->peerC[s] = static_cast<double2*>(q);
+    }
+  }
+  c->peer_ready = true;
+  return FGD_OK;
+}
+
+// every rank's earlier work on its stream completes before any rank's later work starts
+static fgd_status rank_barrier(fgd_ctx* c) {
+  KTimer kt(c, KC_COMM);
+  if (c->loop) {
+    TRYD(loop_publish(c, nullptr));
+    return loop_finish(c);
+  }
+  FGD_NCCL(c, ncclAllReduce(c->bar_buf, c->bar_buf, 1, ncclDouble, ncclSum, comm_of(c), c->stream));
+  return FGD_OK;
+}
+
 // Number of kx chunks of the overlapped round trip (nranks > 1): FGD_OVERLAP (default 4; 1 = the
 // monolithic transpose), at most HxA / 4.
 static int overlap_chunks(const fgd_ctx* c) {
@@ -323,6 +393,76 @@ static int overlap_chunks(const fgd_ctx* c) {
 // leave kCommSMs SMs free for the communication kernels.
 constexpr int kCommSMs = 8;
 fgd_status yz_round_trip(fgd_ctx* c, int ncomp, int zmode, double scale, const double* shift, double mean_ell2) {
+  if (peer_mode(c)) {
+    // R[s][r] on rank s is written by rank r's y-forward and read back by rank r's y-inverse only, and
+    // rank s's z pass runs between the two barriers: no other ordering is needed across round trips
+    TRYD(peer_setup(c));
+    struct On {
+      fgd_ctx* c;
+      explicit On(fgd_ctx* cc) : c(cc) { c->peer_on = true; }
+      ~On() { c->peer_on = false; }
+    } on(c);
+    TRYD(pipe_y(c, ncomp, false));
+    TRYD(rank_barrier(c));
+    TRYD(pipe_z(c, ncomp, zmode, scale, shift, mean_ell2));
+    TRYD(rank_barrier(c));
+    return pipe_y(c, ncomp, true);
+  }
+  // One GPU, large grids: the y passes are bound by the strided side of their transpose and the z
+  // pass by the FP64 pipe, so they can share the SMs: the kx range is cut into K chunks, the z pass of
+  // chunk i runs on a second stream next to the y-forward of chunk i + 1 / the y-inverse of chunk
+  // i - 1, every persistent grid capped so that CTAs of both kernels are resident together
+  // (FGD_YZ_OVERLAP=K, FGD_YZ_SPLIT="ry,rz": SMs' worth of CTAs the y / z grids leave free).
+  if (c->nranks == 1 && c->P == 1 && c->nvox > ((size_t)1 << 21)) {
+    const char* eo = std::getenv("FGD_YZ_OVERLAP");
+    const int Ko = eo ? std::min(std::atoi(eo), c->HxA / 4) : 0;
+    if (Ko > 1) {
+      int ry = 74, rz = 74;
+      if (const char* es = std::getenv("FGD_YZ_SPLIT")) std::sscanf(es, "%d,%d", &ry, &rz);
+      if (!c->comm_stream) FGD_CUDA(c, cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking));
+      while ((int)c->ov_ev.size() < 2 * Ko + 1) {
+        cudaEvent_t e;
+        FGD_CUDA(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        c->ov_ev.push_back(e);
+      }
+      cudaEvent_t* ey = c->ov_ev.data();
+      cudaEvent_t* ez = ey + Ko;
+      std::vector<int> kb(Ko + 1);
+      const int n4 = c->HxA / 4;
+      for (int i = 0; i <= Ko; ++i) kb[i] = 4 * (int)((long long)i * n4 / Ko);
+      cudaStream_t s1 = c->stream, s2 = c->comm_stream;
+      struct Restore {
+        fgd_ctx* c;
+        cudaStream_t s;
+        ~Restore() {
+          c->stream = s;
+          c->sm_reserve = 0;
+        }
+      } restore{c, s1};
+      // s2 starts after everything queued on s1 so far (the x pass that produced the spectra)
+      FGD_CUDA(c, cudaEventRecord(c->ov_ev[2 * Ko], s1));
+      FGD_CUDA(c, cudaStreamWaitEvent(s2, c->ov_ev[2 * Ko], 0));
+      c->sm_reserve = ry;
+      for (int i = 0; i < Ko; ++i) {
+        TRYD(pipe_y(c, ncomp, false, kb[i], kb[i + 1]));
+        FGD_CUDA(c, cudaEventRecord(ey[i], s1));
+      }
+      c->stream = s2;
+      c->sm_reserve = rz;
+      for (int i = 0; i < Ko; ++i) {
+        FGD_CUDA(c, cudaStreamWaitEvent(s2, ey[i], 0));
+        TRYD(pipe_z(c, ncomp, zmode, scale, shift, mean_ell2, kb[i], kb[i + 1]));
+        FGD_CUDA(c, cudaEventRecord(ez[i], s2));
+      }
+      c->stream = s1;
+      c->sm_reserve = ry;
+      for (int i = 0; i < Ko; ++i) {
+        FGD_CUDA(c, cudaStreamWaitEvent(s1, ez[i], 0));
+        TRYD(pipe_y(c, ncomp, true, kb[i], kb[i + 1]));
+      }
+      return FGD_OK;
+    }
+  }
   const int K = c->nranks > 1 ? overlap_chunks(c) : 1;
   if (K <= 1) {
     TRYD(pipe_y(c, ncomp, false));

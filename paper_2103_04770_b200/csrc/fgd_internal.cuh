@@ -52,6 +52,7 @@ inline int grid_cap(int g) {
 
 constexpr int kMaxPhases = 16;
 constexpr int kMaxFields = 4;
+constexpr int kMaxPeers = 8;     // ranks of the peer-store transposes (one NVLink domain)
 constexpr int kMaxN = 512;
 constexpr int kRedSlots = 48;            // doubles per reduction record
 constexpr int kDistSlot = 47;            // local partial of a finalising reduction (nranks > 1)
@@ -167,6 +168,11 @@ struct fgd_ctx {
   std::vector<cudaEvent_t> ov_ev;       // chunk events of the overlapped round trip
   int sm_reserve = 0;          // SMs the persistent kernels leave free (overlapped communication)
   double2* specC = nullptr;    // z-pass buffer when P > 1
+  // peer-store transposes (NEXT#4, FGD_PEER=1): every rank's specC in this process's address space
+  bool peer_on = false, peer_ready = false;
+  double2* peerC[fgd::kMaxPeers] = {};
+  std::vector<void*> peer_ipc;          // mappings opened with cudaIpcOpenMemHandle (NCCL transport)
+  double* bar_buf = nullptr;            // dummy of the allreduce used as a stream-ordered rank barrier
   double* halo = nullptr;      // stencil halo planes (nranks > 1): [field 0 lo, hi][field 1 lo, hi]
   uint8_t* phase_halo = nullptr;
   int Hx = 1;
@@ -293,6 +299,7 @@ fgd_status ensure_partials(fgd_ctx* c, size_t nblocks);
 fgd_status dist_init(fgd_ctx* c, const fgd_dist* d);
 void dist_destroy(fgd_ctx* c);
 fgd_status exchange(fgd_ctx* c, int ncomp, bool fwd);
+bool peer_mode(fgd_ctx* c);   // peer-store transposes requested and possible (nranks in [2, kMaxPeers])
 fgd_status yz_round_trip(fgd_ctx* c, int ncomp, int zmode, double scale, const double* shift, double mean_ell2);
 fgd_status allreduce_sum(fgd_ctx* c, double* dev, int count);
 fgd_status allreduce_max_u64(fgd_ctx* c, unsigned long long* dev);

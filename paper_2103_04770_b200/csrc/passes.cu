@@ -438,6 +438,173 @@ __global__ void __launch_bounds__(256) k_xtan(XTArgs a) {
 }
 
 // ---------------------------------------------------------------------------------------------
+// Ping-pong variant of k_xtan for N = 512 (6-component tangent passes): one 512-thread CTA per SM
+// made of two groups of 256 threads that take alternate tiles, each with its own FFT buffer, and
+// share the ring of two 256-voxel stages.  k_xtan runs its phases one after the other (consume the
+// four chunks of a row pair -> register FFTs -> R2C post-processing -> spectrum stores), so the copy
+// pipeline idles through the FFT/store phase; here one group's FFT/store phase overlaps the other
+// group's consumption.  Chunk q = 4 i + j belongs to local tile i (group i & 1), lives in stage
+// j & 1 and completes on the owner group's mbarrier full[i & 1][j & 1] (a group only ever waits on
+// its own barriers, so their phase parity stays in step with the group); the group that has
+// consumed chunk q refills the stage with chunk q + 2 after its group barrier.  Group-local
+// synchronisation uses named barriers 1 + group; the FFT twiddles of the R2C post-processing come
+// from the global table (L1) instead of shared memory, which is what lets two FFT buffers fit.
+// ---------------------------------------------------------------------------------------------
+__device__ __forceinline__ void group_bar(int grp) { asm volatile("bar.sync %0, 256;" ::"r"(1 + grp) : "memory"); }
+
+template <int N, int MODE, bool CMP>
+constexpr size_t xtpp_smem() {
+  return 64 + ((size_t)2 * 6 * kXR * xline(N / 2) + 240) * sizeof(double2) + (size_t)2 * xt_rows<MODE, CMP>() * 256 * 8;
+}
+
+template <int N, int MODE, bool CMP>
+__global__ void __launch_bounds__(512, 1) k_xtan_pp(XTArgs a) {
+  if (guard_done(a.guard)) return;   // converged Krylov loop: skip
+  static_assert(MODE == XF_TANGENT_CG || MODE == XF_TANGENT, "6-component tangent passes only");
+  constexpr int M = N / 2, Hx = M + 1, LP = xline(M), NC = 6, R = kXR, GT = 256, CW = 256, S = 2;
+  constexpr int NOP = xt_rows<MODE, CMP>();
+  constexpr int C0 = MODE == XF_TANGENT_CG ? 18 : 6;   // first tangent row
+  constexpr int nch = N / CW, CPT = nch * R;           // chunks per tile
+  static_assert(fft_reg_ok<M>() && CPT % S == 0, "register x FFT, stage parity fixed per chunk slot");
+  extern __shared__ __align__(16) unsigned char smraw[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smraw);                  // full[group][stage]
+  double2* fb0 = reinterpret_cast<double2*>(smraw + 64);               // FFT buffers: 2 x NC * R lines of LP
+  double2* twR = fb0 + (size_t)2 * NC * R * LP;                        // [240] register-FFT twiddles
+  double* stg = reinterpret_cast<double*>(twR + 240);                  // [S][NOP][CW]
+  const int grp = threadIdx.x >> 8, gt = threadIdx.x & (GT - 1);
+  double2* fb = fb0 + (size_t)grp * NC * R * LP;
+  double* fbd = reinterpret_cast<double*>(fb);
+  const int ntiles = a.Nz * (a.Ny / R);
+  const size_t n = a.nvox;
+  pdl_trigger();
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < 2 * S; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+  }
+  fft_reg_tables<M>(twR, a.twM);
+  __syncthreads();
+  pdl_wait();
+  const int myrows = (int)blockIdx.x < ntiles ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+  const int nq = myrows * CPT;
+  const bool skip_px = MODE == XF_TANGENT_CG && a.first;   // rows 6..17 (p_old, x) not needed
+  auto issue = [&](int q) {      // one warp (lane = gt)
+    const int i = q / CPT, j = q % CPT;
+    const int t = blockIdx.x + i * gridDim.x, rr = j / nch, h = j % nch;
+    const size_t g0 = ((size_t)t * R + rr) * N + (size_t)h * CW;
+    double* dst = stg + (size_t)(j & 1) * NOP * CW;
+    uint64_t* bar = &bars[(i & 1) * S + (j & 1)];
+    const unsigned bytes = CW * 8;
+    if (gt == 0) {
+      fence_proxy_async();
+      mbar_arrive_expect_tx(bar, bytes * (skip_px ? NOP - 12 : NOP));
+    }
+    __syncwarp();
+    for (int r = gt; r < NOP; r += 32) {
+      if (skip_px && r >= 6 && r < 18) continue;
+      const double* src;
+      if (MODE == XF_TANGENT_CG)
+        src = r < 6 ? a.r + r * n : r < 12 ? a.p + (r - 6) * n : r < 18 ? a.x + (r - 12) * n : a.C + (r - 18) * n;
+      else
+        src = r < 6 ? a.p + r * n : a.C + (r - 6) * n;
+      bulk_g2s(dst + (size_t)r * CW, src + g0, bytes, bar);
+    }
+  };
+  if (threadIdx.x < 32)
+    for (int q = 0; q < S && q < nq; ++q) issue(q);
+  double beta = 0.0, alpha = 0.0;
+  if (MODE == XF_TANGENT_CG) {
+    beta = a.sc->beta;
+    alpha = a.sc->alpha;
+  }
+  double red = 0.0;
+  for (int i = grp, u = 0; i < myrows; i += 2, ++u) {   // u: tiles this group has done before
+    const int t = blockIdx.x + i * gridDim.x;
+#pragma unroll 1
+    for (int j = 0; j < CPT; ++j) {
+      const int q = i * CPT + j, rr = j / nch, h = j % nch;
+      // use number of this group's barrier [j & 1]: u * CPT / S + j / S
+      mbar_wait(&bars[grp * S + (j & 1)], (unsigned)((u * (CPT / S) + j / S) & 1));
+      const double* st = stg + (size_t)(j & 1) * NOP * CW;
+      {
+        const int v = gt, xg = h * CW + v;
+        const size_t g = ((size_t)t * R + rr) * N + xg;
+        double p[6], tv[6];
+        if (MODE == XF_TANGENT_CG) {
+          // CG with the solution update one step late (x += alpha_{k-1} p_{k-1}); see cg_mech
+          if (a.first) {
+#pragma unroll
+            for (int c = 0; c < 6; ++c) {
+              a.x[c * n + g] = 0.0;
+              p[c] = st[c * CW + v];
+              a.p[c * n + g] = p[c];
+            }
+          } else {
+#pragma unroll
+            for (int c = 0; c < 6; ++c) {
+              const double po = st[(6 + c) * CW + v];
+              a.x[c * n + g] = fma(alpha, po, st[(12 + c) * CW + v]);
+              p[c] = fma(beta, po, st[c * CW + v]);
+              a.p[c * n + g] = p[c];
+            }
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < 6; ++c) p[c] = st[c * CW + v];
+        }
+        tangent_smem<CMP>(st + C0 * CW, v, CW, p, tv);
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+          if (MODE == XF_TANGENT_CG) red = fma(p[c], tv[c], red);
+          const int l = c * R + rr;
+          fbd[(size_t)(l * LP + SWZ(l, xg >> 1)) * 2 + (xg & 1)] = tv[c];
+        }
+      }
+      group_bar(grp);                              // the stage has been read by the whole group
+      if (gt < 32 && q + S < nq) issue(q + S);
+    }
+    // ---- this group's FFT / post-processing / stores (the other group consumes meanwhile) ----
+    {
+      constexpr int TPT = fft_reg_tpl<M>();
+      static_assert(NC * R * TPT <= GT && (NC * R * TPT) % 32 == 0, "whole warps of lines within one group");
+      if (gt < NC * R * TPT) fft_reg_inplace<M, false>(fb + (size_t)(gt / TPT) * LP, gt / TPT, gt % TPT, twR);
+    }
+    group_bar(grp);
+    for (int idx = gt; idx < NC * R * (M / 2 + 1); idx += GT) {
+      const int k = idx % (M / 2 + 1), l = idx / (M / 2 + 1);
+      r2c_post<N>(fb + (size_t)l * LP, l, k, a.twN);
+    }
+    group_bar(grp);
+    {
+      const int z = t / (a.Ny / R), y0 = (t % (a.Ny / R)) * R;
+      constexpr int NB = (Hx + kKB - 1) / kKB, KS = GT / 4, NJ = (NB + KS - 1) / KS;
+      static_assert(kKB == 2 && kXR == 2, "store mapping below");
+      const int kl = gt & 1, r2 = (gt >> 1) & 1, kb0 = gt >> 2;
+      const size_t cstep = (size_t)a.Nz * (a.HxA / kKB) * a.Ny * kKB, kstep = (size_t)KS * a.Ny * kKB;
+      double2* g0 = a.spec + (((size_t)z * (a.HxA / kKB) + kb0) * a.Ny + y0 + r2) * kKB + kl;
+      const bool last = (kb0 + (NJ - 1) * KS) * kKB + kl < Hx;
+      double2 val[NC][NJ];
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        const int l = c * R + r2;
+#pragma unroll
+        for (int jj = 0; jj < NJ; ++jj)
+          if (jj < NJ - 1 || last) val[c][jj] = fb[l * LP + SWZ(l, (kb0 + jj * KS) * kKB + kl)];
+      }
+#pragma unroll
+      for (int c = 0; c < NC; ++c)
+#pragma unroll
+        for (int jj = 0; jj < NJ; ++jj)
+          if (jj < NJ - 1 || last) g0[c * cstep + jj * kstep] = val[c][jj];
+    }
+    group_bar(grp);                                // fb is free for the group's next tile
+  }
+  if (MODE == XF_TANGENT_CG) {
+    double rr2[1] = {red};
+    reduce_finalize<1>(rr2, a.partials, a.sc, a.red_op, a.red_slot);
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
 // host launchers
 // ---------------------------------------------------------------------------------------------
 static int pow2_floor(long v) {
@@ -563,6 +730,32 @@ static fgd_status launch_xtan(fgd_ctx* c, int mode, double* r, double* p, double
     e = launch_pdl(kern, dim3(grid), dim3(thr), smem, c->stream, a);                                  \
     if (e == cudaSuccess) e = cudaGetLastError();                                                     \
     if (e != cudaSuccess) return set_err(c, FGD_ECUDA, std::string("k_xtan: ") + cudaGetErrorString(e));         \
+  }
+  static const int pp_env = [] {
+    const char* e = std::getenv("FGD_XT_PP");
+    return e ? std::atoi(e) : 1;   // 1: ping-pong kernel for N = 512 (k_xtan_pp)
+  }();
+  if (pp_env && !helm && Nx == 512 && Ny >= kXR) {
+    auto kern = mode == XF_TANGENT_CG ? (cmp ? k_xtan_pp<512, XF_TANGENT_CG, true> : k_xtan_pp<512, XF_TANGENT_CG, false>)
+                                      : (cmp ? k_xtan_pp<512, XF_TANGENT, true> : k_xtan_pp<512, XF_TANGENT, false>);
+    const size_t smem_pp = mode == XF_TANGENT_CG ? (cmp ? xtpp_smem<512, XF_TANGENT_CG, true>() : xtpp_smem<512, XF_TANGENT_CG, false>())
+                                                 : (cmp ? xtpp_smem<512, XF_TANGENT, true>() : xtpp_smem<512, XF_TANGENT, false>());
+    if (smem_pp <= 227 * 1024) {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_pp);
+      if (e != cudaSuccess) return set_err(c, FGD_ECUDA, std::string("k_xtan_pp smem attr: ") + cudaGetErrorString(e));
+      grid = grid_cap(std::max(1, std::min((ntiles + 1) / 2, sm_count())));
+      if (red_op != RED_NONE) {
+        fgd_status s_ = ensure_partials(c, (size_t)grid);
+        if (s_ != FGD_OK) return s_;
+        a.partials = c->partials;
+      }
+      c->launches++;
+      e = launch_pdl(kern, dim3(grid), dim3(512), smem_pp, c->stream, a);
+      if (e == cudaSuccess) e = cudaGetLastError();
+      if (e != cudaSuccess) return set_err(c, FGD_ECUDA, std::string("k_xtan_pp: ") + cudaGetErrorString(e));
+      *done = true;
+      return FGD_OK;
+    }
   }
   FGD_DISPATCH_N(Nx, XTL)
 #undef XTL

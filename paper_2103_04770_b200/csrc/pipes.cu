@@ -96,7 +96,17 @@ struct YArgs {
   const double2* tw;
   SlabL L;
   int kb0, nkbc;   // kx blocks [kb0, kb0 + nkbc) of TK (or kKB) columns handled by this launch (kx chunk)
+  // Peer-store transposes (FGD_PEER=1, nranks > 1): npeer = P and peer[s] is rank s's
+  // z-pass buffer R, offset so that the S index of an element of y-slab s addresses its place in block
+  // R[s][r] of that rank.  The forward pass then stores straight into the peers' R (NVLink peer
+  // stores), the inverse pass loads from it; no separate transpose.  npeer = 0: B is the local S.
+  int npeer;
+  double2* peer[kMaxPeers];
 };
+// B-side address of the element with S index `sidx` in y-slab `yb` (= ky >> lg_nys)
+__device__ __forceinline__ double2* yb_ptr(const YArgs& a, int yb, size_t sidx) {
+  return (a.npeer ? a.peer[yb] : a.B) + sidx;
+}
 
 struct YTile {
   int c, kx0, z0;
@@ -124,7 +134,8 @@ __device__ __forceinline__ void y_issue(const YArgs& a, int t, double2* buf) {
       const int zz = idx & (TZ - 1), ky = (idx >> a.lgTZ) & (N - 1), kk = idx >> (a.lgTZ + ilog2(N));
       const int kx = T.kx0 + kk, l = zz * TK + kk;
       if (kx < a.Hx)
-        cp_async16(&buf[l * LP + SWZ(l, ky)], &a.B[s_index(a.L, a.ncomp, a.Hx, T.c, kx, ky, T.z0 + zz)]);
+        cp_async16(&buf[l * LP + SWZ(l, ky)],
+                   yb_ptr(a, ky >> a.L.lg_nys, s_index(a.L, a.ncomp, a.Hx, T.c, kx, ky, T.z0 + zz)));
     }
   }
 }
@@ -158,7 +169,8 @@ __global__ void __launch_bounds__(256, 2) k_ypipe(YArgs a) {
       for (int idx = threadIdx.x; idx < TZ * TK * N; idx += blockDim.x) {
         const int zz = idx & (TZ - 1), ky = (idx >> a.lgTZ) & (N - 1), kk = idx >> (a.lgTZ + ilog2(N));
         const int kx = T.kx0 + kk, l = zz * TK + kk;
-        if (kx < a.Hx) a.B[s_index(a.L, a.ncomp, a.Hx, T.c, kx, ky, T.z0 + zz)] = buf[l * LP + SWZ(l, ky)];
+        if (kx < a.Hx)
+          *yb_ptr(a, ky >> a.L.lg_nys, s_index(a.L, a.ncomp, a.Hx, T.c, kx, ky, T.z0 + zz)) = buf[l * LP + SWZ(l, ky)];
       }
     } else {
       for (int idx = threadIdx.x; idx < TZ * TK * N; idx += blockDim.x) {
@@ -736,7 +748,7 @@ __device__ __forceinline__ void y256_issue_inv(const YArgs& a, int tile, double2
     const int kxo = kx0 + k2l;
     if (kxo < a.Hx)
       cp_async16(&buf[(size_t)(k2l * TZ + z2) * ypitch(kZLine, TZ) + ky + (ky >> 4)],
-                 &a.B[s_index(a.L, a.ncomp, a.Hx, c, kxo, ky, z0 + z2)]);
+                 yb_ptr(a, ky >> a.L.lg_nys, s_index(a.L, a.ncomp, a.Hx, c, kxo, ky, z0 + z2)));
   }
 }
 
@@ -806,7 +818,8 @@ __global__ void __launch_bounds__(256, 2) k_yreg256(YArgs a) {
         const int z2 = idx % TZ, ky = (idx / TZ) & (N - 1), k2l = idx / (TZ * N);
         const int kxo = kx0 + k2l;
         if (kxo < a.Hx)
-          a.B[s_index(a.L, a.ncomp, a.Hx, c, kxo, ky, z0 + z2)] = sm[(size_t)(k2l * TZ + z2) * LPY + ky + (ky >> 4)];
+          *yb_ptr(a, ky >> a.L.lg_nys, s_index(a.L, a.ncomp, a.Hx, c, kxo, ky, z0 + z2)) =
+              sm[(size_t)(k2l * TZ + z2) * LPY + ky + (ky >> 4)];
       }
       __syncthreads();
     } else {
@@ -1272,7 +1285,7 @@ __global__ void __launch_bounds__(128, 3) k_yreg512w(YArgs a) {
           for (int j = 0; j < 16; ++j) {
             const int ky = kyb + 32 * j;
             const size_t rr = (row0 + k2l + (size_t)(ky >> a.L.lg_nys) * ybstep) * a.L.nys + (ky & (a.L.nys - 1));
-            a.B[(rr << a.L.lg_nzs) + zl] = sp[(size_t)k2l * TZ * kY5Pitch + 32 * j];
+            *yb_ptr(a, ky >> a.L.lg_nys, (rr << a.L.lg_nzs) + zl) = sp[(size_t)k2l * TZ * kY5Pitch + 32 * j];
           }
         }
       }
@@ -1330,7 +1343,7 @@ __global__ void __launch_bounds__(512, 2) k_yreg512(YArgs a) {
         const int z2 = idx % TZ, ky = (idx / TZ) & (N - 1), k2l = idx / (TZ * N);
         const int kxo = kx0 + k2l;
         if (kxo < a.Hx)
-          a.B[s_index(a.L, a.ncomp, a.Hx, c, kxo, ky, z0 + z2)] =
+          *yb_ptr(a, ky >> a.L.lg_nys, s_index(a.L, a.ncomp, a.Hx, c, kxo, ky, z0 + z2)) =
               sm[(size_t)(k2l * TZ + z2) * LPY + (ky >> 6) * 65 + (ky & 63)];
       }
       __syncthreads();
@@ -1343,7 +1356,7 @@ __global__ void __launch_bounds__(512, 2) k_yreg512(YArgs a) {
         const int kxo = kx0 + k2l;
         if (kxo < a.Hx)
           cp_async16(&sm[(size_t)(k2l * TZ + z2) * LPY + (ky >> 6) * 65 + (ky & 63)],
-                     &a.B[s_index(a.L, a.ncomp, a.Hx, c, kxo, ky, z0 + z2)]);
+                     yb_ptr(a, ky >> a.L.lg_nys, s_index(a.L, a.ncomp, a.Hx, c, kxo, ky, z0 + z2)));
       }
       cp_async_commit();
       cp_async_wait<0>();
@@ -1398,7 +1411,7 @@ __global__ void __launch_bounds__(256, 3) k_yreg512i(YArgs a) {
     if (kx0 >= a.Hx) return;                       // padding block of layout A (HxA = Hx rounded up to 4)
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      const double2* g = a.B + s_index(a.L, a.ncomp, a.Hx, c, kx0, ky0 + 128 * j, z);
+      const double2* g = yb_ptr(a, (ky0 + 128 * j) >> a.L.lg_nys, s_index(a.L, a.ncomp, a.Hx, c, kx0, ky0 + 128 * j, z));
       cp_async16(sb + 130 * j, g);
       if (two) cp_async16(sb + 130 * j + TZ * LPY, g + kxstep);
     }
@@ -1625,10 +1638,25 @@ __device__ __forceinline__ void xi_issue(const XPArgs& a, int t, double2* buf, d
   const int yt = t % nyt, r = t / nyt, z = r % a.Nz, c = r / a.Nz;
   const int y0 = yt * TY;
   constexpr int NB = (Hx + kKB - 1) / kKB;
-  for (int idx = threadIdx.x; idx < NB * TY * kKB; idx += blockDim.x) {
-    // order (kx % kKB, yy, kx / kKB): runs of TY * kKB contiguous elements of layout A
-    const int kl = idx % kKB, yy = (idx / kKB) & (TY - 1), kx = (idx / kKB >> a.lgTY) * kKB + kl;
-    if (kx < Hx) cp_async16(&buf[yy * LP + SWZ(yy, kx)], &a.spec[aidx(a.HxA, a.Ny, a.Nz, c, z, y0 + yy, kx)]);
+  const int kbs = blockDim.x >> (1 + a.lgTY);   // kx blocks per sweep of the CTA (kKB = 2)
+  if (kbs > 0) {
+    // order (kx % kKB, yy, kx / kKB): runs of TY * kKB contiguous elements of layout A.  (kl, yy) and the
+    // first kx block are fixed per thread: one base address per tile, then constant steps
+    static_assert(kKB == 2, "thread mapping below");
+    const int kl = threadIdx.x & 1, yy = (threadIdx.x >> 1) & (TY - 1);
+    int kb = threadIdx.x >> (1 + a.lgTY);
+    const double2* g = a.spec + (((size_t)(c * a.Nz + z) * (a.HxA / kKB) + kb) * a.Ny + y0 + yy) * kKB + kl;
+    const size_t gstep = (size_t)kbs * a.Ny * kKB;
+    double2* sb = buf + yy * LP;
+    for (; kb < NB; kb += kbs, g += gstep) {
+      const int kx = kb * kKB + kl;
+      if (kx < Hx) cp_async16(sb + SWZ(yy, kx), g);
+    }
+  } else {
+    for (int idx = threadIdx.x; idx < NB * TY * kKB; idx += blockDim.x) {
+      const int kl = idx % kKB, yy = (idx / kKB) & (TY - 1), kx = (idx / kKB >> a.lgTY) * kKB + kl;
+      if (kx < Hx) cp_async16(&buf[yy * LP + SWZ(yy, kx)], &a.spec[aidx(a.HxA, a.Ny, a.Nz, c, z, y0 + yy, kx)]);
+    }
   }
   if constexpr (xi_prefetch<N, MODE>()) {
     // rows y0 .. y0 + TY - 1 of plane z are contiguous: TY * N doubles
@@ -1940,6 +1968,17 @@ static SlabL slab_layout(const fgd_ctx* c) {
   return L;
 }
 
+// Peer-store transposes: rank s's R base, offset by (r - s) blocks, so that the S index of an element
+// of y-slab s (block s of the local S layout) lands in block r of rank s's R (same intra-block offset).
+static void fill_peers(const fgd_ctx* c, int ncomp, YArgs* a) {
+  a->npeer = 0;
+  if (!c->peer_on || !c->peer_ready) return;
+  const int P = c->nranks;
+  const long long blk = (long long)ncomp * c->Hx * (c->n[1] / P) * (c->n[2] / P);
+  a->npeer = P;
+  for (int s = 0; s < P; ++s) a->peer[s] = c->peerC[s] + (long long)(c->rank - s) * blk;
+}
+
 fgd_status pipe_y(fgd_ctx* c, int ncomp, bool inv, int kxa, int kxb) {
   const int Ny = c->n[1], Nz = c->nz_l;
   if (kxb < 0) kxb = c->HxA;   // kx chunk [kxa, kxb): multiples of 4 (kx blocks of kKB or TK <= 4)
@@ -1950,6 +1989,7 @@ fgd_status pipe_y(fgd_ctx* c, int ncomp, bool inv, int kxa, int kxb) {
     const int ntiles = ncomp * ((kxb - kxa) / kKB) * (Nz / TZ);
     YArgs a{c->guard ? c->sc : nullptr, c->specA, c->specB, Nz, c->Hx, c->HxA, TZ, kKB, ncomp, ilog2(TZ), ilog2(kKB), c->tabs.tw[ilog2(Ny)],
             slab_layout(c), kxa / kKB, (kxb - kxa) / kKB};
+    fill_peers(c, ncomp, &a);
     KTimer kt(c, inv ? (ncomp == 6 ? KC_YINV6 : KC_YINV1) : (ncomp == 6 ? KC_YFWD6 : KC_YFWD1));
     static const int y512i = [] {
       const char* e = std::getenv("FGD_Y512I");
@@ -1995,6 +2035,7 @@ fgd_status pipe_y(fgd_ctx* c, int ncomp, bool inv, int kxa, int kxb) {
     const int ntiles = ncomp * ((kxb - kxa) / kKB) * (Nz / TZ);
     YArgs a{c->guard ? c->sc : nullptr, c->specA, c->specB, Nz, c->Hx, c->HxA, TZ, kKB, ncomp, ilog2(TZ), ilog2(kKB), c->tabs.tw[ilog2(Ny)],
             slab_layout(c), kxa / kKB, (kxb - kxa) / kKB};
+    fill_peers(c, ncomp, &a);
     KTimer kt(c, inv ? (ncomp == 6 ? KC_YINV6 : KC_YINV1) : (ncomp == 6 ? KC_YFWD6 : KC_YFWD1));
     if (inv) FGD_PLAUNCH(c, k_yreg256<true>, thr, smem, ntiles, a);
     else FGD_PLAUNCH(c, k_yreg256<false>, thr, smem, ntiles, a);
@@ -2019,6 +2060,7 @@ fgd_status pipe_y(fgd_ctx* c, int ncomp, bool inv, int kxa, int kxb) {
   const int ntiles = ncomp * ((kxb - kxa) / TK) * (Nz / TZ);
   YArgs a{c->guard ? c->sc : nullptr, c->specA, c->specB, Nz, c->Hx, c->HxA, TZ, TK, ncomp, ilog2(TZ), ilog2(TK), c->tabs.tw[ilog2(Ny)],
           slab_layout(c), kxa / TK, (kxb - kxa) / TK};
+  fill_peers(c, ncomp, &a);
   KTimer kt(c, inv ? (ncomp == 6 ? KC_YINV6 : KC_YINV1) : (ncomp == 6 ? KC_YFWD6 : KC_YFWD1));
 #define YPP(NN)                                                                  \
   if (inv) FGD_PLAUNCH(c, (k_ypipe<NN, true>), thr, smem, ntiles, a);            \

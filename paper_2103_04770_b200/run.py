@@ -98,8 +98,9 @@ def run_config(cfg, n_incr=None, tol=(1e-4, 1e-6, 1e-8, 1e-6), max_halvings=6, m
             counts["substeps"] += 1
             curve.append((E_try, float(rep["macro_stress"][cfg.load_comp])))
             if log:   # one line per accepted increment: a run cut short still leaves its curve
-                print(json.dumps({"E": E_try, "S": curve[-1][1], "t": time.perf_counter() - t0}), file=sys.stderr,
-                      flush=True)
+                print(json.dumps({"E": E_try, "S": curve[-1][1], "t": time.perf_counter() - t0, "stag": rep["stag"],
+                                  "newton": rep["newton"], "cg": rep["cg"], "helm": rep["helm"], "err": rep["err"]}),
+                      file=sys.stderr, flush=True)
             return True
         if st != _fgd.ENOCONV:
             raise RuntimeError(f"solve_increment failed with status {st}")

@@ -85,14 +85,18 @@ GRIDS = [(2, (16, 8, 8)), (4, (16, 8, 8)), (2, (32, 16, 16)), (4, (8, 32, 32)), 
          (2, (16, 256, 256)), (4, (8, 512, 512))]
 
 
-@pytest.mark.parametrize("overlap", ["1", "4", "3"])
+@pytest.mark.parametrize("overlap", ["1", "4", "3", "peer"])
 @pytest.mark.parametrize("P,n", GRIDS)
 def test_loopback_operators(P, n, overlap, monkeypatch):
     """Projection (with a stress-controlled macroscopic shift on rank 0's zero frequency), projected
     tangent, Helmholtz apply (z-halos) and preconditioner on P ranks vs the oracle on the cell, with
     the monolithic transposes (FGD_OVERLAP=1) and the kx-chunked round trip overlapped on a second
     stream (4 and 3 chunks)."""
-    monkeypatch.setenv("FGD_OVERLAP", overlap)
+    if overlap == "peer":
+        # peer-store transposes (NEXT#4): the y passes write to / read from the peers' z-pass buffers
+        monkeypatch.setenv("FGD_PEER", "1")
+    else:
+        monkeypatch.setenv("FGD_OVERLAP", overlap)
     L = (1.0, 0.9, 1.1)
     g = Grid(n, L)
     tau = gaussian_field(6, g.shape, 1.0, 2)
@@ -123,11 +127,15 @@ def test_loopback_operators(P, n, overlap, monkeypatch):
     assert rel(gather([r[3] for r in res]), apply_precond(g, a, e2)) <= 1e-10
 
 
+@pytest.mark.parametrize("peer", [False, True])
 @pytest.mark.parametrize("P,n", [(2, (16, 8, 8)), (4, (32, 16, 16)), (2, (256, 8, 8)), (2, (16, 256, 256))])
-def test_loopback_krylov(P, n):
+def test_loopback_krylov(P, n, peer, monkeypatch):
     """Mechanical CG and Helmholtz PCG on P ranks: iterates after a fixed number of iterations
     (distributed finalise) and converged solves (batched loops with the device guard: the
-    same iteration count on every rank and +-1 of the oracle's)."""
+    same iteration count on every rank and +-1 of the oracle's); with the NCCL-style transposes and
+    with the peer-store transposes (FGD_PEER=1, NEXT#4)."""
+    if peer:
+        monkeypatch.setenv("FGD_PEER", "1")
     L = (1.0, 1.0, 1.0)
     g = Grid(n, L)
     Cp = random_spd_tangent(g.nvox, 8).reshape((21,) + g.shape)
@@ -171,8 +179,15 @@ def test_loopback_krylov(P, n):
     assert rel(gather([r[5] for r in res]), refh) <= 1e-8
 
 
+@pytest.mark.parametrize("peer", [False, True])
 @pytest.mark.parametrize("P", [2, 4])
-def test_loopback_increments(P):
+def test_loopback_increments(P, peer, monkeypatch):
+    if peer:
+        monkeypatch.setenv("FGD_PEER", "1")
+    _loopback_increments(P)
+
+
+def _loopback_increments(P):
     """Two staggered increments (Algorithm 1) of a 16^3 config-3-type cell (brittle spheres in a
     J2-Lemaitre matrix, two non-local fields) on P ranks: <sigma> and the committed fields against the
     oracle (distributed <sigma>, ERR with the allreduce-max of the strain-change bit patterns)."""
