@@ -149,6 +149,19 @@ fgd_status fgd_solve_helmholtz(fgd_ctx* ctx, int field, const double* src, doubl
 fgd_status fgd_solve_helmholtz_from(fgd_ctx* ctx, int field, const double* src, const double* x0, double* abar,
                                     double tol, int maxit, int* iters, double* relres);
 
+/* All J non-local fields of fgd_set_nonlocal in one call (NEXT#3).  The J generalized Helmholtz
+ * problems of a staggered iteration are independent ("computed independently"), so
+ * they are solved SIDE BY SIDE: one stream, one set of Krylov scalars and work vectors per field,
+ * each running Algorithm 2 exactly as fgd_solve_helmholtz_from does (bitwise the same iterates,
+ * iteration counts and results as J consecutive calls).  On launch-latency-bound grids (<= 2^21
+ * voxels, one GPU) the solves overlap on the device; on larger grids and with nranks > 1 they run
+ * one after another.  src, x0 (NULL = 0), abar: J one-component fields one after another
+ * ([J][N3_local][N2][N1], host or device); iters, relres: arrays of J (may be NULL).
+ * Returns FGD_ENOCONV if any field did not reach tol within maxit (the others are still returned;
+ * consecutive mode stops at the first failing field). */
+fgd_status fgd_solve_helmholtz_all(fgd_ctx* ctx, const double* src, const double* x0, double* abar, double tol,
+                                   int maxit, int* iters, double* relres);
+
 /* Mechanical linear solve of one Newton step: unpreconditioned CG for
  * G*(C : de) = b with de_0 = 0; b must lie in range(G*) (e.g. a Newton residual).  Same
  * stopping rule and NULL conventions as fgd_solve_helmholtz (b == NULL: the residual of the

@@ -78,6 +78,7 @@ _SIGS = {
     "fgd_apply_helmholtz_precond": ([_P, _I, _P, _P], _I),
     "fgd_solve_helmholtz": ([_P, _I, _P, _P, _D, _I, C.POINTER(_I), C.POINTER(_D)], _I),
     "fgd_solve_helmholtz_from": ([_P, _I, _P, _P, _P, _D, _I, C.POINTER(_I), C.POINTER(_D)], _I),
+    "fgd_solve_helmholtz_all": ([_P, _P, _P, _P, _D, _I, C.POINTER(_I), C.POINTER(_D)], _I),
     "fgd_solve_tangent_cg": ([_P, _P, _P, _D, _I, C.POINTER(_I), C.POINTER(_D)], _I),
     "fgd_constitutive": ([_P, _P, _P, _P], _I),
     "fgd_mech_residual": ([_P, _P, _P, C.POINTER(_D)], _I),

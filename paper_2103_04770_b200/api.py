@@ -183,6 +183,15 @@ class Context:
             self._chk(st)
         return it.value, rel.value
 
+    def solve_helmholtz_all(self, src, x0, abar, nfields: int, tol=1e-10, maxit=1000, check=True):
+        """All J fields side by side (fgd_solve_helmholtz_all); src, x0 (None = 0), abar: [J, ...] fields."""
+        it = (C.c_int * int(nfields))()
+        rel = (C.c_double * int(nfields))()
+        st = _fgd.fgd_solve_helmholtz_all(self.h, ptr(src), ptr(x0), ptr(abar), float(tol), int(maxit), it, rel)
+        if check:
+            self._chk(st)
+        return list(it), list(rel)
+
     def solve_tangent_cg(self, b=None, de=None, tol=1e-10, maxit=1000, check=True):
         it, rel = C.c_int(0), C.c_double(0.0)
         st = _fgd.fgd_solve_tangent_cg(self.h, ptr(b), ptr(de), float(tol), int(maxit), C.byref(it), C.byref(rel))

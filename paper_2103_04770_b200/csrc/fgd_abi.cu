@@ -6,6 +6,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <thread>
 
 #include "fgd_internal.cuh"
 
@@ -54,13 +55,14 @@ static fgd_status dalloc(fgd_ctx* c, T** p, size_t count) {
 }
 
 fgd_status ensure_spectral(fgd_ctx* c) {
-  fgd_status s = dalloc(c, &c->specA, 6 * c->nspecA);
+  const size_t nc = (size_t)c->spec_comps;
+  fgd_status s = dalloc(c, &c->specA, nc * c->nspecA);
   if (s != FGD_OK) return s;
   if (c->P > 1) {
-    s = dalloc(c, &c->specC, 6 * c->nspec);
+    s = dalloc(c, &c->specC, nc * c->nspec);
     if (s != FGD_OK) return s;
   }
-  return dalloc(c, &c->specB, 6 * c->nspec);
+  return dalloc(c, &c->specB, nc * c->nspec);
 }
 
 fgd_status ensure_partials(fgd_ctx* c, size_t nblocks) {
@@ -646,6 +648,17 @@ void fgd_destroy(fgd_ctx* c) {
   for (int i = 0; i < 6; ++i)
     if (c->hb[i]) cudaFree(c->hb[i]);
   if (c->hg) cudaFree(c->hg);
+  for (fgd_helm_sub& h : c->hsub) {
+    if (h.stream) cudaStreamSynchronize(h.stream);
+    void* hbufs[] = {h.hb[0], h.hb[1], h.hb[2], h.hb[3], h.hb[4], h.hb[5], h.specA, h.specB, h.specC, h.sc, h.partials};
+    for (void* b : hbufs)
+      if (b) cudaFree(b);
+    if (h.pinned) cudaFreeHost(h.pinned);
+    if (h.ev) cudaEventDestroy(h.ev);
+    if (h.cap) cudaStreamDestroy(h.cap);
+    if (h.stream) cudaStreamDestroy(h.stream);
+  }
+  if (c->hsub_ev) cudaEventDestroy(c->hsub_ev);
   if (c->pinned) cudaFreeHost(c->pinned);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
@@ -824,6 +837,121 @@ fgd_status fgd_apply_helmholtz_precond(fgd_ctx* c, int field, const double* r, d
   return st.finish();
 }
 
+// NEXT#3 -- the J Helmholtz problems of a staggered iteration are independent ("computed
+// independently"): solve them SIDE BY SIDE.  Field 0 runs on the context, every field
+// j >= 1 on a copy of the context that owns its stream, Krylov scalars, work vectors and
+// one-component spectrum buffers (fgd_helm_sub), each driven by its own host thread (the batched
+// loops read their convergence flag from the host).  Every solve executes exactly the kernels,
+// grids and reduction orders of pcg_helmholtz, so the results are bitwise those of J consecutive
+// solves.  On the launch-latency-bound grids (<= 2^21 voxels) the two dependent kernel chains
+// overlap; on HBM-bound grids the solves stay consecutive (persistent grids already fill the GPU).
+// FGD_HELM_CONC = 0 / 1 forces the choice.  One GPU only: the communicator is not shared by threads.
+static bool helm_concurrent(const fgd_ctx* c, int J) {
+  const char* e = std::getenv("FGD_HELM_CONC");   // read per call: tests toggle it
+  if (J < 2 || c->nranks != 1 || c->timing) return false;
+  if (e) return std::atoi(e) != 0;
+  return c->nvox <= ((size_t)1 << 21);
+}
+
+static fgd_status helm_sub_init(fgd_ctx* c, fgd_helm_sub* h) {
+  if (h->stream) return FGD_OK;
+  FGD_CUDA(c, cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+  FGD_CUDA(c, cudaEventCreateWithFlags(&h->ev, cudaEventDisableTiming));
+  TRY(dalloc(c, &h->sc, 1));
+  FGD_CUDA(c, cudaMemsetAsync(h->sc, 0, sizeof(DevScalars), h->stream));
+  FGD_CUDA(c, cudaMallocHost((void**)&h->pinned, 4096));
+  return FGD_OK;
+}
+
+// src, x0 (may be null), out: J fields one after another on the device.  st[j], iters[j], relres[j]
+// per field; returns the first hard error (anything but FGD_ENOCONV), else FGD_OK.
+static fgd_status helm_solve_all(fgd_ctx* c, int J, const double* src, const double* x0, double* out, double tol,
+                                 int maxit, fgd_status* st, int* iters, double* relres) {
+  const size_t n = c->nvox;
+  auto solve = [&](fgd_ctx* cc, int j) {
+    st[j] = pcg_helmholtz(cc, j, src + (size_t)j * n, out + (size_t)j * n, tol, maxit, &iters[j], &relres[j],
+                          x0 ? x0 + (size_t)j * n : nullptr);
+  };
+  if (!helm_concurrent(c, J)) {
+    for (int j = 0; j < J; ++j) {
+      solve(c, j);
+      if (st[j] != FGD_OK && st[j] != FGD_ENOCONV) return st[j];
+      // a failed field stops the sequence like the staggered loop always did
+      if (st[j] == FGD_ENOCONV) {
+        for (int k = j + 1; k < J; ++k) st[k] = FGD_ENOCONV, iters[k] = 0, relres[k] = 0.0;
+        break;
+      }
+    }
+    return FGD_OK;
+  }
+  TRY(ensure_helm(c));
+  TRY(ensure_spectral(c));
+  if ((int)c->hsub.size() < J - 1) c->hsub.resize(J - 1);
+  if (!c->hsub_ev) FGD_CUDA(c, cudaEventCreateWithFlags(&c->hsub_ev, cudaEventDisableTiming));
+  for (int j = 1; j < J; ++j) TRY(helm_sub_init(c, &c->hsub[j - 1]));
+  FGD_CUDA(c, cudaEventRecord(c->hsub_ev, c->stream));
+  std::vector<fgd_ctx> copies;
+  copies.reserve(J - 1);
+  for (int j = 1; j < J; ++j) {
+    fgd_helm_sub& h = c->hsub[j - 1];
+    FGD_CUDA(c, cudaStreamWaitEvent(h.stream, c->hsub_ev, 0));
+    copies.push_back(*c);
+    fgd_ctx& s = copies.back();
+    s.stream = h.stream;
+    s.cap = h.cap;
+    s.own_stream = false;
+    for (int i = 0; i < 6; ++i) s.hb[i] = h.hb[i];
+    s.specA = h.specA;
+    s.specB = h.specB;
+    s.specC = h.specC;
+    s.spec_comps = 1;
+    s.sc = h.sc;
+    s.partials = h.partials;
+    s.partials_cap = h.partials_cap;
+    s.pinned = h.pinned;
+    s.hsub.clear();
+    s.ev_pool.clear();
+    s.ev_rec.clear();
+    s.ov_ev.clear();
+    s.guard = false;
+    s.launches = 0;
+    s.err.clear();
+  }
+  std::vector<std::thread> th;
+  for (int j = 1; j < J; ++j)
+    th.emplace_back([&, j]() {
+      fgd_ctx* s = &copies[j - 1];
+      if (cudaSetDevice(s->device) != cudaSuccess) {
+        st[j] = set_err(s, FGD_ECUDA, "cudaSetDevice failed");
+        return;
+      }
+      solve(s, j);
+      cudaEventRecord(c->hsub[j - 1].ev, s->stream);
+    });
+  solve(c, 0);
+  for (auto& t : th) t.join();
+  fgd_status hard = (st[0] != FGD_OK && st[0] != FGD_ENOCONV) ? st[0] : FGD_OK;
+  for (int j = 1; j < J; ++j) {
+    fgd_helm_sub& h = c->hsub[j - 1];
+    fgd_ctx& s = copies[j - 1];
+    // keep what the copy allocated (work vectors, spectra, partial sums, capture stream)
+    h.cap = s.cap;
+    for (int i = 0; i < 6; ++i) h.hb[i] = s.hb[i];
+    h.specA = s.specA;
+    h.specB = s.specB;
+    h.specC = s.specC;
+    h.partials = s.partials;
+    h.partials_cap = s.partials_cap;
+    c->launches += s.launches;
+    cudaStreamWaitEvent(c->stream, h.ev, 0);
+    if (st[j] != FGD_OK && (st[j] != FGD_ENOCONV || st[0] == FGD_OK) && hard == FGD_OK) {
+      c->err = s.err;
+      if (st[j] != FGD_ENOCONV) hard = st[j];
+    }
+  }
+  return hard;
+}
+
 fgd_status fgd_solve_helmholtz(fgd_ctx* c, int field, const double* src, double* abar, double tol, int maxit,
                                int* iters, double* relres) {
   if (!c) return FGD_EINVAL;
@@ -862,6 +990,32 @@ fgd_status fgd_solve_helmholtz_from(fgd_ctx* c, int field, const double* src, co
   double* dout = nullptr;
   TRY(st.out(abar, c->nvox, &dout));
   fgd_status s = pcg_helmholtz(c, field, ds, dout, tol, maxit, iters, relres, dx0);
+  fgd_status f = st.finish();
+  return s != FGD_OK ? s : f;
+}
+
+fgd_status fgd_solve_helmholtz_all(fgd_ctx* c, const double* src, const double* x0, double* abar, double tol,
+                                   int maxit, int* iters, double* relres) {
+  if (!c) return FGD_EINVAL;
+  if (!c->nonlocal_set || c->nfields < 1) return set_err(c, FGD_ESTATE, "no non-local fields set");
+  if (maxit < 0) return set_err(c, FGD_EINVAL, "maxit < 0");
+  if (!src || !abar) return set_err(c, FGD_EINVAL, "null argument");
+  const int J = c->nfields;
+  Stage st(c);
+  const double *ds = nullptr, *dx0 = nullptr;
+  TRY(st.in(src, (size_t)J * c->nvox, &ds));
+  if (x0) TRY(st.in(x0, (size_t)J * c->nvox, &dx0));
+  double* dout = nullptr;
+  TRY(st.out(abar, (size_t)J * c->nvox, &dout));
+  fgd_status hs[kMaxFields];
+  int hit[kMaxFields] = {};
+  double hrel[kMaxFields] = {};
+  fgd_status s = helm_solve_all(c, J, ds, dx0, dout, tol, maxit, hs, hit, hrel);
+  for (int j = 0; j < J; ++j) {
+    if (iters) iters[j] = hit[j];
+    if (relres) relres[j] = hrel[j];
+    if (s == FGD_OK && hs[j] != FGD_OK) s = hs[j];
+  }
   fgd_status f = st.finish();
   return s != FGD_OK ? s : f;
 }
@@ -1075,19 +1229,22 @@ fgd_status fgd_solve_increment(fgd_ctx* c, const fgd_increment* inc, fgd_report*
     if (!newton_ok) break;
     // Helmholtz solves with the converged sources (A-28)
     bool helm_ok = true;
-    for (int j = 0; j < J && helm_ok; ++j) {
-      int it = 0;
-      fgd_status s = pcg_helmholtz(c, j, c->w_alpha + (size_t)j * n, nullptr, inc->tol_helm, inc->max_helm, &it,
-                                   nullptr, inc->warm_start ? c->w_abar + (size_t)j * n : nullptr);
-      helm_total += it;
-      if (s == FGD_ENOCONV) {
-        why = "Helmholtz PCG did not converge in increment";
-        helm_ok = false;
-        break;
-      }
+    {
+      // the J solves write abar^(k+1) into w_D (kept there until ERR is known), side by side on
+      // launch-bound grids (helm_solve_all)
+      fgd_status hs[kMaxFields];
+      int hit[kMaxFields] = {};
+      double hrel[kMaxFields] = {};
+      fgd_status s = helm_solve_all(c, J, c->w_alpha, inc->warm_start ? c->w_abar : nullptr, c->w_D, inc->tol_helm,
+                                    inc->max_helm, hs, hit, hrel);
       if (s != FGD_OK) return hard(s);
-      // the new non-local field is in hb[0]; w_D holds abar^(k+1) until ERR is known
-      FGD_CUDA(c, cudaMemcpyAsync(c->w_D + (size_t)j * n, c->hb[0], n * 8, cudaMemcpyDeviceToDevice, c->stream));
+      for (int j = 0; j < J; ++j) {
+        helm_total += hit[j];
+        if (hs[j] == FGD_ENOCONV) {
+          why = "Helmholtz PCG did not converge in increment";
+          helm_ok = false;
+        }
+      }
     }
     if (!helm_ok) break;
     // ERR (A-02)

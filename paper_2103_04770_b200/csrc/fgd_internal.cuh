@@ -150,6 +150,20 @@ __host__ __device__ __forceinline__ size_t aidx(int HxA, int Ny, int Nz, int c, 
   return (((size_t)(c * Nz + z) * (HxA / kKB) + kx / kKB) * Ny + y) * kKB + (kx & (kKB - 1));
 }
 
+// Resources of one concurrently solved non-local field j >= 1 (NEXT#3, helm_solve_all): its own
+// stream, Krylov scalars, work vectors and one-component spectrum buffers, so that the J independent
+// Helmholtz solves of a staggered iteration run side by side on the GPU.
+struct fgd_helm_sub {
+  cudaStream_t stream = nullptr, cap = nullptr;
+  cudaEvent_t ev = nullptr;
+  double* hb[6] = {};
+  double2 *specA = nullptr, *specB = nullptr, *specC = nullptr;
+  fgd::DevScalars* sc = nullptr;
+  double* partials = nullptr;
+  size_t partials_cap = 0;
+  double* pinned = nullptr;
+};
+
 struct fgd_ctx {
   int dims = 3;
   int n[3] = {1, 1, 1};        // Nx, Ny, Nz
@@ -217,6 +231,9 @@ struct fgd_ctx {
   double* cg_r = nullptr;
   double* cg_p = nullptr;
   double* hb[6] = {};          // helmholtz work vectors: x r z p0 p1 q
+  int spec_comps = 6;          // components the spectrum buffers hold (1 in a concurrent-field copy)
+  std::vector<fgd_helm_sub> hsub;   // concurrent solves of the fields j >= 1
+  cudaEvent_t hsub_ev = nullptr;
   double* hg = nullptr;        // 3 * nvox: gradient field of the Fourier-form Helmholtz operator
   fgd::DevScalars* sc = nullptr;
   double* partials = nullptr;  // per-CTA partial sums

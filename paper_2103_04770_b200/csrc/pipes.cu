@@ -15,6 +15,7 @@
 #include <cstdlib>
 
 #include "reduce.cuh"
+#include "tma.cuh"
 
 namespace fgd {
 
@@ -1037,18 +1038,29 @@ __device__ __forceinline__ int z5slot(int kz) { return kz; }
 
 // SLAB = false (one slab, P = 1): the z offsets are compile-time immediates from one base pointer
 // (otherwise 32 64-bit addresses stay live across the tile and the kernel spills).
-template <int NC, int MODE, bool SLAB>
+// PF (one slab only): the two z lines of each warp arrive by 1-D bulk copies (8 KB each, the TMA
+// engine) in the warp's own line buffers, completing on a per-warp mbarrier; the copies of the NEXT
+// tile are issued as soon as the warp has read the last exchange of the current one, so they run
+// under the inverse DFT32 and the 32 stores per thread (and under the other CTAs' phases).
+template <int NC, int MODE, bool SLAB, bool PF = false>
 __global__ void __launch_bounds__(NC == 6 ? 96 : 128, NC == 6 ? 4 : 2) k_zreg512w(ZPArgs a) {
   if (guard_done(a.guard)) return;   // converged Krylov loop: skip
+  static_assert(!(PF && SLAB), "prefetched lines must be contiguous (one slab)");
   extern __shared__ double2 sm[];
   constexpr int N = 512;
   const int TL = a.TL;
   const int nl = NC * TL;                       // blockDim.x == 16 * nl
   double2* tw = sm + (size_t)nl * kZ5Line;      // W512^{t k2} at (k2 - 1) * 16 + (t ^ (k2 & 15)), k2 in [1, 32)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(tw + 31 * 16);   // PF: one mbarrier per warp
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   pdl_trigger();
   for (int i = threadIdx.x; i < 31 * 16; i += blockDim.x) {
     const int k2 = 1 + (i >> 4), tt = i & 15;
     tw[(k2 - 1) * 16 + (tt ^ (k2 & 15))] = __ldg(&a.twz[tt * k2]);
+  }
+  if (PF && lane == 0) {
+    mbar_init(&bars[warp], 1);
+    fence_mbar_init();
   }
   __syncthreads();
   pdl_wait();
@@ -1058,14 +1070,34 @@ __global__ void __launch_bounds__(NC == 6 ? 96 : 128, NC == 6 ? 4 : 2) k_zreg512
   const int nyt = a.Nyl / TL;
   const int ntiles = a.nkx * nyt;
   const int BS = NC * a.Hx * a.SL.nys * a.SL.nzs, zm = a.SL.nzs - 1, lgz = a.SL.lg_nzs;
+  // PF: lane 0 of a warp copies the warp's lines 2 warp, 2 warp + 1 of tile tl into their buffers
+  auto prefetch = [&](int tl) {
+    const int kxp = a.kx0 + tl / nyt, kyp = (tl % nyt) * TL;
+    mbar_arrive_expect_tx(&bars[warp], 2 * N * (unsigned)sizeof(double2));
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int lq = 2 * warp + q;
+      bulk_g2s(sm + (size_t)lq * kZ5Line, a.B + r_index(a.SL, NC, a.Hx, lq >> a.lgTL, kxp, kyp + (lq & (TL - 1)), 0),
+               N * (unsigned)sizeof(double2), &bars[warp]);
+    }
+  };
+  unsigned phase = 0;
+  if (PF && lane == 0 && (int)blockIdx.x < ntiles) prefetch(blockIdx.x);
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int kx = a.kx0 + tile / nyt, ky0 = (tile % nyt) * TL;
     const int kyl = ky0 + ll;
     double2* Bl = a.B + r_index(a.SL, NC, a.Hx, c, kx, kyl, 0) + (SLAB ? 0 : t);
     auto zoff = [&](int z) -> size_t { return SLAB ? (size_t)((z >> lgz) * BS + (z & zm)) : (size_t)(z - t); };
     double2 v[32];
+    if (PF) {
+      mbar_wait(&bars[warp], phase);
+      phase ^= 1u;
 #pragma unroll
-    for (int m = 0; m < 32; ++m) v[m] = __ldcg(Bl + zoff(t + 16 * m));
+      for (int m = 0; m < 32; ++m) v[m] = ls[t + 16 * m];
+    } else {
+#pragma unroll
+      for (int m = 0; m < 32; ++m) v[m] = __ldcg(Bl + zoff(t + 16 * m));
+    }
     // ---- forward: DFT32 over m, twiddle, transpose, DFT16 over t ----
     // (each group of 8 outputs of the DFT32 is twiddled and stored at once: register footprint)
     dft32_stage1<false>(v);
@@ -1182,6 +1214,14 @@ __global__ void __launch_bounds__(NC == 6 ? 96 : 128, NC == 6 ? 4 : 2) k_zreg512
     __syncwarp();
 #pragma unroll
     for (int k2 = 0; k2 < 32; ++k2) v[k2] = ls[z5x(k2, t)];
+    if (PF) {
+      // the warp's line buffers are free from here on: refill them with the next tile's lines
+      __syncwarp();
+      if (lane == 0 && tile + (int)gridDim.x < ntiles) {
+        fence_proxy_async();
+        prefetch(tile + gridDim.x);
+      }
+    }
     dft32_stage1<true>(v);
 #pragma unroll
     for (int k1 = 0; k1 < 4; ++k1) {
@@ -2127,11 +2167,17 @@ fgd_status pipe_z(fgd_ctx* c, int ncomp, int mode, double scale, const double* d
     a.TL = TLr;
     a.lgTL = ilog2(TLr);
     const int thr_r = 16 * ncomp * TLr;
-    const size_t smem_r = ((size_t)ncomp * TLr * kZ5Line + 31 * 16) * sizeof(double2);
+    const size_t smem_r = ((size_t)ncomp * TLr * kZ5Line + 31 * 16 + 8) * sizeof(double2);
     const int nt_r = nkx * (Nyl / TLr);
+    static const int z512pf = [] {
+      const char* e = std::getenv("FGD_Z512PF");
+      return e ? std::atoi(e) : 0;   // 1: bulk-copy prefetch of the next tile's lines (one slab, 6 components)
+    }();
     if (c->P > 1) {
       if (ncomp == 6) FGD_PLAUNCH(c, (k_zreg512w<6, Z_PROJECT, true>), thr_r, smem_r, nt_r, a);
       else FGD_PLAUNCH(c, (k_zreg512w<1, Z_PRECOND, true>), thr_r, smem_r, nt_r, a);
+    } else if (ncomp == 6 && z512pf) {
+      FGD_PLAUNCH(c, (k_zreg512w<6, Z_PROJECT, false, true>), thr_r, smem_r, nt_r, a);
     } else {
       if (ncomp == 6) FGD_PLAUNCH(c, (k_zreg512w<6, Z_PROJECT, false>), thr_r, smem_r, nt_r, a);
       else FGD_PLAUNCH(c, (k_zreg512w<1, Z_PRECOND, false>), thr_r, smem_r, nt_r, a);
