@@ -918,17 +918,25 @@ static fgd_status helm_solve_all(fgd_ctx* c, int J, const double* src, const dou
     s.err.clear();
   }
   std::vector<std::thread> th;
-  for (int j = 1; j < J; ++j)
-    th.emplace_back([&, j]() {
-      fgd_ctx* s = &copies[j - 1];
-      if (cudaSetDevice(s->device) != cudaSuccess) {
-        st[j] = set_err(s, FGD_ECUDA, "cudaSetDevice failed");
-        return;
-      }
-      solve(s, j);
-      cudaEventRecord(c->hsub[j - 1].ev, s->stream);
-    });
+  auto run = [&](int j) {
+    fgd_ctx* s = &copies[j - 1];
+    if (cudaSetDevice(s->device) != cudaSuccess) {
+      st[j] = set_err(s, FGD_ECUDA, "cudaSetDevice failed");
+      return;
+    }
+    solve(s, j);
+    cudaEventRecord(c->hsub[j - 1].ev, s->stream);
+  };
+  std::vector<int> inline_fields;   // no thread available: solved on this thread after field 0
+  for (int j = 1; j < J; ++j) {
+    try {
+      th.emplace_back(run, j);
+    } catch (...) {
+      inline_fields.push_back(j);
+    }
+  }
   solve(c, 0);
+  for (int j : inline_fields) run(j);
   for (auto& t : th) t.join();
   fgd_status hard = (st[0] != FGD_OK && st[0] != FGD_ENOCONV) ? st[0] : FGD_OK;
   for (int j = 1; j < J; ++j) {

@@ -97,6 +97,8 @@ struct YArgs {
   const double2* tw;
   SlabL L;
   int kb0, nkbc;   // kx blocks [kb0, kb0 + nkbc) of TK (or kKB) columns handled by this launch (kx chunk)
+  int lgzf;        // 512 kernels: log2 of the z groups that vary fastest in the tile order (then kx blocks, then
+                   // the remaining z groups, then components); < 0 or >= log2(z groups): all z groups fastest
   // Peer-store transposes (FGD_PEER=1, nranks > 1): npeer = P and peer[s] is rank s's
   // z-pass buffer R, offset so that the S index of an element of y-slab s addresses its place in block
   // R[s][r] of that rank.  The forward pass then stores straight into the peers' R (NVLink peer
@@ -105,6 +107,19 @@ struct YArgs {
   double2* peer[kMaxPeers];
 };
 // B-side address of the element with S index `sidx` in y-slab `yb` (= ky >> lg_nys)
+// tile -> (z group, kx block, component) for the 512 kernels (nzt z groups, a power of two).  The
+// tiles that run at the same time (consecutive indices) then cover 2^lgzf neighbouring z groups x
+// many neighbouring kx blocks: contiguous bytes in flight on BOTH strided sides of the transpose
+// (A rows along kx, B runs along z) instead of on the B side only.
+__device__ __forceinline__ void y512_tile(const YArgs& a, int nzt, int lg_nzt, int tile, int* zt, int* kb, int* c) {
+  const int lf = (a.lgzf < 0 || a.lgzf > lg_nzt) ? lg_nzt : a.lgzf;
+  const int lo = tile & ((1 << lf) - 1), r1 = tile >> lf;
+  const int kbi = r1 % a.nkbc, r2 = r1 / a.nkbc;
+  const int hi = r2 & ((nzt >> lf) - 1);
+  *zt = (hi << lf) | lo;
+  *kb = a.kb0 + kbi;
+  *c = r2 >> (lg_nzt - lf);
+}
 __device__ __forceinline__ double2* yb_ptr(const YArgs& a, int yb, size_t sidx) {
   return (a.npeer ? a.peer[yb] : a.B) + sidx;
 }
@@ -402,7 +417,10 @@ __global__ void __launch_bounds__(192, 3) k_zpipe(ZPArgs a) {
 constexpr int kZRowPad = 17;
 constexpr int kZLine = 16 * kZRowPad;
 
-template <int NC, int MODE>
+// PF (one slab: contiguous z lines): the two lines of each warp arrive by 1-D bulk copies (4 KB each)
+// in the first 256 slots of their line buffers, completing on a per-warp mbarrier; the copies of the
+// NEXT tile are issued once the warp has read the last exchange of the current one (see k_zreg512w).
+template <int NC, int MODE, bool PF = false>
 __global__ void __launch_bounds__(NC == 6 ? 96 : 128) __maxnreg__(NC == 6 ? 128 : 128) k_zreg256(ZPArgs a) {
   if (guard_done(a.guard)) return;   // converged Krylov loop: skip
   extern __shared__ double2 sm[];
@@ -411,9 +429,15 @@ __global__ void __launch_bounds__(NC == 6 ? 96 : 128) __maxnreg__(NC == 6 ? 128 
   const int nl = NC * TL;                       // blockDim.x == 16 * nl
   double2* tw = sm + (size_t)nl * kZLine;       // W256^{t k2} at (k2 - 1) * 16 + t
   double2* tws = tw + 240;                      // e^{-2 pi i m / 256} (symbol)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(tws + N);   // PF: one mbarrier per warp
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   pdl_trigger();
   for (int i = threadIdx.x; i < 240; i += blockDim.x) tw[i] = __ldg(&a.twz[(i & 15) * (1 + (i >> 4))]);
   load_table(tws, a.twz, N);
+  if (PF && lane == 0) {
+    mbar_init(&bars[warp], 1);
+    fence_mbar_init();
+  }
   __syncthreads();
   pdl_wait();
   const int line = threadIdx.x >> 4, t = threadIdx.x & 15;
@@ -421,6 +445,18 @@ __global__ void __launch_bounds__(NC == 6 ? 96 : 128) __maxnreg__(NC == 6 ? 128 
   double2* ls = sm + (size_t)line * kZLine;
   const int nyt = a.Nyl / TL;
   const int ntiles = a.nkx * nyt;
+  auto prefetch = [&](int tl) {
+    const int kxp = a.kx0 + tl / nyt, kyp = (tl % nyt) * TL;
+    mbar_arrive_expect_tx(&bars[warp], 2 * N * (unsigned)sizeof(double2));
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int lq = 2 * warp + q;
+      bulk_g2s(sm + (size_t)lq * kZLine, a.B + r_index(a.SL, NC, a.Hx, lq >> a.lgTL, kxp, kyp + (lq & (TL - 1)), 0),
+               N * (unsigned)sizeof(double2), &bars[warp]);
+    }
+  };
+  unsigned phase = 0;
+  if (PF && lane == 0 && (int)blockIdx.x < ntiles) prefetch(blockIdx.x);
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int kx = a.kx0 + tile / nyt, ky0 = (tile % nyt) * TL;
     const int kyl = ky0 + ll;
@@ -428,10 +464,17 @@ __global__ void __launch_bounds__(NC == 6 ? 96 : 128) __maxnreg__(NC == 6 ? 128 
     double2* Bl = a.B + r_index(a.SL, NC, a.Hx, c, kx, kyl, 0);
     const int BS = NC * a.Hx * a.SL.nys * a.SL.nzs, zm = a.SL.nzs - 1, lgz = a.SL.lg_nzs;
     double2 v[16];
+    if (PF) {
+      mbar_wait(&bars[warp], phase);
+      phase ^= 1u;
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      const int z = t + 16 * j;
-      v[j] = __ldcg(Bl + ((z >> lgz) * BS + (z & zm)));
+      for (int j = 0; j < 16; ++j) v[j] = ls[t + 16 * j];
+    } else {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int z = t + 16 * j;
+        v[j] = __ldcg(Bl + ((z >> lgz) * BS + (z & zm)));
+      }
     }
     // ---- forward ----
     dft16<false>(v);
@@ -523,6 +566,14 @@ __global__ void __launch_bounds__(NC == 6 ? 96 : 128) __maxnreg__(NC == 6 ? 128 
     __syncwarp();
 #pragma unroll
     for (int k2 = 0; k2 < 16; ++k2) v[k2] = ls[t * kZRowPad + k2];
+    if (PF) {
+      // the warp's line buffers are free from here on: refill them with the next tile's lines
+      __syncwarp();
+      if (lane == 0 && tile + (int)gridDim.x < ntiles) {
+        fence_proxy_async();
+        prefetch(tile + gridDim.x);
+      }
+    }
     dft16<true>(v);                             // v[n2] = z[t + 16 n2]
 #pragma unroll
     for (int n2 = 0; n2 < 16; ++n2) {
@@ -1263,7 +1314,8 @@ __global__ void __launch_bounds__(128, 3) k_yreg512w(YArgs a) {
   const int nzt = a.Nz / TZ, nkb = a.nkbc, lg_nzt = 31 - __clz(nzt);   // Nz is a power of two
   const int ntiles = a.ncomp * nkb * nzt;
   auto arow_of = [&](int tl) {
-    const int zt = tl & (nzt - 1), r = tl >> lg_nzt, kb = a.kb0 + r % nkb, c = r / nkb;
+    int zt, kb, c;
+    y512_tile(a, nzt, lg_nzt, tl, &zt, &kb, &c);
     return a.A + aidx(a.HxA, N, a.Nz, c, zt * TZ + zz, 0, kb * kKB) + kl + kKB * t;
   };
   double2 v[32];
@@ -1273,7 +1325,8 @@ __global__ void __launch_bounds__(128, 3) k_yreg512w(YArgs a) {
     for (int m = 0; m < 32; ++m) v[m] = __ldcs(A0 + kKB * 16 * m);
   }
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int zt = tile & (nzt - 1), r = tile >> lg_nzt, kb = a.kb0 + r % nkb, c = r / nkb;
+    int zt, kb, c;
+    y512_tile(a, nzt, lg_nzt, tile, &zt, &kb, &c);
     const int z0 = zt * TZ, kx0 = kb * kKB;
     // ---- DFT32 over m, twiddle, transpose (row k2, column t), DFT16 over t ----
     dft32_stage1<false>(v);
@@ -1444,7 +1497,8 @@ __global__ void __launch_bounds__(256, 3) k_yreg512i(YArgs a) {
   const int soff = z2t * LPY + (ky0 >> 6) * 65 + (ky0 & 63);
   const size_t kxstep = (size_t)a.L.nys << a.L.lg_nzs;
   auto issue = [&](int tile, double2* buf) {
-    const int zt = tile & (nzt - 1), r = tile >> lg_nzt, kb = a.kb0 + r % nkb, c = r / nkb;
+    int zt, kb, c;
+    y512_tile(a, nzt, lg_nzt, tile, &zt, &kb, &c);
     const int z = zt * TZ + z2t, kx0 = kb * kKB;
     const bool two = kx0 + 1 < a.Hx;
     double2* sb = buf + soff;
@@ -1469,7 +1523,8 @@ __global__ void __launch_bounds__(256, 3) k_yreg512i(YArgs a) {
     cp_async_commit();
     cp_async_wait<1>();                            // this tile's staging has landed
     __syncthreads();
-    const int zt = tile & (nzt - 1), r = tile >> lg_nzt, kb = a.kb0 + r % nkb, c = r / nkb;
+    int zt, kb, c;
+    y512_tile(a, nzt, lg_nzt, tile, &zt, &kb, &c);
     const int z0 = zt * TZ, kx = kb * kKB + kl;
     double2* ls = cur + (size_t)l * LPY;
     double2 v[8];
@@ -2030,6 +2085,11 @@ fgd_status pipe_y(fgd_ctx* c, int ncomp, bool inv, int kxa, int kxb) {
     YArgs a{c->guard ? c->sc : nullptr, c->specA, c->specB, Nz, c->Hx, c->HxA, TZ, kKB, ncomp, ilog2(TZ), ilog2(kKB), c->tabs.tw[ilog2(Ny)],
             slab_layout(c), kxa / kKB, (kxb - kxa) / kKB};
     fill_peers(c, ncomp, &a);
+    {
+      // tile order of the 512 kernels (y512_tile): FGD_Y512_ZF = log2 of the z groups that vary fastest
+      const char* e = std::getenv("FGD_Y512_ZF");
+      a.lgzf = e ? std::atoi(e) : -1;
+    }
     KTimer kt(c, inv ? (ncomp == 6 ? KC_YINV6 : KC_YINV1) : (ncomp == 6 ? KC_YFWD6 : KC_YFWD1));
     static const int y512i = [] {
       const char* e = std::getenv("FGD_Y512I");
@@ -2155,6 +2215,12 @@ fgd_status pipe_z(fgd_ctx* c, int ncomp, int mode, double scale, const double* d
   a.twy = c->tabs.tw[ilog2(Ny)];
   a.twz = c->tabs.tw[ilog2(Nz)];
   KTimer kt(c, ncomp == 6 ? KC_Z6 : KC_Z1);
+  // 1 (default): the wide 512 z pass takes its lines by bulk copies issued one tile ahead (PF variant;
+  // one slab only).  Measured at 512^3: z6 4.22 -> 3.85 ms per launch.  2: the 256 kernels too.
+  static const int zpf = [] {
+    const char* e = std::getenv("FGD_ZPF");
+    return e ? std::atoi(e) : 1;
+  }();
   static const int z512w = [] {
     const char* e = std::getenv("FGD_Z512");
     return e ? std::atoi(e) : 1;   // 1: wide 32 x 16 plan (k_zreg512w), 0: 8 x 8 x 8 plan (k_zreg512)
@@ -2169,14 +2235,10 @@ fgd_status pipe_z(fgd_ctx* c, int ncomp, int mode, double scale, const double* d
     const int thr_r = 16 * ncomp * TLr;
     const size_t smem_r = ((size_t)ncomp * TLr * kZ5Line + 31 * 16 + 8) * sizeof(double2);
     const int nt_r = nkx * (Nyl / TLr);
-    static const int z512pf = [] {
-      const char* e = std::getenv("FGD_Z512PF");
-      return e ? std::atoi(e) : 0;   // 1: bulk-copy prefetch of the next tile's lines (one slab, 6 components)
-    }();
     if (c->P > 1) {
       if (ncomp == 6) FGD_PLAUNCH(c, (k_zreg512w<6, Z_PROJECT, true>), thr_r, smem_r, nt_r, a);
       else FGD_PLAUNCH(c, (k_zreg512w<1, Z_PRECOND, true>), thr_r, smem_r, nt_r, a);
-    } else if (ncomp == 6 && z512pf) {
+    } else if (ncomp == 6 && zpf) {
       FGD_PLAUNCH(c, (k_zreg512w<6, Z_PROJECT, false, true>), thr_r, smem_r, nt_r, a);
     } else {
       if (ncomp == 6) FGD_PLAUNCH(c, (k_zreg512w<6, Z_PROJECT, false>), thr_r, smem_r, nt_r, a);
@@ -2197,14 +2259,19 @@ fgd_status pipe_z(fgd_ctx* c, int ncomp, int mode, double scale, const double* d
     a.TL = TLr;
     a.lgTL = ilog2(TLr);
     const int thr_r = 16 * ncomp * TLr;
-    const size_t smem_r = ((size_t)ncomp * TLr * kZLine + 240 + 256) * sizeof(double2);
+    const size_t smem_r = ((size_t)ncomp * TLr * kZLine + 240 + 256 + 8) * sizeof(double2);
     const int nt_r = nkx * (Nyl / TLr);
+    // measured at 256^3: no gain from the prefetch (z6 0.432 vs 0.433 ms, z1 0.078 vs 0.082 ms: five
+    // CTAs per SM already hide the 4 KB line loads), so the 256 kernels take it only with FGD_ZPF=2
+    const bool pf = zpf == 2 && c->P == 1 && (ncomp * TLr) % 2 == 0;
     // factorised form (3 transformed components each way) is opt-in: measured 7.66 vs 4.72 ms per
     // 256^3 sweep -- its serial phases leave half of the CTA idle and spill; the FP64 saving does
     // not pay for that at this occupancy
     if (ncomp == 6 && c->scheme == 1 && TLr == 1 && std::getenv("FGD_ZFAC"))
       FGD_PLAUNCH(c, k_zfac256, 96, smem_r, nt_r, a);
+    else if (ncomp == 6 && pf) FGD_PLAUNCH(c, (k_zreg256<6, Z_PROJECT, true>), thr_r, smem_r, nt_r, a);
     else if (ncomp == 6) FGD_PLAUNCH(c, (k_zreg256<6, Z_PROJECT>), thr_r, smem_r, nt_r, a);
+    else if (pf) FGD_PLAUNCH(c, (k_zreg256<1, Z_PRECOND, true>), thr_r, smem_r, nt_r, a);
     else FGD_PLAUNCH(c, (k_zreg256<1, Z_PRECOND>), thr_r, smem_r, nt_r, a);
     return FGD_OK;
   }
