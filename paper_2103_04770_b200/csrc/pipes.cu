@@ -23,6 +23,17 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
 }
+// The same 16-byte copy with an L2 prefetch hint: the L2 fetches the whole aligned 64 / 128 / 256 B
+// block around the address (hint = 1 / 2 / 3; 0 = plain copy).  For the strided side of the y
+// transposes, whose 32-64 B runs are completed by OTHER CTAs running at the same time: one wide
+// DRAM access instead of several isolated sector reads.
+__device__ __forceinline__ void cp_async16_l2(void* smem, const void* gmem, int hint) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  if (hint == 1) asm volatile("cp.async.cg.shared.global.L2::64B [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+  else if (hint == 2) asm volatile("cp.async.cg.shared.global.L2::128B [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+  else if (hint == 3) asm volatile("cp.async.cg.shared.global.L2::256B [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+  else asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int K>
 __device__ __forceinline__ void cp_async_wait() {
@@ -97,6 +108,7 @@ struct YArgs {
   const double2* tw;
   SlabL L;
   int kb0, nkbc;   // kx blocks [kb0, kb0 + nkbc) of TK (or kKB) columns handled by this launch (kx chunk)
+  int l2pf;        // inverse pass: L2 prefetch hint of the strided B-side cp.async reads (0 none, 1/2/3 = 64/128/256 B)
   int lgzf;        // 512 kernels: log2 of the z groups that vary fastest in the tile order (then kx blocks, then
                    // the remaining z groups, then components); < 0 or >= log2(z groups): all z groups fastest
   // Peer-store transposes (FGD_PEER=1, nranks > 1): npeer = P and peer[s] is rank s's
@@ -799,8 +811,8 @@ __device__ __forceinline__ void y256_issue_inv(const YArgs& a, int tile, double2
     const int z2 = idx % TZ, ky = (idx / TZ) & (N - 1), k2l = idx / (TZ * N);
     const int kxo = kx0 + k2l;
     if (kxo < a.Hx)
-      cp_async16(&buf[(size_t)(k2l * TZ + z2) * ypitch(kZLine, TZ) + ky + (ky >> 4)],
-                 yb_ptr(a, ky >> a.L.lg_nys, s_index(a.L, a.ncomp, a.Hx, c, kxo, ky, z0 + z2)));
+      cp_async16_l2(&buf[(size_t)(k2l * TZ + z2) * ypitch(kZLine, TZ) + ky + (ky >> 4)],
+                    yb_ptr(a, ky >> a.L.lg_nys, s_index(a.L, a.ncomp, a.Hx, c, kxo, ky, z0 + z2)), a.l2pf);
   }
 }
 
@@ -1506,8 +1518,8 @@ __global__ void __launch_bounds__(256, 3) k_yreg512i(YArgs a) {
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const double2* g = yb_ptr(a, (ky0 + 128 * j) >> a.L.lg_nys, s_index(a.L, a.ncomp, a.Hx, c, kx0, ky0 + 128 * j, z));
-      cp_async16(sb + 130 * j, g);
-      if (two) cp_async16(sb + 130 * j + TZ * LPY, g + kxstep);
+      cp_async16_l2(sb + 130 * j, g, a.l2pf);
+      if (two) cp_async16_l2(sb + 130 * j + TZ * LPY, g + kxstep, a.l2pf);
     }
   };
   int i = 0;
@@ -2074,6 +2086,16 @@ static void fill_peers(const fgd_ctx* c, int ncomp, YArgs* a) {
   for (int s = 0; s < P; ++s) a->peer[s] = c->peerC[s] + (long long)(c->rank - s) * blk;
 }
 
+// L2 prefetch hint of the y-inverse B-side reads (FGD_Y_L2PF = 0..3; local buffers only: a peer's
+// memory is not cached in this GPU's L2 the same way)
+static int y_l2pf(const fgd_ctx* c) {
+  static const int v = [] {
+    const char* e = std::getenv("FGD_Y_L2PF");
+    return e ? std::atoi(e) : 0;
+  }();
+  return (c->peer_on || c->nranks > 1) ? 0 : v;
+}
+
 fgd_status pipe_y(fgd_ctx* c, int ncomp, bool inv, int kxa, int kxb) {
   const int Ny = c->n[1], Nz = c->nz_l;
   if (kxb < 0) kxb = c->HxA;   // kx chunk [kxa, kxb): multiples of 4 (kx blocks of kKB or TK <= 4)
@@ -2085,6 +2107,7 @@ fgd_status pipe_y(fgd_ctx* c, int ncomp, bool inv, int kxa, int kxb) {
     YArgs a{c->guard ? c->sc : nullptr, c->specA, c->specB, Nz, c->Hx, c->HxA, TZ, kKB, ncomp, ilog2(TZ), ilog2(kKB), c->tabs.tw[ilog2(Ny)],
             slab_layout(c), kxa / kKB, (kxb - kxa) / kKB};
     fill_peers(c, ncomp, &a);
+    a.l2pf = y_l2pf(c);
     {
       // tile order of the 512 kernels (y512_tile): FGD_Y512_ZF = log2 of the z groups that vary fastest
       const char* e = std::getenv("FGD_Y512_ZF");
@@ -2136,6 +2159,7 @@ fgd_status pipe_y(fgd_ctx* c, int ncomp, bool inv, int kxa, int kxb) {
     YArgs a{c->guard ? c->sc : nullptr, c->specA, c->specB, Nz, c->Hx, c->HxA, TZ, kKB, ncomp, ilog2(TZ), ilog2(kKB), c->tabs.tw[ilog2(Ny)],
             slab_layout(c), kxa / kKB, (kxb - kxa) / kKB};
     fill_peers(c, ncomp, &a);
+    a.l2pf = y_l2pf(c);
     KTimer kt(c, inv ? (ncomp == 6 ? KC_YINV6 : KC_YINV1) : (ncomp == 6 ? KC_YFWD6 : KC_YFWD1));
     if (inv) FGD_PLAUNCH(c, k_yreg256<true>, thr, smem, ntiles, a);
     else FGD_PLAUNCH(c, k_yreg256<false>, thr, smem, ntiles, a);

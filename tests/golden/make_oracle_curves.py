@@ -58,6 +58,9 @@ def cases():
         "config2_256": (lambda: synth.config2(256), None),
         # reduced config 3: 32^3 RSA cell (30 spheres, 20 %), ell_m = 5h, ell_p = 3h, E_zz ramp
         "config3_32": (lambda: synth.config3(n=32), None),
+        # BJ config 3 at its own size (128^3, 30 spheres): the first increments only (--incr 2; every
+        # oracle CG iteration at this size takes seconds)
+        "config3_128": (lambda: synth.config3(n=128), None),
         # small cells for quick checks of the generator itself
         "config0_16": (lambda: synth.config0(16, ell_over_L=1.0 / 8.0), None),
     }

@@ -33,7 +33,7 @@ import make_oracle_curves as moc  # noqa: E402
 from paper_2103_04770_b200 import Context, Material  # noqa: E402
 
 ROOT = os.path.dirname(HERE)
-CASES = [c for c in ("config0_32", "config2_64", "config2_256", "config3_32")
+CASES = [c for c in ("config0_32", "config2_64", "config2_256", "config3_32", "config3_128")
          if os.path.exists(os.path.join(HERE, "golden", f"curve_{c}.json"))]
 
 
