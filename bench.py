@@ -204,7 +204,7 @@ def peaks():
 # kernel of each class in the ncu summaries (first candidate present in the newest summary wins)
 TRAFFIC_KERNEL = {"xfwd6cg": ["k_xtan_pp<{n}, 2, 1>", "k_xtan<{n}, 2, 1, 2>"], "xinv6": ["k_xipipe<{n}, 1>"],
                   "stencil": ["k_stencil<1, 4, 1, 2>", "k_stencil<1, 2>"],
-                  "z6": ["k_zreg512w<6, 0, 0>", "k_zreg256<6, 0>"],
+                  "z6": ["k_zreg512w<6, 0, 0, 1>", "k_zreg512w<6, 0, 0>", "k_zreg256<6, 0, 0>", "k_zreg256<6, 0>"],
                   "yfwd6": ["k_yreg512w", "k_yreg512<0>", "k_yreg256<0>"],
                   "yinv6": ["k_yreg512i", "k_yreg256<1>"]}
 
