@@ -554,6 +554,15 @@ def measure(a, n, rank, world, local, nid, e2e_on, extras):
                  if k in per_class)
     t_helm = sum(per_class[k]["ms_per_step"] for k in ("xfwd1", "yfwd1", "z1", "yinv1", "xinv1", "stencil")
                  if k in per_class)
+    b_mech = sum(cb[k] for k in ("xfwd6", "xfwd6cg", "yfwd6", "z6", "yinv6", "xinv6") if k in per_class)
+    b_helm = sum(cb[k] for k in ("xfwd1", "yfwd1", "z1", "yinv1", "xinv1", "stencil") if k in per_class)
+    op_roof = {"what": "operator-level roofline: algorithmic bytes of the kernel classes of the mechanical Krylov "
+                       "solve (projected-tangent applies incl. the fused CG updates) and of the Helmholtz PCG "
+                       "(stencil + preconditioner passes incl. the fused updates) over their event-timed duration",
+               "mech_GBs": b_mech / (t_mech * 1e-3) / 1e9 if t_mech else None,
+               "mech_frac": b_mech / (t_mech * 1e-3) / 1e9 / peak if t_mech else None,
+               "helm_GBs": b_helm / (t_helm * 1e-3) / 1e9 if t_helm else None,
+               "helm_frac": b_helm / (t_helm * 1e-3) / 1e9 / peak if t_helm else None}
     mech_apply_ms = t_mech / (a.kcg + 1) if t_mech else None
     helm_iter_ms = t_helm / (a.khelm + 1) if t_helm else None
     rates = {"mech_cg_iter_per_s": 1e3 / mech_apply_ms if mech_apply_ms else None,
@@ -562,6 +571,7 @@ def measure(a, n, rank, world, local, nid, e2e_on, extras):
              "helm_pcg_iter_per_s": 1e3 / helm_iter_ms if helm_iter_ms else None,
              "helm_pcg_iter_ms": helm_iter_ms,
              "helm_pcg_voxel_iter_per_s": V / (helm_iter_ms * 1e-3) if helm_iter_ms else None,
+             "operator_roofline": op_roof,
              "note": "Krylov iteration rates from the event-timed kernel classes of one rank (the step's "
                      "constitutive update and reductions excluded); value/ms_per_step is the whole step"}
     ctx.close()

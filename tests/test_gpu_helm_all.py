@@ -155,3 +155,37 @@ def test_increments_concurrent_equal_consecutive():
     print(f"two-field increments at 16^3: concurrent {ta:.3f} s, consecutive {tb:.3f} s")
     ca.close()
     cb.close()
+
+
+@pytest.mark.parametrize("P", [2, 4])
+def test_all_fields_emulated_slabs(monkeypatch, P):
+    """The side-by-side solves on the P-slab spectrum layout (FGD_EMULATE_SLABS: every field copy owns
+    its one-component slab buffers)."""
+    monkeypatch.setenv("FGD_EMULATE_SLABS", str(P))
+    n = (32, 16, 8)
+    g, ph, ell, ctx, src, x0 = two_field_ctx(n, 21)
+    out = torch.empty((2,) + g.shape, dtype=torch.float64, device="cuda")
+    with conc(1):
+        its, _ = ctx.solve_helmholtz_all(dev(src), dev(x0), out, 2, tol=0.0, maxit=4)
+        assert its == [4, 4]
+        for j in range(2):
+            ref, _, _ = solve_helmholtz(g, src[j], ell2_field(ph, ell[j]), tol=0.0, maxit=4, x0=x0[j])
+            assert rel(out[j].cpu().numpy(), ref) <= 1e-10, (P, j)
+    ctx.close()
+
+
+def test_single_field_goes_through_all():
+    """J = 1: fgd_solve_helmholtz_all is the plain solve."""
+    n = (16, 16, 1)
+    g = Grid(n, (1.0, 1.0, 1.0))
+    rng = np.random.default_rng(3)
+    ph = (rng.random(g.shape) < 0.4).astype(np.uint8)
+    ctx = Context(n, (1.0, 1.0, 1.0))
+    ctx.set_phases(dev(ph), 2)
+    ctx.set_nonlocal(np.array([[0.05, 0.02]]), [0])
+    src = np.abs(rng.normal(size=(1,) + g.shape))
+    out = torch.empty((1,) + g.shape, dtype=torch.float64, device="cuda")
+    its, rr = ctx.solve_helmholtz_all(dev(src), None, out, 1, tol=1e-10, maxit=500)
+    ref, it_ref, _ = solve_helmholtz(g, src[0], ell2_field(ph, [0.05, 0.02]), tol=1e-10, maxit=500)
+    assert abs(its[0] - it_ref) <= 1 and rel(out[0].cpu().numpy(), ref) <= 1e-8
+    ctx.close()
