@@ -199,6 +199,10 @@ typedef struct {
   int line_search; /* 1: Newton with residual backtracking (reading R-LS of DESIGN.md: a step that
                       does not lower the RMS of -G*(sigma - Sigma) is halved, at most 5 times);
                       0: plain Newton-Raphson */
+  int stag_stall;  /* > 0: return FGD_ENOCONV (rollback) as soon as ERR has not improved on its running
+                      minimum for this many consecutive staggered iterations (a diverging staggered
+                      loop: the caller cuts the step back, A-34, without paying max_stag iterations);
+                      0: off -- Algorithm 1 as printed (the parity setting) */
 } fgd_increment;
 typedef struct {
   double macro_stress[6], macro_strain[6], err;

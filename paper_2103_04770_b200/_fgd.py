@@ -48,7 +48,7 @@ class fgd_increment(C.Structure):
                 ("tol_stag", C.c_double), ("tol_newton", C.c_double), ("tol_cg", C.c_double),
                 ("tol_helm", C.c_double), ("max_stag", C.c_int), ("max_newton", C.c_int),
                 ("max_cg", C.c_int), ("max_helm", C.c_int), ("warm_start", C.c_int),
-                ("line_search", C.c_int)]
+                ("line_search", C.c_int), ("stag_stall", C.c_int)]
 
 
 class fgd_report(C.Structure):

@@ -215,11 +215,11 @@ class Context:
 
     def solve_increment(self, E_target, S_target=None, tol_stag=1e-8, tol_newton=1e-10, tol_cg=1e-11,
                         tol_helm=1e-11, max_stag=100, max_newton=50, max_cg=5000, max_helm=5000, warm_start=False,
-                        line_search=True):
+                        line_search=True, stag_stall=0):
         S_target = np.zeros(6) if S_target is None else S_target
         inc = _fgd.fgd_increment((C.c_double * 6)(*map(float, E_target)), (C.c_double * 6)(*map(float, S_target)),
                                  tol_stag, tol_newton, tol_cg, tol_helm, max_stag, max_newton, max_cg, max_helm,
-                                 1 if warm_start else 0, 1 if line_search else 0)
+                                 1 if warm_start else 0, 1 if line_search else 0, int(stag_stall))
         rep = _fgd.fgd_report()
         st = _fgd.fgd_solve_increment(self.h, C.byref(inc), C.byref(rep))
         if st not in (0, _fgd.ENOCONV):

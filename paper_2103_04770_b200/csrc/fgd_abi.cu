@@ -1161,7 +1161,8 @@ fgd_status fgd_solve_increment(fgd_ctx* c, const fgd_increment* inc, fgd_report*
   for (int i = 0; i < 6; ++i) S[i] = inc->S_target[i] * c->stress_mask[i];
   const double sref = sigma_ref(c);
   int newton_total = 0, cg_total = 0, helm_total = 0, k = 0;
-  double err = INFINITY;
+  double err = INFINITY, err_min = INFINITY;
+  int stalled = 0;
   bool converged = false;
   double macro[6] = {0, 0, 0, 0, 0, 0};
   std::string why = "increment did not converge";
@@ -1275,6 +1276,17 @@ fgd_status fgd_solve_increment(fgd_ctx* c, const fgd_increment* inc, fgd_report*
     if (trace_on() && c->rank == 0) fprintf(stderr, "fgd trace: stag %d ERR %.3e\n", k, err);
     if (err < inc->tol_stag) {   // w_abar = abar^(k) (frozen in the mechanics), w_D = abar^(k+1)
       converged = true;
+      break;
+    }
+    // stag_stall > 0 (off for Algorithm 1 as printed): give up once ERR has not improved on its
+    // running minimum for that many consecutive iterations -- a staggered loop that unfreezes new
+    // damage in every iteration (the step is too large); the caller cuts back (A-34) without
+    // paying max_stag iterations first
+    if (err < err_min) {
+      err_min = err;
+      stalled = 0;
+    } else if (inc->stag_stall > 0 && ++stalled >= inc->stag_stall) {
+      why = "staggered iteration stalled (ERR not improving)";
       break;
     }
     if (J > 0) FGD_CUDA(c, cudaMemcpyAsync(c->w_abar, c->w_D, (size_t)J * n * 8, cudaMemcpyDeviceToDevice, c->stream));

@@ -68,7 +68,7 @@ def adaptive_schedule(solve, E_end, dE0, dE_max=None, dE_min=1e-5, grow=1.5, gro
 
 def run_config(cfg, n_incr=None, tol=(1e-4, 1e-6, 1e-8, 1e-6), max_halvings=6, max_cg=5000, max_helm=5000,
                adaptive=False, de_min=1e-5, log=False, grow=1.5, stop_frac=None, max_stag=100, warm=False,
-               max_newton=50, profile=None):
+               max_newton=50, profile=None, stag_stall=0):
     """Load the cell along cfg.load_comp to n_incr * cfg.dE: fixed increments with deterministic
     halving (A-21), or the adaptive schedule (A-34); returns a result dict."""
     import torch
@@ -88,7 +88,7 @@ def run_config(cfg, n_incr=None, tol=(1e-4, 1e-6, 1e-8, 1e-6), max_halvings=6, m
         Et[cfg.load_comp] = E_try
         st, rep = ctx.solve_increment(Et, np.zeros(6), tol_stag, tol_newton, tol_cg, tol_helm,
                                       max_stag=max_stag, max_newton=max_newton, max_cg=max_cg, max_helm=max_helm,
-                                      warm_start=warm)
+                                      warm_start=warm, stag_stall=stag_stall)
         for k in ("stag", "newton", "cg", "helm"):
             counts[k] += rep[k]
         if log and st != 0:
@@ -126,7 +126,7 @@ def run_config(cfg, n_incr=None, tol=(1e-4, 1e-6, 1e-8, 1e-6), max_halvings=6, m
             Et[cfg.load_comp] = E_try
             st, rep = ctx.solve_increment(Et, np.zeros(6), tol_stag, tol_newton, tol_cg, tol_helm,
                                           max_stag=max_stag, max_newton=max_newton, max_cg=max_cg, max_helm=max_helm,
-                                      warm_start=warm)
+                                          warm_start=warm, stag_stall=stag_stall)
             counts["stag"] += rep["stag"]
             counts["newton"] += rep["newton"]
             counts["cg"] += rep["cg"]
@@ -163,7 +163,7 @@ def run_config(cfg, n_incr=None, tol=(1e-4, 1e-6, 1e-8, 1e-6), max_halvings=6, m
     return dict(config=cfg.name, n=list(cfg.n), load_comp=cfg.load_comp, dE=cfg.dE, wall_s=wall,
                 peak_stress=float(s[ip]), strain_at_peak=float(e[ip]), strain_at_failure=fail,
                 curve=[[float(a), float(b)] for a, b in curve], tolerances=list(tol), max_cg=max_cg,
-                max_halvings=max_halvings, adaptive=adaptive, max_stag=max_stag, warm_start=warm,
+                max_halvings=max_halvings, adaptive=adaptive, max_stag=max_stag, warm_start=warm, stag_stall=stag_stall,
                 ell=np.asarray(cfg.ell).tolist(), **({"profile": prof} if prof else {}), **counts)
 
 
@@ -204,6 +204,8 @@ def main(argv=None):
                    help="adaptive: stop once the load stress falls below this fraction of the peak")
     p.add_argument("--max-stag", type=int, default=100)
     p.add_argument("--warm", action="store_true", help="warm-started Helmholtz PCG (S:262)")
+    p.add_argument("--stag-stall", type=int, default=0,
+                   help="fail an increment once ERR has not improved for this many staggered iterations (0: off)")
     p.add_argument("--max-newton", type=int, default=50)
     p.add_argument("--ell", type=float, default=None,
                    help="gtn2d: matrix ell_M / L (ell_I = min(ell_M, 0.001 L); 1e-4 gives the local variant)")
@@ -229,7 +231,7 @@ def main(argv=None):
         cfg.dE = a.de
     tol = (1e-8, 1e-10, 1e-11, 1e-11) if a.tight else (1e-4, 1e-6, 1e-8, 1e-6)
     print(json.dumps(run_config(cfg, a.incr, tol, a.halvings, a.max_cg, a.max_cg, adaptive=a.adaptive, log=a.log,
-                                grow=a.grow, stop_frac=a.stop_frac, max_stag=a.max_stag, warm=a.warm,
+                                grow=a.grow, stop_frac=a.stop_frac, max_stag=a.max_stag, warm=a.warm, stag_stall=a.stag_stall,
                                 max_newton=a.max_newton, profile=a.profile)), flush=True)
 
 
