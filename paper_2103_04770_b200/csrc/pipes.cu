@@ -1286,12 +1286,17 @@ __global__ void __launch_bounds__(NC == 6 ? 96 : 128, NC == 6 ? 4 : 2) k_zreg512
       }
     }
     dft32_stage1<true>(v);
+    // slab layout: the store offsets are recomputed from an opaque copy of the slab stride, so that
+    // the 32 load offsets are not kept live (as 64-bit registers) across the whole tile -- they spilled
+    int BSs = BS;
+    if (SLAB) asm volatile("" : "+r"(BSs));
 #pragma unroll
     for (int k1 = 0; k1 < 4; ++k1) {
       dft8<true>(v + 8 * k1);                                // v[8 k1 + j] = z[t + 16 (k1 + 4 j)]
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        Bl[zoff(t + 16 * (k1 + 4 * j))] = v[8 * k1 + j];
+        const int z = t + 16 * (k1 + 4 * j);
+        Bl[SLAB ? (size_t)((z >> lgz) * BSs + (z & zm)) : zoff(z)] = v[8 * k1 + j];
       }
     }
   }
